@@ -1,0 +1,183 @@
+/*
+ * kde.h — C ABI of the B200-native all-pairs kernel-sum engine for the bandwidth selectors of
+ * Andrzejewski, Gramacki & Gramacki, "Density Estimations for Approximate Query Processing on
+ * SIMD Architectures" (arxiv 1505.01998).  P:NNN = PAPER.md line NNN.
+ *
+ * Conventions (apply to every call below):
+ *  - Ownership: the caller owns every buffer.  Sample matrices are DEVICE pointers (fp64,
+ *    d x n, row-major: dimension a of sample i at X[a*n + i], the paper's layout
+ *    Eq. 19).  Candidate arrays and outputs are HOST pointers.
+ *  - Errors: a call returns KDE_OK or an error code; on error the outputs are untouched and
+ *    kde_last_error(ctx) holds a one-line message.  No C++ exception crosses the boundary.
+ *    A CUDA or NCCL failure poisons the context (every later call returns the same code).
+ *  - Synchronisation: work is enqueued on the context's stream; each call returns after the
+ *    host results are available (it synchronises that stream).
+ *  - Multi-GPU (SPMD): with world > 1 every rank calls the same function with identical
+ *    arguments (each on its own copy of X).  The upper-triangular tile set is split into
+ *    contiguous ranges across ranks and one NCCL all-reduce of exact fixed-point partial sums
+ *    combines them, so every rank returns bit-identical results, equal to the 1-GPU result.
+ *  - Determinism: results are bit-for-bit reproducible for a given (X, n, d, candidates),
+ *    independent of the number of GPUs, the grid size and of which candidates share a batch.
+ *  - Limits: 2 <= n <= 2^31-1 (1 <= n for kde_raw_sums), 1 <= d <= 16.
+ *  - Threading: a context must not be used from two threads at once.
+ */
+#ifndef KDE_B200_H
+#define KDE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  KDE_OK = 0,
+  KDE_E_INVALID = 1,              /* null pointer, bad size, r not in {4,6,8}, non-finite X     */
+  KDE_E_NOT_UNIVARIATE = 2,       /* PLUGIN / Psi_r with d != 1                          */
+  KDE_E_INSUFFICIENT_SAMPLES = 3, /* n < 2                                                       */
+  KDE_E_DEGENERATE = 4,           /* variance estimate <= 0 (all samples equal)       */
+  KDE_E_SINGULAR_COV = 5,         /* covariance not positive definite (det Sigma <= 0)    */
+  KDE_E_NONPOSITIVE_BW = 6,       /* a candidate h or g <= 0 or non-finite                      */
+  KDE_E_DIM_MISMATCH = 7,         /* d out of range for this call                               */
+  KDE_E_NUMERIC = 8,              /* Psi6-hat >= 0 or Psi4-hat <= 0 (impossible in exact arith.) */
+  KDE_E_NO_FEASIBLE = 9,          /* LSCV_H: no positive-definite vertex to start from          */
+  KDE_E_CUDA = 10,
+  KDE_E_NCCL = 11,
+  KDE_E_OOM = 12
+} kde_status;
+
+typedef struct kde_ctx kde_ctx;
+
+/* Intermediate values of the PLUGIN chain, steps 1-8 of P:203-256 (Eq. 11-18). */
+typedef struct {
+  double V_hat, sigma_hat, psi8_ns, g1, psi6, g2, psi4, h;
+} kde_plugin_trace;
+
+typedef enum { KDE_PLUGIN = 0, KDE_LSCV_h = 1, KDE_LSCV_H = 2 } kde_method;
+
+typedef struct {
+  int32_t n_grid;        /* LSCV_h: number of h on Z(h0) = [h0/f, f*h0]; 150 */
+  double range_factor;   /* LSCV_h: f = 4 (Eq. 27)                                             */
+  int32_t max_iter;      /* LSCV_H Nelder-Mead iterations; 500                                   */
+  double tol_rel;        /* LSCV_H stop when f_worst - f_best <= tol_rel*|f_best|; 1e-7          */
+  double penalty;        /* LSCV_H objective assigned to a non-positive-definite H; 1e300        */
+  int32_t speculative;   /* LSCV_H: 1 = evaluate {reflect, expand, contract_out, contract_in} as
+                            one GPU batch per iteration (same decisions as serial NM); 0 = serial */
+} kde_select_opts;
+
+typedef struct {
+  kde_method method;
+  int32_t d;
+  double h;                /* PLUGIN / LSCV_h bandwidth (scalar)                               */
+  double vechH[136];       /* LSCV_H: vech of the selected H, d(d+1)/2 entries      */
+  double objective;        /* LSCV: g at the selected bandwidth; PLUGIN: 0                      */
+  int32_t iterations;      /* LSCV_H Nelder-Mead iterations; LSCV_h: selected grid index        */
+  int32_t evaluations;     /* number of objective values computed on the GPU                    */
+  int32_t stop_reason;     /* LSCV_H: 1 = tolerance, 2 = max_iter                               */
+  kde_plugin_trace trace;  /* PLUGIN only                                                       */
+} kde_bandwidth;
+
+/* Exact fixed-point value: value = (hi*2^80 + mid*2^40 + lo) * 2^-scale_exp (see kde_fixed_value).
+ * Partial sums from different tiles / ranks add limb-wise without rounding. */
+typedef struct {
+  int64_t hi, mid, lo;
+  int32_t scale_exp;
+  int32_t pad_;
+} kde_fixed;
+
+/* ---------------------------------------------------------------- context & memory */
+
+/* Create a context on CUDA `device`, enqueuing on `cuda_stream` (a cudaStream_t; NULL = the
+ * legacy default stream).  For world > 1, `nccl_unique_id` points to the 128-byte ncclUniqueId
+ * rank 0 obtained from kde_nccl_unique_id() and broadcast to all ranks; the library creates its
+ * own NCCL communicator (NCCL is loaded at run time, libnccl.so.2).  world == 1 ignores it. */
+kde_status kde_create(kde_ctx **out, int device, void *cuda_stream, const void *nccl_unique_id,
+                      int rank, int world);
+void kde_destroy(kde_ctx *ctx);
+const char *kde_last_error(const kde_ctx *ctx);
+/* Fill a 128-byte buffer with a fresh ncclUniqueId (rank 0 only). */
+kde_status kde_nccl_unique_id(void *out128);
+
+/* Device workspace the calls need for (n, d, n_cand); the caller may provide it with
+ * kde_set_workspace (memory stays owned by the caller and must outlive its use); otherwise the
+ * context allocates what it needs with cudaMalloc on first use. */
+size_t kde_workspace_bytes(int64_t n, int32_t d, int32_t n_cand);
+kde_status kde_set_workspace(kde_ctx *ctx, void *dev_ptr, size_t bytes);
+
+void kde_default_opts(kde_select_opts *opts);
+
+/* ---------------------------------------------------------------- the five entry points */
+
+/* Psi_r-hat(g_c) for c < n_g, r in {4,6,8}:
+ *   Psi_r-hat(g) = [2 sum_{i<j} K^(r)((x_i-x_j)/g) + n K^(r)(0)] / (n^2 g^(r+1)),
+ *   K^(r)(u) = He_r(u) exp(-u^2/2)/sqrt(2 pi)   (Eq. 15, Eq. 17; the
+ *   diagonal term read inside the bracket, reading Z1).  x_dev: n fp64 (d = 1).
+ *   Errors: KDE_E_INVALID (r, n<1, NULL), KDE_E_NONPOSITIVE_BW (g <= 0). */
+kde_status kde_psi_r(kde_ctx *ctx, const double *x_dev, int64_t n, int32_t r, const double *g_host,
+                     int32_t n_g, double *psi_host);
+
+/* PLUGIN bandwidth (Sec. 4.4.1): V-hat, sigma-hat, Psi8^NS, g1, Psi6-hat(g1), g2,
+ * Psi4-hat(g2), h.  Errors: KDE_E_INSUFFICIENT_SAMPLES, KDE_E_DEGENERATE, KDE_E_NUMERIC. */
+kde_status kde_plugin_h(kde_ctx *ctx, const double *x_dev, int64_t n, double *h_host,
+                        kde_plugin_trace *trace_or_null);
+
+/* LSCV_h objective g(h_c) for c < n_h (Eq. 24-27 / modified Eq. 36-41):
+ *   g(h) = h^-d [2 n^-2 sum_{i<j} T((X_i-X_j)/h) + n^-1 R(K)],  T = K*K - 2K with the
+ *   Sigma-shaped Gaussian K, R(K) = (4 pi)^{-d/2}|Sigma|^{-1/2} (reading Z2),
+ *   Sigma the unbiased sample covariance (Eq. 20-23).
+ * Errors: KDE_E_SINGULAR_COV, KDE_E_NONPOSITIVE_BW, KDE_E_INSUFFICIENT_SAMPLES. */
+kde_status kde_lscv_h_scores(kde_ctx *ctx, const double *X_dev, int64_t n, int32_t d,
+                             const double *h_host, int32_t n_h, double *g_host);
+
+/* LSCV_H objective g(H_c) for c < n_H (Eq. 30-34):
+ *   g(H) = 2 n^-2 sum_{i<j} [(K*K)_H - 2 K_H](X_i - X_j) + n^-1 (4 pi)^{-d/2} |H|^{-1/2}.
+ * vechH_host: n_H rows of d(d+1)/2 doubles, vech order of P:351-363 (lower triangle, column by
+ * column).  A candidate that fails the Cholesky positive-definiteness test gets `penalty`
+ * (1e300 when penalty_or_nan is NaN) instead of an error. */
+kde_status kde_lscv_H_scores(kde_ctx *ctx, const double *X_dev, int64_t n, int32_t d,
+                             const double *vechH_host, int32_t n_H, double penalty_or_nan,
+                             double *g_host);
+
+/* Full selector: PLUGIN (d = 1), LSCV_h (grid argmin on Z(h0), ties -> smaller h), or LSCV_H
+ * (Nelder-Mead over vech(H) from H_start of Eq. 35).  opts_or_null: NULL = kde_default_opts. */
+kde_status kde_select_bandwidth(kde_ctx *ctx, kde_method method, const double *X_dev, int64_t n,
+                                int32_t d, const kde_select_opts *opts_or_null, kde_bandwidth *out);
+
+/* ---------------------------------------------------------------- lower level (tests, tools) */
+
+typedef enum {
+  KDE_SUM_PSI4 = 4, KDE_SUM_PSI6 = 6, KDE_SUM_PSI8 = 8,  /* 1 sum per candidate g              */
+  KDE_SUM_LSCV_h = 1,   /* 2 sums per candidate h: sum e, sum e^2, e = exp(-S(v)/(4h^2))       */
+  KDE_SUM_LSCV_H = 2    /* 2 sums per candidate H: sum e, sum e^2, e = exp(-v^T H^-1 v / 4)     */
+} kde_sum_kind;
+
+/* The raw pairwise sums RR_fun over the tiles of shard `shard_rank` of `shard_world`
+ * (shard_world = 0: this context's own rank/world, all-reduced), as exact fixed-point values:
+ *   PSI_r : out[c]       = sum_{i<j} He_r(u) exp(-u^2/2),  u = (x_i - x_j)/g_c
+ *   LSCV_h: out[2c+{0,1}] = sum_{i<j} e, e^2 with e = exp(-(X_i-X_j)^T Sigma^-1 (X_i-X_j)/(4h_c^2))
+ *   LSCV_H: out[2c+{0,1}] = sum_{i<j} e, e^2 with e = exp(-(X_i-X_j)^T H_c^-1 (X_i-X_j)/4)
+ * cand_host: g_c, h_c, or vech(H_c) rows.  Non-PD H_c gives KDE_E_INVALID here. */
+kde_status kde_raw_sums(kde_ctx *ctx, kde_sum_kind kind, const double *X_dev, int64_t n, int32_t d,
+                        const double *cand_host, int32_t n_cand, int32_t shard_rank,
+                        int32_t shard_world, kde_fixed *out);
+double kde_fixed_value(const kde_fixed *v);
+/* Exact limb-wise sum of two fixed-point values with the same scale_exp. */
+kde_fixed kde_fixed_add(kde_fixed a, kde_fixed b);
+
+/* Tile traversal (Eq. 42-43, with an exact integer fix-up): linear tile id bx ->
+ * column l and row q (q <= l) of the upper-triangular tile grid, column l holding l+1 tiles. */
+void kde_tile_coords(int64_t bx, int64_t *l, int64_t *q);
+
+/* Kernel timing of the last call on this context: number of pair-kernel launches, their
+ * summed device time (ms, CUDA events on the context stream) and the algorithmic pair-kernel
+ * evaluations they performed (pairs i<j on this rank x candidates). */
+kde_status kde_last_profile(const kde_ctx *ctx, int32_t *launches, double *pair_ms,
+                            double *evals, int32_t *all_launches);
+/* Turn per-launch event timing on/off (default off; adds an event pair per launch). */
+kde_status kde_set_profiling(kde_ctx *ctx, int32_t on);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KDE_B200_H */

@@ -1,0 +1,1098 @@
+// kde_host.cpp — host side of the C ABI in include/kde.h: context, workspace, NCCL glue,
+// the fp64 scalar chains of the three selectors, small linear algebra and Nelder–Mead.
+// P:NNN = PAPER.md line NNN.  Product code: shares nothing with oracle/.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/kde.h"
+#include "kde_internal.h"
+
+using kde::Kind;
+
+// ------------------------------------------------------------------ NCCL (loaded at run time)
+namespace {
+typedef struct ncclComm* ncclComm_t;
+struct ncclUniqueId { char internal[128]; };
+typedef int ncclResult_t;
+constexpr int kNcclInt64 = 4, kNcclSum = 0;
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+      api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
+      api.AllReduce = (decltype(api.AllReduce))dlsym(h, "ncclAllReduce");
+      api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+      api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+      api.ok = api.GetUniqueId && api.CommInitRank && api.AllReduce && api.CommDestroy;
+    }
+  }
+  return api;
+}
+}  // namespace
+
+// ------------------------------------------------------------------ context
+struct kde_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int rank = 0, world = 1;
+  ncclComm_t comm = nullptr;
+  int sm_count = 148;
+  kde_status sticky = KDE_OK;
+  char err[512] = {0};
+  // workspace
+  void* ext_ws = nullptr;
+  size_t ext_bytes = 0;
+  void* own_ws = nullptr;
+  size_t own_bytes = 0;
+  // pinned host staging for limbs
+  long long* h_limbs = nullptr;
+  size_t h_limbs_cap = 0;
+  // profiling
+  bool profiling = false;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  int32_t prof_launches = 0, prof_all = 0;
+  double prof_ms = 0.0, prof_evals = 0.0;
+};
+
+namespace {
+
+kde_status fail(kde_ctx* c, kde_status s, const char* fmt, ...) {
+  if (c) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(c->err, sizeof(c->err), fmt, ap);
+    va_end(ap);
+    if (s == KDE_E_CUDA || s == KDE_E_NCCL) c->sticky = s;
+  }
+  return s;
+}
+
+#define CUDA_TRY(ctx, expr)                                                                 \
+  do {                                                                                      \
+    cudaError_t e_ = (expr);                                                                \
+    if (e_ != cudaSuccess)                                                                  \
+      return fail(ctx, e_ == cudaErrorMemoryAllocation ? KDE_E_OOM : KDE_E_CUDA,            \
+                  "CUDA error %s at %s:%d", cudaGetErrorString(e_), __FILE__, __LINE__);    \
+  } while (0)
+
+#define TRY(expr)                       \
+  do {                                  \
+    kde_status s_ = (expr);             \
+    if (s_ != KDE_OK) return s_;        \
+  } while (0)
+
+constexpr double kPi = 3.14159265358979323846;
+constexpr double kLog2e = 1.44269504088896340736;
+
+// Workspace layout (all offsets 256-byte aligned).
+struct Ws {
+  float* Y;                 // prepared fp32 data, d x ld
+  unsigned long long* limbs;
+  double* part;             // moments partials
+  double* small;            // mean[16], W[256], sums[136]
+};
+
+size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
+
+size_t ws_bytes(int64_t ld, int32_t d, int32_t n_out) {
+  return align256((size_t)d * ld * sizeof(float)) +
+         align256((size_t)std::max(n_out, 1) * kde::kLimbs * sizeof(long long)) +
+         align256((size_t)1024 * 136 * sizeof(double)) + align256((16 + 256 + 136) * sizeof(double));
+}
+
+kde_status get_ws(kde_ctx* c, int64_t ld, int32_t d, int32_t n_out, Ws* w) {
+  size_t need = ws_bytes(ld, d, n_out);
+  char* base;
+  if (c->ext_ws && c->ext_bytes >= need) {
+    base = (char*)c->ext_ws;
+  } else {
+    if (c->own_bytes < need) {
+      if (c->own_ws) {
+        CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+        cudaFree(c->own_ws);
+        c->own_ws = nullptr;
+        c->own_bytes = 0;
+      }
+      size_t cap = need + need / 4;
+      CUDA_TRY(c, cudaMalloc(&c->own_ws, cap));
+      c->own_bytes = cap;
+    }
+    base = (char*)c->own_ws;
+  }
+  w->Y = (float*)base;
+  base += align256((size_t)d * ld * sizeof(float));
+  w->limbs = (unsigned long long*)base;
+  base += align256((size_t)std::max(n_out, 1) * kde::kLimbs * sizeof(long long));
+  w->part = (double*)base;
+  base += align256((size_t)1024 * 136 * sizeof(double));
+  w->small = (double*)base;
+  return KDE_OK;
+}
+
+kde_status check_ctx(kde_ctx* c) {
+  if (!c) return KDE_E_INVALID;
+  if (c->sticky != KDE_OK) return c->sticky;
+  CUDA_TRY(c, cudaSetDevice(c->device));
+  return KDE_OK;
+}
+
+// ------------------------------------------------------------------ small dense linear algebra
+// Row-major d x d matrices in std::vector<double>.
+
+// Cholesky A = L L^T with a relative pivot test (positive-definiteness, reading Z8).
+bool cholesky(const std::vector<double>& A, int d, std::vector<double>& L) {
+  L.assign((size_t)d * d, 0.0);
+  double mx = 0.0;
+  for (int i = 0; i < d; ++i) {
+    if (!std::isfinite(A[i * d + i])) return false;
+    mx = std::max(mx, std::fabs(A[i * d + i]));
+  }
+  for (int i = 0; i < d; ++i)
+    for (int j = 0; j < d; ++j)
+      if (!std::isfinite(A[i * d + j]) || A[i * d + j] != A[j * d + i]) return false;
+  for (int j = 0; j < d; ++j) {
+    double s = A[j * d + j];
+    for (int k = 0; k < j; ++k) s -= L[j * d + k] * L[j * d + k];
+    if (!(s > 1e-12 * mx)) return false;
+    L[j * d + j] = std::sqrt(s);
+    for (int i = j + 1; i < d; ++i) {
+      double t = A[i * d + j];
+      for (int k = 0; k < j; ++k) t -= L[i * d + k] * L[j * d + k];
+      L[i * d + j] = t / L[j * d + j];
+    }
+  }
+  return true;
+}
+
+// Inverse of a lower-triangular matrix by forward substitution.
+std::vector<double> tri_lower_inverse(const std::vector<double>& L, int d) {
+  std::vector<double> M((size_t)d * d, 0.0);
+  for (int col = 0; col < d; ++col) {
+    for (int i = 0; i < d; ++i) {
+      double s = (i == col) ? 1.0 : 0.0;
+      for (int k = 0; k < i; ++k) s -= L[i * d + k] * M[k * d + col];
+      M[i * d + col] = s / L[i * d + i];
+    }
+  }
+  return M;
+}
+
+// SPD inverse from its Cholesky factor: A^-1 = L^-T L^-1.
+std::vector<double> spd_inverse(const std::vector<double>& L, int d) {
+  std::vector<double> Li = tri_lower_inverse(L, d), R((size_t)d * d, 0.0);
+  for (int i = 0; i < d; ++i)
+    for (int j = 0; j < d; ++j) {
+      double s = 0.0;
+      for (int k = std::max(i, j); k < d; ++k) s += Li[k * d + i] * Li[k * d + j];
+      R[i * d + j] = s;
+    }
+  for (int i = 0; i < d; ++i)
+    for (int j = 0; j < i; ++j) R[i * d + j] = R[j * d + i] = 0.5 * (R[i * d + j] + R[j * d + i]);
+  return R;
+}
+
+// Principal square root of an SPD matrix by the Denman–Beavers iteration (the paper used
+// ALGLIB; reading Z9).  Y_{k+1} = (Y_k + Z_k^-1)/2, Z_{k+1} = (Z_k + Y_k^-1)/2.
+bool gen_inverse(const std::vector<double>& A, int d, std::vector<double>& R) {
+  // Gauss–Jordan with partial pivoting on a general matrix.
+  std::vector<double> M = A;
+  R.assign((size_t)d * d, 0.0);
+  for (int i = 0; i < d; ++i) R[i * d + i] = 1.0;
+  for (int c = 0; c < d; ++c) {
+    int p = c;
+    for (int r = c + 1; r < d; ++r)
+      if (std::fabs(M[r * d + c]) > std::fabs(M[p * d + c])) p = r;
+    if (M[p * d + c] == 0.0) return false;
+    if (p != c)
+      for (int k = 0; k < d; ++k) { std::swap(M[p * d + k], M[c * d + k]); std::swap(R[p * d + k], R[c * d + k]); }
+    double piv = M[c * d + c];
+    for (int k = 0; k < d; ++k) { M[c * d + k] /= piv; R[c * d + k] /= piv; }
+    for (int r = 0; r < d; ++r) {
+      if (r == c) continue;
+      double f = M[r * d + c];
+      if (f == 0.0) continue;
+      for (int k = 0; k < d; ++k) { M[r * d + k] -= f * M[c * d + k]; R[r * d + k] -= f * R[c * d + k]; }
+    }
+  }
+  return true;
+}
+
+bool spd_sqrt(const std::vector<double>& A, int d, std::vector<double>& S) {
+  std::vector<double> Y = A, Z((size_t)d * d, 0.0), Yi, Zi;
+  for (int i = 0; i < d; ++i) Z[i * d + i] = 1.0;
+  for (int it = 0; it < 100; ++it) {
+    if (!gen_inverse(Y, d, Yi) || !gen_inverse(Z, d, Zi)) return false;
+    double diff = 0.0, nrm = 0.0;
+    for (size_t k = 0; k < Y.size(); ++k) {
+      double yn = 0.5 * (Y[k] + Zi[k]);
+      double zn = 0.5 * (Z[k] + Yi[k]);
+      diff = std::max(diff, std::fabs(yn - Y[k]));
+      nrm = std::max(nrm, std::fabs(yn));
+      Y[k] = yn;
+      Z[k] = zn;
+    }
+    if (diff <= 1e-15 * nrm) break;
+  }
+  S = Y;
+  for (int i = 0; i < d; ++i)
+    for (int j = 0; j < i; ++j) S[i * d + j] = S[j * d + i] = 0.5 * (S[i * d + j] + S[j * d + i]);
+  return true;
+}
+
+std::vector<double> unvech(const double* v, int d) {
+  std::vector<double> A((size_t)d * d);
+  int t = 0;
+  for (int j = 0; j < d; ++j)
+    for (int i = j; i < d; ++i) { A[i * d + j] = A[j * d + i] = v[t]; ++t; }
+  return A;
+}
+
+void vech(const std::vector<double>& A, int d, double* v) {
+  int t = 0;
+  for (int j = 0; j < d; ++j)
+    for (int i = j; i < d; ++i) v[t++] = A[i * d + j];
+}
+
+// ------------------------------------------------------------------ fixed point
+int scale_exp_for(double bound_per_term, int64_t n) {
+  double pairs = (double)n * (double)(n - 1) * 0.5;
+  double G = std::max(1.0, bound_per_term * std::max(pairs, 1.0));
+  return 100 - (int)std::ceil(std::log2(G));
+}
+
+kde_fixed limbs_to_fixed(const long long* l, int S) {
+  kde_fixed f;
+  f.hi = l[0]; f.mid = l[1]; f.lo = l[2]; f.scale_exp = S; f.pad_ = 0;
+  return f;
+}
+
+double fixed_value(const kde_fixed& f) {
+  __int128 T = (__int128)f.hi * ((__int128)1 << 80) + (__int128)f.mid * ((__int128)1 << 40) + (__int128)f.lo;
+  return std::ldexp((double)T, -f.scale_exp);
+}
+
+// ------------------------------------------------------------------ GPU building blocks
+struct Moments {
+  std::vector<double> mean, cov;   // cov row-major d x d (unbiased)
+};
+
+// Two-pass fp64 moments on the GPU (Eq. 11, Eq. 20-23 read as the unbiased sample covariance,
+// reading Z10).  Returns KDE_E_INVALID for non-finite data.
+kde_status gpu_moments(kde_ctx* c, const double* X, int64_t n, int d, Ws& w, Moments& m) {
+  const int nblk = kde::moments_blocks(n);
+  double* sums = w.small + 16 + 256;
+  double* mean_dev = w.small;
+  double hs[136];
+  CUDA_TRY(c, kde::launch_moments1(X, n, d, w.part, nblk, c->stream));
+  CUDA_TRY(c, kde::launch_reduce_parts(w.part, nblk, d, sums, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(hs, sums, d * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  m.mean.assign(d, 0.0);
+  for (int a = 0; a < d; ++a) {
+    if (!std::isfinite(hs[a])) return fail(c, KDE_E_INVALID, "non-finite sample values");
+    m.mean[a] = hs[a] / (double)n;
+  }
+  CUDA_TRY(c, cudaMemcpyAsync(mean_dev, m.mean.data(), d * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  const int width = d * (d + 1) / 2;
+  CUDA_TRY(c, kde::launch_moments2(X, n, d, mean_dev, w.part, nblk, c->stream));
+  CUDA_TRY(c, kde::launch_reduce_parts(w.part, nblk, width, sums, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(hs, sums, width * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  m.cov.assign((size_t)d * d, 0.0);
+  int t = 0;
+  for (int a = 0; a < d; ++a)
+    for (int b = a; b < d; ++b) {
+      double v = hs[t++] / (double)(n - 1);
+      if (!std::isfinite(v)) return fail(c, KDE_E_INVALID, "non-finite sample values");
+      m.cov[a * d + b] = m.cov[b * d + a] = v;
+    }
+  return KDE_OK;
+}
+
+// y = fp32(W (x - mean)), padded with zeros to ld.
+kde_status gpu_prep(kde_ctx* c, const double* X, int64_t n, int d, const std::vector<double>& W,
+                    const std::vector<double>& mean, int64_t ld, Ws& w) {
+  double* mean_dev = w.small;
+  double* W_dev = w.small + 16;
+  CUDA_TRY(c, cudaMemcpyAsync(mean_dev, mean.data(), d * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(W_dev, W.data(), (size_t)d * d * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, kde::launch_prep(X, n, d, W_dev, mean_dev, w.Y, ld, c->stream));
+  return KDE_OK;
+}
+
+int64_t n_tiles(int64_t n, int T) {
+  int64_t nb = (n + T - 1) / T;
+  return nb * (nb + 1) / 2;
+}
+
+void shard_range(int64_t tiles, int rank, int world, int64_t* b, int64_t* e) {
+  *b = (int64_t)((__int128)tiles * rank / world);
+  *e = (int64_t)((__int128)tiles * (rank + 1) / world);
+}
+
+// Algorithmic pairs i<j inside tiles [b, e).
+double pairs_in_range(int64_t n, int T, int64_t b, int64_t e) {
+  double s = 0.0;
+  for (int64_t t = b; t < e; ++t) {
+    int64_t l, q;
+    kde::tile_coords_host(t, &l, &q);
+    int64_t cols = std::min<int64_t>(T, n - l * (int64_t)T);
+    if (q == l) s += (double)cols * (double)(cols - 1) * 0.5;
+    else s += (double)T * (double)cols;
+  }
+  return s;
+}
+
+cudaEvent_t next_event(kde_ctx* c) {
+  if (c->ev_used == c->ev_pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    c->ev_pool.push_back(e);
+  }
+  return c->ev_pool[c->ev_used++];
+}
+
+void prof_reset(kde_ctx* c) {
+  c->ev_used = 0;
+  c->prof_launches = 0;
+  c->prof_all = 0;
+  c->prof_ms = 0.0;
+  c->prof_evals = 0.0;
+}
+
+kde_status prof_collect(kde_ctx* c) {
+  if (!c->profiling) return KDE_OK;
+  double ms = 0.0;
+  for (size_t k = 0; k + 1 < c->ev_used; k += 2) {
+    float x = 0.f;
+    CUDA_TRY(c, cudaEventElapsedTime(&x, c->ev_pool[k], c->ev_pool[k + 1]));
+    ms += x;
+  }
+  c->prof_ms = ms;
+  return KDE_OK;
+}
+
+// A "sum job": a sequence of pair-kernel launches over the same prepared data, writing
+// n_out fixed-point outputs.  Launch closures receive (LaunchCfg with limbs offset).
+struct SumLaunch {
+  Kind kind;
+  int r = 0;                  // psi order
+  int nb = 1;                 // candidates in this launch
+  int out_offset = 0;         // first output index
+  int n_out = 0;
+  kde::PsiParams psi;
+  kde::LscvScalarParams ls;
+  std::vector<unsigned char> mat;   // LscvMatrixParams or LscvCholParams bytes
+};
+
+// Launch the given pair kernels over shard tiles, all-reduce (if requested), fetch fixed-point
+// outputs.  Data must already be prepared in w.Y with leading dimension ld.
+kde_status run_sums(kde_ctx* c, int d, int64_t n, int64_t ld, int T, int scale, Ws& w,
+                    const std::vector<SumLaunch>& launches, int n_out, int shard_rank,
+                    int shard_world, bool allreduce, std::vector<kde_fixed>& out) {
+  CUDA_TRY(c, cudaMemsetAsync(w.limbs, 0, (size_t)n_out * kde::kLimbs * sizeof(long long), c->stream));
+  int64_t tiles = n_tiles(n, T), tb, te;
+  shard_range(tiles, shard_rank, shard_world, &tb, &te);
+  const double pairs = c->profiling ? pairs_in_range(n, T, tb, te) : 0.0;
+  for (const SumLaunch& L : launches) {
+    kde::LaunchCfg cfg;
+    cfg.X = w.Y; cfg.n = n; cfg.ld = ld; cfg.tile_begin = tb; cfg.tile_end = te; cfg.tile = T;
+    cfg.scale_exp = scale; cfg.limbs = w.limbs + (size_t)L.out_offset * kde::kLimbs;
+    cfg.n_out = L.n_out; cfg.stream = c->stream; cfg.sm_count = c->sm_count;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (c->profiling) { e0 = next_event(c); e1 = next_event(c); cudaEventRecord(e0, c->stream); }
+    cudaError_t err = cudaSuccess;
+    switch (L.kind) {
+      case Kind::Psi4: case Kind::Psi6: case Kind::Psi8: err = kde::launch_psi(L.r, cfg, L.psi); break;
+      case Kind::LscvScalar: err = kde::launch_lscv_scalar(d, L.nb, cfg, L.ls); break;
+      case Kind::LscvMatrix: err = kde::launch_lscv_matrix(d, L.nb, cfg, L.mat.data(), L.mat.size()); break;
+    }
+    if (err != cudaSuccess) return fail(c, KDE_E_CUDA, "pair kernel launch: %s", cudaGetErrorString(err));
+    if (c->profiling) {
+      cudaEventRecord(e1, c->stream);
+      c->prof_launches++;
+      c->prof_evals += pairs * (double)L.nb;
+    }
+  }
+  if (allreduce && c->world > 1) {
+    NcclApi& api = nccl();
+    ncclResult_t r = api.AllReduce(w.limbs, w.limbs, (size_t)n_out * kde::kLimbs, kNcclInt64, kNcclSum,
+                                   c->comm, c->stream);
+    if (r != 0) return fail(c, KDE_E_NCCL, "ncclAllReduce: %s", api.GetErrorString ? api.GetErrorString(r) : "?");
+  }
+  size_t need = (size_t)n_out * kde::kLimbs;
+  if (c->h_limbs_cap < need) {
+    if (c->h_limbs) cudaFreeHost(c->h_limbs);
+    c->h_limbs = nullptr;
+    CUDA_TRY(c, cudaMallocHost(&c->h_limbs, need * sizeof(long long)));
+    c->h_limbs_cap = need;
+  }
+  CUDA_TRY(c, cudaMemcpyAsync(c->h_limbs, w.limbs, need * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  out.resize(n_out);
+  for (int k = 0; k < n_out; ++k) out[k] = limbs_to_fixed(c->h_limbs + (size_t)k * kde::kLimbs, scale);
+  return KDE_OK;
+}
+
+// ------------------------------------------------------------------ Psi_r
+// The kernel evaluates He_r(s = u^2) with exact integer coefficients; the only parameter is
+// the exponent scale: exp(-u^2/2) = 2^(s * c0), c0 = -log2(e)/2.
+void psi_coeffs(int r, kde::PsiParams& p) {
+  (void)r;
+  std::memset(&p, 0, sizeof(p));
+  p.c[0] = (float)(-kLog2e / 2.0);
+}
+
+double he_at_zero(int r) { return r == 4 ? 3.0 : (r == 6 ? -15.0 : 105.0); }
+
+Kind psi_kind(int r) { return r == 4 ? Kind::Psi4 : (r == 6 ? Kind::Psi6 : Kind::Psi8); }
+
+// Raw Psi sums S_r(g) = sum_{i<j} He_r(u) e^{-u^2/2} for each g (one prep + one launch per g).
+kde_status psi_raw(kde_ctx* c, const double* x, int64_t n, int r, const double* g, int ng,
+                   const Moments& m, int shard_rank, int shard_world, bool allreduce,
+                   std::vector<kde_fixed>& out) {
+  const int T = kde::tile_for(psi_kind(r), 1, n);
+  const int64_t ld = (n + T - 1) / T * T;
+  Ws w;
+  TRY(get_ws(c, ld, 1, 1, &w));
+  const int S = scale_exp_for(2.0 * std::fabs(he_at_zero(r)), n);
+  out.clear();
+  for (int k = 0; k < ng; ++k) {
+    std::vector<double> W = {1.0 / g[k]};
+    TRY(gpu_prep(c, x, n, 1, W, m.mean, ld, w));
+    SumLaunch L;
+    L.kind = psi_kind(r); L.r = r; L.nb = 1; L.out_offset = 0; L.n_out = 1;
+    psi_coeffs(r, L.psi);
+    std::vector<kde_fixed> o;
+    TRY(run_sums(c, 1, n, ld, T, S, w, {L}, 1, shard_rank, shard_world, allreduce, o));
+    out.push_back(o[0]);
+  }
+  return KDE_OK;
+}
+
+double psi_finalize(int r, int64_t n, double g, double S) {
+  const double s2p = std::sqrt(2.0 * kPi);
+  const double nn = (double)n;
+  return (2.0 * S / s2p + nn * he_at_zero(r) / s2p) / (nn * nn * std::pow(g, r + 1));
+}
+
+// ------------------------------------------------------------------ LSCV_h
+struct LscvhPrep {
+  std::vector<double> Lc;   // Cholesky of Sigma
+  double det = 0.0;
+};
+
+kde_status lscv_h_prepare(kde_ctx* c, const Moments& m, int d, LscvhPrep& p) {
+  if (!cholesky(m.cov, d, p.Lc)) return fail(c, KDE_E_SINGULAR_COV, "covariance matrix is not positive definite");
+  p.det = 1.0;
+  for (int i = 0; i < d; ++i) p.det *= p.Lc[i * d + i] * p.Lc[i * d + i];
+  if (!(p.det > 0.0) || !std::isfinite(p.det)) return fail(c, KDE_E_SINGULAR_COV, "det(Sigma) <= 0");
+  return KDE_OK;
+}
+
+kde_status lscv_h_raw(kde_ctx* c, const double* X, int64_t n, int d, const double* h, int nh,
+                      const Moments& m, const LscvhPrep& pp, int shard_rank, int shard_world,
+                      bool allreduce, std::vector<kde_fixed>& out) {
+  const int T = kde::tile_for(Kind::LscvScalar, d, n);
+  const int nb = kde::cand_per_launch(Kind::LscvScalar, d);
+  const int64_t ld = (n + T - 1) / T * T;
+  const int nbatch = (nh + nb - 1) / nb;
+  const int n_out = 2 * nbatch * nb;
+  Ws w;
+  TRY(get_ws(c, ld, d, n_out, &w));
+  // W = sqrt(log2 e / 4) L^-1  =>  |W v|^2 = (log2 e / 4) v^T Sigma^-1 v
+  std::vector<double> W = tri_lower_inverse(pp.Lc, d);
+  for (double& v : W) v *= std::sqrt(kLog2e / 4.0);
+  TRY(gpu_prep(c, X, n, d, W, m.mean, ld, w));
+  std::vector<SumLaunch> Ls;
+  for (int b = 0; b < nbatch; ++b) {
+    SumLaunch L;
+    L.kind = Kind::LscvScalar; L.nb = nb; L.out_offset = 2 * b * nb; L.n_out = 2 * nb;
+    for (int j = 0; j < kde::kMaxCand; ++j) {
+      int idx = std::min(b * nb + j, nh - 1);   // pad with a valid candidate
+      L.ls.kappa[j] = (float)(-1.0 / (h[idx] * h[idx]));
+    }
+    Ls.push_back(L);
+  }
+  std::vector<kde_fixed> o;
+  TRY(run_sums(c, d, n, ld, T, scale_exp_for(1.0, n), w, Ls, n_out, shard_rank, shard_world, allreduce, o));
+  out.assign(o.begin(), o.begin() + 2 * nh);
+  return KDE_OK;
+}
+
+double lscv_h_finalize(int64_t n, int d, double det, double h, double S1, double S2) {
+  const double nn = (double)n;
+  const double c4 = std::pow(4.0 * kPi, -0.5 * d) / std::sqrt(det);
+  const double c2 = std::pow(2.0 * kPi, -0.5 * d) / std::sqrt(det);
+  return std::pow(h, -d) * (2.0 * (c4 * S1 - 2.0 * c2 * S2) / (nn * nn) + c4 / nn);
+}
+
+// ------------------------------------------------------------------ LSCV_H
+struct HCand {
+  bool pd = false;
+  double det = 0.0;
+  std::vector<double> coef;   // D<=4: monomial coefficients; D>4: scaled upper factor rows
+};
+
+HCand h_candidate(const double* vh, int d) {
+  HCand hc;
+  std::vector<double> H = unvech(vh, d), L;
+  if (!cholesky(H, d, L)) return hc;
+  hc.pd = true;
+  hc.det = 1.0;
+  for (int i = 0; i < d; ++i) hc.det *= L[i * d + i] * L[i * d + i];
+  std::vector<double> Hi = spd_inverse(L, d);
+  const double sc = kLog2e / 4.0;
+  if (d <= 4) {
+    for (int a = 0; a < d; ++a)
+      for (int b = a; b < d; ++b) hc.coef.push_back(-sc * (a == b ? 1.0 : 2.0) * Hi[a * d + b]);
+  } else {
+    std::vector<double> M(Hi), Lm;
+    if (!cholesky(M, d, Lm)) { hc.pd = false; return hc; }
+    // U = sqrt(sc) Lm^T (upper), rows a: entries b = a..d-1
+    for (int a = 0; a < d; ++a)
+      for (int b = a; b < d; ++b) hc.coef.push_back(std::sqrt(sc) * Lm[b * d + a]);
+  }
+  return hc;
+}
+
+// Raw LSCV_H sums for PD candidates `cands` (all must be PD).
+kde_status lscv_H_raw(kde_ctx* c, const double* X, int64_t n, int d, const std::vector<HCand>& cands,
+                      const Moments& m, int shard_rank, int shard_world, bool allreduce,
+                      std::vector<kde_fixed>& out) {
+  const int T = kde::tile_for(Kind::LscvMatrix, d, n);
+  const int nbmax = kde::cand_per_launch(Kind::LscvMatrix, d);
+  const int64_t ld = (n + T - 1) / T * T;
+  const int nc = (int)cands.size();
+  const int P = d * (d + 1) / 2;
+  std::vector<SumLaunch> Ls;
+  int off = 0;
+  for (int b0 = 0; b0 < nc; b0 += nbmax) {
+    const int cnt = std::min(nbmax, nc - b0);
+    int nb = cnt;
+    if (d <= 4) nb = cnt <= 4 ? 4 : (cnt <= 8 ? 8 : 16);
+    nb = std::min(nb, nbmax);
+    if (d > 4) nb = nbmax;
+    SumLaunch L;
+    L.kind = Kind::LscvMatrix; L.nb = nb; L.out_offset = off; L.n_out = 2 * nb;
+    size_t bytes = d <= 4 ? sizeof(kde::LscvMatrixParams) : sizeof(kde::LscvCholParams);
+    L.mat.assign(bytes, 0);
+    float* f = reinterpret_cast<float*>(L.mat.data());
+    for (int j = 0; j < nb; ++j) {
+      const HCand& hc = cands[b0 + std::min(j, cnt - 1)];
+      for (int u = 0; u < P; ++u) f[j * P + u] = (float)hc.coef[u];
+    }
+    Ls.push_back(std::move(L));
+    off += 2 * nb;
+  }
+  Ws w;
+  TRY(get_ws(c, ld, d, std::max(off, 2), &w));
+  std::vector<double> W((size_t)d * d, 0.0);
+  for (int a = 0; a < d; ++a) W[a * d + a] = 1.0;
+  TRY(gpu_prep(c, X, n, d, W, m.mean, ld, w));
+  std::vector<kde_fixed> o;
+  TRY(run_sums(c, d, n, ld, T, scale_exp_for(1.0, n), w, Ls, std::max(off, 2), shard_rank, shard_world, allreduce, o));
+  out.clear();
+  int k = 0;
+  for (const SumLaunch& L : Ls) {
+    const int cnt = std::min(L.nb, nc - k);
+    for (int j = 0; j < cnt; ++j) {
+      out.push_back(o[L.out_offset + 2 * j]);
+      out.push_back(o[L.out_offset + 2 * j + 1]);
+    }
+    k += cnt;
+  }
+  return KDE_OK;
+}
+
+double lscv_H_finalize(int64_t n, int d, double det, double S1, double S2) {
+  const double nn = (double)n;
+  const double c4 = std::pow(4.0 * kPi, -0.5 * d) / std::sqrt(det);
+  const double c2 = std::pow(2.0 * kPi, -0.5 * d) / std::sqrt(det);
+  return 2.0 * (c4 * S1 - 2.0 * c2 * S2) / (nn * nn) + c4 / nn;
+}
+
+// Evaluate g(H) for a list of vech vectors (non-PD -> penalty); one GPU batch for all PD ones.
+kde_status lscv_H_eval(kde_ctx* c, const double* X, int64_t n, int d, const Moments& m,
+                       const std::vector<std::vector<double>>& vs, double penalty,
+                       std::vector<double>& g, int* evals) {
+  std::vector<HCand> pdc;
+  std::vector<int> idx;
+  g.assign(vs.size(), penalty);
+  for (size_t k = 0; k < vs.size(); ++k) {
+    HCand hc = h_candidate(vs[k].data(), d);
+    if (hc.pd) { pdc.push_back(std::move(hc)); idx.push_back((int)k); }
+  }
+  if (pdc.empty()) return KDE_OK;
+  std::vector<kde_fixed> o;
+  TRY(lscv_H_raw(c, X, n, d, pdc, m, c->rank, c->world, true, o));
+  for (size_t j = 0; j < pdc.size(); ++j)
+    g[idx[j]] = lscv_H_finalize(n, d, pdc[j].det, fixed_value(o[2 * j]), fixed_value(o[2 * j + 1]));
+  if (evals) *evals += (int)pdc.size();
+  return KDE_OK;
+}
+
+kde_status validate_X(kde_ctx* c, const void* X, int64_t n, int32_t d, int64_t nmin) {
+  if (!X) return fail(c, KDE_E_INVALID, "null sample pointer");
+  if (d < 1 || d > kde::kMaxDim) return fail(c, KDE_E_DIM_MISMATCH, "d=%d outside [1,16]", d);
+  if (n < nmin) return fail(c, n < 1 ? KDE_E_INVALID : KDE_E_INSUFFICIENT_SAMPLES, "n=%lld too small", (long long)n);
+  if (n > 2147483647LL) return fail(c, KDE_E_INVALID, "n > 2^31-1");
+  return KDE_OK;
+}
+
+// ------------------------------------------------------------------ Nelder–Mead (reading Z8)
+struct NMResult {
+  std::vector<double> x;
+  double f = 0.0;
+  int iterations = 0, stop = 2, evals = 0;
+};
+
+kde_status nelder_mead(kde_ctx* c, const double* X, int64_t n, int d, const Moments& m,
+                       std::vector<std::vector<double>> sim, int max_iter, double tol,
+                       double penalty, bool speculative, NMResult& res) {
+  const int M = (int)sim.size() - 1;
+  std::vector<double> fs;
+  TRY(lscv_H_eval(c, X, n, d, m, sim, penalty, fs, &res.evals));
+  int it = 0;
+  int stop = 2;
+  auto comb = [](const std::vector<double>& a, double s, const std::vector<double>& b,
+                 const std::vector<double>& cc) {   // a + s (b - cc)
+    std::vector<double> r(a.size());
+    for (size_t k = 0; k < a.size(); ++k) r[k] = a[k] + s * (b[k] - cc[k]);
+    return r;
+  };
+  while (true) {
+    std::vector<int> ord(M + 1);
+    std::iota(ord.begin(), ord.end(), 0);
+    std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return fs[a] < fs[b]; });
+    std::vector<std::vector<double>> s2;
+    std::vector<double> f2;
+    for (int k : ord) { s2.push_back(sim[k]); f2.push_back(fs[k]); }
+    sim.swap(s2);
+    fs.swap(f2);
+    if (fs[M] - fs[0] <= tol * std::fabs(fs[0])) { stop = 1; break; }
+    if (it >= max_iter) { stop = 2; break; }
+    ++it;
+    std::vector<double> xbar(sim[0].size(), 0.0);
+    for (int k = 0; k < M; ++k)
+      for (size_t u = 0; u < xbar.size(); ++u) xbar[u] += sim[k][u];
+    for (double& v : xbar) v /= (double)M;
+    std::vector<double> xr = comb(xbar, 1.0, xbar, sim[M]);
+    std::vector<double> xe = comb(xbar, 2.0, xr, xbar);
+    std::vector<double> xc = comb(xbar, 0.5, xr, xbar);
+    std::vector<double> xcc = comb(xbar, 0.5, sim[M], xbar);
+    double fr, fe = 0, fc = 0, fcc = 0;
+    bool have_all = false;
+    if (speculative) {
+      std::vector<double> g;
+      TRY(lscv_H_eval(c, X, n, d, m, {xr, xe, xc, xcc}, penalty, g, &res.evals));
+      fr = g[0]; fe = g[1]; fc = g[2]; fcc = g[3];
+      have_all = true;
+    } else {
+      std::vector<double> g;
+      TRY(lscv_H_eval(c, X, n, d, m, {xr}, penalty, g, &res.evals));
+      fr = g[0];
+    }
+    auto eval1 = [&](const std::vector<double>& x, double& f) -> kde_status {
+      if (have_all) return KDE_OK;
+      std::vector<double> g;
+      TRY(lscv_H_eval(c, X, n, d, m, {x}, penalty, g, &res.evals));
+      f = g[0];
+      return KDE_OK;
+    };
+    if (fr < fs[0]) {
+      TRY(eval1(xe, fe));
+      if (fe < fr) { sim[M] = xe; fs[M] = fe; } else { sim[M] = xr; fs[M] = fr; }
+      continue;
+    }
+    if (fr < fs[M - 1]) { sim[M] = xr; fs[M] = fr; continue; }
+    if (fr < fs[M]) {
+      TRY(eval1(xc, fc));
+      if (fc <= fr) { sim[M] = xc; fs[M] = fc; continue; }
+    } else {
+      TRY(eval1(xcc, fcc));
+      if (fcc < fs[M]) { sim[M] = xcc; fs[M] = fcc; continue; }
+    }
+    std::vector<std::vector<double>> sh;
+    for (int k = 1; k <= M; ++k) sh.push_back(comb(sim[0], 0.5, sim[k], sim[0]));
+    std::vector<double> g;
+    TRY(lscv_H_eval(c, X, n, d, m, sh, penalty, g, &res.evals));
+    for (int k = 1; k <= M; ++k) { sim[k] = sh[k - 1]; fs[k] = g[k - 1]; }
+  }
+  res.x = sim[0];
+  res.f = fs[0];
+  res.iterations = it;
+  res.stop = stop;
+  return KDE_OK;
+}
+
+}  // namespace
+
+// ================================================================== C ABI
+extern "C" {
+
+void kde_default_opts(kde_select_opts* o) {
+  if (!o) return;
+  o->n_grid = 150;
+  o->range_factor = 4.0;    // Eq. 27
+  o->max_iter = 500;
+  o->tol_rel = 1e-7;
+  o->penalty = 1e300;
+  o->speculative = 1;
+}
+
+kde_status kde_nccl_unique_id(void* out128) {
+  if (!out128) return KDE_E_INVALID;
+  NcclApi& api = nccl();
+  if (!api.ok) return KDE_E_NCCL;
+  ncclUniqueId id;
+  if (api.GetUniqueId(&id) != 0) return KDE_E_NCCL;
+  std::memcpy(out128, &id, sizeof(id));
+  return KDE_OK;
+}
+
+kde_status kde_create(kde_ctx** out, int device, void* stream, const void* nccl_id, int rank, int world) {
+  if (!out || world < 1 || rank < 0 || rank >= world) return KDE_E_INVALID;
+  *out = nullptr;
+  kde_ctx* c = new (std::nothrow) kde_ctx();
+  if (!c) return KDE_E_OOM;
+  c->device = device;
+  c->stream = (cudaStream_t)stream;
+  c->rank = rank;
+  c->world = world;
+  if (cudaSetDevice(device) != cudaSuccess ||
+      cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) {
+    delete c;
+    return KDE_E_CUDA;
+  }
+  if (world > 1) {
+    NcclApi& api = nccl();
+    if (!nccl_id || !api.ok) { delete c; return KDE_E_NCCL; }
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof(id));
+    if (api.CommInitRank(&c->comm, world, id, rank) != 0) { delete c; return KDE_E_NCCL; }
+  }
+  *out = c;
+  return KDE_OK;
+}
+
+void kde_destroy(kde_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream); else cudaDeviceSynchronize();
+  if (c->comm) nccl().CommDestroy(c->comm);
+  if (c->own_ws) cudaFree(c->own_ws);
+  if (c->h_limbs) cudaFreeHost(c->h_limbs);
+  for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+  delete c;
+}
+
+const char* kde_last_error(const kde_ctx* c) { return c ? c->err : "null context"; }
+
+size_t kde_workspace_bytes(int64_t n, int32_t d, int32_t n_cand) {
+  if (n < 1 || d < 1 || d > kde::kMaxDim) return 0;
+  int64_t ld = (n + 2047) / 2048 * 2048;
+  return ws_bytes(ld, d, 2 * (std::max(n_cand, 1) + 2 * kde::kMaxCand));
+}
+
+kde_status kde_set_workspace(kde_ctx* c, void* p, size_t bytes) {
+  if (!c) return KDE_E_INVALID;
+  c->ext_ws = p;
+  c->ext_bytes = p ? bytes : 0;
+  return KDE_OK;
+}
+
+kde_status kde_set_profiling(kde_ctx* c, int32_t on) {
+  if (!c) return KDE_E_INVALID;
+  c->profiling = on != 0;
+  return KDE_OK;
+}
+
+kde_status kde_last_profile(const kde_ctx* c, int32_t* launches, double* ms, double* evals, int32_t* all) {
+  if (!c) return KDE_E_INVALID;
+  if (launches) *launches = c->prof_launches;
+  if (ms) *ms = c->prof_ms;
+  if (evals) *evals = c->prof_evals;
+  if (all) *all = c->prof_all;
+  return KDE_OK;
+}
+
+void kde_tile_coords(int64_t bx, int64_t* l, int64_t* q) {
+  int64_t a = 0, b = 0;
+  if (bx >= 0) kde::tile_coords_host(bx, &a, &b);
+  if (l) *l = a;
+  if (q) *q = b;
+}
+
+double kde_fixed_value(const kde_fixed* v) { return v ? fixed_value(*v) : NAN; }
+
+kde_fixed kde_fixed_add(kde_fixed a, kde_fixed b) {
+  kde_fixed r = a;
+  r.hi = (int64_t)((uint64_t)a.hi + (uint64_t)b.hi);
+  r.mid = (int64_t)((uint64_t)a.mid + (uint64_t)b.mid);
+  r.lo = (int64_t)((uint64_t)a.lo + (uint64_t)b.lo);
+  return r;
+}
+
+kde_status kde_psi_r(kde_ctx* c, const double* x, int64_t n, int32_t r, const double* g, int32_t ng, double* psi) {
+  TRY(check_ctx(c));
+  prof_reset(c);
+  TRY(validate_X(c, x, n, 1, 1));
+  if (!(r == 4 || r == 6 || r == 8)) return fail(c, KDE_E_INVALID, "r=%d not in {4,6,8}", r);
+  if (!g || !psi || ng < 1) return fail(c, KDE_E_INVALID, "null candidate/output array");
+  for (int k = 0; k < ng; ++k)
+    if (!(g[k] > 0.0) || !std::isfinite(g[k])) return fail(c, KDE_E_NONPOSITIVE_BW, "g[%d] <= 0", k);
+  Ws w;
+  TRY(get_ws(c, (n + 2047) / 2048 * 2048, 1, 2, &w));
+  Moments m;
+  if (n >= 2) {
+    TRY(gpu_moments(c, x, n, 1, w, m));
+  } else {
+    m.mean = {0.0};
+  }
+  std::vector<kde_fixed> o;
+  TRY(psi_raw(c, x, n, r, g, ng, m, c->rank, c->world, true, o));
+  TRY(prof_collect(c));
+  for (int k = 0; k < ng; ++k) psi[k] = psi_finalize(r, n, g[k], fixed_value(o[k]));
+  return KDE_OK;
+}
+
+static kde_status plugin_impl(kde_ctx* c, const double* x, int64_t n, kde_plugin_trace* tr) {
+  Ws w;
+  TRY(get_ws(c, (n + 2047) / 2048 * 2048, 1, 2, &w));
+  Moments m;
+  TRY(gpu_moments(c, x, n, 1, w, m));
+  kde_plugin_trace t;
+  const double nn = (double)n, s2p = std::sqrt(2.0 * kPi);
+  t.V_hat = m.cov[0];                                                     // step 1, Eq. 11
+  if (!(t.V_hat > 0.0)) return fail(c, KDE_E_DEGENERATE, "variance estimate <= 0");
+  t.sigma_hat = std::sqrt(t.V_hat);                                      // step 2, Eq. 12
+  t.psi8_ns = 105.0 / (32.0 * std::sqrt(kPi) * std::pow(t.sigma_hat, 9));  // step 3, Eq. 13
+  const double K6_0 = -15.0 / s2p, K4_0 = 3.0 / s2p, mu2 = 1.0;
+  t.g1 = std::pow(-2.0 * K6_0 / (mu2 * t.psi8_ns * nn), 1.0 / 9.0);      // step 4, Eq. 14
+  std::vector<kde_fixed> o;
+  TRY(psi_raw(c, x, n, 6, &t.g1, 1, m, c->rank, c->world, true, o));     // step 5, Eq. 15
+  t.psi6 = psi_finalize(6, n, t.g1, fixed_value(o[0]));
+  if (!(t.psi6 < 0.0)) return fail(c, KDE_E_NUMERIC, "Psi6-hat >= 0");
+  t.g2 = std::pow(-2.0 * K4_0 / (mu2 * t.psi6 * nn), 1.0 / 7.0);         // step 6, Eq. 16
+  TRY(psi_raw(c, x, n, 4, &t.g2, 1, m, c->rank, c->world, true, o));     // step 7, Eq. 17
+  t.psi4 = psi_finalize(4, n, t.g2, fixed_value(o[0]));
+  if (!(t.psi4 > 0.0)) return fail(c, KDE_E_NUMERIC, "Psi4-hat <= 0");
+  const double RK = 1.0 / (2.0 * std::sqrt(kPi));
+  t.h = std::pow(RK / (mu2 * mu2 * t.psi4 * nn), 0.2);                   // step 8, Eq. 18
+  *tr = t;
+  return KDE_OK;
+}
+
+kde_status kde_plugin_h(kde_ctx* c, const double* x, int64_t n, double* h, kde_plugin_trace* tr) {
+  TRY(check_ctx(c));
+  prof_reset(c);
+  TRY(validate_X(c, x, n, 1, 2));
+  if (!h) return fail(c, KDE_E_INVALID, "null output");
+  kde_plugin_trace t;
+  TRY(plugin_impl(c, x, n, &t));
+  TRY(prof_collect(c));
+  *h = t.h;
+  if (tr) *tr = t;
+  return KDE_OK;
+}
+
+static kde_status lscv_h_scores_impl(kde_ctx* c, const double* X, int64_t n, int d, const double* h,
+                                     int nh, double* g) {
+  Ws w;
+  TRY(get_ws(c, (n + 2047) / 2048 * 2048, d, 2, &w));
+  Moments m;
+  TRY(gpu_moments(c, X, n, d, w, m));
+  LscvhPrep pp;
+  TRY(lscv_h_prepare(c, m, d, pp));
+  std::vector<kde_fixed> o;
+  TRY(lscv_h_raw(c, X, n, d, h, nh, m, pp, c->rank, c->world, true, o));
+  for (int k = 0; k < nh; ++k)
+    g[k] = lscv_h_finalize(n, d, pp.det, h[k], fixed_value(o[2 * k]), fixed_value(o[2 * k + 1]));
+  return KDE_OK;
+}
+
+kde_status kde_lscv_h_scores(kde_ctx* c, const double* X, int64_t n, int32_t d, const double* h,
+                             int32_t nh, double* g) {
+  TRY(check_ctx(c));
+  prof_reset(c);
+  TRY(validate_X(c, X, n, d, 2));
+  if (!h || !g || nh < 1) return fail(c, KDE_E_INVALID, "null candidate/output array");
+  for (int k = 0; k < nh; ++k)
+    if (!(h[k] > 0.0) || !std::isfinite(h[k])) return fail(c, KDE_E_NONPOSITIVE_BW, "h[%d] <= 0", k);
+  std::vector<double> tmp(nh);
+  TRY(lscv_h_scores_impl(c, X, n, d, h, nh, tmp.data()));
+  TRY(prof_collect(c));
+  std::copy(tmp.begin(), tmp.end(), g);
+  return KDE_OK;
+}
+
+kde_status kde_lscv_H_scores(kde_ctx* c, const double* X, int64_t n, int32_t d, const double* vh,
+                             int32_t nH, double penalty, double* g) {
+  TRY(check_ctx(c));
+  prof_reset(c);
+  TRY(validate_X(c, X, n, d, 2));
+  if (!vh || !g || nH < 1) return fail(c, KDE_E_INVALID, "null candidate/output array");
+  if (std::isnan(penalty)) penalty = 1e300;
+  const int P = d * (d + 1) / 2;
+  Ws w;
+  TRY(get_ws(c, (n + 2047) / 2048 * 2048, d, 2, &w));
+  Moments m;
+  TRY(gpu_moments(c, X, n, d, w, m));
+  std::vector<std::vector<double>> vs;
+  for (int k = 0; k < nH; ++k) vs.emplace_back(vh + (size_t)k * P, vh + (size_t)(k + 1) * P);
+  std::vector<double> out;
+  TRY(lscv_H_eval(c, X, n, d, m, vs, penalty, out, nullptr));
+  TRY(prof_collect(c));
+  std::copy(out.begin(), out.end(), g);
+  return KDE_OK;
+}
+
+kde_status kde_raw_sums(kde_ctx* c, kde_sum_kind kind, const double* X, int64_t n, int32_t d,
+                        const double* cand, int32_t nc, int32_t srank, int32_t sworld, kde_fixed* out) {
+  TRY(check_ctx(c));
+  prof_reset(c);
+  TRY(validate_X(c, X, n, d, 1));
+  if (!cand || !out || nc < 1) return fail(c, KDE_E_INVALID, "null candidate/output array");
+  bool allreduce = sworld == 0;
+  if (sworld == 0) { srank = c->rank; sworld = c->world; }
+  if (srank < 0 || srank >= sworld) return fail(c, KDE_E_INVALID, "bad shard");
+  Ws w;
+  TRY(get_ws(c, (n + 2047) / 2048 * 2048, d, 2, &w));
+  Moments m;
+  if (n >= 2) {
+    TRY(gpu_moments(c, X, n, d, w, m));
+  } else {
+    m.mean.assign(d, 0.0);
+    m.cov.assign((size_t)d * d, 0.0);
+  }
+  std::vector<kde_fixed> o;
+  if (kind == KDE_SUM_PSI4 || kind == KDE_SUM_PSI6 || kind == KDE_SUM_PSI8) {
+    if (d != 1) return fail(c, KDE_E_NOT_UNIVARIATE, "Psi sums need d = 1");
+    for (int k = 0; k < nc; ++k)
+      if (!(cand[k] > 0.0)) return fail(c, KDE_E_NONPOSITIVE_BW, "g <= 0");
+    TRY(psi_raw(c, X, n, (int)kind, cand, nc, m, srank, sworld, allreduce, o));
+  } else if (kind == KDE_SUM_LSCV_h) {
+    if (n < 2) return fail(c, KDE_E_INSUFFICIENT_SAMPLES, "n < 2");
+    for (int k = 0; k < nc; ++k)
+      if (!(cand[k] > 0.0)) return fail(c, KDE_E_NONPOSITIVE_BW, "h <= 0");
+    LscvhPrep pp;
+    TRY(lscv_h_prepare(c, m, d, pp));
+    TRY(lscv_h_raw(c, X, n, d, cand, nc, m, pp, srank, sworld, allreduce, o));
+  } else if (kind == KDE_SUM_LSCV_H) {
+    const int P = d * (d + 1) / 2;
+    std::vector<HCand> hc;
+    for (int k = 0; k < nc; ++k) {
+      hc.push_back(h_candidate(cand + (size_t)k * P, d));
+      if (!hc.back().pd) return fail(c, KDE_E_INVALID, "candidate %d is not positive definite", k);
+    }
+    if (n < 2) m.mean.assign(d, 0.0);
+    TRY(lscv_H_raw(c, X, n, d, hc, m, srank, sworld, allreduce, o));
+  } else {
+    return fail(c, KDE_E_INVALID, "unknown sum kind");
+  }
+  TRY(prof_collect(c));
+  std::copy(o.begin(), o.end(), out);
+  return KDE_OK;
+}
+
+kde_status kde_select_bandwidth(kde_ctx* c, kde_method method, const double* X, int64_t n, int32_t d,
+                                const kde_select_opts* opts_in, kde_bandwidth* out) {
+  TRY(check_ctx(c));
+  prof_reset(c);
+  if (!out) return fail(c, KDE_E_INVALID, "null output");
+  kde_select_opts o;
+  kde_default_opts(&o);
+  if (opts_in) o = *opts_in;
+  TRY(validate_X(c, X, n, d, 2));
+  kde_bandwidth r;
+  std::memset(&r, 0, sizeof(r));
+  r.method = method;
+  r.d = d;
+  if (method == KDE_PLUGIN) {
+    if (d != 1) return fail(c, KDE_E_NOT_UNIVARIATE, "PLUGIN is univariate (P:196)");
+    TRY(plugin_impl(c, X, n, &r.trace));
+    r.h = r.trace.h;
+    r.evaluations = 2;
+  } else if (method == KDE_LSCV_h) {
+    if (o.n_grid < 2 || !(o.range_factor > 1.0)) return fail(c, KDE_E_INVALID, "bad grid options");
+    // Eq. 25 as written (reading Z3): R(K)/mu2^2 = 1/(2^d pi^{d/2} d^2), R(f'') = d(d+2)/(2^{d+2} pi^{d/2})
+    const double dd = d;
+    const double ratio = 1.0 / (std::pow(2.0, dd) * std::pow(kPi, dd / 2) * dd * dd);
+    const double Rf2 = dd * (dd + 2) / (std::pow(2.0, dd + 2) * std::pow(kPi, dd / 2));
+    const double h0 = std::pow(ratio / (Rf2 * (double)n), 1.0 / (dd + 4));
+    const double lo = h0 / o.range_factor, hi = h0 * o.range_factor;       // Eq. 27
+    std::vector<double> hs(o.n_grid), gs(o.n_grid);
+    for (int k = 0; k < o.n_grid; ++k) hs[k] = lo + k * (hi - lo) / (o.n_grid - 1);
+    TRY(lscv_h_scores_impl(c, X, n, d, hs.data(), o.n_grid, gs.data()));
+    int best = 0;
+    for (int k = 1; k < o.n_grid; ++k)
+      if (gs[k] < gs[best]) best = k;                                    // ties -> smaller h
+    r.h = hs[best];
+    r.objective = gs[best];
+    r.iterations = best;
+    r.evaluations = o.n_grid;
+  } else if (method == KDE_LSCV_H) {
+    Ws w;
+    TRY(get_ws(c, (n + 2047) / 2048 * 2048, d, 2, &w));
+    Moments m;
+    TRY(gpu_moments(c, X, n, d, w, m));
+    std::vector<double> Lc, root;
+    if (!cholesky(m.cov, d, Lc)) return fail(c, KDE_E_SINGULAR_COV, "covariance not positive definite");
+    if (!spd_sqrt(m.cov, d, root)) return fail(c, KDE_E_SINGULAR_COV, "matrix square root failed");
+    // Eq. 35 as written: H_start = (4/(d+2))^{1/(d+4)} n^{-1/(d+4)} Sigma^{1/2}
+    const double f = std::pow(4.0 / (d + 2), 1.0 / (d + 4)) * std::pow((double)n, -1.0 / (d + 4));
+    for (double& v : root) v *= f;
+    const int P = d * (d + 1) / 2;
+    std::vector<double> x0(P);
+    vech(root, d, x0.data());
+    std::vector<std::vector<double>> sim = {x0};
+    int t = 0;
+    for (int b = 0; b < d; ++b)
+      for (int a = b; a < d; ++a) {
+        const double delta = 0.1 * (a == b ? root[a * d + a] : std::sqrt(root[a * d + a] * root[b * d + b]));
+        std::vector<double> v = x0;
+        v[t] += delta;
+        sim.push_back(v);
+        ++t;
+      }
+    NMResult nm;
+    TRY(nelder_mead(c, X, n, d, m, sim, o.max_iter, o.tol_rel, o.penalty, o.speculative != 0, nm));
+    if (!(nm.f < o.penalty)) return fail(c, KDE_E_NO_FEASIBLE, "no positive-definite H found");
+    for (int k = 0; k < P; ++k) r.vechH[k] = nm.x[k];
+    r.objective = nm.f;
+    r.iterations = nm.iterations;
+    r.evaluations = nm.evals;
+    r.stop_reason = nm.stop;
+  } else {
+    return fail(c, KDE_E_INVALID, "unknown method");
+  }
+  TRY(prof_collect(c));
+  *out = r;
+  return KDE_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,69 @@
+// kde_internal.h — declarations shared by the host library (kde_host.cpp) and the CUDA
+// launchers (kde_kernels.cu).  Product code only; nothing here is shared with oracle/.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace kde {
+
+constexpr int kThreads = 256;          // threads per CTA of every pair kernel
+constexpr int kMaxCand = 32;           // candidates per pair-kernel launch (upper bound)
+constexpr int kMaxDim = 16;
+
+// Fixed-point limbs of one output value: value*2^S = hi*2^80 + mid*2^40 + lo.
+constexpr int kLimbs = 3;
+
+// Which functor a launch runs.
+enum class Kind : int { Psi4 = 4, Psi6 = 6, Psi8 = 8, LscvScalar = 1, LscvMatrix = 2 };
+
+// Per-launch parameters (copied into the kernel parameter space = constant bank).
+struct PsiParams {
+  float c[5];        // c[0] = -log2(e)/2 (exponent scale); He_r coefficients are compile-time
+};
+struct LscvScalarParams {
+  float kappa[kMaxCand];   // -1/h_c^2 (data pre-scaled by sqrt(log2 e / 4) L^-1)
+};
+struct LscvMatrixParams {
+  // D <= 4: monomial coefficients m_ab (a <= b, row-major over the upper triangle), for each
+  //         candidate: q = sum m_ab v_a v_b = -(log2 e/4) v^T H^-1 v.
+  // D  > 4: rows of the scaled upper-triangular factor U (U^T U = (log2 e/4) H^-1), q = -|U v|^2.
+  float m[kMaxCand * 10];  // sized for D<=4 monomials at 32 candidates; D>4 uses fewer candidates
+};
+struct LscvCholParams {
+  float u[4 * 136];        // up to 4 candidates of a 16x16 upper-triangular factor
+};
+
+struct LaunchCfg {
+  const float* X;          // D rows of ld floats (fp32, prepared), device
+  int64_t n, ld;           // samples, padded row length (multiple of the tile)
+  int64_t tile_begin, tile_end;
+  int tile;                // tile edge T (rows = columns)
+  int scale_exp;           // fixed-point exponent S
+  unsigned long long* limbs;   // [n_out][3] accumulators, device
+  int n_out;               // outputs written by this launch (<= 2*kMaxCand)
+  cudaStream_t stream;
+  int sm_count;
+};
+
+// Launchers (kde_kernels.cu).  Return cudaSuccess or the launch error.
+cudaError_t launch_psi(int r, const LaunchCfg& c, const PsiParams& p);
+cudaError_t launch_lscv_scalar(int d, int nb, const LaunchCfg& c, const LscvScalarParams& p);
+cudaError_t launch_lscv_matrix(int d, int nb, const LaunchCfg& c, const void* params, size_t bytes);
+int tile_for(Kind k, int d, int64_t n);       // tile edge the launcher uses
+int cand_per_launch(Kind k, int d);           // B
+
+// O(n) kernels.
+cudaError_t launch_moments1(const double* X, int64_t n, int d, double* part, int nblk,
+                            cudaStream_t s);
+cudaError_t launch_moments2(const double* X, int64_t n, int d, const double* mean_dev,
+                            double* part, int nblk, cudaStream_t s);
+cudaError_t launch_reduce_parts(const double* part, int nblk, int width, double* out,
+                                cudaStream_t s);
+cudaError_t launch_prep(const double* X, int64_t n, int d, const double* W_dev,
+                        const double* mean_dev, float* Y, int64_t ld, cudaStream_t s);
+int moments_blocks(int64_t n);
+
+// Host/device tile map (Eq. 42-43 + integer fix-up).
+void tile_coords_host(int64_t bx, int64_t* l, int64_t* q);
+
+}  // namespace kde

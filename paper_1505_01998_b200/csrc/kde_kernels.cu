@@ -1,0 +1,685 @@
+// kde_kernels.cu — sm_100a kernels of the all-pairs kernel-sum engine (arxiv 1505.01998).
+//
+// One persistent pair-kernel family evaluates RR_fun(A) = sum_{i<j} fun(A_i - A_j) (P:472,
+// Sec. 5.4) and RR^v_fun (Sec. 5.5) for a batch of candidate bandwidths per pair
+// visit.  Design:
+//  * work unit = one T x T tile (l, q), q <= l, of the upper-triangular pair matrix,
+//    numbered column by column and mapped back with Eq. 42-43 + an integer fix-up;
+//  * persistent CTAs stride over their rank's contiguous tile range;
+//  * the T column samples (D rows) of the next tile are staged in shared memory by TMA bulk
+//    copies (cp.async.bulk + mbarrier, double-buffered); the T row samples sit in registers
+//    (R per thread); columns are read back with broadcast LDS.128;
+//  * per eval: FP32 difference / quadratic form, one MUFU.EX2, Horner or accumulate FMAs;
+//  * every tile's partial is reduced in a fixed order (fp32 per thread -> fp64 warp butterfly ->
+//    fixed cross-warp order) and added as exact fixed-point limbs with integer atomics, so the
+//    result is independent of grid size, tile-to-CTA assignment, batch composition and GPU count.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+
+#include "kde_internal.h"
+
+namespace kde {
+
+constexpr int nb_scalar(int d);
+constexpr int nb_mono_max(int d);
+constexpr int nb_chol(int d);
+
+// ------------------------------------------------------------------ small device helpers
+
+__host__ __device__ inline void tile_coords(int64_t bx, int64_t& l, int64_t& q) {
+  // Eq. 42: l = ceil((sqrt(8 bx + 9) - 3) / 2);  Eq. 43: q = bx - l(l+1)/2.  The fp64 sqrt is
+  // exact enough to land within +-1 of l for bx < 2^62; the loops make it exact (reading Z13).
+  double s = sqrt(8.0 * (double)bx + 9.0);
+  int64_t L = (int64_t)ceil((s - 3.0) * 0.5);
+  if (L < 0) L = 0;
+  while (L > 0 && L * (L + 1) / 2 > bx) --L;
+  while ((L + 1) * (L + 2) / 2 <= bx) ++L;
+  l = L;
+  q = bx - L * (L + 1) / 2;
+}
+
+void tile_coords_host(int64_t bx, int64_t* l, int64_t* q) { tile_coords(bx, *l, *q); }
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// TMA bulk copy global -> shared, completion counted on `bar` (UBLKCP in SASS).
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Exact fixed-point split of v * 2^S (|v| 2^S < 2^120): sign-magnitude limbs of 40 bits.
+__device__ __forceinline__ void add_limbs(double v, int S, unsigned long long* dst) {
+  double a = fabs(ldexp(v, S));
+  double h = floor(ldexp(a, -80));
+  double r = a - ldexp(h, 80);            // exact: the low bits of a
+  double m = floor(ldexp(r, -40));
+  double lo = rint(r - ldexp(m, 40));     // integer part; rounding < 2^-S absolute
+  long long H = (long long)h, M = (long long)m, L = (long long)lo;
+  if (v < 0) { H = -H; M = -M; L = -L; }
+  atomicAdd(dst + 0, (unsigned long long)H);
+  atomicAdd(dst + 1, (unsigned long long)M);
+  atomicAdd(dst + 2, (unsigned long long)L);
+}
+
+// Per-tile epilogue: fixed-order reduction of NOUT per-thread values, then limb atomics.
+template <int NOUT, int NT>
+__device__ __forceinline__ void commit_tile(double (&v)[NOUT], double* red,
+                                            unsigned long long* limbs, int S) {
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < NOUT; ++k) v[k] = warp_sum(v[k]);
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < NOUT; ++k) red[w * NOUT + k] = v[k];
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < NOUT; k += NT) {
+    double s = red[k];
+#pragma unroll
+    for (int ww = 1; ww < NW; ++ww) s += red[ww * NOUT + k];
+    add_limbs(s, S, limbs + (size_t)k * kLimbs);
+  }
+  __syncthreads();
+}
+
+struct Args {
+  const float* X;
+  int64_t n, ld, tile_begin, tile_end;
+  int scale_exp;
+  unsigned long long* limbs;
+};
+
+// ------------------------------------------------------------------ functors
+
+// Psi_r: term He_r(u) exp(-u^2/2) with x pre-scaled by 1/g, so s = (x_i'-x_j')^2 = u^2.
+// He_r is evaluated by Horner in s with its exact integer coefficients.
+// exp(-s/2) = 2^(s c0) with c0 = -log2(e)/2 is taken from MUFU.EX2 as
+//     2^(s c0) = ex2(s c0 - off_k) * 2^off_k,   off_k = 16 + k/8,  k = accumulator class,
+// because MUFU.EX2's relative error has a near-constant bias (-5.1e-8) only for inputs in
+// [-32,-16), and a different, input-dependent one on (-1, 0] where the dominant near pairs
+// live; the sums of Psi_r cancel 1000-5000x at the PLUGIN bandwidths, so that bias pattern
+// alone cost 2e-5..5e-5 relative.  Offsetting into one binade and averaging over 8 fractional
+// shifts (one per accumulator class, undone exactly in fp64 at the flush) brings the error to
+// ~2e-10 of sum|t| at no per-eval cost (measured by tools/term_error.cu).
+template <int RORD, int NT_>
+struct FPsi {
+  static constexpr int NT = NT_, D = 1, R = 8, T = NT_ * 8, NOUT = 1, CH = 256, MINB = 3;
+  static constexpr int NCLS = 8;   // accumulator class = row slot r
+  using Params = PsiParams;
+  float xr[R];
+  double acc;
+
+  __device__ __forceinline__ void load_rows(const float* __restrict__ X, int64_t ld,
+                                            int64_t i0) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) xr[r] = __ldg(X + i0 + r * NT);
+    acc = 0.0;
+  }
+
+  __device__ __forceinline__ float poly(float s) const {
+    if (RORD == 4) return __fmaf_rn(__fadd_rn(s, -6.f), s, 3.f);                  // s^2-6s+3
+    if (RORD == 6) return __fmaf_rn(__fmaf_rn(__fadd_rn(s, -15.f), s, 45.f), s, -15.f);
+    return __fmaf_rn(__fmaf_rn(__fmaf_rn(__fadd_rn(s, -28.f), s, 210.f), s, -420.f), s, 105.f);
+  }
+
+  // Accumulation: the 4 terms of one float4 column group of row r are summed in
+  // fp32, then added to the row's running sum with Fast2Sum (the rounding error goes to a
+  // compensation register).  A plain fp32 running sum drops the one-signed far-pair tail terms
+  // (~1e-7..1e-6) next to near-pair sums (~10): measured -1.4e-5 relative at T=2048.
+  template <bool MASK>
+  __device__ __forceinline__ void compute(const float* __restrict__ sc, const Params& p, bool diag,
+                                          int jlim) {
+    const int tid = threadIdx.x;
+    const float c0 = p.c[0];
+    for (int jc = 0; jc < T; jc += CH) {
+      if (MASK && jc >= jlim) break;
+      float a[R], cmp[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) a[r] = cmp[r] = 0.f;
+#pragma unroll 2
+      for (int j = jc; j < jc + CH; j += 4) {
+        const float4 c4 = *reinterpret_cast<const float4*>(sc + j);
+        const float cv[4] = {c4.x, c4.y, c4.z, c4.w};
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const float off = 16.0f + 0.125f * (float)r;
+          float grp = 0.f;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float d = __fsub_rn(xr[r], cv[k]);
+            float sq = __fmul_rn(d, d);
+            if (MASK) {
+              const int jj = j + k;
+              const bool ok = (jj < jlim) && (!diag || jj > r * NT + tid);
+              sq = ok ? sq : 1.0e4f;   // 2^(-7229) == 0 exactly; poly(1e4) finite
+            }
+            const float e = ex2(__fmaf_rn(sq, c0, -off));
+            grp = (k == 0) ? __fmul_rn(poly(sq), e) : __fmaf_rn(poly(sq), e, grp);
+          }
+          const float s2 = __fadd_rn(a[r], grp);            // Fast2Sum(a, grp)
+          const float z = __fsub_rn(s2, a[r]);
+          cmp[r] = __fadd_rn(cmp[r], __fsub_rn(grp, z));
+          a[r] = s2;
+        }
+      }
+      double s = 0.0;
+#pragma unroll
+      for (int r = 0; r < R; ++r) s += ((double)a[r] + (double)cmp[r]) * exp2(16.0 + 0.125 * r);
+      acc += s;
+    }
+  }
+
+  __device__ __forceinline__ void outputs(double (&v)[NOUT]) const { v[0] = acc; }
+};
+
+// LSCV_h (any d): data pre-whitened and scaled, x' = sqrt(log2 e / 4) L^-1 (x - mean) with
+// Sigma = L L^T, so s = |x_i' - x_j'|^2 = (log2 e / 4) S(v) (S(v) of Eq. 37) and for candidate
+// h_c:  e = 2^(s * kappa_c) = exp(-S(v)/(4 h_c^2)),  e^2 = exp(-S(v)/(2 h_c^2)).
+template <int D_, int R_, int NB_>
+struct FLscvScalar {
+  static constexpr int NT = kThreads, D = D_, R = R_, T = kThreads * R_, NB = NB_, NOUT = 2 * NB_, MINB = 2;
+  using Params = LscvScalarParams;
+  float xr[D][R];
+  float a1[NB], a2[NB];
+
+  __device__ __forceinline__ void load_rows(const float* __restrict__ X, int64_t ld,
+                                            int64_t i0) {
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int r = 0; r < R; ++r) xr[a][r] = __ldg(X + a * ld + i0 + r * kThreads);
+#pragma unroll
+    for (int c = 0; c < NB; ++c) a1[c] = a2[c] = 0.f;
+  }
+
+  template <bool MASK>
+  __device__ __forceinline__ void compute(const float* __restrict__ sc, const Params& p, bool diag,
+                                          int jlim) {
+    const int tid = threadIdx.x;
+    const int jend = MASK ? ((jlim + 3) & ~3) : T;
+#pragma unroll 1
+    for (int j = 0; j < jend; j += 4) {
+      float cv[D][4];
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        const float4 c4 = *reinterpret_cast<const float4*>(sc + a * T + j);
+        cv[a][0] = c4.x; cv[a][1] = c4.y; cv[a][2] = c4.z; cv[a][3] = c4.w;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          float dd = __fsub_rn(xr[0][r], cv[0][k]);
+          float s = __fmul_rn(dd, dd);
+#pragma unroll
+          for (int a = 1; a < D; ++a) {
+            dd = __fsub_rn(xr[a][r], cv[a][k]);
+            s = __fmaf_rn(dd, dd, s);
+          }
+          if (MASK) {
+            const int jj = j + k;
+            const bool ok = (jj < jlim) && (!diag || jj > r * kThreads + tid);
+            s = ok ? s : __int_as_float(0x7f800000);   // +inf -> e = 2^-inf = 0
+          }
+#pragma unroll
+          for (int c = 0; c < NB; ++c) {
+            const float e = ex2(__fmul_rn(s, p.kappa[c]));
+            a1[c] = __fadd_rn(a1[c], e);
+            a2[c] = __fmaf_rn(e, e, a2[c]);
+          }
+        }
+      }
+    }
+  }
+
+  __device__ __forceinline__ void outputs(double (&v)[NOUT]) const {
+#pragma unroll
+    for (int c = 0; c < NB; ++c) { v[2 * c] = a1[c]; v[2 * c + 1] = a2[c]; }
+  }
+};
+
+// LSCV_H, d <= 4: per pair the differences v and the d(d+1)/2 monomials v_a v_b; per candidate
+// q = sum m_ab v_a v_b = -(log2 e / 4) v^T H^-1 v (the fun2 = x^T M x of Eq. 44-56 expanded in
+// monomials), e = 2^q = exp(-v^T H^-1 v / 4), e^2 = exp(-v^T H^-1 v / 2).
+template <int D_, int R_, int NB_>
+struct FLscvMono {
+  static constexpr int NT = kThreads, D = D_, R = R_, T = kThreads * R_, NB = NB_, NOUT = 2 * NB_, MINB = 2;
+  static constexpr int P = D * (D + 1) / 2;
+  using Params = LscvMatrixParams;
+  float xr[D][R];
+  float a1[NB], a2[NB];
+
+  __device__ __forceinline__ void load_rows(const float* __restrict__ X, int64_t ld,
+                                            int64_t i0) {
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int r = 0; r < R; ++r) xr[a][r] = __ldg(X + a * ld + i0 + r * kThreads);
+#pragma unroll
+    for (int c = 0; c < NB; ++c) a1[c] = a2[c] = 0.f;
+  }
+
+  template <bool MASK>
+  __device__ __forceinline__ void compute(const float* __restrict__ sc, const Params& p, bool diag,
+                                          int jlim) {
+    const int tid = threadIdx.x;
+    const int jend = MASK ? ((jlim + 3) & ~3) : T;
+#pragma unroll 1
+    for (int j = 0; j < jend; j += 4) {
+      float cv[D][4];
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        const float4 c4 = *reinterpret_cast<const float4*>(sc + a * T + j);
+        cv[a][0] = c4.x; cv[a][1] = c4.y; cv[a][2] = c4.z; cv[a][3] = c4.w;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          float v[D];
+#pragma unroll
+          for (int a = 0; a < D; ++a) v[a] = __fsub_rn(xr[a][r], cv[a][k]);
+          float mono[P];
+          int t = 0;
+#pragma unroll
+          for (int a = 0; a < D; ++a)
+#pragma unroll
+            for (int b = a; b < D; ++b) mono[t++] = __fmul_rn(v[a], v[b]);
+          if (MASK) {
+            const int jj = j + k;
+            const bool ok = (jj < jlim) && (!diag || jj > r * kThreads + tid);
+            mono[0] = ok ? mono[0] : __int_as_float(0x7f800000);   // m_00 < 0 -> q = -inf
+          }
+#pragma unroll
+          for (int c = 0; c < NB; ++c) {
+            float q = __fmul_rn(mono[0], p.m[c * P]);
+#pragma unroll
+            for (int u = 1; u < P; ++u) q = __fmaf_rn(mono[u], p.m[c * P + u], q);
+            const float e = ex2(q);
+            a1[c] = __fadd_rn(a1[c], e);
+            a2[c] = __fmaf_rn(e, e, a2[c]);
+          }
+        }
+      }
+    }
+  }
+
+  __device__ __forceinline__ void outputs(double (&v)[NOUT]) const {
+#pragma unroll
+    for (int c = 0; c < NB; ++c) { v[2 * c] = a1[c]; v[2 * c + 1] = a2[c]; }
+  }
+};
+
+// LSCV_H, d > 4: per candidate a scaled upper-triangular factor U_c with
+// U_c^T U_c = (log2 e / 4) H_c^-1, q = -|U_c v|^2 (Eq. 44-56 with M factored), e = 2^q.
+template <int D_, int NB_>
+struct FLscvChol {
+  static constexpr int NT = kThreads, D = D_, R = 1, T = kThreads, NB = NB_, NOUT = 2 * NB_, MINB = 2;
+  static constexpr int P = D * (D + 1) / 2;
+  using Params = LscvCholParams;
+  float xr[D];
+  float a1[NB], a2[NB];
+
+  __device__ __forceinline__ void load_rows(const float* __restrict__ X, int64_t ld,
+                                            int64_t i0) {
+#pragma unroll
+    for (int a = 0; a < D; ++a) xr[a] = __ldg(X + a * ld + i0);
+#pragma unroll
+    for (int c = 0; c < NB; ++c) a1[c] = a2[c] = 0.f;
+  }
+
+  template <bool MASK>
+  __device__ __forceinline__ void compute(const float* __restrict__ sc, const Params& p, bool diag,
+                                          int jlim) {
+    const int tid = threadIdx.x;
+    const int jend = MASK ? jlim : T;
+#pragma unroll 1
+    for (int j = 0; j < jend; ++j) {
+      float v[D];
+#pragma unroll
+      for (int a = 0; a < D; ++a) v[a] = __fsub_rn(xr[a], sc[a * T + j]);
+      const bool ok = !MASK || (!diag || j > tid);
+#pragma unroll
+      for (int c = 0; c < NB; ++c) {
+        float q = 0.f;
+        int t = 0;
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          float z = __fmul_rn(p.u[c * P + t], v[a]);
+          ++t;
+#pragma unroll
+          for (int b = a + 1; b < D; ++b) { z = __fmaf_rn(p.u[c * P + t], v[b], z); ++t; }
+          q = __fmaf_rn(z, z, q);
+        }
+        float e = ex2(-q);
+        if (MASK) e = ok ? e : 0.f;
+        a1[c] = __fadd_rn(a1[c], e);
+        a2[c] = __fmaf_rn(e, e, a2[c]);
+      }
+    }
+  }
+
+  __device__ __forceinline__ void outputs(double (&v)[NOUT]) const {
+#pragma unroll
+    for (int c = 0; c < NB; ++c) { v[2 * c] = a1[c]; v[2 * c + 1] = a2[c]; }
+  }
+};
+
+// ------------------------------------------------------------------ the persistent pair kernel
+
+template <class F>
+__global__ void __launch_bounds__(F::NT, F::MINB) pair_kernel(const Args a,
+                                                        const __grid_constant__ typename F::Params p) {
+  constexpr int T = F::T, D = F::D, NOUT = F::NOUT, NW = F::NT / 32;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* cols = reinterpret_cast<float*>(smem_raw);                 // [2][D][T]
+  double* red = reinterpret_cast<double*>(cols + 2 * D * T);        // [NW][NOUT]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(red + NW * NOUT);      // [2]
+  const int tid = threadIdx.x;
+
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  auto issue = [&](int64_t tile, int buf) {
+    int64_t l, q;
+    tile_coords(tile, l, q);
+    float* dst = cols + buf * D * T;
+    mbar_expect_tx(&bar[buf], (uint32_t)(D * T * sizeof(float)));
+#pragma unroll
+    for (int d = 0; d < D; ++d)
+      tma_load_1d(dst + d * T, a.X + d * a.ld + l * T, (uint32_t)(T * sizeof(float)), &bar[buf]);
+  };
+
+  int64_t t = a.tile_begin + blockIdx.x;
+  if (tid == 0 && t < a.tile_end) issue(t, 0);
+  uint32_t k = 0;
+  for (; t < a.tile_end; t += gridDim.x, ++k) {
+    int64_t l, q;
+    tile_coords(t, l, q);
+    const int64_t tn = t + gridDim.x;
+    if (tid == 0 && tn < a.tile_end) issue(tn, (k + 1) & 1);
+
+    F f;
+    f.load_rows(a.X, a.ld, q * T + tid);
+    mbar_wait(&bar[k & 1], (k >> 1) & 1);
+    const float* sc = cols + (k & 1) * D * T;
+    const bool diag = (q == l);
+    const int64_t jl = a.n - l * (int64_t)T;
+    if (!diag && jl >= T) f.template compute<false>(sc, p, false, T);
+    else f.template compute<true>(sc, p, diag, (int)(jl < T ? jl : T));
+
+    double v[NOUT];
+    f.outputs(v);
+    commit_tile<NOUT, F::NT>(v, red, a.limbs, a.scale_exp);
+  }
+}
+
+template <class F>
+static cudaError_t launch_pair(const LaunchCfg& c, const typename F::Params& p) {
+  if (c.tile_end <= c.tile_begin) return cudaSuccess;
+  const size_t smem = 2 * F::D * F::T * sizeof(float) + (F::NT / 32) * F::NOUT * sizeof(double) + 16;
+  static int occ = -1;   // per-instantiation: resident CTAs per SM
+  if (occ < 0) {
+    cudaError_t e = cudaFuncSetAttribute(pair_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    int o = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, pair_kernel<F>, F::NT, smem);
+    if (e != cudaSuccess) return e;
+    occ = o > 0 ? o : 1;
+  }
+  const int64_t tiles = c.tile_end - c.tile_begin;
+  int64_t grid = (int64_t)c.sm_count * occ;
+  if (grid > tiles) grid = tiles;
+  Args a{c.X, c.n, c.ld, c.tile_begin, c.tile_end, c.scale_exp, c.limbs};
+  pair_kernel<F><<<(unsigned)grid, F::NT, smem, c.stream>>>(a, p);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ dispatch
+
+int tile_for(Kind k, int d, int64_t n) {
+  switch (k) {
+    case Kind::Psi4: case Kind::Psi6: case Kind::Psi8: {
+      static const char* dbg = getenv("KDE_DEBUG_PSI_TILE");   // tests / diagnostics only
+      if (dbg && (atoi(dbg) == 512 || atoi(dbg) == 2048)) return atoi(dbg);
+      return n >= (int64_t)64 * 2048 ? 2048 : 512;
+    }
+    case Kind::LscvScalar: return 512;
+    case Kind::LscvMatrix: return d <= 4 ? 512 : kThreads;
+  }
+  return 512;
+}
+
+int cand_per_launch(Kind k, int d) {
+  switch (k) {
+    case Kind::Psi4: case Kind::Psi6: case Kind::Psi8: return 1;
+    case Kind::LscvScalar: return nb_scalar(d);
+    case Kind::LscvMatrix: return d <= 4 ? nb_mono_max(d) : nb_chol(d);
+  }
+  return 1;
+}
+
+cudaError_t launch_psi(int r, const LaunchCfg& c, const PsiParams& p) {
+  const bool big = c.tile == 2048;
+  switch (r) {
+    case 4: return big ? launch_pair<FPsi<4, 256>>(c, p) : launch_pair<FPsi<4, 64>>(c, p);
+    case 6: return big ? launch_pair<FPsi<6, 256>>(c, p) : launch_pair<FPsi<6, 64>>(c, p);
+    case 8: return big ? launch_pair<FPsi<8, 256>>(c, p) : launch_pair<FPsi<8, 64>>(c, p);
+  }
+  return cudaErrorInvalidValue;
+}
+
+// Candidates per launch: chosen so that no instantiation spills at 128 registers (2 CTAs/SM).
+constexpr int nb_scalar(int d) { return d <= 12 ? 16 : 8; }
+constexpr int nb_mono_max(int d) { return d <= 3 ? 16 : 8; }
+constexpr int nb_chol(int d) { return d <= 5 ? 8 : (d <= 8 ? 4 : (d <= 12 ? 2 : 1)); }
+
+template <int D>
+static cudaError_t lscv_scalar_d(const LaunchCfg& c, const LscvScalarParams& p) {
+  return launch_pair<FLscvScalar<D, 2, nb_scalar(D)>>(c, p);
+}
+
+cudaError_t launch_lscv_scalar(int d, int nb, const LaunchCfg& c, const LscvScalarParams& p) {
+  (void)nb;
+  switch (d) {
+    case 1: return lscv_scalar_d<1>(c, p);   case 2: return lscv_scalar_d<2>(c, p);
+    case 3: return lscv_scalar_d<3>(c, p);   case 4: return lscv_scalar_d<4>(c, p);
+    case 5: return lscv_scalar_d<5>(c, p);   case 6: return lscv_scalar_d<6>(c, p);
+    case 7: return lscv_scalar_d<7>(c, p);   case 8: return lscv_scalar_d<8>(c, p);
+    case 9: return lscv_scalar_d<9>(c, p);   case 10: return lscv_scalar_d<10>(c, p);
+    case 11: return lscv_scalar_d<11>(c, p); case 12: return lscv_scalar_d<12>(c, p);
+    case 13: return lscv_scalar_d<13>(c, p); case 14: return lscv_scalar_d<14>(c, p);
+    case 15: return lscv_scalar_d<15>(c, p); case 16: return lscv_scalar_d<16>(c, p);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <int D>
+static cudaError_t lscv_mono_d(int nb, const LaunchCfg& c, const void* params) {
+  const auto& p = *static_cast<const LscvMatrixParams*>(params);
+  if (nb <= 4) return launch_pair<FLscvMono<D, 2, 4>>(c, p);
+  if constexpr (nb_mono_max(D) == 8) {
+    return launch_pair<FLscvMono<D, 2, 8>>(c, p);
+  } else {
+    if (nb <= 8) return launch_pair<FLscvMono<D, 2, 8>>(c, p);
+    return launch_pair<FLscvMono<D, 2, 16>>(c, p);
+  }
+}
+
+template <int D>
+static cudaError_t lscv_chol_d(const LaunchCfg& c, const void* params) {
+  const auto& p = *static_cast<const LscvCholParams*>(params);
+  constexpr int NB = nb_chol(D);
+  static_assert(NB * D * (D + 1) / 2 <= 4 * 136, "chol params");
+  return launch_pair<FLscvChol<D, NB>>(c, p);
+}
+
+cudaError_t launch_lscv_matrix(int d, int nb, const LaunchCfg& c, const void* params,
+                               size_t bytes) {
+  (void)bytes;
+  switch (d) {
+    case 1: return lscv_mono_d<1>(nb, c, params);
+    case 2: return lscv_mono_d<2>(nb, c, params);
+    case 3: return lscv_mono_d<3>(nb, c, params);
+    case 4: return lscv_mono_d<4>(nb, c, params);
+    case 5: return lscv_chol_d<5>(c, params);   case 6: return lscv_chol_d<6>(c, params);
+    case 7: return lscv_chol_d<7>(c, params);   case 8: return lscv_chol_d<8>(c, params);
+    case 9: return lscv_chol_d<9>(c, params);   case 10: return lscv_chol_d<10>(c, params);
+    case 11: return lscv_chol_d<11>(c, params); case 12: return lscv_chol_d<12>(c, params);
+    case 13: return lscv_chol_d<13>(c, params); case 14: return lscv_chol_d<14>(c, params);
+    case 15: return lscv_chol_d<15>(c, params); case 16: return lscv_chol_d<16>(c, params);
+  }
+  return cudaErrorInvalidValue;
+}
+
+// ------------------------------------------------------------------ O(n) kernels (fp64)
+// Deterministic moments (R_fun): fixed block count for a given n, fixed per-thread
+// order, warp butterfly, fixed cross-warp order, then one block adds the partials in order.
+
+constexpr int kMomThreads = 256;
+
+int moments_blocks(int64_t n) {
+  int64_t b = (n + 4 * kMomThreads - 1) / (4 * kMomThreads);
+  if (b > 1024) b = 1024;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+template <int MODE>   // 1: sum x_a; 2: sum (x_a - m_a)(x_b - m_b), a <= b
+__global__ void __launch_bounds__(kMomThreads) moments_kernel(const double* __restrict__ X, int64_t n,
+                                                               int d, const double* __restrict__ mean,
+                                                               double* __restrict__ part) {
+  __shared__ double red[kMomThreads / 32][kMaxDim * (kMaxDim + 1) / 2];
+  const int width = MODE == 1 ? d : d * (d + 1) / 2;
+  double acc[kMaxDim * (kMaxDim + 1) / 2];
+  for (int k = 0; k < width; ++k) acc[k] = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * kMomThreads;
+  for (int64_t i = (int64_t)blockIdx.x * kMomThreads + threadIdx.x; i < n; i += stride) {
+    if (MODE == 1) {
+      for (int a = 0; a < d; ++a) acc[a] += X[a * n + i];
+    } else {
+      double v[kMaxDim];
+      for (int a = 0; a < d; ++a) v[a] = X[a * n + i] - mean[a];
+      int t = 0;
+      for (int a = 0; a < d; ++a)
+        for (int b = a; b < d; ++b) acc[t++] += v[a] * v[b];
+    }
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int k = 0; k < width; ++k) {
+    double s = warp_sum(acc[k]);
+    if (lane == 0) red[w][k] = s;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < width; k += kMomThreads) {
+    double s = red[0][k];
+    for (int ww = 1; ww < kMomThreads / 32; ++ww) s += red[ww][k];
+    part[(size_t)blockIdx.x * width + k] = s;
+  }
+}
+
+__global__ void reduce_parts_kernel(const double* __restrict__ part, int nblk, int width,
+                                    double* __restrict__ out) {
+  for (int k = threadIdx.x; k < width; k += blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < nblk; ++b) s += part[(size_t)b * width + k];
+    out[k] = s;
+  }
+}
+
+cudaError_t launch_moments1(const double* X, int64_t n, int d, double* part, int nblk,
+                            cudaStream_t s) {
+  moments_kernel<1><<<nblk, kMomThreads, 0, s>>>(X, n, d, nullptr, part);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_moments2(const double* X, int64_t n, int d, const double* mean_dev,
+                            double* part, int nblk, cudaStream_t s) {
+  moments_kernel<2><<<nblk, kMomThreads, 0, s>>>(X, n, d, mean_dev, part);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_parts(const double* part, int nblk, int width, double* out,
+                                cudaStream_t s) {
+  reduce_parts_kernel<<<1, 160, 0, s>>>(part, nblk, width, out);
+  return cudaGetLastError();
+}
+
+// Data prep (row a1 of SURVEY §8(a)): y_a = fp32( sum_b W_ab (x_b - mean_b) ), zero padding.
+__global__ void prep_kernel(const double* __restrict__ X, int64_t n, int d,
+                            const double* __restrict__ W, const double* __restrict__ mean,
+                            float* __restrict__ Y, int64_t ld) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ld; i += stride) {
+    if (i < n) {
+      double v[kMaxDim];
+      for (int b = 0; b < d; ++b) v[b] = X[b * n + i] - mean[b];
+      for (int a = 0; a < d; ++a) {
+        double s = 0.0;
+        for (int b = 0; b < d; ++b) s = fma(W[a * d + b], v[b], s);
+        Y[a * ld + i] = (float)s;
+      }
+    } else {
+      for (int a = 0; a < d; ++a) Y[a * ld + i] = 0.f;
+    }
+  }
+}
+
+cudaError_t launch_prep(const double* X, int64_t n, int d, const double* W_dev,
+                        const double* mean_dev, float* Y, int64_t ld, cudaStream_t s) {
+  int64_t blocks = (ld + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  prep_kernel<<<(unsigned)blocks, 256, 0, s>>>(X, n, d, W_dev, mean_dev, Y, ld);
+  return cudaGetLastError();
+}
+
+}  // namespace kde
