@@ -48,6 +48,26 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+// Packed fp32x2 arithmetic (sm_100a FADD2 / FMUL2 / FFMA2): two lanes per instruction, each
+// rounded to nearest exactly like the scalar op, so packing never changes a result bit.
+typedef unsigned long long f2;
+__device__ __forceinline__ f2 pk(float a, float b) {
+  f2 r;
+  asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void upk(f2 v, float& a, float& b) {
+  asm("mov.b64 {%0,%1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ f2 add2(f2 a, f2 b) { f2 d; asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b)); return d; }
+__device__ __forceinline__ f2 sub2(f2 a, f2 b) { f2 d; asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b)); return d; }
+__device__ __forceinline__ f2 mul2(f2 a, f2 b) { f2 d; asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b)); return d; }
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
+  f2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -148,25 +168,30 @@ struct Args {
 template <int RORD, int NT_>
 struct FPsi {
   static constexpr int NT = NT_, D = 1, R = 8, T = NT_ * 8, NOUT = 1, CH = 256, MINB = 3;
-  static constexpr int NCLS = 8;   // accumulator class = row slot r
+  static constexpr int NP = R / 2;   // row pairs (r = 2p, 2p+1) packed into fp32x2 lanes
   using Params = PsiParams;
-  float xr[R];
+  f2 xr[NP];
   double acc;
 
   __device__ __forceinline__ void load_rows(const float* __restrict__ X, int64_t ld,
                                             int64_t i0) {
 #pragma unroll
-    for (int r = 0; r < R; ++r) xr[r] = __ldg(X + i0 + r * NT);
+    for (int p = 0; p < NP; ++p) xr[p] = pk(__ldg(X + i0 + (2 * p) * NT), __ldg(X + i0 + (2 * p + 1) * NT));
     acc = 0.0;
   }
 
-  __device__ __forceinline__ float poly(float s) const {
-    if (RORD == 4) return __fmaf_rn(__fadd_rn(s, -6.f), s, 3.f);                  // s^2-6s+3
-    if (RORD == 6) return __fmaf_rn(__fmaf_rn(__fadd_rn(s, -15.f), s, 45.f), s, -15.f);
-    return __fmaf_rn(__fmaf_rn(__fmaf_rn(__fadd_rn(s, -28.f), s, 210.f), s, -420.f), s, 105.f);
+  // He_r(s) by Horner with exact integer coefficients, two lanes at once.
+  __device__ __forceinline__ f2 poly(f2 s) const {
+    if (RORD == 4) return fma2(add2(s, pk(-6.f, -6.f)), s, pk(3.f, 3.f));
+    if (RORD == 6) return fma2(fma2(add2(s, pk(-15.f, -15.f)), s, pk(45.f, 45.f)), s, pk(-15.f, -15.f));
+    return fma2(fma2(fma2(add2(s, pk(-28.f, -28.f)), s, pk(210.f, 210.f)), s, pk(-420.f, -420.f)), s,
+                pk(105.f, 105.f));
   }
 
-  // Accumulation: the 4 terms of one float4 column group of row r are summed in
+  // MUFU offset of accumulator class r (= row slot): off_r = 16 + r/8 (see the comment above).
+  static __device__ __forceinline__ float off(int r) { return 16.0f + 0.125f * (float)r; }
+
+  // Accumulation: the 4 terms of one float4 column group of a row are summed in
   // fp32, then added to the row's running sum with Fast2Sum (the rounding error goes to a
   // compensation register).  A plain fp32 running sum drops the one-signed far-pair tail terms
   // (~1e-7..1e-6) next to near-pair sums (~10): measured -1.4e-5 relative at T=2048.
@@ -174,41 +199,52 @@ struct FPsi {
   __device__ __forceinline__ void compute(const float* __restrict__ sc, const Params& p, bool diag,
                                           int jlim) {
     const int tid = threadIdx.x;
-    const float c0 = p.c[0];
+    const f2 c0 = pk(p.c[0], p.c[0]);
     for (int jc = 0; jc < T; jc += CH) {
       if (MASK && jc >= jlim) break;
-      float a[R], cmp[R];
+      f2 a[NP], cmp[NP];
 #pragma unroll
-      for (int r = 0; r < R; ++r) a[r] = cmp[r] = 0.f;
+      for (int q = 0; q < NP; ++q) a[q] = cmp[q] = pk(0.f, 0.f);
 #pragma unroll 2
       for (int j = jc; j < jc + CH; j += 4) {
         const float4 c4 = *reinterpret_cast<const float4*>(sc + j);
         const float cv[4] = {c4.x, c4.y, c4.z, c4.w};
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const float off = 16.0f + 0.125f * (float)r;
-          float grp = 0.f;
+        for (int q = 0; q < NP; ++q) {
+          const f2 noff = pk(-off(2 * q), -off(2 * q + 1));
+          f2 grp = pk(0.f, 0.f);
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            const float d = __fsub_rn(xr[r], cv[k]);
-            float sq = __fmul_rn(d, d);
+            const f2 d = sub2(xr[q], pk(cv[k], cv[k]));
+            f2 sq = mul2(d, d);
             if (MASK) {
               const int jj = j + k;
-              const bool ok = (jj < jlim) && (!diag || jj > r * NT + tid);
-              sq = ok ? sq : 1.0e4f;   // 2^(-7229) == 0 exactly; poly(1e4) finite
+              float s0, s1;
+              upk(sq, s0, s1);
+              const bool ok0 = (jj < jlim) && (!diag || jj > (2 * q) * NT + tid);
+              const bool ok1 = (jj < jlim) && (!diag || jj > (2 * q + 1) * NT + tid);
+              sq = pk(ok0 ? s0 : 1.0e4f, ok1 ? s1 : 1.0e4f);   // 2^(-7229) == 0; poly finite
             }
-            const float e = ex2(__fmaf_rn(sq, c0, -off));
-            grp = (k == 0) ? __fmul_rn(poly(sq), e) : __fmaf_rn(poly(sq), e, grp);
+            float a0, a1;
+            upk(fma2(sq, c0, noff), a0, a1);
+            const f2 e = pk(ex2(a0), ex2(a1));
+            grp = (k == 0) ? mul2(poly(sq), e) : fma2(poly(sq), e, grp);
           }
-          const float s2 = __fadd_rn(a[r], grp);            // Fast2Sum(a, grp)
-          const float z = __fsub_rn(s2, a[r]);
-          cmp[r] = __fadd_rn(cmp[r], __fsub_rn(grp, z));
-          a[r] = s2;
+          const f2 s2 = add2(a[q], grp);                    // Fast2Sum(a, grp), per lane
+          const f2 z = sub2(s2, a[q]);
+          cmp[q] = add2(cmp[q], sub2(grp, z));
+          a[q] = s2;
         }
       }
       double s = 0.0;
 #pragma unroll
-      for (int r = 0; r < R; ++r) s += ((double)a[r] + (double)cmp[r]) * exp2(16.0 + 0.125 * r);
+      for (int q = 0; q < NP; ++q) {
+        float a0, a1, c0_, c1_;
+        upk(a[q], a0, a1);
+        upk(cmp[q], c0_, c1_);
+        s += ((double)a0 + (double)c0_) * exp2((double)off(2 * q));
+        s += ((double)a1 + (double)c1_) * exp2((double)off(2 * q + 1));
+      }
       acc += s;
     }
   }
