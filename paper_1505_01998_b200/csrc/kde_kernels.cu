@@ -255,21 +255,21 @@ struct FPsi {
 // LSCV_h (any d): data pre-whitened and scaled, x' = sqrt(log2 e / 4) L^-1 (x - mean) with
 // Sigma = L L^T, so s = |x_i' - x_j'|^2 = (log2 e / 4) S(v) (S(v) of Eq. 37) and for candidate
 // h_c:  e = 2^(s * kappa_c) = exp(-S(v)/(4 h_c^2)),  e^2 = exp(-S(v)/(2 h_c^2)).
+// The thread's two rows are packed in fp32x2 lanes (lane-exact, halves the issue slots).
 template <int D_, int R_, int NB_>
 struct FLscvScalar {
+  static_assert(R_ == 2, "rows are packed as one fp32x2 pair");
   static constexpr int NT = kThreads, D = D_, R = R_, T = kThreads * R_, NB = NB_, NOUT = 2 * NB_, MINB = 2;
   using Params = LscvScalarParams;
-  float xr[D][R];
-  float a1[NB], a2[NB];
+  f2 xr[D];
+  f2 a1[NB], a2[NB];
 
   __device__ __forceinline__ void load_rows(const float* __restrict__ X, int64_t ld,
                                             int64_t i0) {
 #pragma unroll
-    for (int a = 0; a < D; ++a)
+    for (int a = 0; a < D; ++a) xr[a] = pk(__ldg(X + a * ld + i0), __ldg(X + a * ld + i0 + kThreads));
 #pragma unroll
-      for (int r = 0; r < R; ++r) xr[a][r] = __ldg(X + a * ld + i0 + r * kThreads);
-#pragma unroll
-    for (int c = 0; c < NB; ++c) a1[c] = a2[c] = 0.f;
+    for (int c = 0; c < NB; ++c) a1[c] = a2[c] = pk(0.f, 0.f);
   }
 
   template <bool MASK>
@@ -287,26 +287,29 @@ struct FLscvScalar {
       }
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
+        f2 dd = sub2(xr[0], pk(cv[0][k], cv[0][k]));
+        f2 s = mul2(dd, dd);
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-          float dd = __fsub_rn(xr[0][r], cv[0][k]);
-          float s = __fmul_rn(dd, dd);
+        for (int a = 1; a < D; ++a) {
+          dd = sub2(xr[a], pk(cv[a][k], cv[a][k]));
+          s = fma2(dd, dd, s);
+        }
+        if (MASK) {
+          const int jj = j + k;
+          float s0, s1;
+          upk(s, s0, s1);
+          const float inf = __int_as_float(0x7f800000);   // +inf -> e = 2^-inf = 0
+          const bool ok0 = (jj < jlim) && (!diag || jj > tid);
+          const bool ok1 = (jj < jlim) && (!diag || jj > kThreads + tid);
+          s = pk(ok0 ? s0 : inf, ok1 ? s1 : inf);
+        }
 #pragma unroll
-          for (int a = 1; a < D; ++a) {
-            dd = __fsub_rn(xr[a][r], cv[a][k]);
-            s = __fmaf_rn(dd, dd, s);
-          }
-          if (MASK) {
-            const int jj = j + k;
-            const bool ok = (jj < jlim) && (!diag || jj > r * kThreads + tid);
-            s = ok ? s : __int_as_float(0x7f800000);   // +inf -> e = 2^-inf = 0
-          }
-#pragma unroll
-          for (int c = 0; c < NB; ++c) {
-            const float e = ex2(__fmul_rn(s, p.kappa[c]));
-            a1[c] = __fadd_rn(a1[c], e);
-            a2[c] = __fmaf_rn(e, e, a2[c]);
-          }
+        for (int c = 0; c < NB; ++c) {
+          float q0, q1;
+          upk(mul2(s, pk(p.kappa[c], p.kappa[c])), q0, q1);
+          const f2 e = pk(ex2(q0), ex2(q1));
+          a1[c] = add2(a1[c], e);
+          a2[c] = fma2(e, e, a2[c]);
         }
       }
     }
@@ -314,29 +317,35 @@ struct FLscvScalar {
 
   __device__ __forceinline__ void outputs(double (&v)[NOUT]) const {
 #pragma unroll
-    for (int c = 0; c < NB; ++c) { v[2 * c] = a1[c]; v[2 * c + 1] = a2[c]; }
+    for (int c = 0; c < NB; ++c) {
+      float x0, x1, y0, y1;
+      upk(a1[c], x0, x1);
+      upk(a2[c], y0, y1);
+      v[2 * c] = (double)x0 + (double)x1;
+      v[2 * c + 1] = (double)y0 + (double)y1;
+    }
   }
 };
 
 // LSCV_H, d <= 4: per pair the differences v and the d(d+1)/2 monomials v_a v_b; per candidate
 // q = sum m_ab v_a v_b = -(log2 e / 4) v^T H^-1 v (the fun2 = x^T M x of Eq. 44-56 expanded in
 // monomials), e = 2^q = exp(-v^T H^-1 v / 4), e^2 = exp(-v^T H^-1 v / 2).
+// The thread's two rows are packed in fp32x2 lanes; coefficients are scalar broadcasts.
 template <int D_, int R_, int NB_>
 struct FLscvMono {
+  static_assert(R_ == 2, "rows are packed as one fp32x2 pair");
   static constexpr int NT = kThreads, D = D_, R = R_, T = kThreads * R_, NB = NB_, NOUT = 2 * NB_, MINB = 2;
   static constexpr int P = D * (D + 1) / 2;
   using Params = LscvMatrixParams;
-  float xr[D][R];
-  float a1[NB], a2[NB];
+  f2 xr[D];
+  f2 a1[NB], a2[NB];
 
   __device__ __forceinline__ void load_rows(const float* __restrict__ X, int64_t ld,
                                             int64_t i0) {
 #pragma unroll
-    for (int a = 0; a < D; ++a)
+    for (int a = 0; a < D; ++a) xr[a] = pk(__ldg(X + a * ld + i0), __ldg(X + a * ld + i0 + kThreads));
 #pragma unroll
-      for (int r = 0; r < R; ++r) xr[a][r] = __ldg(X + a * ld + i0 + r * kThreads);
-#pragma unroll
-    for (int c = 0; c < NB; ++c) a1[c] = a2[c] = 0.f;
+    for (int c = 0; c < NB; ++c) a1[c] = a2[c] = pk(0.f, 0.f);
   }
 
   template <bool MASK>
@@ -354,31 +363,34 @@ struct FLscvMono {
       }
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
+        f2 v[D];
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-          float v[D];
+        for (int a = 0; a < D; ++a) v[a] = sub2(xr[a], pk(cv[a][k], cv[a][k]));
+        f2 mono[P];
+        int t = 0;
 #pragma unroll
-          for (int a = 0; a < D; ++a) v[a] = __fsub_rn(xr[a][r], cv[a][k]);
-          float mono[P];
-          int t = 0;
+        for (int a = 0; a < D; ++a)
 #pragma unroll
-          for (int a = 0; a < D; ++a)
+          for (int b = a; b < D; ++b) mono[t++] = mul2(v[a], v[b]);
+        if (MASK) {
+          const int jj = j + k;
+          float m0, m1;
+          upk(mono[0], m0, m1);
+          const float inf = __int_as_float(0x7f800000);   // m_00 < 0 -> q = -inf -> e = 0
+          const bool ok0 = (jj < jlim) && (!diag || jj > tid);
+          const bool ok1 = (jj < jlim) && (!diag || jj > kThreads + tid);
+          mono[0] = pk(ok0 ? m0 : inf, ok1 ? m1 : inf);
+        }
 #pragma unroll
-            for (int b = a; b < D; ++b) mono[t++] = __fmul_rn(v[a], v[b]);
-          if (MASK) {
-            const int jj = j + k;
-            const bool ok = (jj < jlim) && (!diag || jj > r * kThreads + tid);
-            mono[0] = ok ? mono[0] : __int_as_float(0x7f800000);   // m_00 < 0 -> q = -inf
-          }
+        for (int c = 0; c < NB; ++c) {
+          f2 q = mul2(mono[0], pk(p.m[c * P], p.m[c * P]));
 #pragma unroll
-          for (int c = 0; c < NB; ++c) {
-            float q = __fmul_rn(mono[0], p.m[c * P]);
-#pragma unroll
-            for (int u = 1; u < P; ++u) q = __fmaf_rn(mono[u], p.m[c * P + u], q);
-            const float e = ex2(q);
-            a1[c] = __fadd_rn(a1[c], e);
-            a2[c] = __fmaf_rn(e, e, a2[c]);
-          }
+          for (int u = 1; u < P; ++u) q = fma2(mono[u], pk(p.m[c * P + u], p.m[c * P + u]), q);
+          float q0, q1;
+          upk(q, q0, q1);
+          const f2 e = pk(ex2(q0), ex2(q1));
+          a1[c] = add2(a1[c], e);
+          a2[c] = fma2(e, e, a2[c]);
         }
       }
     }
@@ -386,7 +398,13 @@ struct FLscvMono {
 
   __device__ __forceinline__ void outputs(double (&v)[NOUT]) const {
 #pragma unroll
-    for (int c = 0; c < NB; ++c) { v[2 * c] = a1[c]; v[2 * c + 1] = a2[c]; }
+    for (int c = 0; c < NB; ++c) {
+      float x0, x1, y0, y1;
+      upk(a1[c], x0, x1);
+      upk(a2[c], y0, y1);
+      v[2 * c] = (double)x0 + (double)x1;
+      v[2 * c + 1] = (double)y0 + (double)y1;
+    }
   }
 };
 

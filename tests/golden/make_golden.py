@@ -1,0 +1,99 @@
+"""Write the full-size golden values of the BASELINE.json configs with the fp64 oracle.
+
+Calls only oracle/ (and datagen for the seeded inputs).  Each JSON file records the workload,
+the oracle outputs and the PAPER.md passages they follow.  Run (CPU, all cores, ~1 h):
+
+    python tests/golden/make_golden.py [C4] [C2] [C3] [C5]
+"""
+from __future__ import annotations
+
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+
+import datagen  # noqa: E402
+import oracle   # noqa: E402
+
+THREADS = len(os.sched_getaffinity(0))
+
+
+def dump(name, obj):
+    with open(os.path.join(HERE, name), "w") as f:
+        json.dump(obj, f, indent=1)
+
+
+def c4():
+    x = datagen.config_data("C4")[0]
+    t0 = time.time()
+    tr = oracle.plugin(x, threads=THREADS)
+    dump("C4_plugin.json", {
+        "config": "C4", "workload": "PLUGIN, n=2^20, Marron-Wand #2 skewed mixture, datagen seed 4",
+        "cite": "PAPER.md P:203-256 (Sec. 4.4.1 steps 1-8, Eq. 11-18), reading Z1 for Eq. 15/17",
+        "trace": tr, "oracle_seconds": time.time() - t0, "threads": THREADS})
+
+
+def c2():
+    X = datagen.config_data("C2")
+    n = X.shape[1]
+    grid = oracle.lscv_h_grid(n, 1, 1024, 4.0)
+    t0 = time.time()
+    coarse = list(range(0, 1024, 32)) + [1023]
+    sc = oracle.lscv_h_scores(X, grid[coarse], threads=THREADS)
+    k0 = coarse[int(np.argmin(sc))]
+    fine = [k for k in range(max(0, k0 - 24), min(1024, k0 + 25)) if k not in coarse]
+    sf = oracle.lscv_h_scores(X, grid[fine], threads=THREADS)
+    idx = coarse + fine
+    vals = list(sc) + list(sf)
+    order = np.argsort(idx)
+    idx = [int(idx[i]) for i in order]
+    vals = [float(vals[i]) for i in order]
+    best = idx[int(np.argmin(vals))]
+    dump("C2_lscv_h.json", {
+        "config": "C2", "workload": "LSCV_h d=1, n=65536, MW#6 bimodal mixture, datagen seed 2, 1024-point grid",
+        "cite": "PAPER.md P:259-342 (Eq. 20-28), P:402-449 (Eq. 36-41); grid reading Z4, ties Z5",
+        "n_grid": 1024, "h0": oracle.lscv_h0(n, 1), "indices": idx, "h": [float(grid[k]) for k in idx],
+        "g": vals, "argmin_index_among_evaluated": best,
+        "note": "every 32nd grid point plus all points within +-24 of the coarse argmin",
+        "oracle_seconds": time.time() - t0, "threads": THREADS})
+
+
+def c3():
+    X = datagen.config_data("C3")
+    t0 = time.time()
+    trace = []
+    r = oracle.lscv_H_select(X, max_iter=500, tol=1e-7, threads=THREADS, trace=trace)
+    dump("C3_lscv_H.json", {
+        "config": "C3", "workload": "LSCV_H d=2, n=32768, correlated 2-component mixture, datagen seed 3",
+        "cite": "PAPER.md P:346-397 (Eq. 29-35), Nelder-Mead reading Z8",
+        "H_start": oracle.vech(r["H_start"]).tolist(), "vechH": r["x"].tolist(), "f": r["f"],
+        "iterations": r["iterations"], "stop": r["stop"],
+        "final_simplex": [v.tolist() for v in r["simplex"]], "final_fvals": list(map(float, r["fvals"])),
+        "evaluations": len(trace), "oracle_seconds": time.time() - t0, "threads": THREADS})
+
+
+def c5():
+    n = 1 << 18
+    X = datagen.config_data("C5")
+    cands = datagen.c5_candidates(n, 256)
+    pick = list(range(0, 256, 32))
+    t0 = time.time()
+    g = [oracle.lscv_H_score(X, cands[k], threads=THREADS) for k in pick]
+    dump("C5_lscv_H.json", {
+        "config": "C5", "workload": "LSCV_H d=4, n=2^18, 3-component mixture, datagen seed 5; 256 candidates",
+        "cite": "PAPER.md P:368-389 (Eq. 30-34)", "candidate_recipe": "datagen.c5_candidates(n, 256)",
+        "indices": pick, "vechH": [cands[k].tolist() for k in pick], "g": g,
+        "oracle_seconds": time.time() - t0, "threads": THREADS})
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["C4", "C2", "C3", "C5"]
+    for w in which:
+        print("golden", w, flush=True)
+        {"C4": c4, "C2": c2, "C3": c3, "C5": c5}[w]()
