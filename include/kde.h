@@ -169,6 +169,14 @@ kde_fixed kde_fixed_add(kde_fixed a, kde_fixed b);
  * column l and row q (q <= l) of the upper-triangular tile grid, column l holding l+1 tiles. */
 void kde_tile_coords(int64_t bx, int64_t *l, int64_t *q);
 
+/* The work partition the library uses for a sum of `kind` over n samples in d dimensions:
+ * tile edge T, total tiles of the upper-triangular grid, and the contiguous tile range
+ * [*tile_begin, *tile_end) that rank `rank` of `world` evaluates.  Pure host
+ * function (no GPU needed).  Returns KDE_E_INVALID for bad arguments. */
+kde_status kde_shard_tiles(kde_sum_kind kind, int64_t n, int32_t d, int32_t rank, int32_t world,
+                           int32_t *tile_edge, int64_t *tiles_total, int64_t *tile_begin,
+                           int64_t *tile_end);
+
 /* Kernel timing of the last call on this context: number of pair-kernel launches, their
  * summed device time (ms, CUDA events on the context stream) and the algorithmic pair-kernel
  * evaluations they performed (pairs i<j on this rank x candidates). */

@@ -32,7 +32,7 @@ EXPORTS = ["kde_create", "kde_destroy", "kde_last_error", "kde_nccl_unique_id",
            "kde_workspace_bytes", "kde_set_workspace", "kde_default_opts", "kde_psi_r",
            "kde_plugin_h", "kde_lscv_h_scores", "kde_lscv_H_scores", "kde_select_bandwidth",
            "kde_raw_sums", "kde_fixed_value", "kde_fixed_add", "kde_tile_coords",
-           "kde_last_profile", "kde_set_profiling"]
+           "kde_last_profile", "kde_set_profiling", "kde_shard_tiles"]
 
 
 class KDEError(RuntimeError):
@@ -102,6 +102,9 @@ def lib():
     L.kde_tile_coords.argtypes = [i64, ctypes.POINTER(i64), ctypes.POINTER(i64)]; L.kde_tile_coords.restype = None
     L.kde_last_profile.argtypes = [vp, ctypes.POINTER(i32), dp, dp, ctypes.POINTER(i32)]
     L.kde_set_profiling.argtypes = [vp, i32]
+    L.kde_shard_tiles.argtypes = [ctypes.c_int, i64, i32, i32, i32, ctypes.POINTER(i32), ctypes.POINTER(i64),
+                                  ctypes.POINTER(i64), ctypes.POINTER(i64)]
+    L.kde_shard_tiles.restype = ctypes.c_int
     for f in ("kde_create", "kde_nccl_unique_id", "kde_set_workspace", "kde_psi_r", "kde_plugin_h",
               "kde_lscv_h_scores", "kde_lscv_H_scores", "kde_select_bandwidth", "kde_raw_sums",
               "kde_last_profile", "kde_set_profiling"):
@@ -127,6 +130,16 @@ def fixed_value(f: Fixed) -> float:
 
 def fixed_add(a: Fixed, b: Fixed) -> Fixed:
     return lib().kde_fixed_add(a, b)
+
+
+def shard_tiles(kind: int, n: int, d: int, rank: int, world: int):
+    """(tile edge T, total tiles, first tile, end tile) of `rank`'s share (host-only query)."""
+    T, tot, b, e = ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    rc = lib().kde_shard_tiles(int(kind), int(n), int(d), int(rank), int(world), ctypes.byref(T),
+                               ctypes.byref(tot), ctypes.byref(b), ctypes.byref(e))
+    if rc != 0:
+        raise KDEError(rc, "bad shard query")
+    return T.value, tot.value, b.value, e.value
 
 
 def nccl_unique_id() -> bytes:

@@ -847,6 +847,29 @@ void kde_tile_coords(int64_t bx, int64_t* l, int64_t* q) {
   if (q) *q = b;
 }
 
+kde_status kde_shard_tiles(kde_sum_kind kind, int64_t n, int32_t d, int32_t rank, int32_t world,
+                           int32_t* tile_edge, int64_t* tiles_total, int64_t* tb, int64_t* te) {
+  if (n < 1 || d < 1 || d > kde::kMaxDim || world < 1 || rank < 0 || rank >= world) return KDE_E_INVALID;
+  Kind k;
+  switch (kind) {
+    case KDE_SUM_PSI4: k = Kind::Psi4; break;
+    case KDE_SUM_PSI6: k = Kind::Psi6; break;
+    case KDE_SUM_PSI8: k = Kind::Psi8; break;
+    case KDE_SUM_LSCV_h: k = Kind::LscvScalar; break;
+    case KDE_SUM_LSCV_H: k = Kind::LscvMatrix; break;
+    default: return KDE_E_INVALID;
+  }
+  const int T = kde::tile_for(k, d, n);
+  const int64_t tiles = n_tiles(n, T);
+  int64_t b, e;
+  shard_range(tiles, rank, world, &b, &e);
+  if (tile_edge) *tile_edge = T;
+  if (tiles_total) *tiles_total = tiles;
+  if (tb) *tb = b;
+  if (te) *te = e;
+  return KDE_OK;
+}
+
 double kde_fixed_value(const kde_fixed* v) { return v ? fixed_value(*v) : NAN; }
 
 kde_fixed kde_fixed_add(kde_fixed a, kde_fixed b) {

@@ -1,10 +1,19 @@
 #!/bin/bash
-# ncu evidence for the bench workload (run under gpurun; 1 GPU).
+# ncu evidence for every pair-kernel family (run under gpurun; 1 GPU). Output in gpurun_out/.
+# usage: tools/gpu_prof.sh [psi] [lscv]
 mkdir -p gpurun_out
-python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
+if [[ " $* " == *" psi "* || $# -eq 0 ]]; then
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv \
     python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/bench_under_ncu.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:pair_kernel -s 1 -c 2 \
-    -o gpurun_out/prof_psi -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_full.log 2>&1
-tail -3 gpurun_out/ncu_full.log
-ls -la gpurun_out
+ncu --set full --clock-control none --import-source on -k regex:pair_kernel -s 2 -c 2 \
+    -o gpurun_out/prof_psi -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_psi.log 2>&1
+fi
+if [[ " $* " == *" lscv "* || $# -eq 0 ]]; then
+ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:FLscvScalar -s 2 -c 1 \
+    -o gpurun_out/prof_c2 -f python tools/bench_configs.py C2 --reps 1 > gpurun_out/ncu_c2.log 2>&1
+ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:FLscvMono -s 2 -c 1 \
+    -o gpurun_out/prof_c5 -f python tools/bench_configs.py C5 --reps 1 > gpurun_out/ncu_c5.log 2>&1
+ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:FLscvMono -s 30 -c 1 \
+    -o gpurun_out/prof_c3 -f python tools/bench_configs.py C3 --reps 1 > gpurun_out/ncu_c3.log 2>&1
+fi
+ls -la gpurun_out/*.ncu-rep
