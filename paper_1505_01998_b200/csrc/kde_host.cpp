@@ -66,6 +66,9 @@ struct kde_ctx {
   size_t ext_bytes = 0;
   void* own_ws = nullptr;
   size_t own_bytes = 0;
+  // sorted copy of univariate samples (+ CUB temp), context-owned
+  void* sort_ws = nullptr;
+  size_t sort_bytes = 0;
   // pinned host staging for limbs
   long long* h_limbs = nullptr;
   size_t h_limbs_cap = 0;
@@ -332,6 +335,27 @@ kde_status gpu_moments(kde_ctx* c, const double* X, int64_t n, int d, Ws& w, Mom
   return KDE_OK;
 }
 
+// Sorted copy of n univariate samples (context-owned scratch); returns the device pointer.
+kde_status gpu_sorted(kde_ctx* c, const double* x, int64_t n, const double** out) {
+  const size_t tmp = kde::sort_temp_bytes(n);
+  const size_t need = align256((size_t)n * sizeof(double)) + align256(tmp);
+  if (c->sort_bytes < need) {
+    if (c->sort_ws) {
+      CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+      cudaFree(c->sort_ws);
+      c->sort_ws = nullptr;
+      c->sort_bytes = 0;
+    }
+    CUDA_TRY(c, cudaMalloc(&c->sort_ws, need));
+    c->sort_bytes = need;
+  }
+  double* xs = (double*)c->sort_ws;
+  void* temp = (char*)c->sort_ws + align256((size_t)n * sizeof(double));
+  CUDA_TRY(c, kde::launch_sort(x, xs, n, temp, tmp, c->stream));
+  *out = xs;
+  return KDE_OK;
+}
+
 // y = fp32(W (x - mean)), padded with zeros to ld.
 kde_status gpu_prep(kde_ctx* c, const double* X, int64_t n, int d, const std::vector<double>& W,
                     const std::vector<double>& mean, int64_t ld, Ws& w) {
@@ -473,12 +497,17 @@ Kind psi_kind(int r) { return r == 4 ? Kind::Psi4 : (r == 6 ? Kind::Psi6 : Kind:
 // Raw Psi sums S_r(g) = sum_{i<j} He_r(u) e^{-u^2/2} for each g (one prep + one launch per g).
 kde_status psi_raw(kde_ctx* c, const double* x, int64_t n, int r, const double* g, int ng,
                    const Moments& m, int shard_rank, int shard_world, bool allreduce,
-                   std::vector<kde_fixed>& out) {
+                   std::vector<kde_fixed>& out, bool presorted = false) {
   const int T = kde::tile_for(psi_kind(r), 1, n);
   const int64_t ld = (n + T - 1) / T * T;
   Ws w;
   TRY(get_ws(c, ld, 1, 1, &w));
   const int S = scale_exp_for(2.0 * std::fabs(he_at_zero(r)), n);
+  if (!presorted) {
+    const double* xs = nullptr;
+    TRY(gpu_sorted(c, x, n, &xs));
+    x = xs;
+  }
   out.clear();
   for (int k = 0; k < ng; ++k) {
     std::vector<double> W = {1.0 / g[k]};
@@ -805,6 +834,7 @@ void kde_destroy(kde_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream); else cudaDeviceSynchronize();
   if (c->comm) nccl().CommDestroy(c->comm);
   if (c->own_ws) cudaFree(c->own_ws);
+  if (c->sort_ws) cudaFree(c->sort_ws);
   if (c->h_limbs) cudaFreeHost(c->h_limbs);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   delete c;
@@ -916,12 +946,14 @@ static kde_status plugin_impl(kde_ctx* c, const double* x, int64_t n, kde_plugin
   t.psi8_ns = 105.0 / (32.0 * std::sqrt(kPi) * std::pow(t.sigma_hat, 9));  // step 3, Eq. 13
   const double K6_0 = -15.0 / s2p, K4_0 = 3.0 / s2p, mu2 = 1.0;
   t.g1 = std::pow(-2.0 * K6_0 / (mu2 * t.psi8_ns * nn), 1.0 / 9.0);      // step 4, Eq. 14
+  const double* xs = nullptr;                                             // sorted once (§3)
+  TRY(gpu_sorted(c, x, n, &xs));
   std::vector<kde_fixed> o;
-  TRY(psi_raw(c, x, n, 6, &t.g1, 1, m, c->rank, c->world, true, o));     // step 5, Eq. 15
+  TRY(psi_raw(c, xs, n, 6, &t.g1, 1, m, c->rank, c->world, true, o, true));  // step 5, Eq. 15
   t.psi6 = psi_finalize(6, n, t.g1, fixed_value(o[0]));
   if (!(t.psi6 < 0.0)) return fail(c, KDE_E_NUMERIC, "Psi6-hat >= 0");
   t.g2 = std::pow(-2.0 * K4_0 / (mu2 * t.psi6 * nn), 1.0 / 7.0);         // step 6, Eq. 16
-  TRY(psi_raw(c, x, n, 4, &t.g2, 1, m, c->rank, c->world, true, o));     // step 7, Eq. 17
+  TRY(psi_raw(c, xs, n, 4, &t.g2, 1, m, c->rank, c->world, true, o, true));  // step 7, Eq. 17
   t.psi4 = psi_finalize(4, n, t.g2, fixed_value(o[0]));
   if (!(t.psi4 > 0.0)) return fail(c, KDE_E_NUMERIC, "Psi4-hat <= 0");
   const double RK = 1.0 / (2.0 * std::sqrt(kPi));

@@ -62,6 +62,9 @@ cudaError_t launch_reduce_parts(const double* part, int nblk, int width, double*
 cudaError_t launch_prep(const double* X, int64_t n, int d, const double* W_dev,
                         const double* mean_dev, float* Y, int64_t ld, cudaStream_t s);
 int moments_blocks(int64_t n);
+size_t sort_temp_bytes(int64_t n);
+cudaError_t launch_sort(const double* in, double* out, int64_t n, void* temp, size_t temp_bytes,
+                        cudaStream_t s);
 
 // Host/device tile map (Eq. 42-43 + integer fix-up).
 void tile_coords_host(int64_t bx, int64_t* l, int64_t* q);

@@ -18,6 +18,10 @@
 #include <stdint.h>
 #include <stdlib.h>
 
+#include <type_traits>
+
+#include <cub/device/device_radix_sort.cuh>
+
 #include "kde_internal.h"
 
 namespace kde {
@@ -169,16 +173,21 @@ template <int RORD, int NT_>
 struct FPsi {
   static constexpr int NT = NT_, D = 1, R = 8, T = NT_ * 8, NOUT = 1, CH = 256, MINB = 3;
   static constexpr int NP = R / 2;   // row pairs (r = 2p, 2p+1) packed into fp32x2 lanes
+  static constexpr int G = 16;       // columns per compensated group
   using Params = PsiParams;
   f2 xr[NP];
   double acc;
 
+  // Rows are interleaved: thread t owns rows q*T + 8t + r, r = 0..7.  The data are sorted
+  // (kde_host.cpp), so the 8 accumulator classes r see statistically identical distances.
   __device__ __forceinline__ void load_rows(const float* __restrict__ X, int64_t ld,
                                             int64_t i0) {
-#pragma unroll
-    for (int p = 0; p < NP; ++p) xr[p] = pk(__ldg(X + i0 + (2 * p) * NT), __ldg(X + i0 + (2 * p + 1) * NT));
+    const float4* p = reinterpret_cast<const float4*>(X + i0);
+    const float4 u = __ldg(p), v = __ldg(p + 1);
+    xr[0] = pk(u.x, u.y); xr[1] = pk(u.z, u.w); xr[2] = pk(v.x, v.y); xr[3] = pk(v.z, v.w);
     acc = 0.0;
   }
+  static __device__ __forceinline__ int64_t row0(int64_t q) { return q * T + 8 * (int64_t)threadIdx.x; }
 
   // He_r(s) by Horner with exact integer coefficients, two lanes at once.
   __device__ __forceinline__ f2 poly(f2 s) const {
@@ -191,48 +200,57 @@ struct FPsi {
   // MUFU offset of accumulator class r (= row slot): off_r = 16 + r/8 (see the comment above).
   static __device__ __forceinline__ float off(int r) { return 16.0f + 0.125f * (float)r; }
 
-  // Accumulation: the 4 terms of one float4 column group of a row are summed in
-  // fp32, then added to the row's running sum with Fast2Sum (the rounding error goes to a
-  // compensation register).  A plain fp32 running sum drops the one-signed far-pair tail terms
+  // Accumulation: the G = 16 terms of one column group of a row are summed in
+  // fp32 (sorted data: the terms of a group have similar magnitude), then added to the row's
+  // running sum with Fast2Sum (rounding error kept in a compensation register); fp64 flush
+  // every 256 columns.  A plain fp32 running sum drops the one-signed far-pair tail terms
   // (~1e-7..1e-6) next to near-pair sums (~10): measured -1.4e-5 relative at T=2048.
   template <bool MASK>
   __device__ __forceinline__ void compute(const float* __restrict__ sc, const Params& p, bool diag,
                                           int jlim) {
-    const int tid = threadIdx.x;
+    const int ib = 8 * threadIdx.x;   // local index of row r is ib + r
     const f2 c0 = pk(p.c[0], p.c[0]);
     for (int jc = 0; jc < T; jc += CH) {
       if (MASK && jc >= jlim) break;
       f2 a[NP], cmp[NP];
 #pragma unroll
       for (int q = 0; q < NP; ++q) a[q] = cmp[q] = pk(0.f, 0.f);
-#pragma unroll 2
-      for (int j = jc; j < jc + CH; j += 4) {
-        const float4 c4 = *reinterpret_cast<const float4*>(sc + j);
-        const float cv[4] = {c4.x, c4.y, c4.z, c4.w};
+#pragma unroll 1
+      for (int j = jc; j < jc + CH; j += G) {
+        f2 grp[NP];
 #pragma unroll
-        for (int q = 0; q < NP; ++q) {
-          const f2 noff = pk(-off(2 * q), -off(2 * q + 1));
-          f2 grp = pk(0.f, 0.f);
+        for (int q = 0; q < NP; ++q) grp[q] = pk(0.f, 0.f);
+#pragma unroll
+        for (int j4 = 0; j4 < G; j4 += 4) {
+          const float4 c4 = *reinterpret_cast<const float4*>(sc + j + j4);
+          const float cv[4] = {c4.x, c4.y, c4.z, c4.w};
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            const f2 d = sub2(xr[q], pk(cv[k], cv[k]));
-            f2 sq = mul2(d, d);
-            if (MASK) {
-              const int jj = j + k;
-              float s0, s1;
-              upk(sq, s0, s1);
-              const bool ok0 = (jj < jlim) && (!diag || jj > (2 * q) * NT + tid);
-              const bool ok1 = (jj < jlim) && (!diag || jj > (2 * q + 1) * NT + tid);
-              sq = pk(ok0 ? s0 : 1.0e4f, ok1 ? s1 : 1.0e4f);   // 2^(-7229) == 0; poly finite
+#pragma unroll
+            for (int q = 0; q < NP; ++q) {
+              const f2 noff = pk(-off(2 * q), -off(2 * q + 1));
+              const f2 d = sub2(xr[q], pk(cv[k], cv[k]));
+              f2 sq = mul2(d, d);
+              if (MASK) {
+                const int jj = j + j4 + k;
+                float s0, s1;
+                upk(sq, s0, s1);
+                const bool ok0 = (jj < jlim) && (!diag || jj > ib + 2 * q);
+                const bool ok1 = (jj < jlim) && (!diag || jj > ib + 2 * q + 1);
+                sq = pk(ok0 ? s0 : 1.0e4f, ok1 ? s1 : 1.0e4f);   // 2^(-7229) == 0; poly finite
+              }
+              float a0, a1;
+              upk(fma2(sq, c0, noff), a0, a1);
+              const f2 e = pk(ex2(a0), ex2(a1));
+              grp[q] = fma2(poly(sq), e, grp[q]);
             }
-            float a0, a1;
-            upk(fma2(sq, c0, noff), a0, a1);
-            const f2 e = pk(ex2(a0), ex2(a1));
-            grp = (k == 0) ? mul2(poly(sq), e) : fma2(poly(sq), e, grp);
           }
-          const f2 s2 = add2(a[q], grp);                    // Fast2Sum(a, grp), per lane
+        }
+#pragma unroll
+        for (int q = 0; q < NP; ++q) {
+          const f2 s2 = add2(a[q], grp[q]);                 // Fast2Sum(a, grp), per lane
           const f2 z = sub2(s2, a[q]);
-          cmp[q] = add2(cmp[q], sub2(grp, z));
+          cmp[q] = add2(cmp[q], sub2(grp[q], z));
           a[q] = s2;
         }
       }
@@ -465,6 +483,17 @@ struct FLscvChol {
 
 // ------------------------------------------------------------------ the persistent pair kernel
 
+// First row index a thread loads for row-block q (functors may interleave rows).
+template <class F, class = void>
+struct HasRow0 : std::false_type {};
+template <class F>
+struct HasRow0<F, decltype((void)F::row0(0))> : std::true_type {};
+template <class F>
+__device__ __forceinline__ int64_t row_origin(int64_t q) {
+  if constexpr (HasRow0<F>::value) return F::row0(q);
+  else return q * F::T + threadIdx.x;
+}
+
 template <class F>
 __global__ void __launch_bounds__(F::NT, F::MINB) pair_kernel(const Args a,
                                                         const __grid_constant__ typename F::Params p) {
@@ -502,7 +531,7 @@ __global__ void __launch_bounds__(F::NT, F::MINB) pair_kernel(const Args a,
     if (tid == 0 && tn < a.tile_end) issue(tn, (k + 1) & 1);
 
     F f;
-    f.load_rows(a.X, a.ld, q * T + tid);
+    f.load_rows(a.X, a.ld, row_origin<F>(q));
     mbar_wait(&bar[k & 1], (k >> 1) & 1);
     const float* sc = cols + (k & 1) * D * T;
     const bool diag = (q == l);
@@ -726,6 +755,20 @@ __global__ void prep_kernel(const double* __restrict__ X, int64_t n, int d,
       for (int a = 0; a < d; ++a) Y[a * ld + i] = 0.f;
     }
   }
+}
+
+// Ascending sort of n fp64 samples (CUB radix sort, keys only: deterministic).  The pair sums
+// are invariant under permutation; sorted input keeps the term magnitudes inside a column
+// group homogeneous, which makes the fp32 group sums of FPsi nearly lossless.
+size_t sort_temp_bytes(int64_t n) {
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortKeys(nullptr, bytes, (const double*)nullptr, (double*)nullptr, (int)n);
+  return bytes;
+}
+
+cudaError_t launch_sort(const double* in, double* out, int64_t n, void* temp, size_t temp_bytes,
+                        cudaStream_t s) {
+  return cub::DeviceRadixSort::SortKeys(temp, temp_bytes, in, out, (int)n, 0, 64, s);
 }
 
 cudaError_t launch_prep(const double* X, int64_t n, int d, const double* W_dev,
