@@ -144,6 +144,25 @@ kde_status kde_lscv_H_scores(kde_ctx *ctx, const double *X_dev, int64_t n, int32
 kde_status kde_select_bandwidth(kde_ctx *ctx, kde_method method, const double *X_dev, int64_t n,
                                 int32_t d, const kde_select_opts *opts_or_null, kde_bandwidth *out);
 
+/* ---------------------------------------------------------------- using the bandwidth (f2) */
+
+/* KDE evaluation (Eq. kde-def-H / K_H / gaussian): for each query y_q (column q of
+ * the d x m row-major DEVICE array Y_dev),
+ *   f_host[q] = n^-1 sum_i |H|^{-1/2} (2 pi)^{-d/2} exp(-1/2 (y_q - X_i)^T H^-1 (y_q - X_i)).
+ * vechH_host: d(d+1)/2 doubles; the scalar-h estimator of Eq. kde-def is H = h^2 I.
+ * Non-positive-definite H -> KDE_E_NONPOSITIVE_BW.  With world > 1 every rank computes all m
+ * values (no collective). */
+kde_status kde_evaluate(kde_ctx *ctx, const double *X_dev, int64_t n, int32_t d, const double *Y_dev,
+                        int64_t m, const double *vechH_host, double *f_host);
+
+/* Approximate aggregates over a range, univariate (Eq. count, Eq. sum): for interval
+ * q = [lo_host[q], hi_host[q]],  COUNT = n int fhat,  SUM = n int x fhat,  AVG = SUM/COUNT, with
+ * fhat the Gaussian KDE of bandwidth h (closed forms of the integrals, fp64).  Any of the three
+ * output arrays may be NULL. */
+kde_status kde_aqp_1d(kde_ctx *ctx, const double *x_dev, int64_t n, double h, const double *lo_host,
+                      const double *hi_host, int32_t n_q, double *count_host, double *sum_host,
+                      double *avg_host);
+
 /* ---------------------------------------------------------------- lower level (tests, tools) */
 
 typedef enum {

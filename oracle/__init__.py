@@ -55,9 +55,10 @@ def lib():
         L.oracle_lscv_h_modified.argtypes = [dp, i64, i32, dp, f64, dp, i32, dp]
         L.oracle_mean_cov.argtypes = [dp, i64, i32, dp, dp]
         L.oracle_tile_enumerate.argtypes = [i64, ip, ip]
+        L.oracle_kde_eval.argtypes = [dp, i64, i32, dp, i64, dp, f64, dp]
         for f in ("oracle_psi_pairsum_rows", "oracle_psi_r", "oracle_lscv_h_pairsums_rows",
                   "oracle_lscv_H_pairsums_rows", "oracle_lscv_h_modified", "oracle_mean_cov",
-                  "oracle_tile_enumerate"):
+                  "oracle_tile_enumerate", "oracle_kde_eval"):
             getattr(L, f).restype = i32
         _lib = L
     return _lib
@@ -496,3 +497,40 @@ def tile_enumerate(count: int):
     _check(lib().oracle_tile_enumerate(count, l.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
                                        q.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))), "tiles")
     return l, q
+
+
+# --------------------------------------------------------------------------- KDE evaluation / AQP
+def kde_eval(X, Y, H):
+    """fhat(y) for each column y of Y (Eq. kde-def-H / K_H / gaussian).  H is a d x d
+    matrix or its vech; the scalar-h estimator of Eq. kde-def is H = h^2 I."""
+    X = _as_X(X)
+    d, n = X.shape
+    Y = np.ascontiguousarray(np.asarray(Y, float).reshape(d, -1))
+    m = Y.shape[1]
+    H = np.asarray(H, float)
+    if H.ndim == 1:
+        H = unvech(H, d)
+    if cholesky_pd(H) is None:
+        raise ValueError("H not positive definite")
+    Hinv, det = gauss_jordan(H)
+    Hinv = np.ascontiguousarray(Hinv)
+    f = np.zeros(m)
+    _check(lib().oracle_kde_eval(_dp(X), n, d, _dp(Y), m, _dp(Hinv), det, _dp(f)), "kde_eval")
+    return f
+
+
+def aqp_1d(x, h, a, b, epsrel=1e-12):
+    """Approximate COUNT, SUM, AVG of the records with a <= x <= b (Eq. count, sum):
+    COUNT = n * integral_a^b fhat(t) dt,  SUM = n * integral_a^b t fhat(t) dt,  AVG = SUM/COUNT,
+    fhat the scalar-h Gaussian KDE (Eq. kde-def).  The integrals are done by adaptive
+    quadrature (scipy.integrate.quad) of the oracle's own fhat, as the paper allows."""
+    import scipy.integrate as si
+    x = np.asarray(x, float).ravel()
+    n = x.size
+    f = lambda t: float(kde_eval(x[None, :], np.array([[t]]), [h * h])[0])
+    # split the interval at the sample-dense points to help quad
+    pts = np.linspace(a, b, 9)
+    cnt = sum(si.quad(f, p0, p1, epsabs=0, epsrel=epsrel, limit=200)[0] for p0, p1 in zip(pts[:-1], pts[1:]))
+    sm = sum(si.quad(lambda t: t * f(t), p0, p1, epsabs=1e-300, epsrel=epsrel, limit=200)[0]
+             for p0, p1 in zip(pts[:-1], pts[1:]))
+    return n * cnt, n * sm, (sm / cnt if cnt != 0 else float("nan"))

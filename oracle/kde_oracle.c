@@ -186,3 +186,22 @@ int oracle_tile_enumerate(int64_t count, int64_t *l, int64_t *q) {
     for (int64_t row = 0; row <= col && bx < count; ++row, ++bx) { l[bx] = col; q[bx] = row; }
   return 0;
 }
+
+/* KDE evaluation (Eq. kde-def-H, K_H, gaussian):
+ *   fhat(y) = n^-1 sum_i |H|^{-1/2} (2 pi)^{-d/2} exp(-1/2 (y - X_i)^T H^-1 (y - X_i)),
+ * for m query points Y (d x m row-major); Hinv row-major, detH = |H|.  Plain double loop. */
+int oracle_kde_eval(const double *X, int64_t n, int d, const double *Y, int64_t m,
+                    const double *Hinv, double detH, double *f) {
+  if (!X || !Y || !Hinv || !f || n < 1 || m < 0 || d < 1 || d > 16 || !(detH > 0.0)) return 1;
+  double v[16];
+  const double c = pow(2.0 * ORACLE_PI, -0.5 * d) / sqrt(detH);
+  for (int64_t q = 0; q < m; ++q) {
+    nsum a = {0.0, 0.0};
+    for (int64_t i = 0; i < n; ++i) {
+      for (int k = 0; k < d; ++k) v[k] = Y[k * m + q] - X[k * n + i];
+      nadd(&a, c * exp(-0.5 * qform(v, Hinv, d)));
+    }
+    f[q] = (a.s + a.c) / (double)n;
+  }
+  return 0;
+}

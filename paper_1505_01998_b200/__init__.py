@@ -32,7 +32,7 @@ EXPORTS = ["kde_create", "kde_destroy", "kde_last_error", "kde_nccl_unique_id",
            "kde_workspace_bytes", "kde_set_workspace", "kde_default_opts", "kde_psi_r",
            "kde_plugin_h", "kde_lscv_h_scores", "kde_lscv_H_scores", "kde_select_bandwidth",
            "kde_raw_sums", "kde_fixed_value", "kde_fixed_add", "kde_tile_coords",
-           "kde_last_profile", "kde_set_profiling", "kde_shard_tiles"]
+           "kde_last_profile", "kde_set_profiling", "kde_shard_tiles", "kde_evaluate", "kde_aqp_1d"]
 
 
 class KDEError(RuntimeError):
@@ -105,6 +105,10 @@ def lib():
     L.kde_shard_tiles.argtypes = [ctypes.c_int, i64, i32, i32, i32, ctypes.POINTER(i32), ctypes.POINTER(i64),
                                   ctypes.POINTER(i64), ctypes.POINTER(i64)]
     L.kde_shard_tiles.restype = ctypes.c_int
+    L.kde_evaluate.argtypes = [vp, vp, i64, i32, vp, i64, dp, dp]
+    L.kde_evaluate.restype = ctypes.c_int
+    L.kde_aqp_1d.argtypes = [vp, vp, i64, f64, dp, dp, i32, dp, dp, dp]
+    L.kde_aqp_1d.restype = ctypes.c_int
     for f in ("kde_create", "kde_nccl_unique_id", "kde_set_workspace", "kde_psi_r", "kde_plugin_h",
               "kde_lscv_h_scores", "kde_lscv_H_scores", "kde_select_bandwidth", "kde_raw_sums",
               "kde_last_profile", "kde_set_profiling"):
@@ -295,6 +299,34 @@ class Context:
         if method == PLUGIN:
             out["trace"] = r.trace.as_dict()
         return out
+
+    def evaluate(self, X, Y, H) -> np.ndarray:
+        """fhat at the columns of Y (both CUDA tensors, d x n and d x m); H: d x d or vech."""
+        Xd, Yd = _dev_matrix(X), _dev_matrix(Y)
+        d = Xd.shape[0]
+        if Yd.shape[0] != d:
+            raise KDEError(7, "query dimension differs from the sample dimension")
+        Hn = np.asarray(H, dtype=np.float64)
+        vh = Hn if Hn.ndim == 1 else np.array([Hn[i, j] for j in range(d) for i in range(j, d)])
+        vb, vp = _dbuf(vh)
+        out = np.zeros(Yd.shape[1])
+        self._check(lib().kde_evaluate(self._h, ctypes.c_void_p(Xd.data_ptr()), Xd.shape[1], d,
+                                       ctypes.c_void_p(Yd.data_ptr()), Yd.shape[1], vp,
+                                       out.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
+        return out
+
+    def aqp_1d(self, x, h: float, lo, hi):
+        """(COUNT, SUM, AVG) arrays over the intervals [lo_q, hi_q] (univariate)."""
+        Xd = _dev_matrix(x)
+        if Xd.shape[0] != 1:
+            raise KDEError(2, "AQP closed forms are univariate")
+        lb, lp = _dbuf(np.atleast_1d(lo))
+        hb, hp = _dbuf(np.atleast_1d(hi))
+        cnt, sm, av = (np.zeros(lb.size) for _ in range(3))
+        P = lambda a: a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+        self._check(lib().kde_aqp_1d(self._h, ctypes.c_void_p(Xd.data_ptr()), Xd.shape[1], float(h), lp, hp,
+                                     lb.size, P(cnt), P(sm), P(av)))
+        return cnt, sm, av
 
     def raw_sums(self, kind: int, X, cand, shard=None):
         """Exact fixed-point pair sums (list of Fixed).  shard=(rank, world) computes one shard

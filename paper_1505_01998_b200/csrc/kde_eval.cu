@@ -1,0 +1,251 @@
+// kde_eval.cu — KDE evaluation at query points and univariate AQP aggregates.
+//
+// fhat(y_q) = n^-1 |H|^{-1/2} (2 pi)^{-d/2} sum_i exp(-1/2 (y_q - X_i)^T H^-1 (y_q - X_i))
+// (Eq. kde-def-H, K_H, gaussian: P:114-140) over a rectangle of m queries x n samples.  Both sets
+// are whitened on the device, y' = W (y - mu), x' = W (x - mu) with W^T W = (log2 e / 2) H^-1,
+// so every term is 2^-|y' - x'|^2: D sub + D FMA + one MUFU.EX2 per (query, sample).
+//
+// Work unit = (block of 512 query rows, contiguous split of the sample columns).  A unit streams
+// its column tiles through shared memory with TMA bulk copies (double-buffered on mbarriers),
+// keeps two query rows per thread packed in fp32x2 lanes, sums 16-column groups in fp32 and adds
+// them with Fast2Sum, then writes one fp64 partial per (split, row).  A second kernel adds the
+// splits in a fixed order: results do not depend on the grid size.  Terms are all positive (no
+// cancellation), so MUFU.EX2's bias needs no offset scheme here.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "kde_device.cuh"
+#include "kde_internal.h"
+
+namespace kde {
+
+constexpr int kEvNT = 256;            // threads per CTA
+constexpr int kEvRows = 2 * kEvNT;    // query rows per unit (2 per thread, packed)
+constexpr int kEvTC = 1024;           // sample columns per tile
+constexpr int kEvG = 16;              // columns per compensated group
+
+struct EvalArgs {
+  const float* Y;     // D x ldm whitened queries (padded with 0)
+  const float* X;     // D x ldn whitened samples (padded with +inf -> term 0)
+  int64_t m, ldm, ldn;
+  int row_blocks, splits, tiles_per_split, n_tiles;
+  double* part;       // [splits][ldm]
+};
+
+template <int D>
+__global__ void __launch_bounds__(kEvNT, 2) eval_kernel(const EvalArgs a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* cols = reinterpret_cast<float*>(smem_raw);                        // [2][D][TC]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(cols + 2 * D * kEvTC);      // [2]
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  auto issue = [&](int tile, int buf) {
+    float* dst = cols + buf * D * kEvTC;
+    mbar_expect_tx(&bar[buf], (uint32_t)(D * kEvTC * sizeof(float)));
+#pragma unroll
+    for (int d = 0; d < D; ++d)
+      tma_load_1d(dst + d * kEvTC, a.X + d * a.ldn + (int64_t)tile * kEvTC,
+                  (uint32_t)(kEvTC * sizeof(float)), &bar[buf]);
+  };
+
+  const int units = a.row_blocks * a.splits;
+  uint32_t k = 0;   // running tile counter of this CTA (buffer = k & 1, parity = (k >> 1) & 1)
+  for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    const int rb = u % a.row_blocks, cs = u / a.row_blocks;
+    const int t0 = cs * a.tiles_per_split;
+    const int t1 = min(a.n_tiles, t0 + a.tiles_per_split);
+    if (t0 >= t1) continue;
+    __syncthreads();   // previous unit finished reading both buffers
+    if (tid == 0) issue(t0, k & 1);
+    const int64_t r0 = (int64_t)rb * kEvRows + tid;
+    f2 y[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) y[d] = pk(__ldg(a.Y + d * a.ldm + r0), __ldg(a.Y + d * a.ldm + r0 + kEvNT));
+    f2 acc = pk(0.f, 0.f), cmp = pk(0.f, 0.f);
+    for (int t = t0; t < t1; ++t, ++k) {
+      if (tid == 0 && t + 1 < t1) issue(t + 1, (k + 1) & 1);
+      mbar_wait(&bar[k & 1], (k >> 1) & 1);
+      const float* sc = cols + (k & 1) * D * kEvTC;
+#pragma unroll 1
+      for (int j = 0; j < kEvTC; j += kEvG) {
+        f2 grp = pk(0.f, 0.f);
+#pragma unroll
+        for (int j4 = 0; j4 < kEvG; j4 += 4) {
+          float cv[D][4];
+#pragma unroll
+          for (int d = 0; d < D; ++d) {
+            const float4 c4 = *reinterpret_cast<const float4*>(sc + d * kEvTC + j + j4);
+            cv[d][0] = c4.x; cv[d][1] = c4.y; cv[d][2] = c4.z; cv[d][3] = c4.w;
+          }
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            f2 v = sub2(y[0], pk(cv[0][kk], cv[0][kk]));
+            f2 s = mul2(v, v);
+#pragma unroll
+            for (int d = 1; d < D; ++d) {
+              v = sub2(y[d], pk(cv[d][kk], cv[d][kk]));
+              s = fma2(v, v, s);
+            }
+            float s0, s1;
+            upk(s, s0, s1);
+            grp = add2(grp, pk(ex2(-s0), ex2(-s1)));
+          }
+        }
+        const f2 s2 = add2(acc, grp);          // Fast2Sum(acc, grp): terms > 0, acc grows
+        cmp = add2(cmp, sub2(grp, sub2(s2, acc)));
+        acc = s2;
+      }
+      __syncthreads();   // all threads done with this buffer before it is refilled
+    }
+    float a0, a1, c0, c1;
+    upk(acc, a0, a1);
+    upk(cmp, c0, c1);
+    a.part[(int64_t)cs * a.ldm + r0] = (double)a0 + (double)c0;
+    a.part[(int64_t)cs * a.ldm + r0 + kEvNT] = (double)a1 + (double)c1;
+  }
+}
+
+__global__ void eval_reduce_kernel(const double* __restrict__ part, int splits, int64_t ldm,
+                                   int64_t m, double scale, double* __restrict__ out) {
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < m; q += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int c = 0; c < splits; ++c) s += part[(int64_t)c * ldm + q];
+    out[q] = s * scale;
+  }
+}
+
+int eval_rows_per_block() { return kEvRows; }
+int eval_cols_per_tile() { return kEvTC; }
+
+template <int D>
+static cudaError_t launch_eval_d(const EvalLaunch& c) {
+  const size_t smem = 2 * D * kEvTC * sizeof(float) + 16;
+  static int occ = -1;
+  if (occ < 0) {
+    cudaError_t e = cudaFuncSetAttribute(eval_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int o = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, eval_kernel<D>, kEvNT, smem);
+    if (e != cudaSuccess) return e;
+    occ = o > 0 ? o : 1;
+  }
+  EvalArgs a;
+  a.Y = c.Y; a.X = c.X; a.m = c.m; a.ldm = c.ldm; a.ldn = c.ldn;
+  a.row_blocks = (int)(c.ldm / kEvRows);
+  a.n_tiles = (int)(c.ldn / kEvTC);
+  // split the columns so that there are >= 2 waves of units (deterministic for given m, n, SMs)
+  const int target = 2 * c.sm_count * occ;
+  int splits = (target + a.row_blocks - 1) / a.row_blocks;
+  if (splits > a.n_tiles) splits = a.n_tiles;
+  if (splits < 1) splits = 1;
+  a.tiles_per_split = (a.n_tiles + splits - 1) / splits;
+  a.splits = (a.n_tiles + a.tiles_per_split - 1) / a.tiles_per_split;
+  a.part = c.part;
+  if ((size_t)a.splits * (size_t)c.ldm > c.part_capacity) return cudaErrorInvalidValue;
+  const int units = a.row_blocks * a.splits;
+  int grid = c.sm_count * occ;
+  if (grid > units) grid = units;
+  eval_kernel<D><<<grid, kEvNT, smem, c.stream>>>(a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  int blocks = (int)((c.m + 255) / 256);
+  if (blocks > 4096) blocks = 4096;
+  if (blocks < 1) blocks = 1;
+  eval_reduce_kernel<<<blocks, 256, 0, c.stream>>>(c.part, a.splits, c.ldm, c.m, c.scale, c.out);
+  return cudaGetLastError();
+}
+
+int eval_max_splits(int sm_count) { return 2 * sm_count * 8; }
+
+cudaError_t launch_eval(int d, const EvalLaunch& c) {
+  switch (d) {
+    case 1: return launch_eval_d<1>(c);   case 2: return launch_eval_d<2>(c);
+    case 3: return launch_eval_d<3>(c);   case 4: return launch_eval_d<4>(c);
+    case 5: return launch_eval_d<5>(c);   case 6: return launch_eval_d<6>(c);
+    case 7: return launch_eval_d<7>(c);   case 8: return launch_eval_d<8>(c);
+    case 9: return launch_eval_d<9>(c);   case 10: return launch_eval_d<10>(c);
+    case 11: return launch_eval_d<11>(c); case 12: return launch_eval_d<12>(c);
+    case 13: return launch_eval_d<13>(c); case 14: return launch_eval_d<14>(c);
+    case 15: return launch_eval_d<15>(c); case 16: return launch_eval_d<16>(c);
+  }
+  return cudaErrorInvalidValue;
+}
+
+// ------------------------------------------------------------------ univariate AQP
+// For the Gaussian kernel the integrals of Eq. count / Eq. sum have closed forms per sample:
+//   n int_a^b fhat = sum_i [Phi(beta_i) - Phi(alpha_i)],
+//   n int_a^b t fhat = sum_i [x_i (Phi(beta_i) - Phi(alpha_i)) + h (phi(alpha_i) - phi(beta_i))],
+// alpha_i = (a - x_i)/h, beta_i = (b - x_i)/h; evaluated in fp64 (erfc tail form, no
+// cancellation) with a fixed-order block reduction.
+constexpr int kAqpThreads = 256;
+
+__device__ __forceinline__ double phi_diff(double al, double be) {
+  const double r = 0.70710678118654752440;   // 1/sqrt(2)
+  if (al > 0.0) return 0.5 * (erfc(al * r) - erfc(be * r));
+  if (be < 0.0) return 0.5 * (erfc(-be * r) - erfc(-al * r));
+  return 1.0 - 0.5 * (erfc(-al * r) + erfc(be * r));
+}
+
+__global__ void __launch_bounds__(kAqpThreads) aqp_kernel(const double* __restrict__ x, int64_t n,
+                                                          double h, const double* __restrict__ lo,
+                                                          const double* __restrict__ hi,
+                                                          double* __restrict__ part) {
+  __shared__ double red[kAqpThreads / 32][2];
+  const int q = blockIdx.y;
+  const double a = lo[q], b = hi[q], ih = 1.0 / h;
+  const double k = 0.39894228040143267794;   // 1/sqrt(2 pi)
+  double c = 0.0, s = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * kAqpThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kAqpThreads) {
+    const double xi = x[i];
+    const double al = (a - xi) * ih, be = (b - xi) * ih;
+    const double p = phi_diff(al, be);
+    c += p;
+    s += xi * p + h * k * (exp(-0.5 * al * al) - exp(-0.5 * be * be));
+  }
+  c = warp_sum(c);
+  s = warp_sum(s);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) { red[w][0] = c; red[w][1] = s; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double cc = 0.0, ss = 0.0;
+    for (int ww = 0; ww < kAqpThreads / 32; ++ww) { cc += red[ww][0]; ss += red[ww][1]; }
+    part[((int64_t)q * gridDim.x + blockIdx.x) * 2 + 0] = cc;
+    part[((int64_t)q * gridDim.x + blockIdx.x) * 2 + 1] = ss;
+  }
+}
+
+__global__ void aqp_reduce_kernel(const double* __restrict__ part, int nblk, int nq, double* __restrict__ out) {
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += gridDim.x * blockDim.x) {
+    double c = 0.0, s = 0.0;
+    for (int b = 0; b < nblk; ++b) { c += part[((int64_t)q * nblk + b) * 2]; s += part[((int64_t)q * nblk + b) * 2 + 1]; }
+    out[2 * q] = c;
+    out[2 * q + 1] = s;
+  }
+}
+
+int aqp_blocks(int64_t n) {
+  int64_t b = (n + 4 * kAqpThreads - 1) / (4 * kAqpThreads);
+  if (b > 256) b = 256;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+cudaError_t launch_aqp(const double* x, int64_t n, double h, const double* lo, const double* hi, int nq,
+                       double* part, int nblk, double* out, cudaStream_t s) {
+  dim3 grid(nblk, nq);
+  aqp_kernel<<<grid, kAqpThreads, 0, s>>>(x, n, h, lo, hi, part);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  aqp_reduce_kernel<<<(nq + 127) / 128, 128, 0, s>>>(part, nblk, nq, out);
+  return cudaGetLastError();
+}
+
+}  // namespace kde

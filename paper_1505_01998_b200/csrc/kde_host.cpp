@@ -66,6 +66,9 @@ struct kde_ctx {
   size_t ext_bytes = 0;
   void* own_ws = nullptr;
   size_t own_bytes = 0;
+  // KDE evaluation / AQP scratch, context-owned
+  void* ev_ws = nullptr;
+  size_t ev_bytes = 0;
   // sorted copy of univariate samples (+ CUB temp), context-owned
   void* sort_ws = nullptr;
   size_t sort_bytes = 0;
@@ -108,6 +111,7 @@ kde_status fail(kde_ctx* c, kde_status s, const char* fmt, ...) {
   } while (0)
 
 constexpr double kPi = 3.14159265358979323846;
+inline float __int_as_float_host(uint32_t b) { float f; std::memcpy(&f, &b, 4); return f; }
 constexpr double kLog2e = 1.44269504088896340736;
 
 // Workspace layout (all offsets 256-byte aligned).
@@ -332,6 +336,19 @@ kde_status gpu_moments(kde_ctx* c, const double* X, int64_t n, int d, Ws& w, Mom
       if (!std::isfinite(v)) return fail(c, KDE_E_INVALID, "non-finite sample values");
       m.cov[a * d + b] = m.cov[b * d + a] = v;
     }
+  return KDE_OK;
+}
+
+kde_status grow(kde_ctx* c, void** buf, size_t* cap, size_t need) {
+  if (*cap >= need) return KDE_OK;
+  if (*buf) {
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    cudaFree(*buf);
+    *buf = nullptr;
+    *cap = 0;
+  }
+  CUDA_TRY(c, cudaMalloc(buf, need));
+  *cap = need;
   return KDE_OK;
 }
 
@@ -835,6 +852,7 @@ void kde_destroy(kde_ctx* c) {
   if (c->comm) nccl().CommDestroy(c->comm);
   if (c->own_ws) cudaFree(c->own_ws);
   if (c->sort_ws) cudaFree(c->sort_ws);
+  if (c->ev_ws) cudaFree(c->ev_ws);
   if (c->h_limbs) cudaFreeHost(c->h_limbs);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   delete c;
@@ -1071,6 +1089,105 @@ kde_status kde_raw_sums(kde_ctx* c, kde_sum_kind kind, const double* X, int64_t 
   }
   TRY(prof_collect(c));
   std::copy(o.begin(), o.end(), out);
+  return KDE_OK;
+}
+
+kde_status kde_evaluate(kde_ctx* c, const double* X, int64_t n, int32_t d, const double* Y, int64_t m,
+                        const double* vh, double* f) {
+  TRY(check_ctx(c));
+  prof_reset(c);
+  TRY(validate_X(c, X, n, d, 1));
+  if (!Y || !vh || !f || m < 0) return fail(c, KDE_E_INVALID, "null query/bandwidth/output pointer");
+  if (m == 0) return KDE_OK;
+  if (m > 2147483647LL) return fail(c, KDE_E_INVALID, "m > 2^31-1");
+  std::vector<double> H = unvech(vh, d), L;
+  if (!cholesky(H, d, L)) return fail(c, KDE_E_NONPOSITIVE_BW, "bandwidth matrix is not positive definite");
+  double det = 1.0;
+  for (int i = 0; i < d; ++i) det *= L[i * d + i] * L[i * d + i];
+  // W^T W = (log2 e / 2) H^-1  =>  2^-|W v|^2 = exp(-v^T H^-1 v / 2)
+  std::vector<double> W = tri_lower_inverse(L, d);
+  for (double& v : W) v *= std::sqrt(kLog2e / 2.0);
+  const int64_t R = kde::eval_rows_per_block(), TC = kde::eval_cols_per_tile();
+  const int64_t ldm = (m + R - 1) / R * R, ldn = (n + TC - 1) / TC * TC;
+  const size_t parts = (size_t)kde::eval_max_splits(c->sm_count) * (size_t)ldm;
+  const size_t need = align256((size_t)d * ldm * 4) + align256((size_t)d * ldn * 4) + align256(parts * 8) +
+                      align256((size_t)m * 8);
+  TRY(grow(c, &c->ev_ws, &c->ev_bytes, need));
+  char* p = (char*)c->ev_ws;
+  float* Yw = (float*)p; p += align256((size_t)d * ldm * 4);
+  float* Xw = (float*)p; p += align256((size_t)d * ldn * 4);
+  double* part = (double*)p; p += align256(parts * 8);
+  double* out = (double*)p;
+  Ws w;
+  TRY(get_ws(c, 256, d, 2, &w));
+  // centre both sets on the sample mean (fp32 accuracy of the differences)
+  const int nblk = kde::moments_blocks(n);
+  double* sums = w.small + 16 + 256;
+  double hs[16];
+  CUDA_TRY(c, kde::launch_moments1(X, n, d, w.part, nblk, c->stream));
+  CUDA_TRY(c, kde::launch_reduce_parts(w.part, nblk, d, sums, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(hs, sums, d * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  std::vector<double> mean(d);
+  for (int a = 0; a < d; ++a) {
+    if (!std::isfinite(hs[a])) return fail(c, KDE_E_INVALID, "non-finite sample values");
+    mean[a] = hs[a] / (double)n;
+  }
+  double* mean_dev = w.small;
+  double* W_dev = w.small + 16;
+  CUDA_TRY(c, cudaMemcpyAsync(mean_dev, mean.data(), d * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(W_dev, W.data(), (size_t)d * d * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, kde::launch_prep(X, n, d, W_dev, mean_dev, Xw, ldn, c->stream, __int_as_float_host(0x7f800000)));
+  CUDA_TRY(c, kde::launch_prep(Y, m, d, W_dev, mean_dev, Yw, ldm, c->stream, 0.f));
+  kde::EvalLaunch el;
+  el.Y = Yw; el.X = Xw; el.m = m; el.ldm = ldm; el.ldn = ldn; el.part = part; el.part_capacity = parts;
+  el.scale = std::pow(2.0 * kPi, -0.5 * d) / std::sqrt(det) / (double)n;
+  el.out = out; el.stream = c->stream; el.sm_count = c->sm_count;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (c->profiling) { e0 = next_event(c); e1 = next_event(c); cudaEventRecord(e0, c->stream); }
+  cudaError_t err = kde::launch_eval(d, el);
+  if (err != cudaSuccess) return fail(c, KDE_E_CUDA, "eval launch: %s", cudaGetErrorString(err));
+  if (c->profiling) {
+    cudaEventRecord(e1, c->stream);
+    c->prof_launches++;
+    c->prof_evals += (double)m * (double)n;
+  }
+  std::vector<double> tmp(m);
+  CUDA_TRY(c, cudaMemcpyAsync(tmp.data(), out, (size_t)m * 8, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  TRY(prof_collect(c));
+  std::copy(tmp.begin(), tmp.end(), f);
+  return KDE_OK;
+}
+
+kde_status kde_aqp_1d(kde_ctx* c, const double* x, int64_t n, double h, const double* lo, const double* hi,
+                      int32_t nq, double* count, double* sum, double* avg) {
+  TRY(check_ctx(c));
+  prof_reset(c);
+  TRY(validate_X(c, x, n, 1, 1));
+  if (!lo || !hi || nq < 1) return fail(c, KDE_E_INVALID, "null interval arrays");
+  if (!(h > 0.0) || !std::isfinite(h)) return fail(c, KDE_E_NONPOSITIVE_BW, "h <= 0");
+  for (int q = 0; q < nq; ++q)
+    if (!(lo[q] <= hi[q])) return fail(c, KDE_E_INVALID, "interval %d has lo > hi or NaN", q);
+  const int nblk = kde::aqp_blocks(n);
+  const size_t need = align256((size_t)nq * nblk * 2 * 8) + 3 * align256((size_t)nq * 2 * 8);
+  TRY(grow(c, &c->ev_ws, &c->ev_bytes, need));
+  char* p = (char*)c->ev_ws;
+  double* part = (double*)p; p += align256((size_t)nq * nblk * 2 * 8);
+  double* dlo = (double*)p; p += align256((size_t)nq * 2 * 8);
+  double* dhi = (double*)p; p += align256((size_t)nq * 2 * 8);
+  double* out = (double*)p;
+  CUDA_TRY(c, cudaMemcpyAsync(dlo, lo, nq * 8, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(dhi, hi, nq * 8, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, kde::launch_aqp(x, n, h, dlo, dhi, nq, part, nblk, out, c->stream));
+  std::vector<double> tmp((size_t)nq * 2);
+  CUDA_TRY(c, cudaMemcpyAsync(tmp.data(), out, (size_t)nq * 16, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  for (int q = 0; q < nq; ++q) {
+    if (count) count[q] = tmp[2 * q];
+    if (sum) sum[q] = tmp[2 * q + 1];
+    if (avg) avg[q] = tmp[2 * q + 1] / tmp[2 * q];
+  }
   return KDE_OK;
 }
 

@@ -60,7 +60,29 @@ cudaError_t launch_moments2(const double* X, int64_t n, int d, const double* mea
 cudaError_t launch_reduce_parts(const double* part, int nblk, int width, double* out,
                                 cudaStream_t s);
 cudaError_t launch_prep(const double* X, int64_t n, int d, const double* W_dev,
-                        const double* mean_dev, float* Y, int64_t ld, cudaStream_t s);
+                        const double* mean_dev, float* Y, int64_t ld, cudaStream_t s,
+                        float pad = 0.f);
+
+// KDE evaluation on an m x n rectangle (kde_eval.cu).
+struct EvalLaunch {
+  const float* Y;        // D x ldm whitened queries
+  const float* X;        // D x ldn whitened samples, padded with +inf
+  int64_t m, ldm, ldn;   // ldm multiple of eval_rows_per_block(), ldn of eval_cols_per_tile()
+  double* part;          // scratch [splits][ldm]
+  size_t part_capacity;  // doubles available in part
+  double scale;          // n^-1 (2 pi)^{-d/2} |H|^{-1/2}
+  double* out;           // m results (device)
+  cudaStream_t stream;
+  int sm_count;
+};
+cudaError_t launch_eval(int d, const EvalLaunch& c);
+int eval_rows_per_block();
+int eval_cols_per_tile();
+int eval_max_splits(int sm_count);
+// Univariate AQP closed forms (kde_eval.cu): out[2q] = COUNT, out[2q+1] = SUM.
+int aqp_blocks(int64_t n);
+cudaError_t launch_aqp(const double* x, int64_t n, double h, const double* lo, const double* hi, int nq,
+                       double* part, int nblk, double* out, cudaStream_t s);
 int moments_blocks(int64_t n);
 size_t sort_temp_bytes(int64_t n);
 cudaError_t launch_sort(const double* in, double* out, int64_t n, void* temp, size_t temp_bytes,

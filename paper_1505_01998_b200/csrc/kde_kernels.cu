@@ -22,6 +22,7 @@
 
 #include <cub/device/device_radix_sort.cuh>
 
+#include "kde_device.cuh"
 #include "kde_internal.h"
 
 namespace kde {
@@ -45,88 +46,6 @@ __host__ __device__ inline void tile_coords(int64_t bx, int64_t& l, int64_t& q) 
 }
 
 void tile_coords_host(int64_t bx, int64_t* l, int64_t* q) { tile_coords(bx, *l, *q); }
-
-__device__ __forceinline__ float ex2(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-
-// Packed fp32x2 arithmetic (sm_100a FADD2 / FMUL2 / FFMA2): two lanes per instruction, each
-// rounded to nearest exactly like the scalar op, so packing never changes a result bit.
-typedef unsigned long long f2;
-__device__ __forceinline__ f2 pk(float a, float b) {
-  f2 r;
-  asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(a), "f"(b));
-  return r;
-}
-__device__ __forceinline__ void upk(f2 v, float& a, float& b) {
-  asm("mov.b64 {%0,%1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
-}
-__device__ __forceinline__ f2 add2(f2 a, f2 b) { f2 d; asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b)); return d; }
-__device__ __forceinline__ f2 sub2(f2 a, f2 b) { f2 d; asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b)); return d; }
-__device__ __forceinline__ f2 mul2(f2 a, f2 b) { f2 d; asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b)); return d; }
-__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
-  f2 d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-  return d;
-}
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
-// TMA bulk copy global -> shared, completion counted on `bar` (UBLKCP in SASS).
-__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
-                                            uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
-// Exact fixed-point split of v * 2^S (|v| 2^S < 2^120): sign-magnitude limbs of 40 bits.
-__device__ __forceinline__ void add_limbs(double v, int S, unsigned long long* dst) {
-  double a = fabs(ldexp(v, S));
-  double h = floor(ldexp(a, -80));
-  double r = a - ldexp(h, 80);            // exact: the low bits of a
-  double m = floor(ldexp(r, -40));
-  double lo = rint(r - ldexp(m, 40));     // integer part; rounding < 2^-S absolute
-  long long H = (long long)h, M = (long long)m, L = (long long)lo;
-  if (v < 0) { H = -H; M = -M; L = -L; }
-  atomicAdd(dst + 0, (unsigned long long)H);
-  atomicAdd(dst + 1, (unsigned long long)M);
-  atomicAdd(dst + 2, (unsigned long long)L);
-}
 
 // Per-tile epilogue: fixed-order reduction of NOUT per-thread values, then limb atomics.
 template <int NOUT, int NT>
@@ -740,7 +659,7 @@ cudaError_t launch_reduce_parts(const double* part, int nblk, int width, double*
 // Data prep (row a1 of SURVEY §8(a)): y_a = fp32( sum_b W_ab (x_b - mean_b) ), zero padding.
 __global__ void prep_kernel(const double* __restrict__ X, int64_t n, int d,
                             const double* __restrict__ W, const double* __restrict__ mean,
-                            float* __restrict__ Y, int64_t ld) {
+                            float* __restrict__ Y, int64_t ld, float pad) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ld; i += stride) {
     if (i < n) {
@@ -752,7 +671,7 @@ __global__ void prep_kernel(const double* __restrict__ X, int64_t n, int d,
         Y[a * ld + i] = (float)s;
       }
     } else {
-      for (int a = 0; a < d; ++a) Y[a * ld + i] = 0.f;
+      for (int a = 0; a < d; ++a) Y[a * ld + i] = pad;
     }
   }
 }
@@ -772,10 +691,10 @@ cudaError_t launch_sort(const double* in, double* out, int64_t n, void* temp, si
 }
 
 cudaError_t launch_prep(const double* X, int64_t n, int d, const double* W_dev,
-                        const double* mean_dev, float* Y, int64_t ld, cudaStream_t s) {
+                        const double* mean_dev, float* Y, int64_t ld, cudaStream_t s, float pad) {
   int64_t blocks = (ld + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
-  prep_kernel<<<(unsigned)blocks, 256, 0, s>>>(X, n, d, W_dev, mean_dev, Y, ld);
+  prep_kernel<<<(unsigned)blocks, 256, 0, s>>>(X, n, d, W_dev, mean_dev, Y, ld, pad);
   return cudaGetLastError();
 }
 

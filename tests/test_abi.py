@@ -17,7 +17,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def _declared():
     src = open(os.path.join(ROOT, "include", "kde.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(kde_[a-zA-Z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(kde_[a-zA-Z0-9_]+)\s*\(", src)))
 
 
 def test_library_exports_every_declared_symbol():
