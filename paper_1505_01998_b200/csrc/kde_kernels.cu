@@ -271,7 +271,8 @@ struct FLscvScalar {
 template <int D_, int R_, int NB_>
 struct FLscvMono {
   static_assert(R_ == 2, "rows are packed as one fp32x2 pair");
-  static constexpr int NT = kThreads, D = D_, R = R_, T = kThreads * R_, NB = NB_, NOUT = 2 * NB_, MINB = 2;
+  static constexpr int NT = kThreads, D = D_, R = R_, T = kThreads * R_, NB = NB_, NOUT = 2 * NB_;
+  static constexpr int MINB = NB_ >= 16 ? 1 : 2;   // 16 candidates need > 128 registers
   static constexpr int P = D * (D + 1) / 2;
   using Params = LscvMatrixParams;
   f2 xr[D];
@@ -522,7 +523,7 @@ cudaError_t launch_psi(int r, const LaunchCfg& c, const PsiParams& p) {
 
 // Candidates per launch: chosen so that no instantiation spills at 128 registers (2 CTAs/SM).
 constexpr int nb_scalar(int d) { return d <= 12 ? 16 : 8; }
-constexpr int nb_mono_max(int d) { return d <= 3 ? 16 : 8; }
+constexpr int nb_mono_max(int d) { return 16; }
 constexpr int nb_chol(int d) { return d <= 5 ? 8 : (d <= 8 ? 4 : (d <= 12 ? 2 : 1)); }
 
 template <int D>
