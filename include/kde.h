@@ -144,6 +144,19 @@ kde_status kde_lscv_H_scores(kde_ctx *ctx, const double *X_dev, int64_t n, int32
 kde_status kde_select_bandwidth(kde_ctx *ctx, kde_method method, const double *X_dev, int64_t n,
                                 int32_t d, const kde_select_opts *opts_or_null, kde_bandwidth *out);
 
+/* ---------------------------------------------------------------- the paper's own design (f3) */
+
+/* LSCV_h scores by the paper's two-phase algorithm (Sec. 6.2): phase 1 materialises
+ * S(v) = v^T Sigma^-1 v for all pairs of this rank's tiles in device memory (the fun2 tile writer
+ * of Sec. 5.5, Eq. 44-56; 4 bytes per pair, allocated by the context), phase 2 streams it once per
+ * batch of h_per_pass in {1,2,4,8,16} candidates (1 = one pass per h, the paper's grid rows) and
+ * reduces Eq. 38-41.  Same values as kde_lscv_h_scores up to rounding; an HBM-bound ablation.
+ * kde_last_aux_ms() returns phase 1's device time, kde_last_profile() phase 2's. */
+kde_status kde_lscv_h_scores_materialized(kde_ctx *ctx, const double *X_dev, int64_t n, int32_t d,
+                                          const double *h_host, int32_t n_h, int32_t h_per_pass,
+                                          double *g_host);
+double kde_last_aux_ms(const kde_ctx *ctx);
+
 /* ---------------------------------------------------------------- using the bandwidth (f2) */
 
 /* KDE evaluation (Eq. kde-def-H / K_H / gaussian): for each query y_q (column q of

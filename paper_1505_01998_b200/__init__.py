@@ -32,7 +32,8 @@ EXPORTS = ["kde_create", "kde_destroy", "kde_last_error", "kde_nccl_unique_id",
            "kde_workspace_bytes", "kde_set_workspace", "kde_default_opts", "kde_psi_r",
            "kde_plugin_h", "kde_lscv_h_scores", "kde_lscv_H_scores", "kde_select_bandwidth",
            "kde_raw_sums", "kde_fixed_value", "kde_fixed_add", "kde_tile_coords",
-           "kde_last_profile", "kde_set_profiling", "kde_shard_tiles", "kde_evaluate", "kde_aqp_1d"]
+           "kde_last_profile", "kde_set_profiling", "kde_shard_tiles", "kde_evaluate", "kde_aqp_1d",
+           "kde_lscv_h_scores_materialized", "kde_last_aux_ms"]
 
 
 class KDEError(RuntimeError):
@@ -109,6 +110,10 @@ def lib():
     L.kde_evaluate.restype = ctypes.c_int
     L.kde_aqp_1d.argtypes = [vp, vp, i64, f64, dp, dp, i32, dp, dp, dp]
     L.kde_aqp_1d.restype = ctypes.c_int
+    L.kde_lscv_h_scores_materialized.argtypes = [vp, vp, i64, i32, dp, i32, i32, dp]
+    L.kde_lscv_h_scores_materialized.restype = ctypes.c_int
+    L.kde_last_aux_ms.argtypes = [vp]
+    L.kde_last_aux_ms.restype = f64
     for f in ("kde_create", "kde_nccl_unique_id", "kde_set_workspace", "kde_psi_r", "kde_plugin_h",
               "kde_lscv_h_scores", "kde_lscv_H_scores", "kde_select_bandwidth", "kde_raw_sums",
               "kde_last_profile", "kde_set_profiling"):
@@ -299,6 +304,19 @@ class Context:
         if method == PLUGIN:
             out["trace"] = r.trace.as_dict()
         return out
+
+    def lscv_h_scores_materialized(self, X, h, h_per_pass: int = 1) -> np.ndarray:
+        """LSCV_h scores via the paper's two-phase algorithm (materialised S(v) buffer)."""
+        X = _dev_matrix(X)
+        hb, hp = _dbuf(np.atleast_1d(h))
+        out = np.zeros(hb.size)
+        self._check(lib().kde_lscv_h_scores_materialized(self._h, ctypes.c_void_p(X.data_ptr()), X.shape[1],
+                                                         X.shape[0], hp, hb.size, int(h_per_pass),
+                                                         out.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
+        return out
+
+    def last_aux_ms(self) -> float:
+        return lib().kde_last_aux_ms(self._h)
 
     def evaluate(self, X, Y, H) -> np.ndarray:
         """fhat at the columns of Y (both CUDA tensors, d x n and d x m); H: d x d or vech."""

@@ -15,7 +15,7 @@ LIB = os.path.join(HERE, "libkde_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I" + os.path.join(ROOT, "include")]
-SOURCES = ["kde_kernels.cu", "kde_eval.cu", "kde_host.cpp"]
+SOURCES = ["kde_kernels.cu", "kde_eval.cu", "kde_materialized.cu", "kde_host.cpp"]
 HEADERS = ["kde_internal.h", "kde_device.cuh", os.path.join("..", "..", "include", "kde.h")]
 
 

@@ -66,6 +66,10 @@ struct kde_ctx {
   size_t ext_bytes = 0;
   void* own_ws = nullptr;
   size_t own_bytes = 0;
+  // materialised S(v) buffer (f3 ablation), context-owned
+  void* mat_ws = nullptr;
+  size_t mat_bytes = 0;
+  double prof_aux_ms = 0.0;
   // KDE evaluation / AQP scratch, context-owned
   void* ev_ws = nullptr;
   size_t ev_bytes = 0;
@@ -422,6 +426,7 @@ void prof_reset(kde_ctx* c) {
   c->prof_all = 0;
   c->prof_ms = 0.0;
   c->prof_evals = 0.0;
+  c->prof_aux_ms = 0.0;
 }
 
 kde_status prof_collect(kde_ctx* c) {
@@ -853,6 +858,7 @@ void kde_destroy(kde_ctx* c) {
   if (c->own_ws) cudaFree(c->own_ws);
   if (c->sort_ws) cudaFree(c->sort_ws);
   if (c->ev_ws) cudaFree(c->ev_ws);
+  if (c->mat_ws) cudaFree(c->mat_ws);
   if (c->h_limbs) cudaFreeHost(c->h_limbs);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   delete c;
@@ -1190,6 +1196,87 @@ kde_status kde_aqp_1d(kde_ctx* c, const double* x, int64_t n, double h, const do
   }
   return KDE_OK;
 }
+
+kde_status kde_lscv_h_scores_materialized(kde_ctx* c, const double* X, int64_t n, int32_t d, const double* h,
+                                          int32_t nh, int32_t h_per_pass, double* g) {
+  TRY(check_ctx(c));
+  prof_reset(c);
+  TRY(validate_X(c, X, n, d, 2));
+  if (!h || !g || nh < 1) return fail(c, KDE_E_INVALID, "null candidate/output array");
+  if (!(h_per_pass == 1 || h_per_pass == 2 || h_per_pass == 4 || h_per_pass == 8 || h_per_pass == 16))
+    return fail(c, KDE_E_INVALID, "h_per_pass must be 1, 2, 4, 8 or 16");
+  for (int k = 0; k < nh; ++k)
+    if (!(h[k] > 0.0) || !std::isfinite(h[k])) return fail(c, KDE_E_NONPOSITIVE_BW, "h[%d] <= 0", k);
+  const int T = kde::mat_tile();
+  const int64_t ld = (n + T - 1) / T * T;
+  const int B = h_per_pass;
+  const int nbatch = (nh + B - 1) / B;
+  const int n_out = 2 * nbatch * B;
+  Ws w;
+  TRY(get_ws(c, ld, d, n_out, &w));
+  Moments m;
+  TRY(gpu_moments(c, X, n, d, w, m));
+  LscvhPrep pp;
+  TRY(lscv_h_prepare(c, m, d, pp));
+  std::vector<double> W = tri_lower_inverse(pp.Lc, d);
+  for (double& v : W) v *= std::sqrt(kLog2e / 4.0);
+  TRY(gpu_prep(c, X, n, d, W, m.mean, ld, w));
+  int64_t tb, te;
+  shard_range(n_tiles(n, T), c->rank, c->world, &tb, &te);
+  const int64_t nvalues = (te - tb) * (int64_t)T * T;
+  TRY(grow(c, &c->mat_ws, &c->mat_bytes, (size_t)std::max<int64_t>(nvalues, 1) * sizeof(float)));
+  float* buf = (float*)c->mat_ws;
+  cudaEvent_t a0 = nullptr, a1 = nullptr;
+  if (c->profiling) { a0 = next_event(c); a1 = next_event(c); cudaEventRecord(a0, c->stream); }
+  CUDA_TRY(c, kde::launch_mat_write(d, w.Y, n, ld, tb, te, buf, c->sm_count, c->stream));   // phase 1
+  if (c->profiling) cudaEventRecord(a1, c->stream);
+  CUDA_TRY(c, cudaMemsetAsync(w.limbs, 0, (size_t)n_out * kde::kLimbs * sizeof(long long), c->stream));
+  const int S = scale_exp_for(1.0, n);
+  const double pairs = c->profiling ? pairs_in_range(n, T, tb, te) : 0.0;
+  for (int b = 0; b < nbatch; ++b) {                                                          // phase 2
+    kde::LscvScalarParams p;
+    for (int j = 0; j < kde::kMaxCand; ++j) {
+      const int idx = std::min(b * B + j, nh - 1);
+      p.kappa[j] = (float)(-1.0 / (h[idx] * h[idx]));
+    }
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (c->profiling) { e0 = next_event(c); e1 = next_event(c); cudaEventRecord(e0, c->stream); }
+    CUDA_TRY(c, kde::launch_mat_reduce(B, buf, nvalues, p, S, w.limbs + (size_t)2 * b * B * kde::kLimbs,
+                                       c->sm_count, c->stream));
+    if (c->profiling) {
+      cudaEventRecord(e1, c->stream);
+      c->prof_launches++;
+      c->prof_evals += pairs * B;
+    }
+  }
+  if (c->world > 1) {
+    NcclApi& api = nccl();
+    if (api.AllReduce(w.limbs, w.limbs, (size_t)n_out * kde::kLimbs, kNcclInt64, kNcclSum, c->comm, c->stream) != 0)
+      return fail(c, KDE_E_NCCL, "ncclAllReduce failed");
+  }
+  std::vector<long long> hl((size_t)n_out * kde::kLimbs);
+  CUDA_TRY(c, cudaMemcpyAsync(hl.data(), w.limbs, hl.size() * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  if (c->profiling) {
+    float x = 0.f;
+    cudaEventElapsedTime(&x, a0, a1);
+    c->prof_aux_ms = x;
+    double ms = 0.0;
+    for (size_t k = 2; k + 1 < c->ev_used; k += 2) {
+      CUDA_TRY(c, cudaEventElapsedTime(&x, c->ev_pool[k], c->ev_pool[k + 1]));
+      ms += x;
+    }
+    c->prof_ms = ms;
+  }
+  for (int k = 0; k < nh; ++k) {
+    const double S1 = fixed_value(limbs_to_fixed(&hl[(size_t)2 * k * kde::kLimbs], S));
+    const double S2 = fixed_value(limbs_to_fixed(&hl[(size_t)(2 * k + 1) * kde::kLimbs], S));
+    g[k] = lscv_h_finalize(n, d, pp.det, h[k], S1, S2);
+  }
+  return KDE_OK;
+}
+
+double kde_last_aux_ms(const kde_ctx* c) { return c ? c->prof_aux_ms : 0.0; }
 
 kde_status kde_select_bandwidth(kde_ctx* c, kde_method method, const double* X, int64_t n, int32_t d,
                                 const kde_select_opts* opts_in, kde_bandwidth* out) {

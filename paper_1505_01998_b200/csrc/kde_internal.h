@@ -79,6 +79,13 @@ cudaError_t launch_eval(int d, const EvalLaunch& c);
 int eval_rows_per_block();
 int eval_cols_per_tile();
 int eval_max_splits(int sm_count);
+// The paper's two-phase LSCV_h (kde_materialized.cu).
+int mat_tile();
+int64_t mat_chunk();
+cudaError_t launch_mat_write(int d, const float* X, int64_t n, int64_t ld, int64_t tb, int64_t te, float* buf,
+                             int sm_count, cudaStream_t s);
+cudaError_t launch_mat_reduce(int B, const float* buf, int64_t nvalues, const LscvScalarParams& p, int S,
+                              unsigned long long* limbs, int sm_count, cudaStream_t s);
 // Univariate AQP closed forms (kde_eval.cu): out[2q] = COUNT, out[2q+1] = SUM.
 int aqp_blocks(int64_t n);
 cudaError_t launch_aqp(const double* x, int64_t n, double h, const double* lo, const double* hi, int nq,

@@ -81,6 +81,38 @@ def run(cfg, reps):
         line(cfg, "select LSCV_H (Nelder-Mead, speculative batches)", dt, prof,
              {"vechH": r["vechH"].tolist(), "objective": r["objective"], "iterations": r["iterations"],
               "evaluations": r["evaluations"], "stop": r["stop_reason"]})
+    elif cfg == "F3":
+        # the paper's two-phase LSCV_h on the C2 workload: HBM-bound phase 2 at 1 h per pass
+        X = datagen.config_data("C2")
+        Xd = kb.to_device(X)
+        n = X.shape[1]
+        h0 = (4.0 / (3.0 * n)) ** 0.2
+        grid = np.linspace(h0 / 4, 4 * h0, 1024)
+        T = 256
+        tiles = ((n + T - 1) // T) * ((n + T - 1) // T + 1) // 2
+        buf_bytes = tiles * T * T * 4
+        for B in (1, 4, 16):
+            dt, prof, g = timed(lambda: ctx.lscv_h_scores_materialized(Xd, grid, h_per_pass=B), 1)
+            passes = (1024 + B - 1) // B
+            gbs = buf_bytes * passes / (prof["pair_ms"] / 1e3) / 1e9
+            line(cfg, f"materialised S(v) LSCV_h, 1024 h, {B} h per pass", dt, prof,
+                 {"phase1_ms": ctx.last_aux_ms(), "buffer_GB": buf_bytes / 1e9, "phase2_hbm_GBps": gbs,
+                  "hbm_frac_of_measured_6547": gbs / 6547.5, "argmin": int(np.argmin(g))})
+    elif cfg == "F2":
+        # KDE evaluation: n = 2^20 samples (C4 data) at m = 2^16 queries, d = 1; and d = 2 (C3)
+        x = datagen.config_data("C4")
+        y = np.linspace(-3, 4, 1 << 16)[None, :]
+        xd, yd = kb.to_device(x), kb.to_device(y)
+        dt, prof, f = timed(lambda: ctx.evaluate(xd, yd, [0.05 ** 2]), reps)
+        line(cfg, "evaluate fhat, d=1, n=2^20 samples, m=2^16 queries", dt, prof)
+        X = datagen.config_data("C3")
+        Y = datagen.sample_mixture("C3", 1 << 15, 99)
+        Xd, Yd = kb.to_device(X), kb.to_device(Y)
+        dt, prof, f = timed(lambda: ctx.evaluate(Xd, Yd, [0.012, 0.002, 0.011]), reps)
+        line(cfg, "evaluate fhat, d=2, n=32768 samples, m=32768 queries", dt, prof)
+        lo = np.linspace(-3, 3, 64)
+        dt, prof, out = timed(lambda: ctx.aqp_1d(xd, 0.05, lo, lo + 0.5), reps)
+        print(json.dumps({"config": cfg, "what": "aqp_1d 64 ranges, n=2^20", "wall_ms": dt * 1e3}), flush=True)
     elif cfg == "C5":
         n = 1 << 18
         X = datagen.config_data("C5")
