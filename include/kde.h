@@ -64,6 +64,11 @@ typedef struct {
   double penalty;        /* LSCV_H objective assigned to a non-positive-definite H; 1e300        */
   int32_t speculative;   /* LSCV_H: 1 = evaluate {reflect, expand, contract_out, contract_in} as
                             one GPU batch per iteration (same decisions as serial NM); 0 = serial */
+  int32_t refine_steps;  /* LSCV_h: after the grid argmin, up to this many bracket sections (16 new
+                            h per step, one GPU pass each) around it ("Golden ratio"); 0 = off */
+  double refine_tol;     /* LSCV_h: stop refining when the bracket is narrower than tol * h; 1e-9 */
+  int32_t nm_starts;     /* LSCV_H: independent Nelder-Mead runs from vech(H_start) * 4^-k,
+                            k < nm_starts, evaluated together in one GPU batch per round; 1 */
 } kde_select_opts;
 
 typedef struct {
@@ -74,7 +79,7 @@ typedef struct {
   double objective;        /* LSCV: g at the selected bandwidth; PLUGIN: 0                      */
   int32_t iterations;      /* LSCV_H Nelder-Mead iterations; LSCV_h: selected grid index        */
   int32_t evaluations;     /* number of objective values computed on the GPU                    */
-  int32_t stop_reason;     /* LSCV_H: 1 = tolerance, 2 = max_iter                               */
+  int32_t stop_reason;     /* LSCV_H: 1 = tolerance, 2 = max_iter; LSCV_h: refinement steps done */
   kde_plugin_trace trace;  /* PLUGIN only                                                       */
 } kde_bandwidth;
 

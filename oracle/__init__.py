@@ -357,14 +357,37 @@ def lscv_h_grid(n: int, d: int, n_grid: int = 150, range_factor: float = 4.0):
     return np.array([lo + k * (hi - lo) / (n_grid - 1) for k in range(n_grid)])
 
 
-def lscv_h_select(X, n_grid: int = 150, range_factor: float = 4.0, threads: int = 1):
-    """argmin over the grid (Eq. 28), ties -> smaller h (reading Z5)."""
+def lscv_h_select(X, n_grid: int = 150, range_factor: float = 4.0, threads: int = 1,
+                  refine_steps: int = 0, refine_tol: float = 1e-9):
+    """argmin over the grid (Eq. 28), ties -> smaller h (reading Z5).  With refine_steps > 0 the
+    bracket formed by the argmin's grid neighbours is re-sectioned refine_steps times with 16
+    equally spaced interior points each (a batched section search, "Golden ratio")."""
     X = _as_X(X)
     d, n = X.shape
     hs = lscv_h_grid(n, d, n_grid, range_factor)
     g = lscv_h_scores(X, hs, threads)
     k = int(np.argmin(g))          # first minimum = smallest h among ties
-    return dict(h=float(hs[k]), index=k, grid=hs, scores=g)
+    out = dict(h=float(hs[k]), index=k, grid=hs, scores=g, objective=float(g[k]), steps=0)
+    if refine_steps > 0:
+        pts = [(hs[max(k - 1, 0)], g[max(k - 1, 0)])]
+        if k > 0:
+            pts.append((hs[k], g[k]))
+        if k + 1 < n_grid:
+            pts.append((hs[k + 1], g[k + 1]))
+        steps = 0
+        while steps < refine_steps:
+            a, b = pts[0][0], pts[-1][0]
+            if not (b - a > refine_tol * out["h"]):
+                break
+            hh = [a + (i + 1) * (b - a) / 17.0 for i in range(16)]
+            gg = lscv_h_scores(X, hh, threads)
+            pts = sorted(pts + list(zip(hh, gg)))
+            bi = min(range(len(pts)), key=lambda i: (pts[i][1], i))
+            out["h"], out["objective"] = float(pts[bi][0]), float(pts[bi][1])
+            pts = pts[max(bi - 1, 0): min(bi + 2, len(pts))]
+            steps += 1
+        out["steps"] = steps
+    return out
 
 
 # --------------------------------------------------------------------------- LSCV_H (Sec 4.4.3)
@@ -479,16 +502,23 @@ def nelder_mead(f, sim, max_iter: int = 500, tol: float = 1e-7, trace=None):
 
 
 def lscv_H_select(X, max_iter: int = 500, tol: float = 1e-7, penalty: float = PENALTY,
-                  threads: int = 1, trace=None):
-    """LSCV_H: minimise g(H) (Eq. 30) over vech(H) by Nelder–Mead from H_start (Eq. 35)."""
+                  threads: int = 1, trace=None, nm_starts: int = 1):
+    """LSCV_H: minimise g(H) (Eq. 30) over vech(H) by Nelder–Mead from H_start (Eq. 35).
+    nm_starts > 1 (row f4): independent runs from the initial simplex scaled by 4^-k, best kept
+    (ties -> earlier run)."""
     X = _as_X(X)
     d, n = X.shape
     x0 = vech(H_start(X))
-    res = nelder_mead(lambda v: lscv_H_score(X, v, threads, penalty), initial_simplex(x0, d),
-                      max_iter, tol, trace)
-    res["H"] = unvech(res["x"], d)
-    res["H_start"] = unvech(x0, d)
-    return res
+    sim0 = initial_simplex(x0, d)
+    best = None
+    for k in range(max(1, nm_starts)):
+        sim = [v * 4.0 ** (-k) for v in sim0]
+        res = nelder_mead(lambda v: lscv_H_score(X, v, threads, penalty), sim, max_iter, tol, trace)
+        if best is None or res["f"] < best["f"]:
+            best = res
+    best["H"] = unvech(best["x"], d)
+    best["H_start"] = unvech(x0, d)
+    return best
 
 
 def tile_enumerate(count: int):

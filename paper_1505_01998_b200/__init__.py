@@ -54,7 +54,9 @@ class PluginTrace(ctypes.Structure):
 class SelectOpts(ctypes.Structure):
     _fields_ = [("n_grid", ctypes.c_int32), ("range_factor", ctypes.c_double),
                 ("max_iter", ctypes.c_int32), ("tol_rel", ctypes.c_double),
-                ("penalty", ctypes.c_double), ("speculative", ctypes.c_int32)]
+                ("penalty", ctypes.c_double), ("speculative", ctypes.c_int32),
+                ("refine_steps", ctypes.c_int32), ("refine_tol", ctypes.c_double),
+                ("nm_starts", ctypes.c_int32)]
 
 
 class Bandwidth(ctypes.Structure):

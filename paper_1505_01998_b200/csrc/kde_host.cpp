@@ -721,21 +721,32 @@ struct NMResult {
   int iterations = 0, stop = 2, evals = 0;
 };
 
-kde_status nelder_mead(kde_ctx* c, const double* X, int64_t n, int d, const Moments& m,
-                       std::vector<std::vector<double>> sim, int max_iter, double tol,
-                       double penalty, bool speculative, NMResult& res) {
-  const int M = (int)sim.size() - 1;
+// One Nelder–Mead run as a state machine: propose() lists the points whose objective values the
+// next decision needs, accept() takes those values and applies the serial NM logic (rho = 1,
+// chi = 2, gamma = sigma = 1/2; stable order by (f, index); stop on
+// f_worst - f_best <= tol |f_best| or max_iter).  Speculative mode proposes reflect, expand,
+// outside and inside contraction together; the decisions are those of serial NM on the same
+// values.  Several runs can share one GPU batch (multi-start, row f4).
+struct NMRun {
+  enum Phase { INIT, STEP, SERIAL_R, SERIAL_1, SHRINK, DONE } phase = INIT;
+  std::vector<std::vector<double>> sim;
   std::vector<double> fs;
-  TRY(lscv_H_eval(c, X, n, d, m, sim, penalty, fs, &res.evals));
-  int it = 0;
-  int stop = 2;
-  auto comb = [](const std::vector<double>& a, double s, const std::vector<double>& b,
-                 const std::vector<double>& cc) {   // a + s (b - cc)
+  int M = 0, it = 0, max_iter = 500, stop = 2;
+  double tol = 1e-7;
+  bool speculative = true;
+  std::vector<double> xbar, xr, xe, xc, xcc;
+  double fr = 0.0;
+  int serial_pick = 0;   // SERIAL_1: 1 = expand, 2 = outside contraction, 3 = inside contraction
+
+  static std::vector<double> comb(const std::vector<double>& a, double s, const std::vector<double>& b,
+                                  const std::vector<double>& c) {
     std::vector<double> r(a.size());
-    for (size_t k = 0; k < a.size(); ++k) r[k] = a[k] + s * (b[k] - cc[k]);
+    for (size_t k = 0; k < a.size(); ++k) r[k] = a[k] + s * (b[k] - c[k]);
     return r;
-  };
-  while (true) {
+  }
+
+  // Sort, test the stopping rule and prepare the trial points of the next iteration.
+  void begin_iteration() {
     std::vector<int> ord(M + 1);
     std::iota(ord.begin(), ord.end(), 0);
     std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return fs[a] < fs[b]; });
@@ -744,59 +755,117 @@ kde_status nelder_mead(kde_ctx* c, const double* X, int64_t n, int d, const Mome
     for (int k : ord) { s2.push_back(sim[k]); f2.push_back(fs[k]); }
     sim.swap(s2);
     fs.swap(f2);
-    if (fs[M] - fs[0] <= tol * std::fabs(fs[0])) { stop = 1; break; }
-    if (it >= max_iter) { stop = 2; break; }
+    if (fs[M] - fs[0] <= tol * std::fabs(fs[0])) { stop = 1; phase = DONE; return; }
+    if (it >= max_iter) { stop = 2; phase = DONE; return; }
     ++it;
-    std::vector<double> xbar(sim[0].size(), 0.0);
+    xbar.assign(sim[0].size(), 0.0);
     for (int k = 0; k < M; ++k)
       for (size_t u = 0; u < xbar.size(); ++u) xbar[u] += sim[k][u];
     for (double& v : xbar) v /= (double)M;
-    std::vector<double> xr = comb(xbar, 1.0, xbar, sim[M]);
-    std::vector<double> xe = comb(xbar, 2.0, xr, xbar);
-    std::vector<double> xc = comb(xbar, 0.5, xr, xbar);
-    std::vector<double> xcc = comb(xbar, 0.5, sim[M], xbar);
-    double fr, fe = 0, fc = 0, fcc = 0;
-    bool have_all = false;
-    if (speculative) {
-      std::vector<double> g;
-      TRY(lscv_H_eval(c, X, n, d, m, {xr, xe, xc, xcc}, penalty, g, &res.evals));
-      fr = g[0]; fe = g[1]; fc = g[2]; fcc = g[3];
-      have_all = true;
-    } else {
-      std::vector<double> g;
-      TRY(lscv_H_eval(c, X, n, d, m, {xr}, penalty, g, &res.evals));
-      fr = g[0];
-    }
-    auto eval1 = [&](const std::vector<double>& x, double& f) -> kde_status {
-      if (have_all) return KDE_OK;
-      std::vector<double> g;
-      TRY(lscv_H_eval(c, X, n, d, m, {x}, penalty, g, &res.evals));
-      f = g[0];
-      return KDE_OK;
-    };
-    if (fr < fs[0]) {
-      TRY(eval1(xe, fe));
-      if (fe < fr) { sim[M] = xe; fs[M] = fe; } else { sim[M] = xr; fs[M] = fr; }
-      continue;
-    }
-    if (fr < fs[M - 1]) { sim[M] = xr; fs[M] = fr; continue; }
-    if (fr < fs[M]) {
-      TRY(eval1(xc, fc));
-      if (fc <= fr) { sim[M] = xc; fs[M] = fc; continue; }
-    } else {
-      TRY(eval1(xcc, fcc));
-      if (fcc < fs[M]) { sim[M] = xcc; fs[M] = fcc; continue; }
-    }
-    std::vector<std::vector<double>> sh;
-    for (int k = 1; k <= M; ++k) sh.push_back(comb(sim[0], 0.5, sim[k], sim[0]));
-    std::vector<double> g;
-    TRY(lscv_H_eval(c, X, n, d, m, sh, penalty, g, &res.evals));
-    for (int k = 1; k <= M; ++k) { sim[k] = sh[k - 1]; fs[k] = g[k - 1]; }
+    xr = comb(xbar, 1.0, xbar, sim[M]);
+    xe = comb(xbar, 2.0, xr, xbar);
+    xc = comb(xbar, 0.5, xr, xbar);
+    xcc = comb(xbar, 0.5, sim[M], xbar);
+    phase = speculative ? STEP : SERIAL_R;
   }
-  res.x = sim[0];
-  res.f = fs[0];
-  res.iterations = it;
-  res.stop = stop;
+
+  std::vector<std::vector<double>> propose() const {
+    switch (phase) {
+      case INIT: return sim;
+      case STEP: return {xr, xe, xc, xcc};
+      case SERIAL_R: return {xr};
+      case SERIAL_1: return {serial_pick == 1 ? xe : (serial_pick == 2 ? xc : xcc)};
+      case SHRINK: {
+        std::vector<std::vector<double>> sh;
+        for (int k = 1; k <= M; ++k) sh.push_back(comb(sim[0], 0.5, sim[k], sim[0]));
+        return sh;
+      }
+      default: return {};
+    }
+  }
+
+  // Decide with f_r known and (speculatively or not) the one follow-up value.
+  // Returns true if the follow-up value is still needed (serial mode).
+  void decide(double fr_, bool have_follow, double fe, double fc, double fcc) {
+    if (fr_ < fs[0]) {
+      if (!have_follow) { serial_pick = 1; fr = fr_; phase = SERIAL_1; return; }
+      if (fe < fr_) { sim[M] = xe; fs[M] = fe; } else { sim[M] = xr; fs[M] = fr_; }
+      begin_iteration();
+      return;
+    }
+    if (fr_ < fs[M - 1]) { sim[M] = xr; fs[M] = fr_; begin_iteration(); return; }
+    if (fr_ < fs[M]) {
+      if (!have_follow) { serial_pick = 2; fr = fr_; phase = SERIAL_1; return; }
+      if (fc <= fr_) { sim[M] = xc; fs[M] = fc; begin_iteration(); return; }
+    } else {
+      if (!have_follow) { serial_pick = 3; fr = fr_; phase = SERIAL_1; return; }
+      if (fcc < fs[M]) { sim[M] = xcc; fs[M] = fcc; begin_iteration(); return; }
+    }
+    phase = SHRINK;
+  }
+
+  void accept(const std::vector<double>& g) {
+    switch (phase) {
+      case INIT: fs = g; begin_iteration(); break;
+      case STEP: decide(g[0], true, g[1], g[2], g[3]); break;
+      case SERIAL_R: decide(g[0], false, 0, 0, 0); break;
+      case SERIAL_1: {
+        const double v = g[0];
+        decide(fr, true, serial_pick == 1 ? v : 0, serial_pick == 2 ? v : 0, serial_pick == 3 ? v : 0);
+        break;
+      }
+      case SHRINK: {
+        for (int k = 1; k <= M; ++k) { sim[k] = comb(sim[0], 0.5, sim[k], sim[0]); fs[k] = g[k - 1]; }
+        begin_iteration();
+        break;
+      }
+      default: break;
+    }
+  }
+};
+
+// Run several NM instances in lockstep; every round evaluates the union of their proposals as
+// one GPU batch (lscv_H_eval), so per-run decisions equal those of a lone run.
+kde_status nelder_mead_multi(kde_ctx* c, const double* X, int64_t n, int d, const Moments& m,
+                             const std::vector<std::vector<std::vector<double>>>& sims, int max_iter,
+                             double tol, double penalty, bool speculative, NMResult& best, int* total_evals) {
+  std::vector<NMRun> runs(sims.size());
+  for (size_t r = 0; r < sims.size(); ++r) {
+    runs[r].sim = sims[r];
+    runs[r].M = (int)sims[r].size() - 1;
+    runs[r].max_iter = max_iter;
+    runs[r].tol = tol;
+    runs[r].speculative = speculative;
+  }
+  int evals = 0;
+  while (true) {
+    std::vector<std::vector<double>> batch;
+    std::vector<std::pair<size_t, size_t>> span;   // (run, count)
+    for (size_t r = 0; r < runs.size(); ++r) {
+      if (runs[r].phase == NMRun::DONE) continue;
+      auto p = runs[r].propose();
+      span.push_back({r, p.size()});
+      for (auto& v : p) batch.push_back(std::move(v));
+    }
+    if (batch.empty()) break;
+    std::vector<double> g;
+    TRY(lscv_H_eval(c, X, n, d, m, batch, penalty, g, &evals));
+    size_t off = 0;
+    for (auto& sp : span) {
+      std::vector<double> gv(g.begin() + off, g.begin() + off + sp.second);
+      off += sp.second;
+      runs[sp.first].accept(gv);
+    }
+  }
+  size_t bi = 0;
+  for (size_t r = 1; r < runs.size(); ++r)
+    if (runs[r].fs[0] < runs[bi].fs[0]) bi = r;
+  best.x = runs[bi].sim[0];
+  best.f = runs[bi].fs[0];
+  best.iterations = runs[bi].it;
+  best.stop = runs[bi].stop;
+  best.evals = evals;
+  if (total_evals) *total_evals = evals;
   return KDE_OK;
 }
 
@@ -813,6 +882,9 @@ void kde_default_opts(kde_select_opts* o) {
   o->tol_rel = 1e-7;
   o->penalty = 1e300;
   o->speculative = 1;
+  o->refine_steps = 0;
+  o->refine_tol = 1e-9;
+  o->nm_starts = 1;
 }
 
 kde_status kde_nccl_unique_id(void* out128) {
@@ -1314,6 +1386,36 @@ kde_status kde_select_bandwidth(kde_ctx* c, kde_method method, const double* X, 
     r.objective = gs[best];
     r.iterations = best;
     r.evaluations = o.n_grid;
+    // Optional refinement (f4): bracket = the grid neighbours of the argmin; each step scores
+    // 16 equally spaced interior points in one pass and re-brackets around the best known point
+    // (ties -> smaller h).  A batched form of the section search the paper suggests.
+    if (o.refine_steps > 0) {
+      std::vector<std::pair<double, double>> pts;   // (h, g) known inside the bracket, sorted by h
+      pts.push_back({hs[best > 0 ? best - 1 : 0], gs[best > 0 ? best - 1 : 0]});
+      if (best > 0) pts.push_back({hs[best], gs[best]});
+      if (best + 1 < o.n_grid) pts.push_back({hs[best + 1], gs[best + 1]});
+      int steps = 0;
+      while (steps < o.refine_steps) {
+        const double a = pts.front().first, b = pts.back().first;
+        if (!(b - a > o.refine_tol * r.h)) break;
+        std::vector<double> hh(16), gg(16);
+        for (int k = 0; k < 16; ++k) hh[k] = a + (k + 1) * (b - a) / 17.0;
+        TRY(lscv_h_scores_impl(c, X, n, d, hh.data(), 16, gg.data()));
+        r.evaluations += 16;
+        for (int k = 0; k < 16; ++k) pts.push_back({hh[k], gg[k]});
+        std::sort(pts.begin(), pts.end());
+        size_t bi = 0;
+        for (size_t k = 1; k < pts.size(); ++k)
+          if (pts[k].second < pts[bi].second) bi = k;
+        r.h = pts[bi].first;
+        r.objective = pts[bi].second;
+        const size_t lo_i = bi > 0 ? bi - 1 : 0, hi_i = bi + 1 < pts.size() ? bi + 1 : bi;
+        std::vector<std::pair<double, double>> nb(pts.begin() + lo_i, pts.begin() + hi_i + 1);
+        pts.swap(nb);
+        ++steps;
+      }
+      r.stop_reason = steps;
+    }
   } else if (method == KDE_LSCV_H) {
     Ws w;
     TRY(get_ws(c, (n + 2047) / 2048 * 2048, d, 2, &w));
@@ -1338,8 +1440,21 @@ kde_status kde_select_bandwidth(kde_ctx* c, kde_method method, const double* X, 
         sim.push_back(v);
         ++t;
       }
+    // start k of o.nm_starts: vech(H_start) scaled by 4^-k (the paper's Eq. 35 start first)
+    std::vector<std::vector<std::vector<double>>> sims;
+    const int K = std::max(1, o.nm_starts);
+    for (int k = 0; k < K; ++k) {
+      const double sc = std::pow(4.0, -k);
+      std::vector<std::vector<double>> sk;
+      for (const auto& v : sim) {
+        std::vector<double> w(v);
+        for (double& e : w) e *= sc;
+        sk.push_back(w);
+      }
+      sims.push_back(sk);
+    }
     NMResult nm;
-    TRY(nelder_mead(c, X, n, d, m, sim, o.max_iter, o.tol_rel, o.penalty, o.speculative != 0, nm));
+    TRY(nelder_mead_multi(c, X, n, d, m, sims, o.max_iter, o.tol_rel, o.penalty, o.speculative != 0, nm, nullptr));
     if (!(nm.f < o.penalty)) return fail(c, KDE_E_NO_FEASIBLE, "no positive-definite H found");
     for (int k = 0; k < P; ++k) r.vechH[k] = nm.x[k];
     r.objective = nm.f;

@@ -1,0 +1,55 @@
+"""GPU parity for the optimizer variants of SURVEY §8(f) f4: LSCV_h grid refinement and
+multi-start Nelder-Mead for LSCV_H (lockstep runs sharing one GPU batch per round)."""
+import numpy as np
+import pytest
+
+import datagen
+import oracle
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+import paper_1505_01998_b200 as kb  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = kb.Context()
+    yield c
+    c.close()
+
+
+def test_lscv_h_refinement_matches_oracle(ctx):
+    X = datagen.sample_mixture("bimodal", 2500, 31)
+    got = ctx.select_bandwidth(kb.LSCV_h, kb.to_device(X), n_grid=64, refine_steps=6, refine_tol=1e-9)
+    ref = oracle.lscv_h_select(X, n_grid=64, refine_steps=6, refine_tol=1e-9)
+    assert got["iterations"] == ref["index"]
+    g_or_at_gpu = oracle.lscv_h_scores(X, [got["h"]])[0]
+    eps = abs(got["objective"] - g_or_at_gpu) / abs(g_or_at_gpu)
+    assert eps < 1e-5
+    # same h to 1e-4, or indistinguishable objective (tie rule)
+    assert abs(got["h"] - ref["h"]) / ref["h"] < 1e-4 or g_or_at_gpu - ref["objective"] <= 2 * eps * abs(ref["objective"])
+    assert got["objective"] <= ctx.lscv_h_scores(kb.to_device(X), [ref["grid"][ref["index"]]])[0]
+
+
+def test_multistart_nm_matches_oracle(ctx):
+    X = datagen.sample_mixture("C3", 500, 17)
+    got = ctx.select_bandwidth(kb.LSCV_H, kb.to_device(X), max_iter=300, nm_starts=3)
+    ref = oracle.lscv_H_select(X, max_iter=300, nm_starts=3)
+    Hg = datagen.unvech(got["vechH"], 2)
+    g_or = oracle.lscv_H_score(X, Hg)
+    eps = abs(got["objective"] - g_or) / abs(g_or)
+    assert eps < 1e-5
+    close = np.max(np.abs(Hg - ref["H"])) / np.max(np.diag(ref["H"])) < 1e-4
+    assert close or g_or <= ref["f"] + max(2 * eps, 1e-7) * abs(ref["f"])
+    single = ctx.select_bandwidth(kb.LSCV_H, kb.to_device(X), max_iter=300, nm_starts=1)
+    assert got["objective"] <= single["objective"]
+
+
+def test_multistart_single_equals_default(ctx):
+    X = kb.to_device(datagen.sample_mixture("C3", 1500, 5))
+    a = ctx.select_bandwidth(kb.LSCV_H, X, max_iter=100)
+    b = ctx.select_bandwidth(kb.LSCV_H, X, max_iter=100, nm_starts=1, speculative=0)
+    assert np.array_equal(a["vechH"], b["vechH"]) and a["iterations"] == b["iterations"]

@@ -178,3 +178,16 @@ def test_lscv_H_select_small():
     gs = [oracle.lscv_H_score(x, [h * h]) for h in hs]
     hstar = hs[int(np.argmin(gs))]
     assert math.sqrt(r1["H"][0, 0]) == pytest.approx(hstar, rel=0.05)
+
+
+def test_lscv_h_refinement_finds_continuous_minimum():
+    # The refined LSCV_h argmin agrees with a bounded scalar minimiser on the same objective
+    # (scipy.optimize.minimize_scalar) inside the grid bracket (f4 row).
+    X = datagen.sample_mixture("bimodal", 400, 12)
+    r = oracle.lscv_h_select(X, n_grid=40, refine_steps=8, refine_tol=1e-10)
+    k = r["index"]
+    lo, hi = r["grid"][max(k - 1, 0)], r["grid"][min(k + 1, 39)]
+    ref = so.minimize_scalar(lambda h: oracle.lscv_h_scores(X, [h])[0], bounds=(lo, hi), method="bounded",
+                             options=dict(xatol=1e-12))
+    assert r["h"] == pytest.approx(ref.x, rel=1e-6)
+    assert r["objective"] <= ref.fun + 1e-15

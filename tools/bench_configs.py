@@ -98,6 +98,21 @@ def run(cfg, reps):
             line(cfg, f"materialised S(v) LSCV_h, 1024 h, {B} h per pass", dt, prof,
                  {"phase1_ms": ctx.last_aux_ms(), "buffer_GB": buf_bytes / 1e9, "phase2_hbm_GBps": gbs,
                   "hbm_frac_of_measured_6547": gbs / 6547.5, "argmin": int(np.argmin(g))})
+    elif cfg == "F4":
+        # optimizer variants: LSCV_h 150-point grid + 6 refinement sections vs the 1024 grid (C2),
+        # and 4-start lockstep Nelder-Mead for LSCV_H (C3)
+        X = datagen.config_data("C2")
+        Xd = kb.to_device(X)
+        dt, prof, r = timed(lambda: ctx.select_bandwidth(kb.LSCV_h, Xd, n_grid=150, refine_steps=6), 1)
+        line(cfg, "select LSCV_h, 150-point grid + 6 x 16-point refinement (C2 data)", dt, prof,
+             {"h": r["h"], "objective": r["objective"], "evaluations": r["evaluations"], "steps": r["stop_reason"]})
+        X = datagen.config_data("C3")
+        Xd = kb.to_device(X)
+        for K in (1, 4):
+            dt, prof, r = timed(lambda: ctx.select_bandwidth(kb.LSCV_H, Xd, nm_starts=K), 1)
+            line(cfg, f"select LSCV_H, {K}-start Nelder-Mead (C3)", dt, prof,
+                 {"vechH": r["vechH"].tolist(), "objective": r["objective"], "iterations": r["iterations"],
+                  "evaluations": r["evaluations"]})
     elif cfg == "F2":
         # KDE evaluation: n = 2^20 samples (C4 data) at m = 2^16 queries, d = 1; and d = 2 (C3)
         x = datagen.config_data("C4")
