@@ -197,7 +197,7 @@ def main():
     sampler = ClockSampler(local)
     sampler.start()
     barrier()
-    step_ms, pair_ms, pair_launches = [], 0.0, 0
+    step_ms, pair_ms, pair_launches, kernel_launches = [], 0.0, 0, 0
     for _ in range(args.steps):
         flush.random_(0, 255)                                 # L2 flush, outside the events
         e0 = torch.cuda.Event(enable_timing=True)
@@ -210,6 +210,7 @@ def main():
         prof = ctx.last_profile()
         pair_ms += prof["pair_ms"]
         pair_launches += prof["pair_launches"]
+        kernel_launches += prof["kernel_launches"]
     barrier()
     clocks = sampler.stop()
     total_ms = sum(step_ms)
@@ -257,7 +258,7 @@ def main():
                          "traffic": load_traffic(), "kernel": "pair_kernel<FPsi<6|4,8>>",
                          "peak_basis": "16 MUFU.EX2/clk/SM x SMs x 1965 MHz (guide unit counts; tools/peaks.cu measured 4.646e12/s)"},
             "clocks": clocks,
-            "gpu_launches": 8 * args.steps,
+            "gpu_launches": kernel_launches,
             "e2e": e2e,
         }
         if not args.no_cpu_baseline and world == 1:

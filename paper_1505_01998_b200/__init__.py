@@ -247,7 +247,7 @@ class Context:
         a, b = ctypes.c_int32(), ctypes.c_int32()
         ms, ev = ctypes.c_double(), ctypes.c_double()
         self._check(lib().kde_last_profile(self._h, ctypes.byref(a), ctypes.byref(ms), ctypes.byref(ev), ctypes.byref(b)))
-        return {"pair_launches": a.value, "pair_ms": ms.value, "pair_evals": ev.value}
+        return {"pair_launches": a.value, "pair_ms": ms.value, "pair_evals": ev.value, "kernel_launches": b.value}
 
     # ---- the five entry points
     def psi_r(self, x, r: int, g) -> np.ndarray:

@@ -319,6 +319,7 @@ kde_status gpu_moments(kde_ctx* c, const double* X, int64_t n, int d, Ws& w, Mom
   double hs[136];
   CUDA_TRY(c, kde::launch_moments1(X, n, d, w.part, nblk, c->stream));
   CUDA_TRY(c, kde::launch_reduce_parts(w.part, nblk, d, sums, c->stream));
+  c->prof_all += 2;
   CUDA_TRY(c, cudaMemcpyAsync(hs, sums, d * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   m.mean.assign(d, 0.0);
@@ -330,6 +331,7 @@ kde_status gpu_moments(kde_ctx* c, const double* X, int64_t n, int d, Ws& w, Mom
   const int width = d * (d + 1) / 2;
   CUDA_TRY(c, kde::launch_moments2(X, n, d, mean_dev, w.part, nblk, c->stream));
   CUDA_TRY(c, kde::launch_reduce_parts(w.part, nblk, width, sums, c->stream));
+  c->prof_all += 2;
   CUDA_TRY(c, cudaMemcpyAsync(hs, sums, width * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   m.cov.assign((size_t)d * d, 0.0);
@@ -373,6 +375,7 @@ kde_status gpu_sorted(kde_ctx* c, const double* x, int64_t n, const double** out
   double* xs = (double*)c->sort_ws;
   void* temp = (char*)c->sort_ws + align256((size_t)n * sizeof(double));
   CUDA_TRY(c, kde::launch_sort(x, xs, n, temp, tmp, c->stream));
+  c->prof_all += 10;   // CUB onesweep for 64-bit keys: histogram, exclusive sum, 8 passes
   *out = xs;
   return KDE_OK;
 }
@@ -385,6 +388,7 @@ kde_status gpu_prep(kde_ctx* c, const double* X, int64_t n, int d, const std::ve
   CUDA_TRY(c, cudaMemcpyAsync(mean_dev, mean.data(), d * sizeof(double), cudaMemcpyHostToDevice, c->stream));
   CUDA_TRY(c, cudaMemcpyAsync(W_dev, W.data(), (size_t)d * d * sizeof(double), cudaMemcpyHostToDevice, c->stream));
   CUDA_TRY(c, kde::launch_prep(X, n, d, W_dev, mean_dev, w.Y, ld, c->stream));
+  c->prof_all += 1;
   return KDE_OK;
 }
 
@@ -477,6 +481,7 @@ kde_status run_sums(kde_ctx* c, int d, int64_t n, int64_t ld, int T, int scale, 
       case Kind::LscvMatrix: err = kde::launch_lscv_matrix(d, L.nb, cfg, L.mat.data(), L.mat.size()); break;
     }
     if (err != cudaSuccess) return fail(c, KDE_E_CUDA, "pair kernel launch: %s", cudaGetErrorString(err));
+    if (tb < te) c->prof_all += 1;
     if (c->profiling) {
       cudaEventRecord(e1, c->stream);
       c->prof_launches++;
@@ -1223,6 +1228,7 @@ kde_status kde_evaluate(kde_ctx* c, const double* X, int64_t n, int32_t d, const
   el.out = out; el.stream = c->stream; el.sm_count = c->sm_count;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (c->profiling) { e0 = next_event(c); e1 = next_event(c); cudaEventRecord(e0, c->stream); }
+  c->prof_all += 1 + 2 + 2 + 2;   // moments1 + reduce, 2 x prep, eval + reduce
   cudaError_t err = kde::launch_eval(d, el);
   if (err != cudaSuccess) return fail(c, KDE_E_CUDA, "eval launch: %s", cudaGetErrorString(err));
   if (c->profiling) {
@@ -1258,6 +1264,7 @@ kde_status kde_aqp_1d(kde_ctx* c, const double* x, int64_t n, double h, const do
   CUDA_TRY(c, cudaMemcpyAsync(dlo, lo, nq * 8, cudaMemcpyHostToDevice, c->stream));
   CUDA_TRY(c, cudaMemcpyAsync(dhi, hi, nq * 8, cudaMemcpyHostToDevice, c->stream));
   CUDA_TRY(c, kde::launch_aqp(x, n, h, dlo, dhi, nq, part, nblk, out, c->stream));
+  c->prof_all += 2;
   std::vector<double> tmp((size_t)nq * 2);
   CUDA_TRY(c, cudaMemcpyAsync(tmp.data(), out, (size_t)nq * 16, cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
@@ -1301,6 +1308,7 @@ kde_status kde_lscv_h_scores_materialized(kde_ctx* c, const double* X, int64_t n
   cudaEvent_t a0 = nullptr, a1 = nullptr;
   if (c->profiling) { a0 = next_event(c); a1 = next_event(c); cudaEventRecord(a0, c->stream); }
   CUDA_TRY(c, kde::launch_mat_write(d, w.Y, n, ld, tb, te, buf, c->sm_count, c->stream));   // phase 1
+  c->prof_all += 1;
   if (c->profiling) cudaEventRecord(a1, c->stream);
   CUDA_TRY(c, cudaMemsetAsync(w.limbs, 0, (size_t)n_out * kde::kLimbs * sizeof(long long), c->stream));
   const int S = scale_exp_for(1.0, n);
@@ -1315,6 +1323,7 @@ kde_status kde_lscv_h_scores_materialized(kde_ctx* c, const double* X, int64_t n
     if (c->profiling) { e0 = next_event(c); e1 = next_event(c); cudaEventRecord(e0, c->stream); }
     CUDA_TRY(c, kde::launch_mat_reduce(B, buf, nvalues, p, S, w.limbs + (size_t)2 * b * B * kde::kLimbs,
                                        c->sm_count, c->stream));
+    c->prof_all += 1;
     if (c->profiling) {
       cudaEventRecord(e1, c->stream);
       c->prof_launches++;
