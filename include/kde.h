@@ -96,7 +96,8 @@ typedef struct {
 /* Create a context on CUDA `device`, enqueuing on `cuda_stream` (a cudaStream_t; NULL = the
  * legacy default stream).  For world > 1, `nccl_unique_id` points to the 128-byte ncclUniqueId
  * rank 0 obtained from kde_nccl_unique_id() and broadcast to all ranks; the library creates its
- * own NCCL communicator (NCCL is loaded at run time, libnccl.so.2).  world == 1 ignores it. */
+ * own NCCL communicator (NCCL is loaded at run time, libnccl.so.2).  world == 1 with a non-NULL
+ * id creates a single-rank communicator, so the collective path runs (used by the tests). */
 kde_status kde_create(kde_ctx **out, int device, void *cuda_stream, const void *nccl_unique_id,
                       int rank, int world);
 void kde_destroy(kde_ctx *ctx);

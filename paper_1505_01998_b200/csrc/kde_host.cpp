@@ -488,7 +488,7 @@ kde_status run_sums(kde_ctx* c, int d, int64_t n, int64_t ld, int T, int scale, 
       c->prof_evals += pairs * (double)L.nb;
     }
   }
-  if (allreduce && c->world > 1) {
+  if (allreduce && c->comm) {
     NcclApi& api = nccl();
     ncclResult_t r = api.AllReduce(w.limbs, w.limbs, (size_t)n_out * kde::kLimbs, kNcclInt64, kNcclSum,
                                    c->comm, c->stream);
@@ -916,7 +916,7 @@ kde_status kde_create(kde_ctx** out, int device, void* stream, const void* nccl_
     delete c;
     return KDE_E_CUDA;
   }
-  if (world > 1) {
+  if (world > 1 || nccl_id) {   // world == 1 with an id: single-rank communicator (tests)
     NcclApi& api = nccl();
     if (!nccl_id || !api.ok) { delete c; return KDE_E_NCCL; }
     ncclUniqueId id;
@@ -1330,7 +1330,7 @@ kde_status kde_lscv_h_scores_materialized(kde_ctx* c, const double* X, int64_t n
       c->prof_evals += pairs * B;
     }
   }
-  if (c->world > 1) {
+  if (c->comm) {
     NcclApi& api = nccl();
     if (api.AllReduce(w.limbs, w.limbs, (size_t)n_out * kde::kLimbs, kNcclInt64, kNcclSum, c->comm, c->stream) != 0)
       return fail(c, KDE_E_NCCL, "ncclAllReduce failed");
