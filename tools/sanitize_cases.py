@@ -1,0 +1,23 @@
+"""Small invocations of every kernel family, for compute-sanitizer (memcheck/racecheck/synccheck)."""
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import datagen  # noqa: E402
+import paper_1505_01998_b200 as kb  # noqa: E402
+
+ctx = kb.Context()
+x = kb.to_device(datagen.sample_mixture("skewed", 1500, 1))
+print("plugin", ctx.plugin_h(x)[0])
+print("psi8", ctx.psi_r(x, 8, [0.3]))
+X = kb.to_device(datagen.sample_mixture("C3", 700, 2))
+print("lscv_h", ctx.lscv_h_scores(X, np.linspace(0.1, 1, 5)))
+print("lscv_H", ctx.lscv_H_scores(X, [[0.05, 0.01, 0.04], [0.2, -0.02, 0.1]]))
+X5 = kb.to_device(np.random.default_rng(1).normal(size=(5, 300)))
+print("lscv_H d5", ctx.lscv_H_scores(X5, [np.eye(5)[np.tril_indices(5)[::-1]].ravel() * 0 + datagen.vech(np.eye(5) * 0.3)]))
+print("eval", ctx.evaluate(X, kb.to_device(datagen.sample_mixture("C3", 600, 3)), [0.05, 0.0, 0.05])[:3])
+print("aqp", ctx.aqp_1d(x, 0.2, [-1.0], [1.0]))
+print("materialized", ctx.lscv_h_scores_materialized(X, np.linspace(0.1, 1, 4), 4))
+print("select H", ctx.select_bandwidth(kb.LSCV_H, X, max_iter=5)["objective"])
