@@ -15,8 +15,9 @@ LIB = os.path.join(HERE, "libkde_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I" + os.path.join(ROOT, "include")]
-SOURCES = ["kde_kernels.cu", "kde_eval.cu", "kde_materialized.cu", "kde_host.cpp"]
-HEADERS = ["kde_internal.h", "kde_device.cuh", os.path.join("..", "..", "include", "kde.h")]
+SOURCES = ["kde_psi.cu", "kde_lscv_scalar.cu", "kde_lscv_matrix.cu", "kde_eval.cu", "kde_materialized.cu",
+           "kde_host.cpp"]
+HEADERS = ["kde_internal.h", "kde_device.cuh", "kde_pair.cuh", os.path.join("..", "..", "include", "kde.h")]
 
 
 def _newer(target: str, deps) -> bool:
@@ -28,16 +29,22 @@ def _newer(target: str, deps) -> bool:
 
 def build(force: bool = False, verbose: bool = False) -> str:
     hdrs = [os.path.join(CSRC, h) for h in HEADERS]
-    objs = []
+    objs, cmds = [], []
     for s in SOURCES:
         src = os.path.join(CSRC, s)
         obj = os.path.join(CSRC, s + ".o")
         objs.append(obj)
         if force or _newer(obj, [src] + hdrs):
             cmd = [NVCC] + ARCH + FLAGS + ["-c", src, "-o", obj]
-            if s.endswith(".cu"):
-                cmd += ["-Xptxas", "-v"] if verbose else []
-            subprocess.check_call(cmd)
+            if s.endswith(".cu") and verbose:
+                cmd += ["-Xptxas", "-v"]
+            cmds.append(cmd)
+    # translation units compile in parallel (the pair-kernel instantiations dominate)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=max(1, min(len(cmds), os.cpu_count() or 1))) as ex:
+        for rc, cmd in zip(ex.map(lambda c: subprocess.call(c), cmds), cmds):
+            if rc != 0:
+                raise subprocess.CalledProcessError(rc, cmd)
     if force or _newer(LIB, objs):
         subprocess.check_call([NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-ldl"])
     return LIB

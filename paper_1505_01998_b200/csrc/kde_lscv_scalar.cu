@@ -1,0 +1,30 @@
+// kde_lscv_scalar.cu — LSCV_h pair-kernel instantiations (see kde_pair.cuh).
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdlib.h>
+
+#include "kde_pair.cuh"
+
+namespace kde {
+
+template <int D>
+static cudaError_t lscv_scalar_d(const LaunchCfg& c, const LscvScalarParams& p) {
+  return launch_pair<FLscvScalar<D, 256, nb_scalar(D)>>(c, p);
+}
+
+cudaError_t launch_lscv_scalar(int d, int nb, const LaunchCfg& c, const LscvScalarParams& p) {
+  (void)nb;
+  switch (d) {
+    case 1: return lscv_scalar_d<1>(c, p);   case 2: return lscv_scalar_d<2>(c, p);
+    case 3: return lscv_scalar_d<3>(c, p);   case 4: return lscv_scalar_d<4>(c, p);
+    case 5: return lscv_scalar_d<5>(c, p);   case 6: return lscv_scalar_d<6>(c, p);
+    case 7: return lscv_scalar_d<7>(c, p);   case 8: return lscv_scalar_d<8>(c, p);
+    case 9: return lscv_scalar_d<9>(c, p);   case 10: return lscv_scalar_d<10>(c, p);
+    case 11: return lscv_scalar_d<11>(c, p); case 12: return lscv_scalar_d<12>(c, p);
+    case 13: return lscv_scalar_d<13>(c, p); case 14: return lscv_scalar_d<14>(c, p);
+    case 15: return lscv_scalar_d<15>(c, p); case 16: return lscv_scalar_d<16>(c, p);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace kde

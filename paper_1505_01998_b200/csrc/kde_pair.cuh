@@ -1,4 +1,5 @@
-// kde_kernels.cu — sm_100a kernels of the all-pairs kernel-sum engine (arxiv 1505.01998).
+#pragma once
+// kde_pair.cuh — sm_100a kernels of the all-pairs kernel-sum engine (arxiv 1505.01998).
 //
 // One persistent pair-kernel family evaluates RR_fun(A) = sum_{i<j} fun(A_i - A_j) (P:472,
 // Sec. 5.4) and RR^v_fun (Sec. 5.5) for a batch of candidate bandwidths per pair
@@ -20,16 +21,16 @@
 
 #include <type_traits>
 
-#include <cub/device/device_radix_sort.cuh>
-
 #include "kde_device.cuh"
 #include "kde_internal.h"
 
 namespace kde {
 
-constexpr int nb_scalar(int d);
-constexpr int nb_mono_max(int d);
-constexpr int nb_chol(int d);
+// Candidates per launch: chosen so that no instantiation spills at 128 registers (2 CTAs/SM).
+constexpr int nb_scalar(int d) { return d <= 12 ? 16 : 8; }
+constexpr int nb_mono_max(int d) { return 16; }
+constexpr int nb_chol(int d) { return d <= 5 ? 8 : (d <= 8 ? 4 : (d <= 12 ? 2 : 1)); }
+
 
 // ------------------------------------------------------------------ small device helpers
 
@@ -45,7 +46,6 @@ __host__ __device__ inline void tile_coords(int64_t bx, int64_t& l, int64_t& q) 
   q = bx - L * (L + 1) / 2;
 }
 
-void tile_coords_host(int64_t bx, int64_t* l, int64_t* q) { tile_coords(bx, *l, *q); }
 
 // Per-tile epilogue: fixed-order reduction of NOUT per-thread values, then limb atomics.
 template <int NOUT, int NT>
@@ -193,10 +193,9 @@ struct FPsi {
 // Sigma = L L^T, so s = |x_i' - x_j'|^2 = (log2 e / 4) S(v) (S(v) of Eq. 37) and for candidate
 // h_c:  e = 2^(s * kappa_c) = exp(-S(v)/(4 h_c^2)),  e^2 = exp(-S(v)/(2 h_c^2)).
 // The thread's two rows are packed in fp32x2 lanes (lane-exact, halves the issue slots).
-template <int D_, int R_, int NB_>
+template <int D_, int NT_, int NB_>
 struct FLscvScalar {
-  static_assert(R_ == 2, "rows are packed as one fp32x2 pair");
-  static constexpr int NT = kThreads, D = D_, R = R_, T = kThreads * R_, NB = NB_, NOUT = 2 * NB_, MINB = 2;
+  static constexpr int NT = NT_, D = D_, R = 2, T = NT_ * 2, NB = NB_, NOUT = 2 * NB_, MINB = 512 / NT_;
   using Params = LscvScalarParams;
   f2 xr[D];
   f2 a1[NB], a2[NB];
@@ -204,7 +203,7 @@ struct FLscvScalar {
   __device__ __forceinline__ void load_rows(const float* __restrict__ X, int64_t ld,
                                             int64_t i0) {
 #pragma unroll
-    for (int a = 0; a < D; ++a) xr[a] = pk(__ldg(X + a * ld + i0), __ldg(X + a * ld + i0 + kThreads));
+    for (int a = 0; a < D; ++a) xr[a] = pk(__ldg(X + a * ld + i0), __ldg(X + a * ld + i0 + NT));
 #pragma unroll
     for (int c = 0; c < NB; ++c) a1[c] = a2[c] = pk(0.f, 0.f);
   }
@@ -237,7 +236,7 @@ struct FLscvScalar {
           upk(s, s0, s1);
           const float inf = __int_as_float(0x7f800000);   // +inf -> e = 2^-inf = 0
           const bool ok0 = (jj < jlim) && (!diag || jj > tid);
-          const bool ok1 = (jj < jlim) && (!diag || jj > kThreads + tid);
+          const bool ok1 = (jj < jlim) && (!diag || jj > NT + tid);
           s = pk(ok0 ? s0 : inf, ok1 ? s1 : inf);
         }
 #pragma unroll
@@ -268,11 +267,10 @@ struct FLscvScalar {
 // q = sum m_ab v_a v_b = -(log2 e / 4) v^T H^-1 v (the fun2 = x^T M x of Eq. 44-56 expanded in
 // monomials), e = 2^q = exp(-v^T H^-1 v / 4), e^2 = exp(-v^T H^-1 v / 2).
 // The thread's two rows are packed in fp32x2 lanes; coefficients are scalar broadcasts.
-template <int D_, int R_, int NB_>
+template <int D_, int NT_, int NB_>
 struct FLscvMono {
-  static_assert(R_ == 2, "rows are packed as one fp32x2 pair");
-  static constexpr int NT = kThreads, D = D_, R = R_, T = kThreads * R_, NB = NB_, NOUT = 2 * NB_;
-  static constexpr int MINB = NB_ >= 16 ? 1 : 2;   // 16 candidates need > 128 registers
+  static constexpr int NT = NT_, D = D_, R = 2, T = NT_ * 2, NB = NB_, NOUT = 2 * NB_;
+  static constexpr int MINB = (NB_ >= 16 ? 256 : 512) / NT_;   // 16 candidates need > 128 registers
   static constexpr int P = D * (D + 1) / 2;
   using Params = LscvMatrixParams;
   f2 xr[D];
@@ -281,7 +279,7 @@ struct FLscvMono {
   __device__ __forceinline__ void load_rows(const float* __restrict__ X, int64_t ld,
                                             int64_t i0) {
 #pragma unroll
-    for (int a = 0; a < D; ++a) xr[a] = pk(__ldg(X + a * ld + i0), __ldg(X + a * ld + i0 + kThreads));
+    for (int a = 0; a < D; ++a) xr[a] = pk(__ldg(X + a * ld + i0), __ldg(X + a * ld + i0 + NT));
 #pragma unroll
     for (int c = 0; c < NB; ++c) a1[c] = a2[c] = pk(0.f, 0.f);
   }
@@ -316,7 +314,7 @@ struct FLscvMono {
           upk(mono[0], m0, m1);
           const float inf = __int_as_float(0x7f800000);   // m_00 < 0 -> q = -inf -> e = 0
           const bool ok0 = (jj < jlim) && (!diag || jj > tid);
-          const bool ok1 = (jj < jlim) && (!diag || jj > kThreads + tid);
+          const bool ok1 = (jj < jlim) && (!diag || jj > NT + tid);
           mono[0] = pk(ok0 ? m0 : inf, ok1 ? m1 : inf);
         }
 #pragma unroll
@@ -466,7 +464,7 @@ __global__ void __launch_bounds__(F::NT, F::MINB) pair_kernel(const Args a,
 }
 
 template <class F>
-static cudaError_t launch_pair(const LaunchCfg& c, const typename F::Params& p) {
+inline cudaError_t launch_pair(const LaunchCfg& c, const typename F::Params& p) {
   if (c.tile_end <= c.tile_begin) return cudaSuccess;
   const size_t smem = 2 * F::D * F::T * sizeof(float) + (F::NT / 32) * F::NOUT * sizeof(double) + 16;
   static int occ = -1;   // per-instantiation: resident CTAs per SM
@@ -487,216 +485,5 @@ static cudaError_t launch_pair(const LaunchCfg& c, const typename F::Params& p) 
   return cudaGetLastError();
 }
 
-// ------------------------------------------------------------------ dispatch
-
-int tile_for(Kind k, int d, int64_t n) {
-  switch (k) {
-    case Kind::Psi4: case Kind::Psi6: case Kind::Psi8: {
-      static const char* dbg = getenv("KDE_DEBUG_PSI_TILE");   // tests / diagnostics only
-      if (dbg && (atoi(dbg) == 512 || atoi(dbg) == 2048)) return atoi(dbg);
-      return n >= (int64_t)64 * 2048 ? 2048 : 512;
-    }
-    case Kind::LscvScalar: return 512;
-    case Kind::LscvMatrix: return d <= 4 ? 512 : kThreads;
-  }
-  return 512;
-}
-
-int cand_per_launch(Kind k, int d) {
-  switch (k) {
-    case Kind::Psi4: case Kind::Psi6: case Kind::Psi8: return 1;
-    case Kind::LscvScalar: return nb_scalar(d);
-    case Kind::LscvMatrix: return d <= 4 ? nb_mono_max(d) : nb_chol(d);
-  }
-  return 1;
-}
-
-cudaError_t launch_psi(int r, const LaunchCfg& c, const PsiParams& p) {
-  const bool big = c.tile == 2048;
-  switch (r) {
-    case 4: return big ? launch_pair<FPsi<4, 256>>(c, p) : launch_pair<FPsi<4, 64>>(c, p);
-    case 6: return big ? launch_pair<FPsi<6, 256>>(c, p) : launch_pair<FPsi<6, 64>>(c, p);
-    case 8: return big ? launch_pair<FPsi<8, 256>>(c, p) : launch_pair<FPsi<8, 64>>(c, p);
-  }
-  return cudaErrorInvalidValue;
-}
-
-// Candidates per launch: chosen so that no instantiation spills at 128 registers (2 CTAs/SM).
-constexpr int nb_scalar(int d) { return d <= 12 ? 16 : 8; }
-constexpr int nb_mono_max(int d) { return 16; }
-constexpr int nb_chol(int d) { return d <= 5 ? 8 : (d <= 8 ? 4 : (d <= 12 ? 2 : 1)); }
-
-template <int D>
-static cudaError_t lscv_scalar_d(const LaunchCfg& c, const LscvScalarParams& p) {
-  return launch_pair<FLscvScalar<D, 2, nb_scalar(D)>>(c, p);
-}
-
-cudaError_t launch_lscv_scalar(int d, int nb, const LaunchCfg& c, const LscvScalarParams& p) {
-  (void)nb;
-  switch (d) {
-    case 1: return lscv_scalar_d<1>(c, p);   case 2: return lscv_scalar_d<2>(c, p);
-    case 3: return lscv_scalar_d<3>(c, p);   case 4: return lscv_scalar_d<4>(c, p);
-    case 5: return lscv_scalar_d<5>(c, p);   case 6: return lscv_scalar_d<6>(c, p);
-    case 7: return lscv_scalar_d<7>(c, p);   case 8: return lscv_scalar_d<8>(c, p);
-    case 9: return lscv_scalar_d<9>(c, p);   case 10: return lscv_scalar_d<10>(c, p);
-    case 11: return lscv_scalar_d<11>(c, p); case 12: return lscv_scalar_d<12>(c, p);
-    case 13: return lscv_scalar_d<13>(c, p); case 14: return lscv_scalar_d<14>(c, p);
-    case 15: return lscv_scalar_d<15>(c, p); case 16: return lscv_scalar_d<16>(c, p);
-  }
-  return cudaErrorInvalidValue;
-}
-
-template <int D>
-static cudaError_t lscv_mono_d(int nb, const LaunchCfg& c, const void* params) {
-  const auto& p = *static_cast<const LscvMatrixParams*>(params);
-  if (nb <= 4) return launch_pair<FLscvMono<D, 2, 4>>(c, p);
-  if constexpr (nb_mono_max(D) == 8) {
-    return launch_pair<FLscvMono<D, 2, 8>>(c, p);
-  } else {
-    if (nb <= 8) return launch_pair<FLscvMono<D, 2, 8>>(c, p);
-    return launch_pair<FLscvMono<D, 2, 16>>(c, p);
-  }
-}
-
-template <int D>
-static cudaError_t lscv_chol_d(const LaunchCfg& c, const void* params) {
-  const auto& p = *static_cast<const LscvCholParams*>(params);
-  constexpr int NB = nb_chol(D);
-  static_assert(NB * D * (D + 1) / 2 <= 4 * 136, "chol params");
-  return launch_pair<FLscvChol<D, NB>>(c, p);
-}
-
-cudaError_t launch_lscv_matrix(int d, int nb, const LaunchCfg& c, const void* params,
-                               size_t bytes) {
-  (void)bytes;
-  switch (d) {
-    case 1: return lscv_mono_d<1>(nb, c, params);
-    case 2: return lscv_mono_d<2>(nb, c, params);
-    case 3: return lscv_mono_d<3>(nb, c, params);
-    case 4: return lscv_mono_d<4>(nb, c, params);
-    case 5: return lscv_chol_d<5>(c, params);   case 6: return lscv_chol_d<6>(c, params);
-    case 7: return lscv_chol_d<7>(c, params);   case 8: return lscv_chol_d<8>(c, params);
-    case 9: return lscv_chol_d<9>(c, params);   case 10: return lscv_chol_d<10>(c, params);
-    case 11: return lscv_chol_d<11>(c, params); case 12: return lscv_chol_d<12>(c, params);
-    case 13: return lscv_chol_d<13>(c, params); case 14: return lscv_chol_d<14>(c, params);
-    case 15: return lscv_chol_d<15>(c, params); case 16: return lscv_chol_d<16>(c, params);
-  }
-  return cudaErrorInvalidValue;
-}
-
-// ------------------------------------------------------------------ O(n) kernels (fp64)
-// Deterministic moments (R_fun): fixed block count for a given n, fixed per-thread
-// order, warp butterfly, fixed cross-warp order, then one block adds the partials in order.
-
-constexpr int kMomThreads = 256;
-
-int moments_blocks(int64_t n) {
-  int64_t b = (n + 4 * kMomThreads - 1) / (4 * kMomThreads);
-  if (b > 1024) b = 1024;
-  if (b < 1) b = 1;
-  return (int)b;
-}
-
-template <int MODE>   // 1: sum x_a; 2: sum (x_a - m_a)(x_b - m_b), a <= b
-__global__ void __launch_bounds__(kMomThreads) moments_kernel(const double* __restrict__ X, int64_t n,
-                                                               int d, const double* __restrict__ mean,
-                                                               double* __restrict__ part) {
-  __shared__ double red[kMomThreads / 32][kMaxDim * (kMaxDim + 1) / 2];
-  const int width = MODE == 1 ? d : d * (d + 1) / 2;
-  double acc[kMaxDim * (kMaxDim + 1) / 2];
-  for (int k = 0; k < width; ++k) acc[k] = 0.0;
-  const int64_t stride = (int64_t)gridDim.x * kMomThreads;
-  for (int64_t i = (int64_t)blockIdx.x * kMomThreads + threadIdx.x; i < n; i += stride) {
-    if (MODE == 1) {
-      for (int a = 0; a < d; ++a) acc[a] += X[a * n + i];
-    } else {
-      double v[kMaxDim];
-      for (int a = 0; a < d; ++a) v[a] = X[a * n + i] - mean[a];
-      int t = 0;
-      for (int a = 0; a < d; ++a)
-        for (int b = a; b < d; ++b) acc[t++] += v[a] * v[b];
-    }
-  }
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int k = 0; k < width; ++k) {
-    double s = warp_sum(acc[k]);
-    if (lane == 0) red[w][k] = s;
-  }
-  __syncthreads();
-  for (int k = threadIdx.x; k < width; k += kMomThreads) {
-    double s = red[0][k];
-    for (int ww = 1; ww < kMomThreads / 32; ++ww) s += red[ww][k];
-    part[(size_t)blockIdx.x * width + k] = s;
-  }
-}
-
-__global__ void reduce_parts_kernel(const double* __restrict__ part, int nblk, int width,
-                                    double* __restrict__ out) {
-  for (int k = threadIdx.x; k < width; k += blockDim.x) {
-    double s = 0.0;
-    for (int b = 0; b < nblk; ++b) s += part[(size_t)b * width + k];
-    out[k] = s;
-  }
-}
-
-cudaError_t launch_moments1(const double* X, int64_t n, int d, double* part, int nblk,
-                            cudaStream_t s) {
-  moments_kernel<1><<<nblk, kMomThreads, 0, s>>>(X, n, d, nullptr, part);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_moments2(const double* X, int64_t n, int d, const double* mean_dev,
-                            double* part, int nblk, cudaStream_t s) {
-  moments_kernel<2><<<nblk, kMomThreads, 0, s>>>(X, n, d, mean_dev, part);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_reduce_parts(const double* part, int nblk, int width, double* out,
-                                cudaStream_t s) {
-  reduce_parts_kernel<<<1, 160, 0, s>>>(part, nblk, width, out);
-  return cudaGetLastError();
-}
-
-// Data prep (row a1 of SURVEY §8(a)): y_a = fp32( sum_b W_ab (x_b - mean_b) ), zero padding.
-__global__ void prep_kernel(const double* __restrict__ X, int64_t n, int d,
-                            const double* __restrict__ W, const double* __restrict__ mean,
-                            float* __restrict__ Y, int64_t ld, float pad) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ld; i += stride) {
-    if (i < n) {
-      double v[kMaxDim];
-      for (int b = 0; b < d; ++b) v[b] = X[b * n + i] - mean[b];
-      for (int a = 0; a < d; ++a) {
-        double s = 0.0;
-        for (int b = 0; b < d; ++b) s = fma(W[a * d + b], v[b], s);
-        Y[a * ld + i] = (float)s;
-      }
-    } else {
-      for (int a = 0; a < d; ++a) Y[a * ld + i] = pad;
-    }
-  }
-}
-
-// Ascending sort of n fp64 samples (CUB radix sort, keys only: deterministic).  The pair sums
-// are invariant under permutation; sorted input keeps the term magnitudes inside a column
-// group homogeneous, which makes the fp32 group sums of FPsi nearly lossless.
-size_t sort_temp_bytes(int64_t n) {
-  size_t bytes = 0;
-  cub::DeviceRadixSort::SortKeys(nullptr, bytes, (const double*)nullptr, (double*)nullptr, (int)n);
-  return bytes;
-}
-
-cudaError_t launch_sort(const double* in, double* out, int64_t n, void* temp, size_t temp_bytes,
-                        cudaStream_t s) {
-  return cub::DeviceRadixSort::SortKeys(temp, temp_bytes, in, out, (int)n, 0, 64, s);
-}
-
-cudaError_t launch_prep(const double* X, int64_t n, int d, const double* W_dev,
-                        const double* mean_dev, float* Y, int64_t ld, cudaStream_t s, float pad) {
-  int64_t blocks = (ld + 255) / 256;
-  if (blocks > 148 * 16) blocks = 148 * 16;
-  prep_kernel<<<(unsigned)blocks, 256, 0, s>>>(X, n, d, W_dev, mean_dev, Y, ld, pad);
-  return cudaGetLastError();
-}
 
 }  // namespace kde

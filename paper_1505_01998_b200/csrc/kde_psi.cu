@@ -1,0 +1,168 @@
+// kde_psi.cu — Psi_r pair-kernel instantiations, tile/batch policy, O(n) kernels (see kde_pair.cuh).
+#include <cub/device/device_radix_sort.cuh>
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdlib.h>
+
+#include "kde_pair.cuh"
+
+namespace kde {
+
+void tile_coords_host(int64_t bx, int64_t* l, int64_t* q) { tile_coords(bx, *l, *q); }
+
+// ------------------------------------------------------------------ dispatch
+
+int tile_for(Kind k, int d, int64_t n) {
+  switch (k) {
+    case Kind::Psi4: case Kind::Psi6: case Kind::Psi8: {
+      static const char* dbg = getenv("KDE_DEBUG_PSI_TILE");   // tests / diagnostics only
+      if (dbg && (atoi(dbg) == 512 || atoi(dbg) == 2048)) return atoi(dbg);
+      return n >= (int64_t)64 * 2048 ? 2048 : 512;
+    }
+    case Kind::LscvScalar: return 512;
+    case Kind::LscvMatrix: {
+      if (d > 4) return kThreads;
+      // 512-row tiles unless that leaves fewer than ~20 tiles per resident CTA (wave tail)
+      const int64_t nb = (n + 511) / 512;
+      return nb * (nb + 1) / 2 >= 6000 ? 512 : 256;
+    }
+  }
+  return 512;
+}
+
+int cand_per_launch(Kind k, int d) {
+  switch (k) {
+    case Kind::Psi4: case Kind::Psi6: case Kind::Psi8: return 1;
+    case Kind::LscvScalar: return nb_scalar(d);
+    case Kind::LscvMatrix: return d <= 4 ? nb_mono_max(d) : nb_chol(d);
+  }
+  return 1;
+}
+
+cudaError_t launch_psi(int r, const LaunchCfg& c, const PsiParams& p) {
+  const bool big = c.tile == 2048;
+  switch (r) {
+    case 4: return big ? launch_pair<FPsi<4, 256>>(c, p) : launch_pair<FPsi<4, 64>>(c, p);
+    case 6: return big ? launch_pair<FPsi<6, 256>>(c, p) : launch_pair<FPsi<6, 64>>(c, p);
+    case 8: return big ? launch_pair<FPsi<8, 256>>(c, p) : launch_pair<FPsi<8, 64>>(c, p);
+  }
+  return cudaErrorInvalidValue;
+}
+
+// Candidates per launch: chosen so that no instantiation spills at 128 registers (2 CTAs/SM).
+// ------------------------------------------------------------------ O(n) kernels (fp64)
+// Deterministic moments (R_fun): fixed block count for a given n, fixed per-thread
+// order, warp butterfly, fixed cross-warp order, then one block adds the partials in order.
+
+constexpr int kMomThreads = 256;
+
+int moments_blocks(int64_t n) {
+  int64_t b = (n + 4 * kMomThreads - 1) / (4 * kMomThreads);
+  if (b > 1024) b = 1024;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+template <int MODE>   // 1: sum x_a; 2: sum (x_a - m_a)(x_b - m_b), a <= b
+__global__ void __launch_bounds__(kMomThreads) moments_kernel(const double* __restrict__ X, int64_t n,
+                                                               int d, const double* __restrict__ mean,
+                                                               double* __restrict__ part) {
+  __shared__ double red[kMomThreads / 32][kMaxDim * (kMaxDim + 1) / 2];
+  const int width = MODE == 1 ? d : d * (d + 1) / 2;
+  double acc[kMaxDim * (kMaxDim + 1) / 2];
+  for (int k = 0; k < width; ++k) acc[k] = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * kMomThreads;
+  for (int64_t i = (int64_t)blockIdx.x * kMomThreads + threadIdx.x; i < n; i += stride) {
+    if (MODE == 1) {
+      for (int a = 0; a < d; ++a) acc[a] += X[a * n + i];
+    } else {
+      double v[kMaxDim];
+      for (int a = 0; a < d; ++a) v[a] = X[a * n + i] - mean[a];
+      int t = 0;
+      for (int a = 0; a < d; ++a)
+        for (int b = a; b < d; ++b) acc[t++] += v[a] * v[b];
+    }
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int k = 0; k < width; ++k) {
+    double s = warp_sum(acc[k]);
+    if (lane == 0) red[w][k] = s;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < width; k += kMomThreads) {
+    double s = red[0][k];
+    for (int ww = 1; ww < kMomThreads / 32; ++ww) s += red[ww][k];
+    part[(size_t)blockIdx.x * width + k] = s;
+  }
+}
+
+__global__ void reduce_parts_kernel(const double* __restrict__ part, int nblk, int width,
+                                    double* __restrict__ out) {
+  for (int k = threadIdx.x; k < width; k += blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < nblk; ++b) s += part[(size_t)b * width + k];
+    out[k] = s;
+  }
+}
+
+cudaError_t launch_moments1(const double* X, int64_t n, int d, double* part, int nblk,
+                            cudaStream_t s) {
+  moments_kernel<1><<<nblk, kMomThreads, 0, s>>>(X, n, d, nullptr, part);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_moments2(const double* X, int64_t n, int d, const double* mean_dev,
+                            double* part, int nblk, cudaStream_t s) {
+  moments_kernel<2><<<nblk, kMomThreads, 0, s>>>(X, n, d, mean_dev, part);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_parts(const double* part, int nblk, int width, double* out,
+                                cudaStream_t s) {
+  reduce_parts_kernel<<<1, 160, 0, s>>>(part, nblk, width, out);
+  return cudaGetLastError();
+}
+
+// Data prep (row a1 of SURVEY §8(a)): y_a = fp32( sum_b W_ab (x_b - mean_b) ), zero padding.
+__global__ void prep_kernel(const double* __restrict__ X, int64_t n, int d,
+                            const double* __restrict__ W, const double* __restrict__ mean,
+                            float* __restrict__ Y, int64_t ld, float pad) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ld; i += stride) {
+    if (i < n) {
+      double v[kMaxDim];
+      for (int b = 0; b < d; ++b) v[b] = X[b * n + i] - mean[b];
+      for (int a = 0; a < d; ++a) {
+        double s = 0.0;
+        for (int b = 0; b < d; ++b) s = fma(W[a * d + b], v[b], s);
+        Y[a * ld + i] = (float)s;
+      }
+    } else {
+      for (int a = 0; a < d; ++a) Y[a * ld + i] = pad;
+    }
+  }
+}
+
+// Ascending sort of n fp64 samples (CUB radix sort, keys only: deterministic).  The pair sums
+// are invariant under permutation; sorted input keeps the term magnitudes inside a column
+// group homogeneous, which makes the fp32 group sums of FPsi nearly lossless.
+size_t sort_temp_bytes(int64_t n) {
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortKeys(nullptr, bytes, (const double*)nullptr, (double*)nullptr, (int)n);
+  return bytes;
+}
+
+cudaError_t launch_sort(const double* in, double* out, int64_t n, void* temp, size_t temp_bytes,
+                        cudaStream_t s) {
+  return cub::DeviceRadixSort::SortKeys(temp, temp_bytes, in, out, (int)n, 0, 64, s);
+}
+
+cudaError_t launch_prep(const double* X, int64_t n, int d, const double* W_dev,
+                        const double* mean_dev, float* Y, int64_t ld, cudaStream_t s, float pad) {
+  int64_t blocks = (ld + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  prep_kernel<<<(unsigned)blocks, 256, 0, s>>>(X, n, d, W_dev, mean_dev, Y, ld, pad);
+  return cudaGetLastError();
+}
+
+}  // namespace kde

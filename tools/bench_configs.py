@@ -77,7 +77,7 @@ def run(cfg, reps):
     elif cfg == "C3":
         X = datagen.config_data("C3")
         Xd = kb.to_device(X)
-        dt, prof, r = timed(lambda: ctx.select_bandwidth(kb.LSCV_H, Xd), 1)
+        dt, prof, r = timed(lambda: ctx.select_bandwidth(kb.LSCV_H, Xd), reps)
         line(cfg, "select LSCV_H (Nelder-Mead, speculative batches)", dt, prof,
              {"vechH": r["vechH"].tolist(), "objective": r["objective"], "iterations": r["iterations"],
               "evaluations": r["evaluations"], "stop": r["stop_reason"]})
@@ -109,7 +109,7 @@ def run(cfg, reps):
         X = datagen.config_data("C3")
         Xd = kb.to_device(X)
         for K in (1, 4):
-            dt, prof, r = timed(lambda: ctx.select_bandwidth(kb.LSCV_H, Xd, nm_starts=K), 1)
+            dt, prof, r = timed(lambda: ctx.select_bandwidth(kb.LSCV_H, Xd, nm_starts=K), reps)
             line(cfg, f"select LSCV_H, {K}-start Nelder-Mead (C3)", dt, prof,
                  {"vechH": r["vechH"].tolist(), "objective": r["objective"], "iterations": r["iterations"],
                   "evaluations": r["evaluations"]})
