@@ -123,7 +123,8 @@ struct Ws {
   float* Y;                 // prepared fp32 data, d x ld
   unsigned long long* limbs;
   double* part;             // moments partials
-  double* small;            // mean[16], W[256], sums[136]
+  double* small;            // mean[16], W[256], sums[136], flags (2 x 8 bytes) at small + 408
+  unsigned long long* flag() const { return reinterpret_cast<unsigned long long*>(small + 408); }
 };
 
 size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
@@ -131,7 +132,7 @@ size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
 size_t ws_bytes(int64_t ld, int32_t d, int32_t n_out) {
   return align256((size_t)d * ld * sizeof(float)) +
          align256((size_t)std::max(n_out, 1) * kde::kLimbs * sizeof(long long)) +
-         align256((size_t)1024 * 136 * sizeof(double)) + align256((16 + 256 + 136) * sizeof(double));
+         align256((size_t)1024 * 136 * sizeof(double)) + align256((16 + 256 + 136 + 16) * sizeof(double));
 }
 
 kde_status get_ws(kde_ctx* c, int64_t ld, int32_t d, int32_t n_out, Ws* w) {
@@ -382,12 +383,13 @@ kde_status gpu_sorted(kde_ctx* c, const double* x, int64_t n, const double** out
 
 // y = fp32(W (x - mean)), padded with zeros to ld.
 kde_status gpu_prep(kde_ctx* c, const double* X, int64_t n, int d, const std::vector<double>& W,
-                    const std::vector<double>& mean, int64_t ld, Ws& w) {
+                    const std::vector<double>& mean, int64_t ld, Ws& w, double clamp_thresh = 0.0) {
   double* mean_dev = w.small;
   double* W_dev = w.small + 16;
   CUDA_TRY(c, cudaMemcpyAsync(mean_dev, mean.data(), d * sizeof(double), cudaMemcpyHostToDevice, c->stream));
   CUDA_TRY(c, cudaMemcpyAsync(W_dev, W.data(), (size_t)d * d * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-  CUDA_TRY(c, kde::launch_prep(X, n, d, W_dev, mean_dev, w.Y, ld, c->stream));
+  CUDA_TRY(c, cudaMemsetAsync(w.flag(), 0, 2 * sizeof(unsigned long long), c->stream));
+  CUDA_TRY(c, kde::launch_prep(X, n, d, W_dev, mean_dev, w.Y, ld, c->stream, 0.f, w.flag(), clamp_thresh));
   c->prof_all += 1;
   return KDE_OK;
 }
@@ -472,6 +474,7 @@ kde_status run_sums(kde_ctx* c, int d, int64_t n, int64_t ld, int T, int scale, 
     cfg.X = w.Y; cfg.n = n; cfg.ld = ld; cfg.tile_begin = tb; cfg.tile_end = te; cfg.tile = T;
     cfg.scale_exp = scale; cfg.limbs = w.limbs + (size_t)L.out_offset * kde::kLimbs;
     cfg.n_out = L.n_out; cfg.stream = c->stream; cfg.sm_count = c->sm_count;
+    cfg.clamp = w.flag() + 1;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (c->profiling) { e0 = next_event(c); e1 = next_event(c); cudaEventRecord(e0, c->stream); }
     cudaError_t err = cudaSuccess;
@@ -502,7 +505,10 @@ kde_status run_sums(kde_ctx* c, int d, int64_t n, int64_t ld, int T, int scale, 
     c->h_limbs_cap = need;
   }
   CUDA_TRY(c, cudaMemcpyAsync(c->h_limbs, w.limbs, need * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+  unsigned long long overflow = 0;
+  CUDA_TRY(c, cudaMemcpyAsync(&overflow, w.flag(), sizeof(overflow), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  if (overflow) return fail(c, KDE_E_INVALID, "scaled sample differences exceed 1e18 (outliers vs. bandwidth)");
   out.resize(n_out);
   for (int k = 0; k < n_out; ++k) out[k] = limbs_to_fixed(c->h_limbs + (size_t)k * kde::kLimbs, scale);
   return KDE_OK;
@@ -538,7 +544,7 @@ kde_status psi_raw(kde_ctx* c, const double* x, int64_t n, int r, const double* 
   out.clear();
   for (int k = 0; k < ng; ++k) {
     std::vector<double> W = {1.0 / g[k]};
-    TRY(gpu_prep(c, x, n, 1, W, m.mean, ld, w));
+    TRY(gpu_prep(c, x, n, 1, W, m.mean, ld, w, 3.0e4));
     SumLaunch L;
     L.kind = psi_kind(r); L.r = r; L.nb = 1; L.out_offset = 0; L.n_out = 1;
     psi_coeffs(r, L.psi);
@@ -1220,8 +1226,9 @@ kde_status kde_evaluate(kde_ctx* c, const double* X, int64_t n, int32_t d, const
   double* W_dev = w.small + 16;
   CUDA_TRY(c, cudaMemcpyAsync(mean_dev, mean.data(), d * sizeof(double), cudaMemcpyHostToDevice, c->stream));
   CUDA_TRY(c, cudaMemcpyAsync(W_dev, W.data(), (size_t)d * d * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-  CUDA_TRY(c, kde::launch_prep(X, n, d, W_dev, mean_dev, Xw, ldn, c->stream, __int_as_float_host(0x7f800000)));
-  CUDA_TRY(c, kde::launch_prep(Y, m, d, W_dev, mean_dev, Yw, ldm, c->stream, 0.f));
+  CUDA_TRY(c, cudaMemsetAsync(w.flag(), 0, sizeof(unsigned long long), c->stream));
+  CUDA_TRY(c, kde::launch_prep(X, n, d, W_dev, mean_dev, Xw, ldn, c->stream, __int_as_float_host(0x7f800000), w.flag()));
+  CUDA_TRY(c, kde::launch_prep(Y, m, d, W_dev, mean_dev, Yw, ldm, c->stream, 0.f, w.flag()));
   kde::EvalLaunch el;
   el.Y = Yw; el.X = Xw; el.m = m; el.ldm = ldm; el.ldn = ldn; el.part = part; el.part_capacity = parts;
   el.scale = std::pow(2.0 * kPi, -0.5 * d) / std::sqrt(det) / (double)n;
@@ -1238,7 +1245,10 @@ kde_status kde_evaluate(kde_ctx* c, const double* X, int64_t n, int32_t d, const
   }
   std::vector<double> tmp(m);
   CUDA_TRY(c, cudaMemcpyAsync(tmp.data(), out, (size_t)m * 8, cudaMemcpyDeviceToHost, c->stream));
+  unsigned long long overflow = 0;
+  CUDA_TRY(c, cudaMemcpyAsync(&overflow, w.flag(), sizeof(overflow), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  if (overflow) return fail(c, KDE_E_INVALID, "whitened sample/query values exceed 1e18");
   TRY(prof_collect(c));
   std::copy(tmp.begin(), tmp.end(), f);
   return KDE_OK;
@@ -1337,7 +1347,10 @@ kde_status kde_lscv_h_scores_materialized(kde_ctx* c, const double* X, int64_t n
   }
   std::vector<long long> hl((size_t)n_out * kde::kLimbs);
   CUDA_TRY(c, cudaMemcpyAsync(hl.data(), w.limbs, hl.size() * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+  unsigned long long overflow = 0;
+  CUDA_TRY(c, cudaMemcpyAsync(&overflow, w.flag(), sizeof(overflow), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  if (overflow) return fail(c, KDE_E_INVALID, "scaled sample differences exceed 1e18");
   if (c->profiling) {
     float x = 0.f;
     cudaEventElapsedTime(&x, a0, a1);

@@ -43,9 +43,10 @@ struct LaunchCfg {
   int n_out;               // outputs written by this launch (<= 2*kMaxCand)
   cudaStream_t stream;
   int sm_count;
+  const unsigned long long* clamp = nullptr;   // Psi: device flag "some |x'| > 3e4"
 };
 
-// Launchers (kde_kernels.cu).  Return cudaSuccess or the launch error.
+// Launchers (kde_psi.cu, kde_lscv_scalar.cu, kde_lscv_matrix.cu).  Return cudaSuccess or the launch error.
 cudaError_t launch_psi(int r, const LaunchCfg& c, const PsiParams& p);
 cudaError_t launch_lscv_scalar(int d, int nb, const LaunchCfg& c, const LscvScalarParams& p);
 cudaError_t launch_lscv_matrix(int d, int nb, const LaunchCfg& c, const void* params, size_t bytes);
@@ -61,7 +62,8 @@ cudaError_t launch_reduce_parts(const double* part, int nblk, int width, double*
                                 cudaStream_t s);
 cudaError_t launch_prep(const double* X, int64_t n, int d, const double* W_dev,
                         const double* mean_dev, float* Y, int64_t ld, cudaStream_t s,
-                        float pad = 0.f);
+                        float pad = 0.f, unsigned long long* overflow_flag = nullptr,
+                        double clamp_thresh = 0.0);
 
 // KDE evaluation on an m x n rectangle (kde_eval.cu).
 struct EvalLaunch {

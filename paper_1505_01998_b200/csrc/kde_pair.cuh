@@ -74,6 +74,7 @@ struct Args {
   int64_t n, ld, tile_begin, tile_end;
   int scale_exp;
   unsigned long long* limbs;
+  const unsigned long long* clamp;   // device flag set by the prep kernel (Psi only), or null
 };
 
 // ------------------------------------------------------------------ functors
@@ -93,6 +94,7 @@ struct FPsi {
   static constexpr int NT = NT_, D = 1, R = 8, T = NT_ * 8, NOUT = 1, CH = 256, MINB = 3;
   static constexpr int NP = R / 2;   // row pairs (r = 2p, 2p+1) packed into fp32x2 lanes
   static constexpr int G = 16;       // columns per compensated group
+  static constexpr bool kClampable = true;
   using Params = PsiParams;
   f2 xr[NP];
   double acc;
@@ -124,7 +126,7 @@ struct FPsi {
   // running sum with Fast2Sum (rounding error kept in a compensation register); fp64 flush
   // every 256 columns.  A plain fp32 running sum drops the one-signed far-pair tail terms
   // (~1e-7..1e-6) next to near-pair sums (~10): measured -1.4e-5 relative at T=2048.
-  template <bool MASK>
+  template <bool MASK, bool CLAMP = false>
   __device__ __forceinline__ void compute(const float* __restrict__ sc, const Params& p, bool diag,
                                           int jlim) {
     const int ib = 8 * threadIdx.x;   // local index of row r is ib + r
@@ -150,13 +152,24 @@ struct FPsi {
               const f2 noff = pk(-off(2 * q), -off(2 * q + 1));
               const f2 d = sub2(xr[q], pk(cv[k], cv[k]));
               f2 sq = mul2(d, d);
-              if (MASK) {
-                const int jj = j + j4 + k;
+              if (MASK || CLAMP) {
+                // s >= 1e4 gives 2^(-7229) == 0 exactly.  CLAMP (data with |x'| > 3e4, flagged by
+                // the prep kernel) keeps He_r(s) finite for far outliers (s^4 overflows fp32
+                // beyond s ~ 4e9), so no inf * 0 = NaN; other data never need it.
                 float s0, s1;
                 upk(sq, s0, s1);
-                const bool ok0 = (jj < jlim) && (!diag || jj > ib + 2 * q);
-                const bool ok1 = (jj < jlim) && (!diag || jj > ib + 2 * q + 1);
-                sq = pk(ok0 ? s0 : 1.0e4f, ok1 ? s1 : 1.0e4f);   // 2^(-7229) == 0; poly finite
+                if (CLAMP) {
+                  s0 = fminf(s0, 1.0e4f);
+                  s1 = fminf(s1, 1.0e4f);
+                }
+                if (MASK) {
+                  const int jj = j + j4 + k;
+                  const bool ok0 = (jj < jlim) && (!diag || jj > ib + 2 * q);
+                  const bool ok1 = (jj < jlim) && (!diag || jj > ib + 2 * q + 1);
+                  s0 = ok0 ? s0 : 1.0e4f;
+                  s1 = ok1 ? s1 : 1.0e4f;
+                }
+                sq = pk(s0, s1);
               }
               float a0, a1;
               upk(fma2(sq, c0, noff), a0, a1);
@@ -196,6 +209,7 @@ struct FPsi {
 template <int D_, int NT_, int NB_>
 struct FLscvScalar {
   static constexpr int NT = NT_, D = D_, R = 2, T = NT_ * 2, NB = NB_, NOUT = 2 * NB_, MINB = 512 / NT_;
+  static constexpr bool kClampable = false;
   using Params = LscvScalarParams;
   f2 xr[D];
   f2 a1[NB], a2[NB];
@@ -208,7 +222,7 @@ struct FLscvScalar {
     for (int c = 0; c < NB; ++c) a1[c] = a2[c] = pk(0.f, 0.f);
   }
 
-  template <bool MASK>
+  template <bool MASK, bool CLAMP = false>
   __device__ __forceinline__ void compute(const float* __restrict__ sc, const Params& p, bool diag,
                                           int jlim) {
     const int tid = threadIdx.x;
@@ -272,6 +286,7 @@ struct FLscvMono {
   static constexpr int NT = NT_, D = D_, R = 2, T = NT_ * 2, NB = NB_, NOUT = 2 * NB_;
   static constexpr int MINB = (NB_ >= 16 ? 256 : 512) / NT_;   // 16 candidates need > 128 registers
   static constexpr int P = D * (D + 1) / 2;
+  static constexpr bool kClampable = false;
   using Params = LscvMatrixParams;
   f2 xr[D];
   f2 a1[NB], a2[NB];
@@ -284,7 +299,7 @@ struct FLscvMono {
     for (int c = 0; c < NB; ++c) a1[c] = a2[c] = pk(0.f, 0.f);
   }
 
-  template <bool MASK>
+  template <bool MASK, bool CLAMP = false>
   __device__ __forceinline__ void compute(const float* __restrict__ sc, const Params& p, bool diag,
                                           int jlim) {
     const int tid = threadIdx.x;
@@ -350,6 +365,7 @@ template <int D_, int NB_>
 struct FLscvChol {
   static constexpr int NT = kThreads, D = D_, R = 1, T = kThreads, NB = NB_, NOUT = 2 * NB_, MINB = 2;
   static constexpr int P = D * (D + 1) / 2;
+  static constexpr bool kClampable = false;
   using Params = LscvCholParams;
   float xr[D];
   float a1[NB], a2[NB];
@@ -362,7 +378,7 @@ struct FLscvChol {
     for (int c = 0; c < NB; ++c) a1[c] = a2[c] = 0.f;
   }
 
-  template <bool MASK>
+  template <bool MASK, bool CLAMP = false>
   __device__ __forceinline__ void compute(const float* __restrict__ sc, const Params& p, bool diag,
                                           int jlim) {
     const int tid = threadIdx.x;
@@ -439,6 +455,7 @@ __global__ void __launch_bounds__(F::NT, F::MINB) pair_kernel(const Args a,
       tma_load_1d(dst + d * T, a.X + d * a.ld + l * T, (uint32_t)(T * sizeof(float)), &bar[buf]);
   };
 
+  const bool clamp = F::kClampable && a.clamp != nullptr && *a.clamp != 0;   // uniform per launch
   int64_t t = a.tile_begin + blockIdx.x;
   if (tid == 0 && t < a.tile_end) issue(t, 0);
   uint32_t k = 0;
@@ -454,8 +471,13 @@ __global__ void __launch_bounds__(F::NT, F::MINB) pair_kernel(const Args a,
     const float* sc = cols + (k & 1) * D * T;
     const bool diag = (q == l);
     const int64_t jl = a.n - l * (int64_t)T;
-    if (!diag && jl >= T) f.template compute<false>(sc, p, false, T);
-    else f.template compute<true>(sc, p, diag, (int)(jl < T ? jl : T));
+    if (clamp) {
+      if (!diag && jl >= T) f.template compute<false, true>(sc, p, false, T);
+      else f.template compute<true, true>(sc, p, diag, (int)(jl < T ? jl : T));
+    } else {
+      if (!diag && jl >= T) f.template compute<false, false>(sc, p, false, T);
+      else f.template compute<true, false>(sc, p, diag, (int)(jl < T ? jl : T));
+    }
 
     double v[NOUT];
     f.outputs(v);
@@ -480,7 +502,7 @@ inline cudaError_t launch_pair(const LaunchCfg& c, const typename F::Params& p) 
   const int64_t tiles = c.tile_end - c.tile_begin;
   int64_t grid = (int64_t)c.sm_count * occ;
   if (grid > tiles) grid = tiles;
-  Args a{c.X, c.n, c.ld, c.tile_begin, c.tile_end, c.scale_exp, c.limbs};
+  Args a{c.X, c.n, c.ld, c.tile_begin, c.tile_end, c.scale_exp, c.limbs, c.clamp};
   pair_kernel<F><<<(unsigned)grid, F::NT, smem, c.stream>>>(a, p);
   return cudaGetLastError();
 }

@@ -126,8 +126,11 @@ cudaError_t launch_reduce_parts(const double* part, int nblk, int width, double*
 // Data prep (row a1 of SURVEY §8(a)): y_a = fp32( sum_b W_ab (x_b - mean_b) ), zero padding.
 __global__ void prep_kernel(const double* __restrict__ X, int64_t n, int d,
                             const double* __restrict__ W, const double* __restrict__ mean,
-                            float* __restrict__ Y, int64_t ld, float pad) {
+                            float* __restrict__ Y, int64_t ld, float pad,
+                            unsigned long long* __restrict__ flag, double clamp_thresh) {
+  // flag[0]: some scaled value beyond 1e18 (error); flag[1]: some beyond clamp_thresh (> 0)
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  bool bad = false, big = false;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ld; i += stride) {
     if (i < n) {
       double v[kMaxDim];
@@ -135,12 +138,25 @@ __global__ void prep_kernel(const double* __restrict__ X, int64_t n, int d,
       for (int a = 0; a < d; ++a) {
         double s = 0.0;
         for (int b = 0; b < d; ++b) s = fma(W[a * d + b], v[b], s);
+        bad |= !(fabs(s) <= 1.0e18);   // squares of differences must stay finite in fp32
+        big |= clamp_thresh > 0.0 && fabs(s) > clamp_thresh;
         Y[a * ld + i] = (float)s;
       }
     } else {
       for (int a = 0; a < d; ++a) Y[a * ld + i] = pad;
     }
   }
+  if (bad && flag) atomicOr(flag, 1ull);
+  if (big && flag) atomicOr(flag + 1, 1ull);
+}
+
+cudaError_t launch_prep(const double* X, int64_t n, int d, const double* W_dev,
+                        const double* mean_dev, float* Y, int64_t ld, cudaStream_t s, float pad,
+                        unsigned long long* flag, double clamp_thresh) {
+  int64_t blocks = (ld + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  prep_kernel<<<(unsigned)blocks, 256, 0, s>>>(X, n, d, W_dev, mean_dev, Y, ld, pad, flag, clamp_thresh);
+  return cudaGetLastError();
 }
 
 // Ascending sort of n fp64 samples (CUB radix sort, keys only: deterministic).  The pair sums
@@ -157,12 +173,5 @@ cudaError_t launch_sort(const double* in, double* out, int64_t n, void* temp, si
   return cub::DeviceRadixSort::SortKeys(temp, temp_bytes, in, out, (int)n, 0, 64, s);
 }
 
-cudaError_t launch_prep(const double* X, int64_t n, int d, const double* W_dev,
-                        const double* mean_dev, float* Y, int64_t ld, cudaStream_t s, float pad) {
-  int64_t blocks = (ld + 255) / 256;
-  if (blocks > 148 * 16) blocks = 148 * 16;
-  prep_kernel<<<(unsigned)blocks, 256, 0, s>>>(X, n, d, W_dev, mean_dev, Y, ld, pad);
-  return cudaGetLastError();
-}
 
 }  // namespace kde

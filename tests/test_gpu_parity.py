@@ -221,3 +221,21 @@ def test_lscv_H_speculative_equals_serial(ctx):
     b = ctx.select_bandwidth(kb.LSCV_H, X, max_iter=120, speculative=0)
     assert np.array_equal(a["vechH"], b["vechH"]) and a["objective"] == b["objective"]
     assert a["iterations"] == b["iterations"]
+
+
+def test_psi_with_far_outliers_stays_finite(ctx):
+    # s = u^2 beyond ~1e9.5 would overflow He_8(s) in fp32; the kernel clamps s at 1e4 where
+    # the term is exactly 0, so far outliers contribute 0 (as in exact arithmetic, to 1e-300).
+    x = datagen.sample_mixture("N01", 3000, 5)
+    x[0, :3] = [5e4, -7e4, 1e5]
+    for r in (4, 6, 8):
+        got = ctx.psi_r(dev(x), r, [0.05])[0]
+        ref = oracle.psi_r(x[0], r, 0.05)
+        assert np.isfinite(got) and rel(got, ref) < RTOL
+
+
+def test_absurd_scale_is_rejected(ctx):
+    x = np.array([[0.0, 1.0, 2.0, 1e30]])
+    with pytest.raises(kb.KDEError) as e:
+        ctx.psi_r(dev(x), 6, [1e-3])
+    assert e.value.status == "KDE_E_INVALID"
