@@ -13,6 +13,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: ranges cost nothing without a profiler
+
 #include "../../include/kde.h"
 #include "kde_internal.h"
 
@@ -88,6 +90,12 @@ struct kde_ctx {
 };
 
 namespace {
+
+// Scoped NVTX range (tracing): moments, prep, sort, psi pass, lscv batch, allreduce...
+struct Range {
+  explicit Range(const char* name) { nvtxRangePushA(name); }
+  ~Range() { nvtxRangePop(); }
+};
 
 kde_status fail(kde_ctx* c, kde_status s, const char* fmt, ...) {
   if (c) {
@@ -314,6 +322,7 @@ struct Moments {
 // Two-pass fp64 moments on the GPU (Eq. 11, Eq. 20-23 read as the unbiased sample covariance,
 // reading Z10).  Returns KDE_E_INVALID for non-finite data.
 kde_status gpu_moments(kde_ctx* c, const double* X, int64_t n, int d, Ws& w, Moments& m) {
+  Range r("kde.moments");
   const int nblk = kde::moments_blocks(n);
   double* sums = w.small + 16 + 256;
   double* mean_dev = w.small;
@@ -361,6 +370,7 @@ kde_status grow(kde_ctx* c, void** buf, size_t* cap, size_t need) {
 
 // Sorted copy of n univariate samples (context-owned scratch); returns the device pointer.
 kde_status gpu_sorted(kde_ctx* c, const double* x, int64_t n, const double** out) {
+  Range r("kde.sort");
   const size_t tmp = kde::sort_temp_bytes(n);
   const size_t need = align256((size_t)n * sizeof(double)) + align256(tmp);
   if (c->sort_bytes < need) {
@@ -384,6 +394,7 @@ kde_status gpu_sorted(kde_ctx* c, const double* x, int64_t n, const double** out
 // y = fp32(W (x - mean)), padded with zeros to ld.
 kde_status gpu_prep(kde_ctx* c, const double* X, int64_t n, int d, const std::vector<double>& W,
                     const std::vector<double>& mean, int64_t ld, Ws& w, double clamp_thresh = 0.0) {
+  Range r("kde.prep");
   double* mean_dev = w.small;
   double* W_dev = w.small + 16;
   CUDA_TRY(c, cudaMemcpyAsync(mean_dev, mean.data(), d * sizeof(double), cudaMemcpyHostToDevice, c->stream));
@@ -465,6 +476,7 @@ struct SumLaunch {
 kde_status run_sums(kde_ctx* c, int d, int64_t n, int64_t ld, int T, int scale, Ws& w,
                     const std::vector<SumLaunch>& launches, int n_out, int shard_rank,
                     int shard_world, bool allreduce, std::vector<kde_fixed>& out) {
+  Range rr("kde.pair_pass");
   CUDA_TRY(c, cudaMemsetAsync(w.limbs, 0, (size_t)n_out * kde::kLimbs * sizeof(long long), c->stream));
   int64_t tiles = n_tiles(n, T), tb, te;
   shard_range(tiles, shard_rank, shard_world, &tb, &te);
@@ -492,6 +504,7 @@ kde_status run_sums(kde_ctx* c, int d, int64_t n, int64_t ld, int T, int scale, 
     }
   }
   if (allreduce && c->comm) {
+    Range ra("kde.allreduce");
     NcclApi& api = nccl();
     ncclResult_t r = api.AllReduce(w.limbs, w.limbs, (size_t)n_out * kde::kLimbs, kNcclInt64, kNcclSum,
                                    c->comm, c->stream);
