@@ -98,6 +98,14 @@ def run(cfg, reps):
             line(cfg, f"materialised S(v) LSCV_h, 1024 h, {B} h per pass", dt, prof,
                  {"phase1_ms": ctx.last_aux_ms(), "buffer_GB": buf_bytes / 1e9, "phase2_hbm_GBps": gbs,
                   "hbm_frac_of_measured_6547": gbs / 6547.5, "argmin": int(np.argmin(g))})
+    elif cfg == "F1":
+        # LSCV_h for d > 1 (whitened scalar h, row f1): n = 65536, 1024 h, d = 2 and 4
+        for d in (2, 4):
+            X = datagen.config_data("C5", n=65536)[:d]
+            Xd = kb.to_device(X)
+            grid = np.linspace(0.05, 1.5, 1024)
+            dt, prof, g = timed(lambda: ctx.lscv_h_scores(Xd, grid), reps)
+            line(cfg, f"lscv_h_scores d={d}, n=65536, 1024 h", dt, prof, {"argmin": int(np.argmin(g))})
     elif cfg == "F4":
         # optimizer variants: LSCV_h 150-point grid + 6 refinement sections vs the 1024 grid (C2),
         # and 4-start lockstep Nelder-Mead for LSCV_H (C3)
