@@ -93,9 +93,13 @@ __global__ void __launch_bounds__(kEvNT, 2) eval_kernel(const EvalArgs a) {
               v = sub2(y[d], pk(cv[d][kk], cv[d][kk]));
               s = fma2(v, v, s);
             }
-            float s0, s1;
-            upk(s, s0, s1);
-            grp = add2(grp, pk(ex2(-s0), ex2(-s1)));
+            if (kk == 3) {   // a quarter of the exponentials on the FMA pipe (slot kk = 3)
+              grp = add2(grp, exp2_sw2(sub2(pk(0.f, 0.f), s)));
+            } else {
+              float s0, s1;
+              upk(s, s0, s1);
+              grp = add2(grp, pk(ex2(-s0), ex2(-s1)));
+            }
           }
         }
         const f2 s2 = add2(acc, grp);          // Fast2Sum(acc, grp): terms > 0, acc grows
