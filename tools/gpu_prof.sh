@@ -16,4 +16,8 @@ ncu --set full --clock-control none --import-source on --kernel-name-base demang
 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:FLscvMono -s 30 -c 1 \
     -o gpurun_out/prof_c3 -f python tools/bench_configs.py C3 --reps 1 > gpurun_out/ncu_c3.log 2>&1
 fi
+if [[ " $* " == *" eval "* || $# -eq 0 ]]; then
+ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:eval_kernel -s 1 -c 1 \
+    -o gpurun_out/prof_f2 -f python tools/bench_configs.py F2 --reps 2 > gpurun_out/ncu_f2.log 2>&1
+fi
 ls -la gpurun_out/*.ncu-rep
