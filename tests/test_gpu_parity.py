@@ -239,3 +239,12 @@ def test_absurd_scale_is_rejected(ctx):
     with pytest.raises(kb.KDEError) as e:
         ctx.psi_r(dev(x), 6, [1e-3])
     assert e.value.status == "KDE_E_INVALID"
+
+
+def test_bitwise_reproducible_over_ten_runs(ctx):
+    x = dev(datagen.sample_mixture("skewed", 30000, 11))
+    X = dev(datagen.sample_mixture("C3", 6000, 11))
+    hs = np.linspace(0.05, 1.0, 24)
+    ref = (ctx.plugin_h(x), ctx.lscv_h_scores(X, hs).tolist(), ctx.lscv_H_scores(X, [[0.05, 0.01, 0.04]]).tolist())
+    for _ in range(9):
+        assert (ctx.plugin_h(x), ctx.lscv_h_scores(X, hs).tolist(), ctx.lscv_H_scores(X, [[0.05, 0.01, 0.04]]).tolist()) == ref
