@@ -655,9 +655,11 @@ HCand h_candidate(const double* vh, int d) {
 }
 
 // Raw LSCV_H sums for PD candidates `cands` (all must be PD).
+// prepared_Y (optional): within one API call, the workspace pointer whose fp32 copy of X is already
+// prepared; the prep kernel is skipped while the workspace has not moved (Nelder-Mead loop).
 kde_status lscv_H_raw(kde_ctx* c, const double* X, int64_t n, int d, const std::vector<HCand>& cands,
                       const Moments& m, int shard_rank, int shard_world, bool allreduce,
-                      std::vector<kde_fixed>& out) {
+                      std::vector<kde_fixed>& out, const float** prepared_Y = nullptr) {
   const int T = kde::tile_for(Kind::LscvMatrix, d, n);
   const int nbmax = kde::cand_per_launch(Kind::LscvMatrix, d);
   const int64_t ld = (n + T - 1) / T * T;
@@ -685,9 +687,12 @@ kde_status lscv_H_raw(kde_ctx* c, const double* X, int64_t n, int d, const std::
   }
   Ws w;
   TRY(get_ws(c, ld, d, std::max(off, 2), &w));
-  std::vector<double> W((size_t)d * d, 0.0);
-  for (int a = 0; a < d; ++a) W[a * d + a] = 1.0;
-  TRY(gpu_prep(c, X, n, d, W, m.mean, ld, w));
+  if (!prepared_Y || *prepared_Y != w.Y) {
+    std::vector<double> W((size_t)d * d, 0.0);
+    for (int a = 0; a < d; ++a) W[a * d + a] = 1.0;
+    TRY(gpu_prep(c, X, n, d, W, m.mean, ld, w));
+    if (prepared_Y) *prepared_Y = w.Y;
+  }
   std::vector<kde_fixed> o;
   TRY(run_sums(c, d, n, ld, T, scale_exp_for(1.0, n), w, Ls, std::max(off, 2), shard_rank, shard_world, allreduce, o));
   out.clear();
@@ -713,7 +718,7 @@ double lscv_H_finalize(int64_t n, int d, double det, double S1, double S2) {
 // Evaluate g(H) for a list of vech vectors (non-PD -> penalty); one GPU batch for all PD ones.
 kde_status lscv_H_eval(kde_ctx* c, const double* X, int64_t n, int d, const Moments& m,
                        const std::vector<std::vector<double>>& vs, double penalty,
-                       std::vector<double>& g, int* evals) {
+                       std::vector<double>& g, int* evals, const float** prepared_Y = nullptr) {
   std::vector<HCand> pdc;
   std::vector<int> idx;
   g.assign(vs.size(), penalty);
@@ -723,7 +728,7 @@ kde_status lscv_H_eval(kde_ctx* c, const double* X, int64_t n, int d, const Mome
   }
   if (pdc.empty()) return KDE_OK;
   std::vector<kde_fixed> o;
-  TRY(lscv_H_raw(c, X, n, d, pdc, m, c->rank, c->world, true, o));
+  TRY(lscv_H_raw(c, X, n, d, pdc, m, c->rank, c->world, true, o, prepared_Y));
   for (size_t j = 0; j < pdc.size(); ++j)
     g[idx[j]] = lscv_H_finalize(n, d, pdc[j].det, fixed_value(o[2 * j]), fixed_value(o[2 * j + 1]));
   if (evals) *evals += (int)pdc.size();
@@ -862,6 +867,15 @@ kde_status nelder_mead_multi(kde_ctx* c, const double* X, int64_t n, int d, cons
     runs[r].speculative = speculative;
   }
   int evals = 0;
+  // size the workspace for the largest batch up front so the prepared data never move
+  {
+    const int T = kde::tile_for(Kind::LscvMatrix, d, n);
+    size_t maxb = 0;
+    for (const auto& sk : sims) maxb += std::max<size_t>(sk.size(), 4);
+    Ws w;
+    TRY(get_ws(c, (n + T - 1) / T * T, d, (int)(2 * (maxb + 32)), &w));
+  }
+  const float* prepared = nullptr;
   while (true) {
     std::vector<std::vector<double>> batch;
     std::vector<std::pair<size_t, size_t>> span;   // (run, count)
@@ -873,7 +887,7 @@ kde_status nelder_mead_multi(kde_ctx* c, const double* X, int64_t n, int d, cons
     }
     if (batch.empty()) break;
     std::vector<double> g;
-    TRY(lscv_H_eval(c, X, n, d, m, batch, penalty, g, &evals));
+    TRY(lscv_H_eval(c, X, n, d, m, batch, penalty, g, &evals, &prepared));
     size_t off = 0;
     for (auto& sp : span) {
       std::vector<double> gv(g.begin() + off, g.begin() + off + sp.second);
