@@ -1,0 +1,40 @@
+"""Single-GPU emulation of the multi-GPU partition ('fake multi-GPU'): for P in
+{1, 2, 4, 8}, time every rank's shard of the C4 PLUGIN pair passes (kde_raw_sums with
+shard=(r, P), the exact tile ranges rank r would run) and project the P-GPU step time as
+  redundant O(n) work (moments + sort + prep, measured) + max_r shard time of each pass
+  + 2 all-reduces (24 B each; NVLink/NCCL latency taken as 30 us, not measured here).
+This is a projection from measured per-rank work, not a multi-GPU measurement."""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import datagen  # noqa: E402
+import paper_1505_01998_b200 as kb  # noqa: E402
+
+ctx = kb.Context(profiling=True)
+x = kb.to_device(datagen.config_data("C4"))
+h, tr = ctx.plugin_h(x)        # warm up + g1, g2
+full = []
+for _ in range(3):
+    torch.cuda.synchronize(); t0 = time.perf_counter(); ctx.plugin_h(x); torch.cuda.synchronize()
+    full.append((time.perf_counter() - t0) * 1e3)
+pair_full = ctx.last_profile()["pair_ms"]
+t1 = min(full)
+overhead = t1 - pair_full
+res = {"P1_measured_ms": t1, "pair_ms_P1": pair_full, "redundant_overhead_ms": overhead}
+for P in (2, 4, 8):
+    worst = [0.0, 0.0]
+    for r in range(P):
+        for k, (kind, g) in enumerate(((kb.SUM_PSI6, tr["g1"]), (kb.SUM_PSI4, tr["g2"]))):
+            ctx.raw_sums(kind, x, [g], shard=(r, P))
+            worst[k] = max(worst[k], ctx.last_profile()["pair_ms"])
+    proj = overhead + worst[0] + worst[1] + 2 * 0.030
+    res[f"P{P}"] = {"max_shard_pair_ms": worst, "projected_step_ms": proj,
+                    "projected_efficiency": t1 / (P * proj)}
+print(json.dumps(res))
