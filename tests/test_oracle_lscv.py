@@ -191,3 +191,16 @@ def test_lscv_h_refinement_finds_continuous_minimum():
                              options=dict(xatol=1e-12))
     assert r["h"] == pytest.approx(ref.x, rel=1e-6)
     assert r["objective"] <= ref.fun + 1e-15
+
+
+def test_mean_cov_matches_numpy():
+    # Eq. 20-23 (unbiased sample covariance, reading Z10) vs numpy's library routine
+    X = datagen.sample_mixture("C5", 500, 3)
+    m, S = oracle.mean_cov(X)
+    np.testing.assert_allclose(m, X.mean(axis=1), rtol=1e-13, atol=1e-15)
+    np.testing.assert_allclose(S, np.cov(X), rtol=1e-12, atol=1e-15)
+    # Eq. 11 one-pass form equals the two-pass value for well-scaled data
+    x = X[0]
+    n = x.size
+    V11 = (x ** 2).sum() / (n - 1) - x.sum() ** 2 / (n * (n - 1))
+    assert S[0, 0] == pytest.approx(V11, rel=1e-12)
