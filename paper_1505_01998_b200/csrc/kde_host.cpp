@@ -629,7 +629,7 @@ double lscv_h_finalize(int64_t n, int d, double det, double h, double S1, double
 struct HCand {
   bool pd = false;
   double det = 0.0;
-  std::vector<double> coef;   // D<=4: monomial coefficients; D>4: scaled upper factor rows
+  std::vector<double> Hi;     // H^-1 (row-major), fp64
 };
 
 HCand h_candidate(const double* vh, int d) {
@@ -639,19 +639,44 @@ HCand h_candidate(const double* vh, int d) {
   hc.pd = true;
   hc.det = 1.0;
   for (int i = 0; i < d; ++i) hc.det *= L[i * d + i] * L[i * d + i];
-  std::vector<double> Hi = spd_inverse(L, d);
+  hc.Hi = spd_inverse(L, d);
+  return hc;
+}
+
+// Kernel coefficients of a candidate for data whitened as x' = Lw^-1 (x - mean) (Lw = the
+// Cholesky factor of the sample covariance, or I): M = Lw^T H^-1 Lw, so that
+// v^T H^-1 v = v'^T M v'.  Whitening keeps M well conditioned for the candidates LSCV_H visits
+// (H ~ c Sigma or c Sigma^(1/2)), which matters because the fp32 monomial form loses accuracy in
+// proportion to cond(M).  D <= 4: monomial coefficients -(log2 e/4)(2-delta_ab) M_ab;
+// D > 4: rows of U with U^T U = (log2 e/4) M.  Returns false if M is not numerically PD.
+bool h_coefficients(const HCand& hc, int d, const std::vector<double>& Lw, std::vector<double>& coef) {
+  std::vector<double> M((size_t)d * d, 0.0), T((size_t)d * d, 0.0);
+  for (int i = 0; i < d; ++i)          // T = H^-1 Lw
+    for (int j = 0; j < d; ++j) {
+      double s = 0.0;
+      for (int k = 0; k < d; ++k) s += hc.Hi[i * d + k] * Lw[k * d + j];
+      T[i * d + j] = s;
+    }
+  for (int i = 0; i < d; ++i)          // M = Lw^T T
+    for (int j = 0; j < d; ++j) {
+      double s = 0.0;
+      for (int k = 0; k < d; ++k) s += Lw[k * d + i] * T[k * d + j];
+      M[i * d + j] = s;
+    }
+  for (int i = 0; i < d; ++i)
+    for (int j = 0; j < i; ++j) M[i * d + j] = M[j * d + i] = 0.5 * (M[i * d + j] + M[j * d + i]);
   const double sc = kLog2e / 4.0;
+  coef.clear();
   if (d <= 4) {
     for (int a = 0; a < d; ++a)
-      for (int b = a; b < d; ++b) hc.coef.push_back(-sc * (a == b ? 1.0 : 2.0) * Hi[a * d + b]);
-  } else {
-    std::vector<double> M(Hi), Lm;
-    if (!cholesky(M, d, Lm)) { hc.pd = false; return hc; }
-    // U = sqrt(sc) Lm^T (upper), rows a: entries b = a..d-1
-    for (int a = 0; a < d; ++a)
-      for (int b = a; b < d; ++b) hc.coef.push_back(std::sqrt(sc) * Lm[b * d + a]);
+      for (int b = a; b < d; ++b) coef.push_back(-sc * (a == b ? 1.0 : 2.0) * M[a * d + b]);
+    return true;
   }
-  return hc;
+  std::vector<double> Lm;
+  if (!cholesky(M, d, Lm)) return false;
+  for (int a = 0; a < d; ++a)          // U = sqrt(sc) Lm^T (upper), rows a: entries b = a..d-1
+    for (int b = a; b < d; ++b) coef.push_back(std::sqrt(sc) * Lm[b * d + a]);
+  return true;
 }
 
 // Raw LSCV_H sums for PD candidates `cands` (all must be PD).
@@ -662,6 +687,16 @@ kde_status lscv_H_raw(kde_ctx* c, const double* X, int64_t n, int d, const std::
                       std::vector<kde_fixed>& out, const float** prepared_Y = nullptr) {
   const int T = kde::tile_for(Kind::LscvMatrix, d, n);
   const int nbmax = kde::cand_per_launch(Kind::LscvMatrix, d);
+  // whitening transform: the sample covariance's Cholesky factor when it is PD, else identity
+  std::vector<double> Lw((size_t)d * d, 0.0);
+  if (m.cov.size() != (size_t)d * d || !cholesky(m.cov, d, Lw)) {
+    Lw.assign((size_t)d * d, 0.0);
+    for (int a = 0; a < d; ++a) Lw[a * d + a] = 1.0;
+  }
+  std::vector<std::vector<double>> coefs(cands.size());
+  for (size_t k = 0; k < cands.size(); ++k)
+    if (!h_coefficients(cands[k], d, Lw, coefs[k]))
+      return fail(c, KDE_E_NUMERIC, "candidate %zu: whitened H^-1 not positive definite", k);
   const int64_t ld = (n + T - 1) / T * T;
   const int nc = (int)cands.size();
   const int P = d * (d + 1) / 2;
@@ -679,8 +714,8 @@ kde_status lscv_H_raw(kde_ctx* c, const double* X, int64_t n, int d, const std::
     L.mat.assign(bytes, 0);
     float* f = reinterpret_cast<float*>(L.mat.data());
     for (int j = 0; j < nb; ++j) {
-      const HCand& hc = cands[b0 + std::min(j, cnt - 1)];
-      for (int u = 0; u < P; ++u) f[j * P + u] = (float)hc.coef[u];
+      const std::vector<double>& cf = coefs[b0 + std::min(j, cnt - 1)];
+      for (int u = 0; u < P; ++u) f[j * P + u] = (float)cf[u];
     }
     Ls.push_back(std::move(L));
     off += 2 * nb;
@@ -688,8 +723,7 @@ kde_status lscv_H_raw(kde_ctx* c, const double* X, int64_t n, int d, const std::
   Ws w;
   TRY(get_ws(c, ld, d, std::max(off, 2), &w));
   if (!prepared_Y || *prepared_Y != w.Y) {
-    std::vector<double> W((size_t)d * d, 0.0);
-    for (int a = 0; a < d; ++a) W[a * d + a] = 1.0;
+    const std::vector<double> W = tri_lower_inverse(Lw, d);    // x' = Lw^-1 (x - mean)
     TRY(gpu_prep(c, X, n, d, W, m.mean, ld, w));
     if (prepared_Y) *prepared_Y = w.Y;
   }
