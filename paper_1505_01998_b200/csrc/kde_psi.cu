@@ -17,7 +17,7 @@ int tile_for(Kind k, int d, int64_t n) {
     case Kind::Psi4: case Kind::Psi6: case Kind::Psi8: {
       static const char* dbg = getenv("KDE_DEBUG_PSI_TILE");   // tests / diagnostics only
       if (dbg && (atoi(dbg) == 512 || atoi(dbg) == 2048)) return atoi(dbg);
-      return n >= (int64_t)64 * 2048 ? 2048 : 512;
+      return n >= (int64_t)128 * 2048 ? 2048 : 512;
     }
     case Kind::LscvScalar: return 512;
     case Kind::LscvMatrix: {

@@ -49,8 +49,8 @@ def test_psi_r_matches_oracle(ctx, n):
 
 
 def test_psi_r_large_tile_path(ctx):
-    # n >= 64*2048 selects the 2048-row tiles (the launch configuration of bench.py);
-    # compared on the exact pair sum over all pairs (oracle, 4 threads).
+    # the largest n served by 512-row tiles (n >= 128*2048 switches to 2048-row tiles, the bench.py
+    # configuration, covered at full size by test_gpu_golden.py); exact pair sum over all pairs.
     n = 64 * 2048 + 37
     x = datagen.sample_mixture("skewed", n, 7)
     g = 0.2
