@@ -123,13 +123,11 @@ def run_reference(args, rank, world):
         return
     import datagen
     x = datagen.config_data("C4")[0]
-    # g1, g2 of the PLUGIN chain for this sample (scalar steps, oracle)
-    import oracle
-    _, C = oracle.mean_cov(x[None, :])
-    sig = C[0, 0] ** 0.5
-    psi8 = 105.0 / (32.0 * np.pi ** 0.5 * sig ** 9)
-    g1 = (2 * 15 / (2 * np.pi) ** 0.5 / (psi8 * x.size)) ** (1 / 9)
-    g2 = g1 * 0.47   # representative; the reference arm times the sums, not the chain
+    # g1, g2 of this sample's PLUGIN chain, as the oracle computed them once at full size
+    # (tests/golden/make_golden.py, which calls only oracle/); each step times the oracle's two
+    # pair sums on a bounded row sample at those bandwidths.
+    tr = json.load(open(os.path.join(ROOT, "tests", "golden", "C4_plugin.json")))["trace"]
+    g1, g2 = tr["g1"], tr["g2"]
     times, vals = [], []
     for s in range(args.warmup + args.steps):
         r = cpu_baseline_sample(x, (g1, g2), seconds=max(2.0, 20.0 / max(1, args.steps)))

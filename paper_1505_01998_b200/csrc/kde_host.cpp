@@ -415,15 +415,20 @@ void shard_range(int64_t tiles, int rank, int world, int64_t* b, int64_t* e) {
   *e = (int64_t)((__int128)tiles * (rank + 1) / world);
 }
 
-// Algorithmic pairs i<j inside tiles [b, e).
+// Algorithmic pairs i<j inside tiles [b, e), one column of tiles at a time (the tile numbering
+// is column-major, Eq. 42-43): O(#columns) instead of O(#tiles) host work per pass.
 double pairs_in_range(int64_t n, int T, int64_t b, int64_t e) {
+  if (e <= b) return 0.0;
+  int64_t lb, qb, le, qe;
+  kde::tile_coords_host(b, &lb, &qb);
+  kde::tile_coords_host(e - 1, &le, &qe);
   double s = 0.0;
-  for (int64_t t = b; t < e; ++t) {
-    int64_t l, q;
-    kde::tile_coords_host(t, &l, &q);
-    int64_t cols = std::min<int64_t>(T, n - l * (int64_t)T);
-    if (q == l) s += (double)cols * (double)(cols - 1) * 0.5;
-    else s += (double)T * (double)cols;
+  for (int64_t l = lb; l <= le; ++l) {
+    const int64_t q0 = (l == lb) ? qb : 0, q1 = (l == le) ? qe : l;   // tiles q0..q1 of column l
+    const double cols = (double)std::min<int64_t>(T, n - l * (int64_t)T);
+    const int64_t off = std::min<int64_t>(q1, l - 1) - q0 + 1;          // q < l: T x cols pairs
+    if (off > 0) s += (double)off * (double)T * cols;
+    if (q1 == l) s += cols * (cols - 1.0) * 0.5;                        // diagonal tile
   }
   return s;
 }
@@ -528,12 +533,17 @@ kde_status run_sums(kde_ctx* c, int d, int64_t n, int64_t ld, int T, int scale, 
 }
 
 // ------------------------------------------------------------------ Psi_r
-// The kernel evaluates He_r(s = u^2) with exact integer coefficients; the only parameter is
-// the exponent scale: exp(-u^2/2) = 2^(s * c0), c0 = -log2(e)/2.
+// The kernel evaluates He_r in t = u^2 - (r-1) with exact integer coefficients; the parameters
+// are the exponent scale c0 and, per accumulator class k, the MUFU offset o_k and the exact
+// fp64 factor that undoes it: 2^(u^2 c0) = 2^(t c0 + o_k) * 2^((r-1) c0 - o_k).
 void psi_coeffs(int r, kde::PsiParams& p) {
-  (void)r;
   std::memset(&p, 0, sizeof(p));
-  p.c[0] = (float)(-kLog2e / 2.0);
+  p.c0 = (float)(-kLog2e / 2.0);
+  const double Kc0 = (double)(r - 1) * (double)p.c0;             // exact in fp64
+  for (int k = 0; k < 8; ++k) {
+    p.o[k] = (float)(Kc0 - (16.0 + k / 8.0));
+    p.fac[k] = std::exp2(Kc0 - (double)p.o[k]);                    // exponent exact in fp64
+  }
 }
 
 double he_at_zero(int r) { return r == 4 ? 3.0 : (r == 6 ? -15.0 : 105.0); }

@@ -80,20 +80,27 @@ struct Args {
 // ------------------------------------------------------------------ functors
 
 // Psi_r: term He_r(u) exp(-u^2/2) with x pre-scaled by 1/g, so s = (x_i'-x_j')^2 = u^2.
-// He_r is evaluated by Horner in s with its exact integer coefficients.
-// exp(-s/2) = 2^(s c0) with c0 = -log2(e)/2 is taken from MUFU.EX2 as
-//     2^(s c0) = ex2(s c0 - off_k) * 2^off_k,   off_k = 16 + k/8,  k = accumulator class,
-// because MUFU.EX2's relative error has a near-constant bias (-5.1e-8) only for inputs in
-// [-32,-16), and a different, input-dependent one on (-1, 0] where the dominant near pairs
-// live; the sums of Psi_r cancel 1000-5000x at the PLUGIN bandwidths, so that bias pattern
-// alone cost 2e-5..5e-5 relative.  Offsetting into one binade and averaging over 8 fractional
-// shifts (one per accumulator class, undone exactly in fp64 at the flush) brings the error to
-// ~2e-10 of sum|t| at no per-eval cost (measured by tools/term_error.cu).
+// He_r is a polynomial in s with integer coefficients.  Shifting by the mean of
+// its roots, t = s - K with K = r - 1, removes the next-to-leading term and keeps the
+// coefficients exact integers (depressed form; expand (t+K) to recover P:231/P:247):
+//     He_4 = t^2 - 6,   He_6 = t (t^2 - 30) - 40,   He_8 = ((t^2 - 84) t - 224) t + 252,
+// and t comes from the difference in one FFMA, t = fma(d, d, -K): one FP32 op per eval fewer
+// than Horner in s (r = 6: 6 instead of 7).  exp(-s/2) = 2^(s c0), c0 = -log2(e)/2, is taken
+// from MUFU.EX2 as
+//     2^(s c0) = ex2(t c0 + o_k) * 2^(K c0 - o_k),   o_k = fp32(K c0 - 16 - k/8),
+// k = accumulator class (the row slot), with the factor 2^(K c0 - o_k) applied exactly in fp64
+// at the flush.  The MUFU input is then s c0 - (16 + k/8) up to one rounding: MUFU.EX2's
+// relative error has a near-constant bias (-5.1e-8) only for inputs in [-32,-16), and a
+// different, input-dependent one on (-1, 0] where the dominant near pairs live; the sums of
+// Psi_r cancel 1000-5000x at the PLUGIN bandwidths, so that bias pattern alone cost 2e-5..5e-5
+// relative.  Offsetting into one binade and averaging over 8 fractional shifts brings the error
+// to ~2e-10 of sum|t| at no per-eval cost (measured by tools/term_error.cu).
 template <int RORD, int NT_>
 struct FPsi {
   static constexpr int NT = NT_, D = 1, R = 8, T = NT_ * 8, NOUT = 1, CH = T < 1024 ? T : 1024, MINB = 768 / NT_;
   static constexpr int NP = R / 2;   // row pairs (r = 2p, 2p+1) packed into fp32x2 lanes
   static constexpr int G = 16;       // columns per compensated group
+  static constexpr float K = (float)(RORD - 1);
   static constexpr bool kClampable = true;
   using Params = PsiParams;
   f2 xr[NP];
@@ -110,27 +117,27 @@ struct FPsi {
   }
   static __device__ __forceinline__ int64_t row0(int64_t q) { return q * T + 8 * (int64_t)threadIdx.x; }
 
-  // He_r(s) by Horner with exact integer coefficients, two lanes at once.
-  __device__ __forceinline__ f2 poly(f2 s) const {
-    if (RORD == 4) return fma2(add2(s, pk(-6.f, -6.f)), s, pk(3.f, 3.f));
-    if (RORD == 6) return fma2(fma2(add2(s, pk(-15.f, -15.f)), s, pk(45.f, 45.f)), s, pk(-15.f, -15.f));
-    return fma2(fma2(fma2(add2(s, pk(-28.f, -28.f)), s, pk(210.f, 210.f)), s, pk(-420.f, -420.f)), s,
-                pk(105.f, 105.f));
+  // He_r(t + K) in the depressed form, two lanes at once.
+  __device__ __forceinline__ f2 poly(f2 t) const {
+    if (RORD == 4) return fma2(t, t, pk(-6.f, -6.f));
+    if (RORD == 6) return fma2(fma2(t, t, pk(-30.f, -30.f)), t, pk(-40.f, -40.f));
+    return fma2(fma2(fma2(t, t, pk(-84.f, -84.f)), t, pk(-224.f, -224.f)), t, pk(252.f, 252.f));
   }
-
-  // MUFU offset of accumulator class r (= row slot): off_r = 16 + r/8 (see the comment above).
-  static __device__ __forceinline__ float off(int r) { return 16.0f + 0.125f * (float)r; }
 
   // Accumulation: the G = 16 terms of one column group of a row are summed in
   // fp32 (sorted data: the terms of a group have similar magnitude), then added to the row's
   // running sum with Fast2Sum (rounding error kept in a compensation register); fp64 flush
-  // every 256 columns.  A plain fp32 running sum drops the one-signed far-pair tail terms
+  // every 1024 columns.  A plain fp32 running sum drops the one-signed far-pair tail terms
   // (~1e-7..1e-6) next to near-pair sums (~10): measured -1.4e-5 relative at T=2048.
   template <bool MASK, bool CLAMP = false>
   __device__ __forceinline__ void compute(const float* __restrict__ sc, const Params& p, bool diag,
                                           int jlim) {
     const int ib = 8 * threadIdx.x;   // local index of row r is ib + r
-    const f2 c0 = pk(p.c[0], p.c[0]);
+    const f2 c0 = pk(p.c0, p.c0);
+    const f2 mk = pk(-K, -K);
+    f2 o[NP];
+#pragma unroll
+    for (int q = 0; q < NP; ++q) o[q] = pk(p.o[2 * q], p.o[2 * q + 1]);
     for (int jc = 0; jc < T; jc += CH) {
       if (MASK && jc >= jlim) break;
       f2 a[NP], cmp[NP];
@@ -149,32 +156,31 @@ struct FPsi {
           for (int k = 0; k < 4; ++k) {
 #pragma unroll
             for (int q = 0; q < NP; ++q) {
-              const f2 noff = pk(-off(2 * q), -off(2 * q + 1));
               const f2 d = sub2(xr[q], pk(cv[k], cv[k]));
-              f2 sq = mul2(d, d);
+              f2 t = fma2(d, d, mk);                        // t = s - K, one rounding
               if (MASK || CLAMP) {
-                // s >= 1e4 gives 2^(-7229) == 0 exactly.  CLAMP (data with |x'| > 3e4, flagged by
-                // the prep kernel) keeps He_r(s) finite for far outliers (s^4 overflows fp32
-                // beyond s ~ 4e9), so no inf * 0 = NaN; other data never need it.
-                float s0, s1;
-                upk(sq, s0, s1);
+                // t >= 1e4 gives 2^(-7213) == 0 exactly.  CLAMP (data with |x'| > 3e4, flagged
+                // by the prep kernel) keeps He_r finite for far outliers (t^4 overflows fp32
+                // beyond t ~ 4e9), so no inf * 0 = NaN; other data never need it.
+                float t0, t1;
+                upk(t, t0, t1);
                 if (CLAMP) {
-                  s0 = fminf(s0, 1.0e4f);
-                  s1 = fminf(s1, 1.0e4f);
+                  t0 = fminf(t0, 1.0e4f);
+                  t1 = fminf(t1, 1.0e4f);
                 }
                 if (MASK) {
                   const int jj = j + j4 + k;
                   const bool ok0 = (jj < jlim) && (!diag || jj > ib + 2 * q);
                   const bool ok1 = (jj < jlim) && (!diag || jj > ib + 2 * q + 1);
-                  s0 = ok0 ? s0 : 1.0e4f;
-                  s1 = ok1 ? s1 : 1.0e4f;
+                  t0 = ok0 ? t0 : 1.0e4f;
+                  t1 = ok1 ? t1 : 1.0e4f;
                 }
-                sq = pk(s0, s1);
+                t = pk(t0, t1);
               }
               float a0, a1;
-              upk(fma2(sq, c0, noff), a0, a1);
+              upk(fma2(t, c0, o[q]), a0, a1);
               const f2 e = pk(ex2(a0), ex2(a1));
-              grp[q] = fma2(poly(sq), e, grp[q]);
+              grp[q] = fma2(poly(t), e, grp[q]);
             }
           }
         }
@@ -192,8 +198,8 @@ struct FPsi {
         float a0, a1, c0_, c1_;
         upk(a[q], a0, a1);
         upk(cmp[q], c0_, c1_);
-        s += ((double)a0 + (double)c0_) * exp2((double)off(2 * q));
-        s += ((double)a1 + (double)c1_) * exp2((double)off(2 * q + 1));
+        s += ((double)a0 + (double)c0_) * p.fac[2 * q];
+        s += ((double)a1 + (double)c1_) * p.fac[2 * q + 1];
       }
       acc += s;
     }

@@ -96,12 +96,22 @@ __global__ void __launch_bounds__(kMomThreads) moments_kernel(const double* __re
   }
 }
 
-__global__ void reduce_parts_kernel(const double* __restrict__ part, int nblk, int width,
-                                    double* __restrict__ out) {
-  for (int k = threadIdx.x; k < width; k += blockDim.x) {
-    double s = 0.0;
-    for (int b = 0; b < nblk; ++b) s += part[(size_t)b * width + k];
-    out[k] = s;
+// One block per output k; thread t adds partials t, t+256, ... in order, then the fixed warp
+// butterfly and fixed cross-warp order: deterministic for a given block count.
+__global__ void __launch_bounds__(kMomThreads) reduce_parts_kernel(const double* __restrict__ part,
+                                                                   int nblk, int width,
+                                                                   double* __restrict__ out) {
+  __shared__ double red[kMomThreads / 32];
+  const int k = blockIdx.x;
+  double s = 0.0;
+  for (int b = threadIdx.x; b < nblk; b += kMomThreads) s += part[(size_t)b * width + k];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = red[0];
+    for (int w = 1; w < kMomThreads / 32; ++w) t += red[w];
+    out[k] = t;
   }
 }
 
@@ -119,7 +129,7 @@ cudaError_t launch_moments2(const double* X, int64_t n, int d, const double* mea
 
 cudaError_t launch_reduce_parts(const double* part, int nblk, int width, double* out,
                                 cudaStream_t s) {
-  reduce_parts_kernel<<<1, 160, 0, s>>>(part, nblk, width, out);
+  reduce_parts_kernel<<<width, kMomThreads, 0, s>>>(part, nblk, width, out);
   return cudaGetLastError();
 }
 

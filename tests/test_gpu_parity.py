@@ -198,6 +198,18 @@ def test_shards_add_up_exactly(ctx, kind, world):
     assert [f.key() for f in acc] == [f.key() for f in full]
 
 
+@pytest.mark.parametrize("n,world", [(9000, 3), (300001, 8)])
+def test_profiled_pair_counts_partition_all_pairs(ctx, n, world):
+    # The library's algorithmic eval count (bench.py's roofline numerator) summed over the
+    # shards of a ragged n is exactly n(n-1)/2 per candidate (512- and 2048-tiles).
+    x = dev(datagen.sample_mixture("skewed", n, 4))
+    tot = 0.0
+    for r in range(world):
+        ctx.raw_sums(kb.SUM_PSI6, x, [0.3], shard=(r, world))
+        tot += ctx.last_profile()["pair_evals"]
+    assert tot == n * (n - 1) / 2
+
+
 # ----------------------------------------------------------------------------- NM selector
 def test_lscv_H_select_small_matches_oracle(ctx):
     X = datagen.sample_mixture("C3", 600, 13)

@@ -1,0 +1,14 @@
+#!/bin/bash
+# Psi kernel iteration: GPU tests, bench, ncu of the Psi6 and Psi4 launches (separately).
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.txt 2>&1
+tail -3 gpurun_out/pytest_gpu.txt
+timeout 600 python bench.py ${BENCH_ARGS} > gpurun_out/bench.json 2> gpurun_out/bench.err
+cat gpurun_out/bench.json
+for r in 6 4; do
+timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"FPsi<$r" -s 1 -c 1 \
+    -o gpurun_out/prof_psi$r -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_psi$r.log 2>&1
+done
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv \
+    python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/bench_under_ncu.log 2>&1
+ls gpurun_out
