@@ -97,7 +97,7 @@ struct Args {
 // to ~2e-10 of sum|t| at no per-eval cost (measured by tools/term_error.cu).
 template <int RORD, int NT_>
 struct FPsi {
-  static constexpr int NT = NT_, D = 1, R = 8, T = NT_ * 8, NOUT = 1, CH = T < 1024 ? T : 1024, MINB = 768 / NT_;
+  static constexpr int NT = NT_, D = 1, R = 8, T = NT_ * 8, NOUT = 1, CH = T < 1024 ? T : 1024, MINB = 1024 / NT_;
   static constexpr int NP = R / 2;   // row pairs (r = 2p, 2p+1) packed into fp32x2 lanes
   static constexpr int G = 16;       // columns per compensated group
   static constexpr float K = (float)(RORD - 1);
