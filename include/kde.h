@@ -4,9 +4,13 @@
  * SIMD Architectures" (arxiv 1505.01998).  P:NNN = PAPER.md line NNN.
  *
  * Conventions (apply to every call below):
- *  - Ownership: the caller owns every buffer.  Sample matrices are DEVICE pointers (fp64,
- *    d x n, row-major: dimension a of sample i at X[a*n + i], the paper's layout
- *    Eq. 19).  Candidate arrays and outputs are HOST pointers.
+ *  - Ownership: the caller owns every buffer.  Sample matrices (X; Y of kde_evaluate) are fp64,
+ *    d x n, row-major: dimension a of sample i at X[a*n + i], the paper's layout (P:263-273,
+ *    Eq. 19).  They may be DEVICE pointers on the context's GPU or HOST pointers (pageable or
+ *    pinned, told apart with cudaPointerGetAttributes): a host array is copied once per call
+ *    into a context-owned device buffer on the context stream, and all compute runs on the GPU.
+ *    A device pointer of another GPU is KDE_E_INVALID.  Candidate arrays and outputs are HOST
+ *    pointers.  (Parameter names keep the _dev suffix of the common, device-resident case.)
  *  - Errors: a call returns KDE_OK or an error code; on error the outputs are untouched and
  *    kde_last_error(ctx) holds a one-line message.  No C++ exception crosses the boundary.
  *    A CUDA or NCCL failure poisons the context (every later call returns the same code).

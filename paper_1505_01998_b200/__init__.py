@@ -4,7 +4,9 @@ Thin ctypes binding over the C ABI in include/kde.h (libkde_b200.so, built in-tr
 paper_1505_01998_b200.build).  Argument marshalling only: every step of the path (moments,
 data prep, pair sums, reductions, the NCCL all-reduce) runs in the library.  PyTorch provides
 device memory, the CUDA stream and (for world > 1) the process group used to broadcast the
-NCCL unique id.  There is no CPU fallback: if the library is missing this module raises.
+NCCL unique id.  Sample matrices may be CUDA tensors or host arrays (the library copies host
+arrays to the GPU inside the call).  There is no CPU fallback: if the library is missing this
+module raises.
 """
 from __future__ import annotations
 
@@ -167,20 +169,43 @@ def default_opts() -> SelectOpts:
     return o
 
 
-def _dev_matrix(X):
-    """(d, n) view of a CUDA fp64 tensor; raises for anything else (no host fallback)."""
+class _Samples:
+    """A (d, n) fp64 sample matrix as the C ABI sees it: pointer, d, n (plus a reference that
+    keeps the memory alive for the duration of the call)."""
+    __slots__ = ("ptr", "d", "n", "host", "_keep")
+
+    def __init__(self, ptr, d, n, host, keep):
+        self.ptr, self.d, self.n, self.host, self._keep = ctypes.c_void_p(ptr), d, n, host, keep
+
+    @property
+    def shape(self):
+        return (self.d, self.n)
+
+
+def _samples(X) -> _Samples:
+    """Marshal a sample matrix, (n,) or (d, n) fp64.  A CUDA tensor is passed as a device
+    pointer; a host array (numpy, or a CPU tensor, pinned or not) as a host pointer, which the
+    library copies to the GPU inside the call (include/kde.h).  There is no CPU compute path."""
     import torch
-    if not isinstance(X, torch.Tensor) or not X.is_cuda:
-        raise TypeError("sample matrix must be a CUDA torch.Tensor (use to_device())")
-    if X.dtype != torch.float64:
-        raise TypeError("sample matrix must be float64")
-    if X.dim() == 1:
-        X = X.unsqueeze(0)
-    if X.dim() != 2:
-        raise ValueError("sample matrix must be (n,) or (d, n)")
-    if not X.is_contiguous():
+    if isinstance(X, torch.Tensor):
+        if X.dtype != torch.float64:
+            raise TypeError("sample matrix must be float64")
+        if X.dim() == 1:
+            X = X.unsqueeze(0)
+        if X.dim() != 2:
+            raise ValueError("sample matrix must be (n,) or (d, n)")
         X = X.contiguous()
-    return X
+        return _Samples(X.data_ptr(), X.shape[0], X.shape[1], not X.is_cuda, X)
+    if not isinstance(X, np.ndarray):
+        raise TypeError("sample matrix must be a torch.Tensor or a numpy array")
+    if X.dtype != np.float64:
+        raise TypeError("sample matrix must be float64")
+    if X.ndim == 1:
+        X = X[None, :]
+    if X.ndim != 2:
+        raise ValueError("sample matrix must be (n,) or (d, n)")
+    X = np.ascontiguousarray(X)
+    return _Samples(X.ctypes.data, X.shape[0], X.shape[1], True, X)
 
 
 def to_device(X, device=None, pinned: bool = True):
@@ -251,52 +276,52 @@ class Context:
 
     # ---- the five entry points
     def psi_r(self, x, r: int, g) -> np.ndarray:
-        X = _dev_matrix(x)
+        X = _samples(x)
         if X.shape[0] != 1:
             raise KDEError(2, "Psi_r needs univariate data")
         gb, gp = _dbuf(np.atleast_1d(g))
         out = np.zeros(gb.size)
-        self._check(lib().kde_psi_r(self._h, ctypes.c_void_p(X.data_ptr()), X.shape[1], int(r), gp,
+        self._check(lib().kde_psi_r(self._h, X.ptr, X.shape[1], int(r), gp,
                                     gb.size, out.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
         return out
 
     def plugin_h(self, x):
-        X = _dev_matrix(x)
+        X = _samples(x)
         if X.shape[0] != 1:
             raise KDEError(2, "PLUGIN needs univariate data")
         h = ctypes.c_double()
         tr = PluginTrace()
-        self._check(lib().kde_plugin_h(self._h, ctypes.c_void_p(X.data_ptr()), X.shape[1],
+        self._check(lib().kde_plugin_h(self._h, X.ptr, X.shape[1],
                                        ctypes.byref(h), ctypes.byref(tr)))
         return h.value, tr.as_dict()
 
     def lscv_h_scores(self, X, h) -> np.ndarray:
-        X = _dev_matrix(X)
+        X = _samples(X)
         hb, hp = _dbuf(np.atleast_1d(h))
         out = np.zeros(hb.size)
-        self._check(lib().kde_lscv_h_scores(self._h, ctypes.c_void_p(X.data_ptr()), X.shape[1], X.shape[0],
+        self._check(lib().kde_lscv_h_scores(self._h, X.ptr, X.shape[1], X.shape[0],
                                             hp, hb.size, out.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
         return out
 
     def lscv_H_scores(self, X, vechs, penalty: float = float("nan")) -> np.ndarray:
-        X = _dev_matrix(X)
+        X = _samples(X)
         d = X.shape[0]
         vb, vp = _dbuf(np.atleast_2d(vechs))
         if vb.shape[1] != d * (d + 1) // 2:
             raise KDEError(7, "vech length does not match d")
         out = np.zeros(vb.shape[0])
-        self._check(lib().kde_lscv_H_scores(self._h, ctypes.c_void_p(X.data_ptr()), X.shape[1], d, vp,
+        self._check(lib().kde_lscv_H_scores(self._h, X.ptr, X.shape[1], d, vp,
                                             vb.shape[0], float(penalty),
                                             out.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
         return out
 
     def select_bandwidth(self, method: int, X, **opts) -> dict:
-        X = _dev_matrix(X)
+        X = _samples(X)
         o = default_opts()
         for k, v in opts.items():
             setattr(o, k, v)
         r = Bandwidth()
-        self._check(lib().kde_select_bandwidth(self._h, int(method), ctypes.c_void_p(X.data_ptr()), X.shape[1],
+        self._check(lib().kde_select_bandwidth(self._h, int(method), X.ptr, X.shape[1],
                                                X.shape[0], ctypes.byref(o), ctypes.byref(r)))
         d = X.shape[0]
         out = {"method": r.method, "d": r.d, "h": r.h, "objective": r.objective,
@@ -309,10 +334,10 @@ class Context:
 
     def lscv_h_scores_materialized(self, X, h, h_per_pass: int = 1) -> np.ndarray:
         """LSCV_h scores via the paper's two-phase algorithm (materialised S(v) buffer)."""
-        X = _dev_matrix(X)
+        X = _samples(X)
         hb, hp = _dbuf(np.atleast_1d(h))
         out = np.zeros(hb.size)
-        self._check(lib().kde_lscv_h_scores_materialized(self._h, ctypes.c_void_p(X.data_ptr()), X.shape[1],
+        self._check(lib().kde_lscv_h_scores_materialized(self._h, X.ptr, X.shape[1],
                                                          X.shape[0], hp, hb.size, int(h_per_pass),
                                                          out.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
         return out
@@ -322,7 +347,7 @@ class Context:
 
     def evaluate(self, X, Y, H) -> np.ndarray:
         """fhat at the columns of Y (both CUDA tensors, d x n and d x m); H: d x d or vech."""
-        Xd, Yd = _dev_matrix(X), _dev_matrix(Y)
+        Xd, Yd = _samples(X), _samples(Y)
         d = Xd.shape[0]
         if Yd.shape[0] != d:
             raise KDEError(7, "query dimension differs from the sample dimension")
@@ -330,35 +355,35 @@ class Context:
         vh = Hn if Hn.ndim == 1 else np.array([Hn[i, j] for j in range(d) for i in range(j, d)])
         vb, vp = _dbuf(vh)
         out = np.zeros(Yd.shape[1])
-        self._check(lib().kde_evaluate(self._h, ctypes.c_void_p(Xd.data_ptr()), Xd.shape[1], d,
-                                       ctypes.c_void_p(Yd.data_ptr()), Yd.shape[1], vp,
+        self._check(lib().kde_evaluate(self._h, Xd.ptr, Xd.shape[1], d,
+                                       Yd.ptr, Yd.shape[1], vp,
                                        out.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
         return out
 
     def aqp_1d(self, x, h: float, lo, hi):
         """(COUNT, SUM, AVG) arrays over the intervals [lo_q, hi_q] (univariate)."""
-        Xd = _dev_matrix(x)
+        Xd = _samples(x)
         if Xd.shape[0] != 1:
             raise KDEError(2, "AQP closed forms are univariate")
         lb, lp = _dbuf(np.atleast_1d(lo))
         hb, hp = _dbuf(np.atleast_1d(hi))
         cnt, sm, av = (np.zeros(lb.size) for _ in range(3))
         P = lambda a: a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
-        self._check(lib().kde_aqp_1d(self._h, ctypes.c_void_p(Xd.data_ptr()), Xd.shape[1], float(h), lp, hp,
+        self._check(lib().kde_aqp_1d(self._h, Xd.ptr, Xd.shape[1], float(h), lp, hp,
                                      lb.size, P(cnt), P(sm), P(av)))
         return cnt, sm, av
 
     def raw_sums(self, kind: int, X, cand, shard=None):
         """Exact fixed-point pair sums (list of Fixed).  shard=(rank, world) computes one shard
         without the collective; None = this context's rank/world, all-reduced."""
-        Xd = _dev_matrix(X)
+        Xd = _samples(X)
         cb, cp = _dbuf(cand)
         d = Xd.shape[0]
         nc = cb.size if kind in (SUM_PSI4, SUM_PSI6, SUM_PSI8, SUM_LSCV_h) else cb.reshape(-1, d * (d + 1) // 2).shape[0]
         nout = nc if kind in (SUM_PSI4, SUM_PSI6, SUM_PSI8) else 2 * nc
         out = (Fixed * nout)()
         sr, sw = (0, 0) if shard is None else shard
-        self._check(lib().kde_raw_sums(self._h, int(kind), ctypes.c_void_p(Xd.data_ptr()), Xd.shape[1], d,
+        self._check(lib().kde_raw_sums(self._h, int(kind), Xd.ptr, Xd.shape[1], d,
                                        cp, nc, int(sr), int(sw), out))
         return list(out)
 

@@ -78,6 +78,9 @@ struct kde_ctx {
   // sorted copy of univariate samples (+ CUB temp), context-owned
   void* sort_ws = nullptr;
   size_t sort_bytes = 0;
+  // device copies of host-resident inputs (slot 0: samples X, slot 1: queries Y), context-owned
+  void* in_ws[2] = {nullptr, nullptr};
+  size_t in_bytes[2] = {0, 0};
   // pinned host staging for limbs
   long long* h_limbs = nullptr;
   size_t h_limbs_cap = 0;
@@ -779,12 +782,34 @@ kde_status lscv_H_eval(kde_ctx* c, const double* X, int64_t n, int d, const Mome
   return KDE_OK;
 }
 
-kde_status validate_X(kde_ctx* c, const void* X, int64_t n, int32_t d, int64_t nmin) {
+// Input arrays may be device or host memory (include/kde.h): a host array (pageable or pinned)
+// is copied into a context-owned device buffer on the context stream, so the rest of the call
+// always reads device memory.  A device pointer of another GPU is rejected.
+kde_status stage_input(kde_ctx* c, const double*& X, size_t count, int slot) {
+  cudaPointerAttributes at;
+  cudaError_t e = cudaPointerGetAttributes(&at, X);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(c, KDE_E_INVALID, "cannot classify the input pointer: %s", cudaGetErrorString(e));
+  }
+  if (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) {
+    if (at.type == cudaMemoryTypeDevice && at.device != c->device)
+      return fail(c, KDE_E_INVALID, "input lives on device %d, context on device %d", at.device, c->device);
+    return KDE_OK;
+  }
+  Range r("kde.h2d");
+  TRY(grow(c, &c->in_ws[slot], &c->in_bytes[slot], std::max<size_t>(count, 1) * sizeof(double)));
+  CUDA_TRY(c, cudaMemcpyAsync(c->in_ws[slot], X, count * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  X = static_cast<const double*>(c->in_ws[slot]);
+  return KDE_OK;
+}
+
+kde_status validate_X(kde_ctx* c, const double*& X, int64_t n, int32_t d, int64_t nmin) {
   if (!X) return fail(c, KDE_E_INVALID, "null sample pointer");
   if (d < 1 || d > kde::kMaxDim) return fail(c, KDE_E_DIM_MISMATCH, "d=%d outside [1,16]", d);
   if (n < nmin) return fail(c, n < 1 ? KDE_E_INVALID : KDE_E_INSUFFICIENT_SAMPLES, "n=%lld too small", (long long)n);
   if (n > 2147483647LL) return fail(c, KDE_E_INVALID, "n > 2^31-1");
-  return KDE_OK;
+  return stage_input(c, X, (size_t)n * (size_t)d, 0);
 }
 
 // ------------------------------------------------------------------ Nelder–Mead (reading Z8)
@@ -1013,6 +1038,8 @@ void kde_destroy(kde_ctx* c) {
   if (c->sort_ws) cudaFree(c->sort_ws);
   if (c->ev_ws) cudaFree(c->ev_ws);
   if (c->mat_ws) cudaFree(c->mat_ws);
+  for (void* p : c->in_ws)
+    if (p) cudaFree(p);
   if (c->h_limbs) cudaFreeHost(c->h_limbs);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   delete c;
@@ -1260,6 +1287,7 @@ kde_status kde_evaluate(kde_ctx* c, const double* X, int64_t n, int32_t d, const
   if (!Y || !vh || !f || m < 0) return fail(c, KDE_E_INVALID, "null query/bandwidth/output pointer");
   if (m == 0) return KDE_OK;
   if (m > 2147483647LL) return fail(c, KDE_E_INVALID, "m > 2^31-1");
+  TRY(stage_input(c, Y, (size_t)m * (size_t)d, 1));
   std::vector<double> H = unvech(vh, d), L;
   if (!cholesky(H, d, L)) return fail(c, KDE_E_NONPOSITIVE_BW, "bandwidth matrix is not positive definite");
   double det = 1.0;

@@ -81,6 +81,12 @@ def test_null_context_is_rejected():
     assert L.kde_last_error(None) == b"null context"
 
 
-def test_binding_refuses_host_arrays():
+def test_binding_marshals_host_and_rejects_other_dtypes():
+    # host fp64 arrays are passed as host pointers (the library copies them to the GPU inside
+    # the call); anything that is not fp64 is refused before the C ABI is reached
+    s = kb._samples(np.zeros(4))
+    assert s.shape == (1, 4) and s.host and s.ptr.value
     with pytest.raises(TypeError):
-        kb._dev_matrix(np.zeros((1, 4)))
+        kb._samples(np.zeros((1, 4), dtype=np.float32))
+    with pytest.raises(TypeError):
+        kb._samples([0.0, 1.0])

@@ -260,3 +260,19 @@ def test_bitwise_reproducible_over_ten_runs(ctx):
     ref = (ctx.plugin_h(x), ctx.lscv_h_scores(X, hs).tolist(), ctx.lscv_H_scores(X, [[0.05, 0.01, 0.04]]).tolist())
     for _ in range(9):
         assert (ctx.plugin_h(x), ctx.lscv_h_scores(X, hs).tolist(), ctx.lscv_H_scores(X, [[0.05, 0.01, 0.04]]).tolist()) == ref
+
+
+def test_host_inputs_equal_device_inputs(ctx):
+    # Host sample arrays (pageable numpy, pinned tensor) go through the same C ABI calls; the
+    # library copies them to the GPU inside the call, so results are bit-identical.
+    x = datagen.sample_mixture("skewed", 20000, 12)
+    X = datagen.sample_mixture("C3", 3000, 12)
+    Y = datagen.sample_mixture("C3", 700, 13)
+    hs = np.linspace(0.05, 1.0, 10)
+    H = [[0.05, 0.01, 0.04]]
+    xp = torch.from_numpy(x).pin_memory()
+    assert ctx.plugin_h(x) == ctx.plugin_h(dev(x)) == ctx.plugin_h(xp)
+    assert ctx.lscv_h_scores(X, hs).tolist() == ctx.lscv_h_scores(dev(X), hs).tolist()
+    assert ctx.lscv_H_scores(X, H).tolist() == ctx.lscv_H_scores(dev(X), H).tolist()
+    assert ctx.evaluate(X, Y, H[0]).tolist() == ctx.evaluate(dev(X), dev(Y), H[0]).tolist()
+    assert ctx.evaluate(dev(X), Y, H[0]).tolist() == ctx.evaluate(X, dev(Y), H[0]).tolist()
