@@ -265,6 +265,13 @@ class Context:
         if rc != 0:
             raise KDEError(rc, lib().kde_last_error(self._h).decode(errors="replace"))
 
+    def set_workspace(self, buf):
+        """Hand the library a caller-owned device workspace (a CUDA tensor that must outlive its
+        use; kde_workspace_bytes tells the size a call needs)."""
+        self._ws = buf
+        self._check(lib().kde_set_workspace(self._h, ctypes.c_void_p(buf.data_ptr()),
+                                            buf.numel() * buf.element_size()))
+
     def set_profiling(self, on: bool):
         self._check(lib().kde_set_profiling(self._h, 1 if on else 0))
 

@@ -129,7 +129,9 @@ constexpr double kPi = 3.14159265358979323846;
 inline float __int_as_float_host(uint32_t b) { float f; std::memcpy(&f, &b, 4); return f; }
 constexpr double kLog2e = 1.44269504088896340736;
 
-// Workspace layout (all offsets 256-byte aligned).
+// Workspace layout (all offsets 256-byte aligned): Y | part | small | limbs.  Everything but the
+// limbs sits at offsets that depend only on (d, ld), so a call that prepares Y once and then
+// launches batches with different output counts (Nelder-Mead) sees the same prep flags.
 struct Ws {
   float* Y;                 // prepared fp32 data, d x ld
   unsigned long long* limbs;
@@ -167,11 +169,11 @@ kde_status get_ws(kde_ctx* c, int64_t ld, int32_t d, int32_t n_out, Ws* w) {
   }
   w->Y = (float*)base;
   base += align256((size_t)d * ld * sizeof(float));
-  w->limbs = (unsigned long long*)base;
-  base += align256((size_t)std::max(n_out, 1) * kde::kLimbs * sizeof(long long));
   w->part = (double*)base;
   base += align256((size_t)1024 * 136 * sizeof(double));
   w->small = (double*)base;
+  base += align256((16 + 256 + 136 + 16) * sizeof(double));
+  w->limbs = (unsigned long long*)base;
   return KDE_OK;
 }
 

@@ -53,3 +53,19 @@ def test_multistart_single_equals_default(ctx):
     a = ctx.select_bandwidth(kb.LSCV_H, X, max_iter=100)
     b = ctx.select_bandwidth(kb.LSCV_H, X, max_iter=100, nm_starts=1, speculative=0)
     assert np.array_equal(a["vechH"], b["vechH"]) and a["iterations"] == b["iterations"]
+
+
+def test_multistart_nm_on_dirty_caller_workspace():
+    # Regression: the prep flags must sit at an offset that does not depend on a batch's output
+    # count (Nelder-Mead prepares the data once, then launches batches of 4..16 candidates).  A
+    # caller workspace filled with 0xFF bytes exposes any read of a flag the prep did not write.
+    X = datagen.sample_mixture("C3", 4000, 23)
+    clean = kb.Context()
+    ref = clean.select_bandwidth(kb.LSCV_H, X, max_iter=60, nm_starts=4)
+    clean.close()
+    c = kb.Context()
+    ws = torch.full((kb.lib().kde_workspace_bytes(4000, 2, 64),), 255, dtype=torch.uint8, device="cuda")
+    c.set_workspace(ws)
+    got = c.select_bandwidth(kb.LSCV_H, X, max_iter=60, nm_starts=4)
+    c.close()
+    assert np.array_equal(got["vechH"], ref["vechH"]) and got["objective"] == ref["objective"]

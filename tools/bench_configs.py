@@ -142,7 +142,13 @@ def run(cfg, reps):
         Xd = kb.to_device(X)
         cands = datagen.c5_candidates(n, 256)
         dt, prof, g = timed(lambda: ctx.lscv_H_scores(Xd, cands), reps)
-        line(cfg, "lscv_H_scores 256 H, d=4, n=2^18", dt, prof, {"g_first": g[:4].tolist()})
+        # d = 4 is FMA-bound: per eval 10 (quadratic form) + 2 (accumulate) FP32
+        # lane-ops, plus 4 + 10 per pair over the 16 candidates of a visit, at the measured
+        # 125 FP32 lane-ops/clk/SM (tools/pipes.cu)
+        fma_peak = 125.0 / (12 + 14 / 16) * SMS * 1965e6
+        ev = prof["pair_evals"] / (prof["pair_ms"] / 1e3)
+        line(cfg, "lscv_H_scores 256 H, d=4, n=2^18", dt, prof,
+             {"g_first": g[:4].tolist(), "fma_bound_evals_per_s": fma_peak, "frac_fma_bound": ev / fma_peak})
 
 
 if __name__ == "__main__":
