@@ -21,3 +21,8 @@ print("eval", ctx.evaluate(X, kb.to_device(datagen.sample_mixture("C3", 600, 3))
 print("aqp", ctx.aqp_1d(x, 0.2, [-1.0], [1.0]))
 print("materialized", ctx.lscv_h_scores_materialized(X, np.linspace(0.1, 1, 4), 4))
 print("select H", ctx.select_bandwidth(kb.LSCV_H, X, max_iter=5)["objective"])
+print("select H multistart", ctx.select_bandwidth(kb.LSCV_H, X, max_iter=8, nm_starts=3)["objective"])
+print("select h refine", ctx.select_bandwidth(kb.LSCV_h, X, n_grid=20, refine_steps=2)["h"])
+print("plugin host input", ctx.plugin_h(datagen.sample_mixture("skewed", 1500, 1))[0])
+print("psi shards", [kb.fixed_value(f) for r in range(3) for f in ctx.raw_sums(kb.SUM_PSI6, x, [0.3], shard=(r, 3))])
+print("select plugin", ctx.select_bandwidth(kb.PLUGIN, x)["h"])
