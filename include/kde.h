@@ -67,7 +67,9 @@ typedef struct {
   double tol_rel;        /* LSCV_H stop when f_worst - f_best <= tol_rel*|f_best|; 1e-7          */
   double penalty;        /* LSCV_H objective assigned to a non-positive-definite H; 1e300        */
   int32_t speculative;   /* LSCV_H: 1 = evaluate {reflect, expand, contract_out, contract_in} as
-                            one GPU batch per iteration (same decisions as serial NM); 0 = serial */
+                            one GPU batch per iteration; 0 (default) = serial NM, 1-2 GPU rounds of
+                            1 candidate per iteration.  Same decisions either way; serial does ~2x
+                            fewer evaluations and is ~1.5x faster end to end */
   int32_t refine_steps;  /* LSCV_h: after the grid argmin, up to this many bracket sections (16 new
                             h per step, one GPU pass each) around it ("Golden ratio"); 0 = off */
   double refine_tol;     /* LSCV_h: stop refining when the bracket is narrower than tol * h; 1e-9 */

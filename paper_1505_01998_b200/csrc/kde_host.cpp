@@ -720,7 +720,7 @@ kde_status lscv_H_raw(kde_ctx* c, const double* X, int64_t n, int d, const std::
   for (int b0 = 0; b0 < nc; b0 += nbmax) {
     const int cnt = std::min(nbmax, nc - b0);
     int nb = cnt;
-    if (d <= 4) nb = cnt <= 4 ? 4 : (cnt <= 8 ? 8 : 16);
+    if (d <= 4) nb = cnt <= 2 ? cnt : (cnt <= 4 ? 4 : (cnt <= 8 ? 8 : 16));
     nb = std::min(nb, nbmax);
     if (d > 4) nb = nbmax;
     SumLaunch L;
@@ -990,7 +990,7 @@ void kde_default_opts(kde_select_opts* o) {
   o->max_iter = 500;
   o->tol_rel = 1e-7;
   o->penalty = 1e300;
-  o->speculative = 1;
+  o->speculative = 0;       // serial rounds: fewer candidates, faster on B200
   o->refine_steps = 0;
   o->refine_tol = 1e-9;
   o->nm_starts = 1;

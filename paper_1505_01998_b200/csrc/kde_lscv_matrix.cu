@@ -9,6 +9,8 @@ namespace kde {
 
 template <int D, int NT>
 static cudaError_t lscv_mono_dt(int nb, const LaunchCfg& c, const LscvMatrixParams& p) {
+  if (nb <= 1) return launch_pair<FLscvMono<D, NT, 1>>(c, p);   // serial Nelder-Mead steps
+  if (nb <= 2) return launch_pair<FLscvMono<D, NT, 2>>(c, p);
   if (nb <= 4) return launch_pair<FLscvMono<D, NT, 4>>(c, p);
   if (nb <= 8) return launch_pair<FLscvMono<D, NT, 8>>(c, p);
   return launch_pair<FLscvMono<D, NT, 16>>(c, p);

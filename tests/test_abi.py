@@ -67,7 +67,7 @@ def test_fixed_point_value_and_exact_add():
 
 def test_default_opts_and_workspace_size():
     o = kb.default_opts()
-    assert (o.n_grid, o.range_factor, o.max_iter, o.tol_rel, o.penalty, o.speculative) == (150, 4.0, 500, 1e-7, 1e300, 1)
+    assert (o.n_grid, o.range_factor, o.max_iter, o.tol_rel, o.penalty, o.speculative) == (150, 4.0, 500, 1e-7, 1e300, 0)
     L = kb.lib()
     assert L.kde_workspace_bytes(1 << 20, 1, 1) >= (1 << 20) * 4
     assert L.kde_workspace_bytes(0, 1, 1) == 0

@@ -51,7 +51,7 @@ def test_multistart_nm_matches_oracle(ctx):
 def test_multistart_single_equals_default(ctx):
     X = kb.to_device(datagen.sample_mixture("C3", 1500, 5))
     a = ctx.select_bandwidth(kb.LSCV_H, X, max_iter=100)
-    b = ctx.select_bandwidth(kb.LSCV_H, X, max_iter=100, nm_starts=1, speculative=0)
+    b = ctx.select_bandwidth(kb.LSCV_H, X, max_iter=100, nm_starts=1, speculative=1)
     assert np.array_equal(a["vechH"], b["vechH"]) and a["iterations"] == b["iterations"]
 
 

@@ -78,7 +78,7 @@ def run(cfg, reps):
         X = datagen.config_data("C3")
         Xd = kb.to_device(X)
         dt, prof, r = timed(lambda: ctx.select_bandwidth(kb.LSCV_H, Xd), reps)
-        line(cfg, "select LSCV_H (Nelder-Mead, speculative batches)", dt, prof,
+        line(cfg, "select LSCV_H (Nelder-Mead, default serial rounds)", dt, prof,
              {"vechH": r["vechH"].tolist(), "objective": r["objective"], "iterations": r["iterations"],
               "evaluations": r["evaluations"], "stop": r["stop_reason"]})
     elif cfg == "F3":
