@@ -114,8 +114,9 @@ kde_status kde_nccl_unique_id(void *out128);
 /* Device workspace the pair-sum calls need for (n, d, n_cand); the caller may provide it with
  * kde_set_workspace (memory stays owned by the caller and must outlive its use); otherwise the
  * context allocates what it needs with cudaMalloc on first use.  The sorted-sample copy (Psi),
- * KDE-evaluation scratch and the materialised S(v) buffer are always context-owned (freed by
- * kde_destroy). */
+ * the per-candidate whitened data sets (LSCV_H, d x n fp32 per candidate, up to 256 candidates or
+ * 1 GiB per launch), KDE-evaluation scratch, staged host inputs and the materialised S(v) buffer
+ * are always context-owned (freed by kde_destroy). */
 size_t kde_workspace_bytes(int64_t n, int32_t d, int32_t n_cand);
 kde_status kde_set_workspace(kde_ctx *ctx, void *dev_ptr, size_t bytes);
 

@@ -75,6 +75,9 @@ struct kde_ctx {
   // KDE evaluation / AQP scratch, context-owned
   void* ev_ws = nullptr;
   size_t ev_bytes = 0;
+  // per-candidate whitened LSCV_H data sets, context-owned
+  void* white_ws = nullptr;
+  size_t white_bytes = 0;
   // sorted copy of univariate samples (+ CUB temp), context-owned
   void* sort_ws = nullptr;
   size_t sort_bytes = 0;
@@ -396,18 +399,25 @@ kde_status gpu_sorted(kde_ctx* c, const double* x, int64_t n, const double** out
   return KDE_OK;
 }
 
-// y = fp32(W (x - mean)), padded with zeros to ld.
-kde_status gpu_prep(kde_ctx* c, const double* X, int64_t n, int d, const std::vector<double>& W,
-                    const std::vector<double>& mean, int64_t ld, Ws& w, double clamp_thresh = 0.0) {
+// y = fp32(W (x - mean)), padded with zeros to ld, written to Y (default: the workspace's Y).
+// gpu_prep_into does not clear the prep flags (several sets prepared for one launch share them).
+kde_status gpu_prep_into(kde_ctx* c, const double* X, int64_t n, int d, const std::vector<double>& W,
+                         const std::vector<double>& mean, int64_t ld, Ws& w, float* Y,
+                         double clamp_thresh = 0.0) {
   Range r("kde.prep");
   double* mean_dev = w.small;
   double* W_dev = w.small + 16;
   CUDA_TRY(c, cudaMemcpyAsync(mean_dev, mean.data(), d * sizeof(double), cudaMemcpyHostToDevice, c->stream));
   CUDA_TRY(c, cudaMemcpyAsync(W_dev, W.data(), (size_t)d * d * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-  CUDA_TRY(c, cudaMemsetAsync(w.flag(), 0, 2 * sizeof(unsigned long long), c->stream));
-  CUDA_TRY(c, kde::launch_prep(X, n, d, W_dev, mean_dev, w.Y, ld, c->stream, 0.f, w.flag(), clamp_thresh));
+  CUDA_TRY(c, kde::launch_prep(X, n, d, W_dev, mean_dev, Y, ld, c->stream, 0.f, w.flag(), clamp_thresh));
   c->prof_all += 1;
   return KDE_OK;
+}
+
+kde_status gpu_prep(kde_ctx* c, const double* X, int64_t n, int d, const std::vector<double>& W,
+                    const std::vector<double>& mean, int64_t ld, Ws& w, double clamp_thresh = 0.0) {
+  CUDA_TRY(c, cudaMemsetAsync(w.flag(), 0, 2 * sizeof(unsigned long long), c->stream));
+  return gpu_prep_into(c, X, n, d, W, mean, ld, w, w.Y, clamp_thresh);
 }
 
 int64_t n_tiles(int64_t n, int T) {
@@ -478,7 +488,9 @@ struct SumLaunch {
   int n_out = 0;
   kde::PsiParams psi;
   kde::LscvScalarParams ls;
-  std::vector<unsigned char> mat;   // LscvMatrixParams or LscvCholParams bytes
+  const float* X = nullptr;         // prepared data if not the workspace's Y (LSCV_H sets)
+  int n_sets = 1;                   // LSCV_H: candidates (one data set each), n_out per set
+  int64_t set_stride = 0;
 };
 
 // Launch the given pair kernels over shard tiles, all-reduce (if requested), fetch fixed-point
@@ -497,20 +509,23 @@ kde_status run_sums(kde_ctx* c, int d, int64_t n, int64_t ld, int T, int scale, 
     cfg.scale_exp = scale; cfg.limbs = w.limbs + (size_t)L.out_offset * kde::kLimbs;
     cfg.n_out = L.n_out; cfg.stream = c->stream; cfg.sm_count = c->sm_count;
     cfg.clamp = w.flag() + 1;
+    if (L.X) cfg.X = L.X;
+    cfg.n_sets = L.n_sets;
+    cfg.set_stride = L.set_stride;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (c->profiling) { e0 = next_event(c); e1 = next_event(c); cudaEventRecord(e0, c->stream); }
     cudaError_t err = cudaSuccess;
     switch (L.kind) {
       case Kind::Psi4: case Kind::Psi6: case Kind::Psi8: err = kde::launch_psi(L.r, cfg, L.psi); break;
       case Kind::LscvScalar: err = kde::launch_lscv_scalar(d, L.nb, cfg, L.ls); break;
-      case Kind::LscvMatrix: err = kde::launch_lscv_matrix(d, L.nb, cfg, L.mat.data(), L.mat.size()); break;
+      case Kind::LscvMatrix: err = kde::launch_lscv_white(d, cfg); break;
     }
     if (err != cudaSuccess) return fail(c, KDE_E_CUDA, "pair kernel launch: %s", cudaGetErrorString(err));
     if (tb < te) c->prof_all += 1;
     if (c->profiling) {
       cudaEventRecord(e1, c->stream);
       c->prof_launches++;
-      c->prof_evals += pairs * (double)L.nb;
+      c->prof_evals += pairs * (double)L.nb * (double)L.n_sets;
     }
   }
   if (allreduce && c->comm) {
@@ -644,7 +659,7 @@ double lscv_h_finalize(int64_t n, int d, double det, double h, double S1, double
 struct HCand {
   bool pd = false;
   double det = 0.0;
-  std::vector<double> Hi;     // H^-1 (row-major), fp64
+  std::vector<double> L;      // Cholesky factor of H (row-major lower), fp64
 };
 
 HCand h_candidate(const double* vh, int d) {
@@ -654,105 +669,44 @@ HCand h_candidate(const double* vh, int d) {
   hc.pd = true;
   hc.det = 1.0;
   for (int i = 0; i < d; ++i) hc.det *= L[i * d + i] * L[i * d + i];
-  hc.Hi = spd_inverse(L, d);
+  hc.L = std::move(L);
   return hc;
 }
 
-// Kernel coefficients of a candidate for data whitened as x' = Lw^-1 (x - mean) (Lw = the
-// Cholesky factor of the sample covariance, or I): M = Lw^T H^-1 Lw, so that
-// v^T H^-1 v = v'^T M v'.  Whitening keeps M well conditioned for the candidates LSCV_H visits
-// (H ~ c Sigma or c Sigma^(1/2)), which matters because the fp32 monomial form loses accuracy in
-// proportion to cond(M).  D <= 4: monomial coefficients -(log2 e/4)(2-delta_ab) M_ab;
-// D > 4: rows of U with U^T U = (log2 e/4) M.  Returns false if M is not numerically PD.
-bool h_coefficients(const HCand& hc, int d, const std::vector<double>& Lw, std::vector<double>& coef) {
-  std::vector<double> M((size_t)d * d, 0.0), T((size_t)d * d, 0.0);
-  for (int i = 0; i < d; ++i)          // T = H^-1 Lw
-    for (int j = 0; j < d; ++j) {
-      double s = 0.0;
-      for (int k = 0; k < d; ++k) s += hc.Hi[i * d + k] * Lw[k * d + j];
-      T[i * d + j] = s;
-    }
-  for (int i = 0; i < d; ++i)          // M = Lw^T T
-    for (int j = 0; j < d; ++j) {
-      double s = 0.0;
-      for (int k = 0; k < d; ++k) s += Lw[k * d + i] * T[k * d + j];
-      M[i * d + j] = s;
-    }
-  for (int i = 0; i < d; ++i)
-    for (int j = 0; j < i; ++j) M[i * d + j] = M[j * d + i] = 0.5 * (M[i * d + j] + M[j * d + i]);
-  const double sc = kLog2e / 4.0;
-  coef.clear();
-  if (d <= 4) {
-    for (int a = 0; a < d; ++a)
-      for (int b = a; b < d; ++b) coef.push_back(-sc * (a == b ? 1.0 : 2.0) * M[a * d + b]);
-    return true;
-  }
-  std::vector<double> Lm;
-  if (!cholesky(M, d, Lm)) return false;
-  for (int a = 0; a < d; ++a)          // U = sqrt(sc) Lm^T (upper), rows a: entries b = a..d-1
-    for (int b = a; b < d; ++b) coef.push_back(std::sqrt(sc) * Lm[b * d + a]);
-  return true;
-}
-
-// Raw LSCV_H sums for PD candidates `cands` (all must be PD).
-// prepared_Y (optional): within one API call, the workspace pointer whose fp32 copy of X is already
-// prepared; the prep kernel is skipped while the workspace has not moved (Nelder-Mead loop).
+// Raw LSCV_H sums for PD candidates `cands` (all must be PD).  Each candidate gets its own
+// whitened fp32 copy of the data, x'_c = sqrt(log2 e / 4) L_c^-1 (x - mean) with H_c = L_c L_c^T,
+// so that v^T H_c^-1 v = (4 / log2 e) |x'_ci - x'_cj|^2: the pair kernel then needs no quadratic
+// form (2d + 2 FP32 ops per eval instead of d(d+1)/2 + 2 per candidate plus the monomials), and
+// the sum of squares does not lose accuracy with cond(H).  Candidates are
+// independent work units, so a candidate's sums are bit-identical alone or inside any batch.
 kde_status lscv_H_raw(kde_ctx* c, const double* X, int64_t n, int d, const std::vector<HCand>& cands,
                       const Moments& m, int shard_rank, int shard_world, bool allreduce,
-                      std::vector<kde_fixed>& out, const float** prepared_Y = nullptr) {
+                      std::vector<kde_fixed>& out) {
   const int T = kde::tile_for(Kind::LscvMatrix, d, n);
-  const int nbmax = kde::cand_per_launch(Kind::LscvMatrix, d);
-  // whitening transform: the sample covariance's Cholesky factor when it is PD, else identity
-  std::vector<double> Lw((size_t)d * d, 0.0);
-  if (m.cov.size() != (size_t)d * d || !cholesky(m.cov, d, Lw)) {
-    Lw.assign((size_t)d * d, 0.0);
-    for (int a = 0; a < d; ++a) Lw[a * d + a] = 1.0;
-  }
-  std::vector<std::vector<double>> coefs(cands.size());
-  for (size_t k = 0; k < cands.size(); ++k)
-    if (!h_coefficients(cands[k], d, Lw, coefs[k]))
-      return fail(c, KDE_E_NUMERIC, "candidate %zu: whitened H^-1 not positive definite", k);
   const int64_t ld = (n + T - 1) / T * T;
+  const int64_t set_floats = (int64_t)d * ld;
   const int nc = (int)cands.size();
-  const int P = d * (d + 1) / 2;
-  std::vector<SumLaunch> Ls;
-  int off = 0;
-  for (int b0 = 0; b0 < nc; b0 += nbmax) {
-    const int cnt = std::min(nbmax, nc - b0);
-    int nb = cnt;
-    if (d <= 4) nb = cnt <= 2 ? cnt : (cnt <= 4 ? 4 : (cnt <= 8 ? 8 : 16));
-    nb = std::min(nb, nbmax);
-    if (d > 4) nb = nbmax;
-    SumLaunch L;
-    L.kind = Kind::LscvMatrix; L.nb = nb; L.out_offset = off; L.n_out = 2 * nb;
-    size_t bytes = d <= 4 ? sizeof(kde::LscvMatrixParams) : sizeof(kde::LscvCholParams);
-    L.mat.assign(bytes, 0);
-    float* f = reinterpret_cast<float*>(L.mat.data());
-    for (int j = 0; j < nb; ++j) {
-      const std::vector<double>& cf = coefs[b0 + std::min(j, cnt - 1)];
-      for (int u = 0; u < P; ++u) f[j * P + u] = (float)cf[u];
-    }
-    Ls.push_back(std::move(L));
-    off += 2 * nb;
-  }
+  // sets per launch: up to 256 candidates within ~1 GiB of prepared data
+  const int per_launch = (int)std::max<int64_t>(1, std::min<int64_t>(256, (1LL << 28) / set_floats));
   Ws w;
-  TRY(get_ws(c, ld, d, std::max(off, 2), &w));
-  if (!prepared_Y || *prepared_Y != w.Y) {
-    const std::vector<double> W = tri_lower_inverse(Lw, d);    // x' = Lw^-1 (x - mean)
-    TRY(gpu_prep(c, X, n, d, W, m.mean, ld, w));
-    if (prepared_Y) *prepared_Y = w.Y;
-  }
-  std::vector<kde_fixed> o;
-  TRY(run_sums(c, d, n, ld, T, scale_exp_for(1.0, n), w, Ls, std::max(off, 2), shard_rank, shard_world, allreduce, o));
+  TRY(get_ws(c, ld, d, 2 * std::min(nc, per_launch), &w));
   out.clear();
-  int k = 0;
-  for (const SumLaunch& L : Ls) {
-    const int cnt = std::min(L.nb, nc - k);
+  for (int b0 = 0; b0 < nc; b0 += per_launch) {
+    const int cnt = std::min(per_launch, nc - b0);
+    TRY(grow(c, &c->white_ws, &c->white_bytes, (size_t)cnt * set_floats * sizeof(float)));
+    float* Yw = static_cast<float*>(c->white_ws);
+    CUDA_TRY(c, cudaMemsetAsync(w.flag(), 0, 2 * sizeof(unsigned long long), c->stream));
     for (int j = 0; j < cnt; ++j) {
-      out.push_back(o[L.out_offset + 2 * j]);
-      out.push_back(o[L.out_offset + 2 * j + 1]);
+      std::vector<double> W = tri_lower_inverse(cands[b0 + j].L, d);
+      for (double& v : W) v *= std::sqrt(kLog2e / 4.0);
+      TRY(gpu_prep_into(c, X, n, d, W, m.mean, ld, w, Yw + (size_t)j * set_floats));
     }
-    k += cnt;
+    SumLaunch L;
+    L.kind = Kind::LscvMatrix; L.nb = 1; L.out_offset = 0; L.n_out = 2 * cnt;
+    L.X = Yw; L.n_sets = cnt; L.set_stride = set_floats;
+    std::vector<kde_fixed> o;
+    TRY(run_sums(c, d, n, ld, T, scale_exp_for(1.0, n), w, {L}, 2 * cnt, shard_rank, shard_world, allreduce, o));
+    out.insert(out.end(), o.begin(), o.end());
   }
   return KDE_OK;
 }
@@ -767,7 +721,7 @@ double lscv_H_finalize(int64_t n, int d, double det, double S1, double S2) {
 // Evaluate g(H) for a list of vech vectors (non-PD -> penalty); one GPU batch for all PD ones.
 kde_status lscv_H_eval(kde_ctx* c, const double* X, int64_t n, int d, const Moments& m,
                        const std::vector<std::vector<double>>& vs, double penalty,
-                       std::vector<double>& g, int* evals, const float** prepared_Y = nullptr) {
+                       std::vector<double>& g, int* evals) {
   std::vector<HCand> pdc;
   std::vector<int> idx;
   g.assign(vs.size(), penalty);
@@ -777,7 +731,7 @@ kde_status lscv_H_eval(kde_ctx* c, const double* X, int64_t n, int d, const Mome
   }
   if (pdc.empty()) return KDE_OK;
   std::vector<kde_fixed> o;
-  TRY(lscv_H_raw(c, X, n, d, pdc, m, c->rank, c->world, true, o, prepared_Y));
+  TRY(lscv_H_raw(c, X, n, d, pdc, m, c->rank, c->world, true, o));
   for (size_t j = 0; j < pdc.size(); ++j)
     g[idx[j]] = lscv_H_finalize(n, d, pdc[j].det, fixed_value(o[2 * j]), fixed_value(o[2 * j + 1]));
   if (evals) *evals += (int)pdc.size();
@@ -938,15 +892,6 @@ kde_status nelder_mead_multi(kde_ctx* c, const double* X, int64_t n, int d, cons
     runs[r].speculative = speculative;
   }
   int evals = 0;
-  // size the workspace for the largest batch up front so the prepared data never move
-  {
-    const int T = kde::tile_for(Kind::LscvMatrix, d, n);
-    size_t maxb = 0;
-    for (const auto& sk : sims) maxb += std::max<size_t>(sk.size(), 4);
-    Ws w;
-    TRY(get_ws(c, (n + T - 1) / T * T, d, (int)(2 * (maxb + 32)), &w));
-  }
-  const float* prepared = nullptr;
   while (true) {
     std::vector<std::vector<double>> batch;
     std::vector<std::pair<size_t, size_t>> span;   // (run, count)
@@ -958,7 +903,7 @@ kde_status nelder_mead_multi(kde_ctx* c, const double* X, int64_t n, int d, cons
     }
     if (batch.empty()) break;
     std::vector<double> g;
-    TRY(lscv_H_eval(c, X, n, d, m, batch, penalty, g, &evals, &prepared));
+    TRY(lscv_H_eval(c, X, n, d, m, batch, penalty, g, &evals));
     size_t off = 0;
     for (auto& sp : span) {
       std::vector<double> gv(g.begin() + off, g.begin() + off + sp.second);
@@ -1038,6 +983,7 @@ void kde_destroy(kde_ctx* c) {
   if (c->comm) nccl().CommDestroy(c->comm);
   if (c->own_ws) cudaFree(c->own_ws);
   if (c->sort_ws) cudaFree(c->sort_ws);
+  if (c->white_ws) cudaFree(c->white_ws);
   if (c->ev_ws) cudaFree(c->ev_ws);
   if (c->mat_ws) cudaFree(c->mat_ws);
   for (void* p : c->in_ws)

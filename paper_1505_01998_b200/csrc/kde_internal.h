@@ -26,16 +26,6 @@ struct PsiParams {
 struct LscvScalarParams {
   float kappa[kMaxCand];   // -1/h_c^2 (data pre-scaled by sqrt(log2 e / 4) L^-1)
 };
-struct LscvMatrixParams {
-  // D <= 4: monomial coefficients m_ab (a <= b, row-major over the upper triangle), for each
-  //         candidate: q = sum m_ab v_a v_b = -(log2 e/4) v^T H^-1 v.
-  // D  > 4: rows of the scaled upper-triangular factor U (U^T U = (log2 e/4) H^-1), q = -|U v|^2.
-  float m[kMaxCand * 10];  // sized for D<=4 monomials at 32 candidates; D>4 uses fewer candidates
-};
-struct LscvCholParams {
-  float u[4 * 136];        // up to 4 candidates of a 16x16 upper-triangular factor
-};
-
 struct LaunchCfg {
   const float* X;          // D rows of ld floats (fp32, prepared), device
   int64_t n, ld;           // samples, padded row length (multiple of the tile)
@@ -47,12 +37,17 @@ struct LaunchCfg {
   cudaStream_t stream;
   int sm_count;
   const unsigned long long* clamp = nullptr;   // Psi: device flag "some |x'| > 3e4"
+  // Several prepared data sets (LSCV_H: one per candidate) in one launch: set s lives at
+  // X + s * set_stride and writes outputs [s * n_out, (s + 1) * n_out); work unit = (set, tile).
+  int n_sets = 1;
+  int64_t set_stride = 0;  // floats
 };
 
 // Launchers (kde_psi.cu, kde_lscv_scalar.cu, kde_lscv_matrix.cu).  Return cudaSuccess or the launch error.
 cudaError_t launch_psi(int r, const LaunchCfg& c, const PsiParams& p);
 cudaError_t launch_lscv_scalar(int d, int nb, const LaunchCfg& c, const LscvScalarParams& p);
-cudaError_t launch_lscv_matrix(int d, int nb, const LaunchCfg& c, const void* params, size_t bytes);
+// LSCV_H with per-candidate whitened data (one candidate per set, c.n_sets sets).
+cudaError_t launch_lscv_white(int d, const LaunchCfg& c);
 int tile_for(Kind k, int d, int64_t n);       // tile edge the launcher uses
 int cand_per_launch(Kind k, int d);           // B
 

@@ -28,8 +28,6 @@ namespace kde {
 
 // Candidates per launch: chosen so that no instantiation spills at 128 registers (2 CTAs/SM).
 constexpr int nb_scalar(int d) { return d <= 12 ? 16 : 8; }
-constexpr int nb_mono_max(int d) { return 16; }
-constexpr int nb_chol(int d) { return d <= 5 ? 8 : (d <= 8 ? 4 : (d <= 12 ? 2 : 1)); }
 
 
 // ------------------------------------------------------------------ small device helpers
@@ -75,6 +73,8 @@ struct Args {
   int scale_exp;
   unsigned long long* limbs;
   const unsigned long long* clamp;   // device flag set by the prep kernel (Psi only), or null
+  int n_sets;                        // data sets (work unit = (set, tile)), set s at X + s*set_stride
+  int64_t set_stride;
 };
 
 // ------------------------------------------------------------------ functors
@@ -212,9 +212,15 @@ struct FPsi {
 // Sigma = L L^T, so s = |x_i' - x_j'|^2 = (log2 e / 4) S(v) (S(v) of Eq. 37) and for candidate
 // h_c:  e = 2^(s * kappa_c) = exp(-S(v)/(4 h_c^2)),  e^2 = exp(-S(v)/(2 h_c^2)).
 // The thread's two rows are packed in fp32x2 lanes (lane-exact, halves the issue slots).
-template <int D_, int NT_, int NB_>
+// UNIT (LSCV_H, one candidate per data set): the data are whitened by the candidate itself,
+// x' = sqrt(log2 e / 4) L_c^-1 (x - mean) with H_c = L_c L_c^T, so s = (log2 e / 4) v^T H_c^-1 v
+// and e = 2^-s (the negation is a MUFU operand modifier): 2d + 2 FP32 ops per eval.
+template <int D_, int NT_, int NB_, bool UNIT = false>
 struct FLscvScalar {
-  static constexpr int NT = NT_, D = D_, R = 2, T = NT_ * 2, NB = NB_, NOUT = 2 * NB_, MINB = 512 / NT_;
+  static_assert(!UNIT || NB_ == 1, "UNIT sets carry one candidate");
+  static constexpr int NT = NT_, D = D_, R = 2, T = NT_ * 2, NB = NB_, NOUT = 2 * NB_;
+  static constexpr int MINB = (UNIT && D <= 4 ? 1024 : 512) / NT_;   // UNIT d<=4: 4 CTAs of 256, 64 regs
+  static constexpr int UNR = UNIT && D <= 4 ? (D <= 3 ? 4 : 2) : 1;   // UNIT: short body, unroll the column loop
   static constexpr bool kClampable = false;
   using Params = LscvScalarParams;
   f2 xr[D];
@@ -233,7 +239,7 @@ struct FLscvScalar {
                                           int jlim) {
     const int tid = threadIdx.x;
     const int jend = MASK ? ((jlim + 3) & ~3) : T;
-#pragma unroll 1
+#pragma unroll UNR
     for (int j = 0; j < jend; j += 4) {
       float cv[D][4];
 #pragma unroll
@@ -259,13 +265,21 @@ struct FLscvScalar {
           const bool ok1 = (jj < jlim) && (!diag || jj > NT + tid);
           s = pk(ok0 ? s0 : inf, ok1 ? s1 : inf);
         }
-#pragma unroll
-        for (int c = 0; c < NB; ++c) {
+        if (UNIT) {
           float q0, q1;
-          upk(mul2(s, pk(p.kappa[c], p.kappa[c])), q0, q1);
-          const f2 e = pk(ex2(q0), ex2(q1));
-          a1[c] = add2(a1[c], e);
-          a2[c] = fma2(e, e, a2[c]);
+          upk(s, q0, q1);
+          const f2 e = pk(ex2(-q0), ex2(-q1));
+          a1[0] = add2(a1[0], e);
+          a2[0] = fma2(e, e, a2[0]);
+        } else {
+#pragma unroll
+          for (int c = 0; c < NB; ++c) {
+            float q0, q1;
+            upk(mul2(s, pk(p.kappa[c], p.kappa[c])), q0, q1);
+            const f2 e = pk(ex2(q0), ex2(q1));
+            a1[c] = add2(a1[c], e);
+            a2[c] = fma2(e, e, a2[c]);
+          }
         }
       }
     }
@@ -280,144 +294,6 @@ struct FLscvScalar {
       v[2 * c] = (double)x0 + (double)x1;
       v[2 * c + 1] = (double)y0 + (double)y1;
     }
-  }
-};
-
-// LSCV_H, d <= 4: per pair the differences v and the d(d+1)/2 monomials v_a v_b; per candidate
-// q = sum m_ab v_a v_b = -(log2 e / 4) v^T H^-1 v (the fun2 = x^T M x of Eq. 44-56 expanded in
-// monomials), e = 2^q = exp(-v^T H^-1 v / 4), e^2 = exp(-v^T H^-1 v / 2).
-// The thread's two rows are packed in fp32x2 lanes; coefficients are scalar broadcasts.
-template <int D_, int NT_, int NB_>
-struct FLscvMono {
-  static constexpr int NT = NT_, D = D_, R = 2, T = NT_ * 2, NB = NB_, NOUT = 2 * NB_;
-  static constexpr int MINB = (NB_ >= 16 ? 256 : 512) / NT_;   // 16 candidates need > 128 registers
-  static constexpr int P = D * (D + 1) / 2;
-  static constexpr bool kClampable = false;
-  using Params = LscvMatrixParams;
-  f2 xr[D];
-  f2 a1[NB], a2[NB];
-
-  __device__ __forceinline__ void load_rows(const float* __restrict__ X, int64_t ld,
-                                            int64_t i0) {
-#pragma unroll
-    for (int a = 0; a < D; ++a) xr[a] = pk(__ldg(X + a * ld + i0), __ldg(X + a * ld + i0 + NT));
-#pragma unroll
-    for (int c = 0; c < NB; ++c) a1[c] = a2[c] = pk(0.f, 0.f);
-  }
-
-  template <bool MASK, bool CLAMP = false>
-  __device__ __forceinline__ void compute(const float* __restrict__ sc, const Params& p, bool diag,
-                                          int jlim) {
-    const int tid = threadIdx.x;
-    const int jend = MASK ? ((jlim + 3) & ~3) : T;
-#pragma unroll 1
-    for (int j = 0; j < jend; j += 4) {
-      float cv[D][4];
-#pragma unroll
-      for (int a = 0; a < D; ++a) {
-        const float4 c4 = *reinterpret_cast<const float4*>(sc + a * T + j);
-        cv[a][0] = c4.x; cv[a][1] = c4.y; cv[a][2] = c4.z; cv[a][3] = c4.w;
-      }
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        f2 v[D];
-#pragma unroll
-        for (int a = 0; a < D; ++a) v[a] = sub2(xr[a], pk(cv[a][k], cv[a][k]));
-        f2 mono[P];
-        int t = 0;
-#pragma unroll
-        for (int a = 0; a < D; ++a)
-#pragma unroll
-          for (int b = a; b < D; ++b) mono[t++] = mul2(v[a], v[b]);
-        if (MASK) {
-          const int jj = j + k;
-          float m0, m1;
-          upk(mono[0], m0, m1);
-          const float inf = __int_as_float(0x7f800000);   // m_00 < 0 -> q = -inf -> e = 0
-          const bool ok0 = (jj < jlim) && (!diag || jj > tid);
-          const bool ok1 = (jj < jlim) && (!diag || jj > NT + tid);
-          mono[0] = pk(ok0 ? m0 : inf, ok1 ? m1 : inf);
-        }
-#pragma unroll
-        for (int c = 0; c < NB; ++c) {
-          f2 q = mul2(mono[0], pk(p.m[c * P], p.m[c * P]));
-#pragma unroll
-          for (int u = 1; u < P; ++u) q = fma2(mono[u], pk(p.m[c * P + u], p.m[c * P + u]), q);
-          float q0, q1;
-          upk(q, q0, q1);
-          const f2 e = pk(ex2(q0), ex2(q1));
-          a1[c] = add2(a1[c], e);
-          a2[c] = fma2(e, e, a2[c]);
-        }
-      }
-    }
-  }
-
-  __device__ __forceinline__ void outputs(double (&v)[NOUT]) const {
-#pragma unroll
-    for (int c = 0; c < NB; ++c) {
-      float x0, x1, y0, y1;
-      upk(a1[c], x0, x1);
-      upk(a2[c], y0, y1);
-      v[2 * c] = (double)x0 + (double)x1;
-      v[2 * c + 1] = (double)y0 + (double)y1;
-    }
-  }
-};
-
-// LSCV_H, d > 4: per candidate a scaled upper-triangular factor U_c with
-// U_c^T U_c = (log2 e / 4) H_c^-1, q = -|U_c v|^2 (Eq. 44-56 with M factored), e = 2^q.
-template <int D_, int NB_>
-struct FLscvChol {
-  static constexpr int NT = kThreads, D = D_, R = 1, T = kThreads, NB = NB_, NOUT = 2 * NB_, MINB = 2;
-  static constexpr int P = D * (D + 1) / 2;
-  static constexpr bool kClampable = false;
-  using Params = LscvCholParams;
-  float xr[D];
-  float a1[NB], a2[NB];
-
-  __device__ __forceinline__ void load_rows(const float* __restrict__ X, int64_t ld,
-                                            int64_t i0) {
-#pragma unroll
-    for (int a = 0; a < D; ++a) xr[a] = __ldg(X + a * ld + i0);
-#pragma unroll
-    for (int c = 0; c < NB; ++c) a1[c] = a2[c] = 0.f;
-  }
-
-  template <bool MASK, bool CLAMP = false>
-  __device__ __forceinline__ void compute(const float* __restrict__ sc, const Params& p, bool diag,
-                                          int jlim) {
-    const int tid = threadIdx.x;
-    const int jend = MASK ? jlim : T;
-#pragma unroll 1
-    for (int j = 0; j < jend; ++j) {
-      float v[D];
-#pragma unroll
-      for (int a = 0; a < D; ++a) v[a] = __fsub_rn(xr[a], sc[a * T + j]);
-      const bool ok = !MASK || (!diag || j > tid);
-#pragma unroll
-      for (int c = 0; c < NB; ++c) {
-        float q = 0.f;
-        int t = 0;
-#pragma unroll
-        for (int a = 0; a < D; ++a) {
-          float z = __fmul_rn(p.u[c * P + t], v[a]);
-          ++t;
-#pragma unroll
-          for (int b = a + 1; b < D; ++b) { z = __fmaf_rn(p.u[c * P + t], v[b], z); ++t; }
-          q = __fmaf_rn(z, z, q);
-        }
-        float e = ex2(-q);
-        if (MASK) e = ok ? e : 0.f;
-        a1[c] = __fadd_rn(a1[c], e);
-        a2[c] = __fmaf_rn(e, e, a2[c]);
-      }
-    }
-  }
-
-  __device__ __forceinline__ void outputs(double (&v)[NOUT]) const {
-#pragma unroll
-    for (int c = 0; c < NB; ++c) { v[2 * c] = a1[c]; v[2 * c + 1] = a2[c]; }
   }
 };
 
@@ -451,28 +327,35 @@ __global__ void __launch_bounds__(F::NT, F::MINB) pair_kernel(const Args a,
   }
   __syncthreads();
 
-  auto issue = [&](int64_t tile, int buf) {
+  // Work units u in [0, n_sets * tiles): set = u / tiles, tile = tile_begin + u % tiles (set-major,
+  // so consecutive CTAs share a set's data in L2).
+  const int64_t per = a.tile_end - a.tile_begin;
+  const int64_t units = per * a.n_sets;
+  auto issue = [&](int64_t u, int buf) {
+    const int64_t set = u / per;
     int64_t l, q;
-    tile_coords(tile, l, q);
+    tile_coords(a.tile_begin + (u - set * per), l, q);
+    const float* Xs = a.X + set * a.set_stride;
     float* dst = cols + buf * D * T;
     mbar_expect_tx(&bar[buf], (uint32_t)(D * T * sizeof(float)));
 #pragma unroll
     for (int d = 0; d < D; ++d)
-      tma_load_1d(dst + d * T, a.X + d * a.ld + l * T, (uint32_t)(T * sizeof(float)), &bar[buf]);
+      tma_load_1d(dst + d * T, Xs + d * a.ld + l * T, (uint32_t)(T * sizeof(float)), &bar[buf]);
   };
 
   const bool clamp = F::kClampable && a.clamp != nullptr && *a.clamp != 0;   // uniform per launch
-  int64_t t = a.tile_begin + blockIdx.x;
-  if (tid == 0 && t < a.tile_end) issue(t, 0);
+  int64_t u = blockIdx.x;
+  if (tid == 0 && u < units) issue(u, 0);
   uint32_t k = 0;
-  for (; t < a.tile_end; t += gridDim.x, ++k) {
+  for (; u < units; u += gridDim.x, ++k) {
+    const int64_t set = u / per;
     int64_t l, q;
-    tile_coords(t, l, q);
-    const int64_t tn = t + gridDim.x;
-    if (tid == 0 && tn < a.tile_end) issue(tn, (k + 1) & 1);
+    tile_coords(a.tile_begin + (u - set * per), l, q);
+    const int64_t un = u + gridDim.x;
+    if (tid == 0 && un < units) issue(un, (k + 1) & 1);
 
     F f;
-    f.load_rows(a.X, a.ld, row_origin<F>(q));
+    f.load_rows(a.X + set * a.set_stride, a.ld, row_origin<F>(q));
     mbar_wait(&bar[k & 1], (k >> 1) & 1);
     const float* sc = cols + (k & 1) * D * T;
     const bool diag = (q == l);
@@ -487,7 +370,7 @@ __global__ void __launch_bounds__(F::NT, F::MINB) pair_kernel(const Args a,
 
     double v[NOUT];
     f.outputs(v);
-    commit_tile<NOUT, F::NT>(v, red, a.limbs, a.scale_exp);
+    commit_tile<NOUT, F::NT>(v, red, a.limbs + set * NOUT * kLimbs, a.scale_exp);
   }
 }
 
@@ -505,10 +388,10 @@ inline cudaError_t launch_pair(const LaunchCfg& c, const typename F::Params& p) 
     if (e != cudaSuccess) return e;
     occ = o > 0 ? o : 1;
   }
-  const int64_t tiles = c.tile_end - c.tile_begin;
+  const int64_t units = (c.tile_end - c.tile_begin) * c.n_sets;
   int64_t grid = (int64_t)c.sm_count * occ;
-  if (grid > tiles) grid = tiles;
-  Args a{c.X, c.n, c.ld, c.tile_begin, c.tile_end, c.scale_exp, c.limbs, c.clamp};
+  if (grid > units) grid = units;
+  Args a{c.X, c.n, c.ld, c.tile_begin, c.tile_end, c.scale_exp, c.limbs, c.clamp, c.n_sets, c.set_stride};
   pair_kernel<F><<<(unsigned)grid, F::NT, smem, c.stream>>>(a, p);
   return cudaGetLastError();
 }

@@ -21,7 +21,6 @@ int tile_for(Kind k, int d, int64_t n) {
     }
     case Kind::LscvScalar: return 512;
     case Kind::LscvMatrix: {
-      if (d > 4) return kThreads;
       // 512-row tiles unless that leaves fewer than ~20 tiles per resident CTA (wave tail)
       const int64_t nb = (n + 511) / 512;
       return nb * (nb + 1) / 2 >= 6000 ? 512 : 256;
@@ -34,7 +33,7 @@ int cand_per_launch(Kind k, int d) {
   switch (k) {
     case Kind::Psi4: case Kind::Psi6: case Kind::Psi8: return 1;
     case Kind::LscvScalar: return nb_scalar(d);
-    case Kind::LscvMatrix: return d <= 4 ? nb_mono_max(d) : nb_chol(d);
+    case Kind::LscvMatrix: return 1;   // one candidate per whitened data set
   }
   return 1;
 }

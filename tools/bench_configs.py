@@ -136,18 +136,19 @@ def run(cfg, reps):
         lo = np.linspace(-3, 3, 64)
         dt, prof, out = timed(lambda: ctx.aqp_1d(xd, 0.05, lo, lo + 0.5), reps)
         print(json.dumps({"config": cfg, "what": "aqp_1d 64 ranges, n=2^20", "wall_ms": dt * 1e3}), flush=True)
-    elif cfg == "C5":
+    elif cfg in ("C5", "C5P"):
+        # C5P: the first 16 of the 256 candidates (same kernel, short enough for ncu --set full)
         n = 1 << 18
         X = datagen.config_data("C5")
         Xd = kb.to_device(X)
-        cands = datagen.c5_candidates(n, 256)
+        cands = datagen.c5_candidates(n, 256)[: 16 if cfg == "C5P" else 256]
         dt, prof, g = timed(lambda: ctx.lscv_H_scores(Xd, cands), reps)
-        # d = 4 is FMA-bound: per eval 10 (quadratic form) + 2 (accumulate) FP32
-        # lane-ops, plus 4 + 10 per pair over the 16 candidates of a visit, at the measured
-        # 125 FP32 lane-ops/clk/SM (tools/pipes.cu)
-        fma_peak = 125.0 / (12 + 14 / 16) * SMS * 1965e6
+        # d = 4 is FMA-bound: per eval, on data whitened by the candidate, 4 sub +
+        # 4 (sum of squares) + 2 (accumulate) FP32 lane-ops at the measured 125 FP32 lane-ops/clk/SM
+        # (tools/pipes.cu)
+        fma_peak = 125.0 / (2 * 4 + 2) * SMS * 1965e6
         ev = prof["pair_evals"] / (prof["pair_ms"] / 1e3)
-        line(cfg, "lscv_H_scores 256 H, d=4, n=2^18", dt, prof,
+        line(cfg, f"lscv_H_scores {len(cands)} H, d=4, n=2^18", dt, prof,
              {"g_first": g[:4].tolist(), "fma_bound_evals_per_s": fma_peak, "frac_fma_bound": ev / fma_peak})
 
 
