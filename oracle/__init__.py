@@ -9,8 +9,10 @@ here in plain Python floats (IEEE fp64), each following the cited passage of PAP
 
 Parity status: every function below is pinned by tests/test_oracle_*.py against something
 other than itself (quadrature identities, library routines, closed forms, invariants, MC
-expectations) EXCEPT the Nelder–Mead decision path on near-flat objectives, which is
-"parity unpinned" beyond the scipy step-for-step comparison (reading Z8).
+expectations); nelder_mead is pinned step for step to scipy's Nelder–Mead.  The GPU selector's
+NM decision path is checked against this one by replay (tests/test_gpu_nm_replay.py: identical
+decisions on seeded inputs); where an fp32-term objective could legitimately flip a near-tie
+comparison, the SURVEY §8(c) c5 tie rule applies.
 """
 from __future__ import annotations
 

@@ -1,0 +1,59 @@
+"""Nelder–Mead decision-path parity (SURVEY §8(c) c5 "replay parity").
+
+The library's NM (C++, kde_host.cpp) and the oracle's NM (Python, oracle.nelder_mead, itself
+pinned step for step to scipy in tests/test_oracle_lscv.py) are independent implementations of
+the reading-Z8 spec.  Three checks on seeded inputs:
+  (a) the oracle NM driven by the GPU objective takes exactly the library's path (same
+      iterations, same final vech to rounding of the start point): pins the library's host logic;
+  (b) replay: every H that path visits has GPU objective within 1e-5 of the fp64 oracle's;
+  (c) the all-oracle NM (fp64 objective) takes the same decision sequence: the fp32-term
+      objective changes no decision on these inputs.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import datagen
+import oracle
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+import paper_1505_01998_b200 as kb  # noqa: E402
+
+THREADS = len(os.sched_getaffinity(0))
+
+
+@pytest.mark.parametrize("mix,d,n,seed,max_iter", [("C3", 2, 1500, 41, 300), ("C5", 3, 700, 42, 150)])
+def test_nm_path_library_gpu_driven_and_oracle_agree(mix, d, n, seed, max_iter):
+    X = datagen.sample_mixture(mix, n, seed)[:d]
+    ctx = kb.Context()
+    Xd = kb.to_device(X)
+    lib_sel = ctx.select_bandwidth(kb.LSCV_H, Xd, max_iter=max_iter)
+
+    sim0 = oracle.initial_simplex(oracle.vech(oracle.H_start(X)), d)
+    f_gpu = lambda v: float(ctx.lscv_H_scores(Xd, [v])[0])
+    tg = []
+    gpu_driven = oracle.nelder_mead(f_gpu, sim0, max_iter=max_iter, trace=tg)
+    ctx.close()
+    # (a) same path as the library's own NM
+    assert lib_sel["iterations"] == gpu_driven["iterations"]
+    assert np.max(np.abs(lib_sel["vechH"] - gpu_driven["x"])) <= 1e-10 * np.max(np.abs(gpu_driven["x"]))
+    # (the start points differ in the last bits: Jacobi vs Denman-Beavers square roots)
+    assert abs(lib_sel["objective"] - gpu_driven["f"]) <= 1e-9 * abs(gpu_driven["f"])
+    # (b) replay parity of every visited candidate
+    f_or = [oracle.lscv_H_score(X, x, threads=THREADS) for x, _ in tg]
+    for (x, fg), fo in zip(tg, f_or):
+        if fo == oracle.PENALTY:
+            assert fg == fo
+        else:
+            assert abs(fg - fo) <= 1e-5 * abs(fo), (x, fg, fo)
+    # (c) the fp64 oracle NM makes the same decisions (identical visited points)
+    to = []
+    oracle.nelder_mead(lambda v: oracle.lscv_H_score(X, v, threads=THREADS), sim0, max_iter=max_iter, trace=to)
+    assert len(to) == len(tg)
+    for (xo, _), (xg, _) in zip(to, tg):
+        assert np.array_equal(xo, xg)

@@ -276,3 +276,18 @@ def test_host_inputs_equal_device_inputs(ctx):
     assert ctx.lscv_H_scores(X, H).tolist() == ctx.lscv_H_scores(dev(X), H).tolist()
     assert ctx.evaluate(X, Y, H[0]).tolist() == ctx.evaluate(dev(X), dev(Y), H[0]).tolist()
     assert ctx.evaluate(dev(X), Y, H[0]).tolist() == ctx.evaluate(X, dev(Y), H[0]).tolist()
+
+
+def test_lscv_H_many_candidates_span_launches(ctx):
+    # 300 candidates need two launches of per-candidate whitened data sets (<= 256 per launch);
+    # every candidate's sums are bit-identical to evaluating it alone, and match the oracle.
+    X = datagen.sample_mixture("C3", 700, 31)
+    cands = _spd_cands(2, 300, 8, 0.1)
+    Xd = dev(X)
+    allc = ctx.raw_sums(kb.SUM_LSCV_H, Xd, cands)
+    for k in (0, 255, 256, 299):
+        solo = ctx.raw_sums(kb.SUM_LSCV_H, Xd, cands[k:k + 1])
+        assert [f.key() for f in solo] == [f.key() for f in allc[2 * k:2 * k + 2]]
+    g = ctx.lscv_H_scores(Xd, cands[[0, 256, 299]])
+    for v, c in zip(g, cands[[0, 256, 299]]):
+        assert rel(v, oracle.lscv_H_score(X, c)) < RTOL
