@@ -1086,31 +1086,95 @@ kde_status kde_psi_r(kde_ctx* c, const double* x, int64_t n, int32_t r, const do
   return KDE_OK;
 }
 
+// One Psi_r pair pass of the device-resident PLUGIN chain: kernel over this rank's tiles into
+// `limbs`, then (world > 1) the all-reduce of the 3 limbs, all enqueued on the context stream.
+static kde_status plugin_pass(kde_ctx* c, int r, int64_t n, int64_t ld, int T, int S, Ws& w,
+                              unsigned long long* limbs, int64_t tb, int64_t te, double pairs) {
+  Range rr("kde.pair_pass");
+  kde::LaunchCfg cfg;
+  cfg.X = w.Y; cfg.n = n; cfg.ld = ld; cfg.tile_begin = tb; cfg.tile_end = te; cfg.tile = T;
+  cfg.scale_exp = S; cfg.limbs = limbs; cfg.n_out = 1; cfg.stream = c->stream; cfg.sm_count = c->sm_count;
+  cfg.clamp = w.flag() + 1;
+  kde::PsiParams p;
+  psi_coeffs(r, p);
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (c->profiling) { e0 = next_event(c); e1 = next_event(c); cudaEventRecord(e0, c->stream); }
+  cudaError_t err = kde::launch_psi(r, cfg, p);
+  if (err != cudaSuccess) return fail(c, KDE_E_CUDA, "pair kernel launch: %s", cudaGetErrorString(err));
+  if (tb < te) c->prof_all += 1;
+  if (c->profiling) {
+    cudaEventRecord(e1, c->stream);
+    c->prof_launches++;
+    c->prof_evals += pairs;
+  }
+  if (c->comm) {
+    Range ra("kde.allreduce");
+    NcclApi& api = nccl();
+    ncclResult_t rc = api.AllReduce(limbs, limbs, kde::kLimbs, kNcclInt64, kNcclSum, c->comm, c->stream);
+    if (rc != 0) return fail(c, KDE_E_NCCL, "ncclAllReduce: %s", api.GetErrorString ? api.GetErrorString(rc) : "?");
+  }
+  return KDE_OK;
+}
+
+// PLUGIN (Sec. 4.4.1): moments, sort, prep and the two pair passes, with the scalar
+// steps 1-8 computed by single-thread kernels on the device between them, so the whole chain is
+// enqueued without a host round trip and the call synchronises once.  The steps' formulas are those
+// of the host reading (Z1, Z10, Z11); failures are recorded on the device and reported in order.
 static kde_status plugin_impl(kde_ctx* c, const double* x, int64_t n, kde_plugin_trace* tr) {
+  const int T = kde::tile_for(Kind::Psi6, 1, n);
+  const int64_t ld = (n + T - 1) / T * T;
   Ws w;
-  TRY(get_ws(c, (n + 2047) / 2048 * 2048, 1, 2, &w));
-  Moments m;
-  TRY(gpu_moments(c, x, n, 1, w, m));
-  kde_plugin_trace t;
-  const double nn = (double)n, s2p = std::sqrt(2.0 * kPi);
-  t.V_hat = m.cov[0];                                                     // step 1, Eq. 11
-  if (!(t.V_hat > 0.0)) return fail(c, KDE_E_DEGENERATE, "variance estimate <= 0");
-  t.sigma_hat = std::sqrt(t.V_hat);                                      // step 2, Eq. 12
-  t.psi8_ns = 105.0 / (32.0 * std::sqrt(kPi) * std::pow(t.sigma_hat, 9));  // step 3, Eq. 13
-  const double K6_0 = -15.0 / s2p, K4_0 = 3.0 / s2p, mu2 = 1.0;
-  t.g1 = std::pow(-2.0 * K6_0 / (mu2 * t.psi8_ns * nn), 1.0 / 9.0);      // step 4, Eq. 14
-  const double* xs = nullptr;                                             // sorted once (§3)
+  TRY(get_ws(c, ld, 1, 2, &w));
+  kde::PluginDev dv(w.small);
+  const int nblk = kde::moments_blocks(n);
+  cudaStream_t st = c->stream;
+  // flags (2 x u64), trace (8) and status (1) start at zero
+  CUDA_TRY(c, cudaMemsetAsync(w.flag(), 0, (kde::kSmallDoubles - 408) * sizeof(double), st));
+  {
+    Range r("kde.moments");
+    CUDA_TRY(c, kde::launch_moments1(x, n, 1, w.part, nblk, st));
+    CUDA_TRY(c, kde::launch_reduce_parts(w.part, nblk, 1, dv.sums, st));
+    CUDA_TRY(c, kde::launch_plugin_chain(0, n, w.small, nullptr, 0, st));             // mean
+    CUDA_TRY(c, kde::launch_moments2(x, n, 1, dv.mean, w.part, nblk, st));
+    CUDA_TRY(c, kde::launch_reduce_parts(w.part, nblk, 1, dv.sums, st));
+    CUDA_TRY(c, kde::launch_plugin_chain(1, n, w.small, nullptr, 0, st));             // steps 1-4
+    c->prof_all += 6;
+  }
+  const double* xs = nullptr;                                                          // sorted once (§3)
   TRY(gpu_sorted(c, x, n, &xs));
-  std::vector<kde_fixed> o;
-  TRY(psi_raw(c, xs, n, 6, &t.g1, 1, m, c->rank, c->world, true, o, true));  // step 5, Eq. 15
-  t.psi6 = psi_finalize(6, n, t.g1, fixed_value(o[0]));
-  if (!(t.psi6 < 0.0)) return fail(c, KDE_E_NUMERIC, "Psi6-hat >= 0");
-  t.g2 = std::pow(-2.0 * K4_0 / (mu2 * t.psi6 * nn), 1.0 / 7.0);         // step 6, Eq. 16
-  TRY(psi_raw(c, xs, n, 4, &t.g2, 1, m, c->rank, c->world, true, o, true));  // step 7, Eq. 17
-  t.psi4 = psi_finalize(4, n, t.g2, fixed_value(o[0]));
-  if (!(t.psi4 > 0.0)) return fail(c, KDE_E_NUMERIC, "Psi4-hat <= 0");
-  const double RK = 1.0 / (2.0 * std::sqrt(kPi));
-  t.h = std::pow(RK / (mu2 * mu2 * t.psi4 * nn), 0.2);                   // step 8, Eq. 18
+  int64_t tb, te;
+  shard_range(n_tiles(n, T), c->rank, c->world, &tb, &te);
+  const double pairs = c->profiling ? pairs_in_range(n, T, tb, te) : 0.0;
+  const int S6 = scale_exp_for(2.0 * 15.0, n), S4 = scale_exp_for(2.0 * 3.0, n);
+  CUDA_TRY(c, cudaMemsetAsync(w.limbs, 0, 2 * kde::kLimbs * sizeof(long long), st));
+  CUDA_TRY(c, kde::launch_prep(xs, n, 1, dv.W, dv.mean, w.Y, ld, st, 0.f, w.flag(), 3.0e4));   // x/g1
+  TRY(plugin_pass(c, 6, n, ld, T, S6, w, w.limbs, tb, te, pairs));                     // step 5
+  CUDA_TRY(c, kde::launch_plugin_chain(2, n, w.small, w.limbs, S6, st));               // Psi6, g2
+  CUDA_TRY(c, kde::launch_prep(xs, n, 1, dv.W, dv.mean, w.Y, ld, st, 0.f, w.flag(), 3.0e4));   // x/g2
+  TRY(plugin_pass(c, 4, n, ld, T, S4, w, w.limbs + kde::kLimbs, tb, te, pairs));       // step 7
+  CUDA_TRY(c, kde::launch_plugin_chain(3, n, w.small, w.limbs + kde::kLimbs, S4, st)); // Psi4, h
+  c->prof_all += 4;
+  const size_t cnt = kde::kSmallDoubles - 408;   // flags, trace, status
+  if (c->h_limbs_cap < cnt) {
+    if (c->h_limbs) cudaFreeHost(c->h_limbs);
+    c->h_limbs = nullptr;
+    CUDA_TRY(c, cudaMallocHost(&c->h_limbs, cnt * sizeof(long long)));
+    c->h_limbs_cap = cnt;
+  }
+  CUDA_TRY(c, cudaMemcpyAsync(c->h_limbs, w.flag(), cnt * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(c, cudaStreamSynchronize(st));
+  const unsigned long long* flags = reinterpret_cast<const unsigned long long*>(c->h_limbs);
+  double res[9];
+  std::memcpy(res, c->h_limbs + 2, sizeof(res));
+  const int status = (int)res[8];
+  if (status == KDE_E_INVALID) return fail(c, KDE_E_INVALID, "non-finite sample values");
+  if (status == KDE_E_DEGENERATE) return fail(c, KDE_E_DEGENERATE, "variance estimate <= 0");
+  if (flags[0]) return fail(c, KDE_E_INVALID, "scaled sample differences exceed 1e18 (outliers vs. bandwidth)");
+  if (status == KDE_E_NUMERIC)
+    return fail(c, KDE_E_NUMERIC, !(res[4] < 0.0) ? "Psi6-hat >= 0" : "Psi4-hat <= 0");
+  kde_plugin_trace t;
+  t.V_hat = res[0]; t.sigma_hat = res[1]; t.psi8_ns = res[2]; t.g1 = res[3];
+  t.psi6 = res[4]; t.g2 = res[5]; t.psi4 = res[6]; t.h = res[7];
   *tr = t;
   return KDE_OK;
 }

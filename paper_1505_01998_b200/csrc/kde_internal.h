@@ -63,6 +63,17 @@ cudaError_t launch_prep(const double* X, int64_t n, int d, const double* W_dev,
                         float pad = 0.f, unsigned long long* overflow_flag = nullptr,
                         double clamp_thresh = 0.0);
 
+// Device-resident PLUGIN chain (kde_psi.cu).  Layout of the workspace's `small` block (doubles):
+// mean[16] | W[256] | sums[136] | flags (2 x u64) | trace[8] | status.
+struct PluginDev {
+  double *mean, *W, *sums, *trace, *status;
+  __host__ __device__ explicit PluginDev(double* small)
+      : mean(small), W(small + 16), sums(small + 272), trace(small + 410), status(small + 418) {}
+};
+constexpr int kSmallDoubles = 424;
+cudaError_t launch_plugin_chain(int stage, int64_t n, double* small, const unsigned long long* limbs, int S,
+                                cudaStream_t s);
+
 // KDE evaluation on an m x n rectangle (kde_eval.cu).
 struct EvalLaunch {
   const float* Y;        // D x ldm whitened queries

@@ -101,7 +101,7 @@ struct FPsi {
   static constexpr int NP = R / 2;   // row pairs (r = 2p, 2p+1) packed into fp32x2 lanes
   static constexpr int G = 16;       // columns per compensated group
   static constexpr float K = (float)(RORD - 1);
-  static constexpr bool kClampable = true;
+  static constexpr bool kClampable = true, kSets = false;
   using Params = PsiParams;
   f2 xr[NP];
   double acc;
@@ -221,7 +221,7 @@ struct FLscvScalar {
   static constexpr int NT = NT_, D = D_, R = 2, T = NT_ * 2, NB = NB_, NOUT = 2 * NB_;
   static constexpr int MINB = (UNIT && D <= 4 ? 1024 : 512) / NT_;   // UNIT d<=4: 4 CTAs of 256, 64 regs
   static constexpr int UNR = UNIT && D <= 4 ? (D <= 3 ? 4 : 2) : 1;   // UNIT: short body, unroll the column loop
-  static constexpr bool kClampable = false;
+  static constexpr bool kClampable = false, kSets = UNIT;
   using Params = LscvScalarParams;
   f2 xr[D];
   f2 a1[NB], a2[NB];
@@ -327,6 +327,64 @@ __global__ void __launch_bounds__(F::NT, F::MINB) pair_kernel(const Args a,
   }
   __syncthreads();
 
+  auto issue = [&](int64_t tile, int buf) {
+    int64_t l, q;
+    tile_coords(tile, l, q);
+    float* dst = cols + buf * D * T;
+    mbar_expect_tx(&bar[buf], (uint32_t)(D * T * sizeof(float)));
+#pragma unroll
+    for (int d = 0; d < D; ++d)
+      tma_load_1d(dst + d * T, a.X + d * a.ld + l * T, (uint32_t)(T * sizeof(float)), &bar[buf]);
+  };
+
+  const bool clamp = F::kClampable && a.clamp != nullptr && *a.clamp != 0;   // uniform per launch
+  int64_t t = a.tile_begin + blockIdx.x;
+  if (tid == 0 && t < a.tile_end) issue(t, 0);
+  uint32_t k = 0;
+  for (; t < a.tile_end; t += gridDim.x, ++k) {
+    int64_t l, q;
+    tile_coords(t, l, q);
+    const int64_t tn = t + gridDim.x;
+    if (tid == 0 && tn < a.tile_end) issue(tn, (k + 1) & 1);
+
+    F f;
+    f.load_rows(a.X, a.ld, row_origin<F>(q));
+    mbar_wait(&bar[k & 1], (k >> 1) & 1);
+    const float* sc = cols + (k & 1) * D * T;
+    const bool diag = (q == l);
+    const int64_t jl = a.n - l * (int64_t)T;
+    if (clamp) {
+      if (!diag && jl >= T) f.template compute<false, true>(sc, p, false, T);
+      else f.template compute<true, true>(sc, p, diag, (int)(jl < T ? jl : T));
+    } else {
+      if (!diag && jl >= T) f.template compute<false, false>(sc, p, false, T);
+      else f.template compute<true, false>(sc, p, diag, (int)(jl < T ? jl : T));
+    }
+
+    double v[NOUT];
+    f.outputs(v);
+    commit_tile<NOUT, F::NT>(v, red, a.limbs, a.scale_exp);
+  }
+}
+
+// Several data sets per launch (LSCV_H: one whitened copy of the data per candidate).
+template <class F>
+__global__ void __launch_bounds__(F::NT, F::MINB) pair_kernel_sets(const Args a,
+                                                        const __grid_constant__ typename F::Params p) {
+  constexpr int T = F::T, D = F::D, NOUT = F::NOUT, NW = F::NT / 32;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* cols = reinterpret_cast<float*>(smem_raw);                 // [2][D][T]
+  double* red = reinterpret_cast<double*>(cols + 2 * D * T);        // [NW][NOUT]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(red + NW * NOUT);      // [2]
+  const int tid = threadIdx.x;
+
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
   // Work units u in [0, n_sets * tiles): set = u / tiles, tile = tile_begin + u % tiles (set-major,
   // so consecutive CTAs share a set's data in L2).
   const int64_t per = a.tile_end - a.tile_begin;
@@ -380,11 +438,13 @@ inline cudaError_t launch_pair(const LaunchCfg& c, const typename F::Params& p) 
   const size_t smem = 2 * F::D * F::T * sizeof(float) + (F::NT / 32) * F::NOUT * sizeof(double) + 16;
   static int occ = -1;   // per-instantiation: resident CTAs per SM
   if (occ < 0) {
-    cudaError_t e = cudaFuncSetAttribute(pair_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+    const void* kern;
+    if constexpr (F::kSets) kern = (const void*)pair_kernel_sets<F>;
+    else kern = (const void*)pair_kernel<F>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int o = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, pair_kernel<F>, F::NT, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, F::NT, smem);
     if (e != cudaSuccess) return e;
     occ = o > 0 ? o : 1;
   }
@@ -392,7 +452,8 @@ inline cudaError_t launch_pair(const LaunchCfg& c, const typename F::Params& p) 
   int64_t grid = (int64_t)c.sm_count * occ;
   if (grid > units) grid = units;
   Args a{c.X, c.n, c.ld, c.tile_begin, c.tile_end, c.scale_exp, c.limbs, c.clamp, c.n_sets, c.set_stride};
-  pair_kernel<F><<<(unsigned)grid, F::NT, smem, c.stream>>>(a, p);
+  if constexpr (F::kSets) pair_kernel_sets<F><<<(unsigned)grid, F::NT, smem, c.stream>>>(a, p);
+  else pair_kernel<F><<<(unsigned)grid, F::NT, smem, c.stream>>>(a, p);
   return cudaGetLastError();
 }
 

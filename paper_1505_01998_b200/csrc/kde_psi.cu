@@ -168,6 +168,63 @@ cudaError_t launch_prep(const double* X, int64_t n, int d, const double* W_dev,
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ device-resident PLUGIN chain
+// The scalar steps of Sec. 4.4.1 (Eq. 11-18) run in single-thread kernels between the
+// O(n) and O(n^2) kernels, so kde_plugin_h enqueues the whole chain without a host round trip
+// (one synchronisation at the end).  State in the workspace's `small` block (PluginDev layout).
+__device__ __forceinline__ double limbs_value_dev(const unsigned long long* l, int S) {
+  const __int128 T = (__int128)(long long)l[0] * ((__int128)1 << 80) +
+                     (__int128)(long long)l[1] * ((__int128)1 << 40) + (__int128)(long long)l[2];
+  return ldexp((double)T, -S);
+}
+
+__device__ __forceinline__ void set_status(double* st, int code) {
+  if (st[0] == 0.0) st[0] = (double)code;   // first failure wins
+}
+
+// stage 0: mean = sum / n.  stage 1: V-hat, sigma-hat, Psi8^NS, g1 (steps 1-4), W = 1/g1.
+// stage 2: Psi6-hat(g1) (step 5), g2 (step 6), W = 1/g2.  stage 3: Psi4-hat(g2) (step 7), h (8).
+__global__ void plugin_chain_kernel(int stage, int64_t n, double* small, const unsigned long long* limbs,
+                                    int S) {
+  PluginDev dv(small);
+  const double nn = (double)n, pi = 3.14159265358979323846, s2p = sqrt(2.0 * pi);
+  double* t = dv.trace;   // V_hat, sigma_hat, psi8_ns, g1, psi6, g2, psi4, h
+  if (stage == 0) {
+    const double sum = dv.sums[0];
+    if (!isfinite(sum)) set_status(dv.status, 1);                          // KDE_E_INVALID
+    dv.mean[0] = sum / nn;
+  } else if (stage == 1) {
+    const double V = dv.sums[0] / (nn - 1.0);
+    if (!isfinite(V)) set_status(dv.status, 1);
+    t[0] = V;                                                              // Eq. 11
+    if (!(V > 0.0)) set_status(dv.status, 4);                              // KDE_E_DEGENERATE
+    t[1] = sqrt(V);                                                        // Eq. 12
+    t[2] = 105.0 / (32.0 * sqrt(pi) * pow(t[1], 9.0));                     // Eq. 13
+    const double K6_0 = -15.0 / s2p;
+    t[3] = pow(-2.0 * K6_0 / (t[2] * nn), 1.0 / 9.0);                      // Eq. 14
+    dv.W[0] = 1.0 / t[3];
+  } else if (stage == 2) {
+    const double Sr = limbs_value_dev(limbs, S);
+    t[4] = (2.0 * Sr / s2p + nn * -15.0 / s2p) / (nn * nn * pow(t[3], 7.0));   // Eq. 15, reading Z1
+    if (!(t[4] < 0.0)) set_status(dv.status, 8);                           // KDE_E_NUMERIC
+    const double K4_0 = 3.0 / s2p;
+    t[5] = pow(-2.0 * K4_0 / (t[4] * nn), 1.0 / 7.0);                      // Eq. 16
+    dv.W[0] = 1.0 / t[5];
+  } else {
+    const double Sr = limbs_value_dev(limbs, S);
+    t[6] = (2.0 * Sr / s2p + nn * 3.0 / s2p) / (nn * nn * pow(t[5], 5.0));     // Eq. 17
+    if (!(t[6] > 0.0)) set_status(dv.status, 8);
+    const double RK = 1.0 / (2.0 * sqrt(pi));
+    t[7] = pow(RK / (t[6] * nn), 0.2);                                     // Eq. 18
+  }
+}
+
+cudaError_t launch_plugin_chain(int stage, int64_t n, double* small, const unsigned long long* limbs, int S,
+                                cudaStream_t s) {
+  plugin_chain_kernel<<<1, 1, 0, s>>>(stage, n, small, limbs, S);
+  return cudaGetLastError();
+}
+
 // Ascending sort of n fp64 samples (CUB radix sort, keys only: deterministic).  The pair sums
 // are invariant under permutation; sorted input keeps the term magnitudes inside a column
 // group homogeneous, which makes the fp32 group sums of FPsi nearly lossless.
