@@ -95,9 +95,13 @@ struct Args {
 // Psi_r cancel 1000-5000x at the PLUGIN bandwidths, so that bias pattern alone cost 2e-5..5e-5
 // relative.  Offsetting into one binade and averaging over 8 fractional shifts brings the error
 // to ~2e-10 of sum|t| at no per-eval cost (measured by tools/term_error.cu).
-template <int RORD, int NT_>
+// CS_ > 1 (small n): each tile's columns are split into CS_ chunks that are separate work units,
+// so a launch over few tiles still spreads over the GPU (the split is fixed by n: deterministic).
+template <int RORD, int NT_, int CS_ = 1>
 struct FPsi {
-  static constexpr int NT = NT_, D = 1, R = 8, T = NT_ * 8, NOUT = 1, CH = T < 1024 ? T : 1024, MINB = 1024 / NT_;
+  static constexpr int NT = NT_, D = 1, R = 8, T = NT_ * 8, NOUT = 1, MINB = 1024 / NT_;
+  static constexpr int CS = CS_, CW = T / CS_;                     // column chunks per tile, width
+  static constexpr int CH = CS_ > 1 ? CW : (T < 1024 ? T : 1024);  // columns per fp64 flush
   static constexpr int NP = R / 2;   // row pairs (r = 2p, 2p+1) packed into fp32x2 lanes
   static constexpr int G = 16;       // columns per compensated group
   static constexpr float K = (float)(RORD - 1);
@@ -105,6 +109,7 @@ struct FPsi {
   using Params = PsiParams;
   f2 xr[NP];
   double acc;
+  int jbase;   // first column of this work unit's chunk (CS > 1)
 
   // Rows are interleaved: thread t owns rows q*T + 8t + r, r = 0..7.  The data are sorted
   // (kde_host.cpp), so the 8 accumulator classes r see statistically identical distances.
@@ -138,7 +143,8 @@ struct FPsi {
     f2 o[NP];
 #pragma unroll
     for (int q = 0; q < NP; ++q) o[q] = pk(p.o[2 * q], p.o[2 * q + 1]);
-    for (int jc = 0; jc < T; jc += CH) {
+    const int J0 = CS > 1 ? jbase : 0, J1 = CS > 1 ? jbase + CW : T;
+    for (int jc = J0; jc < J1; jc += CH) {
       if (MASK && jc >= jlim) break;
       f2 a[NP], cmp[NP];
 #pragma unroll
@@ -222,6 +228,7 @@ struct FLscvScalar {
   static constexpr int MINB = (UNIT && D <= 4 ? 1024 : 512) / NT_;   // UNIT d<=4: 4 CTAs of 256, 64 regs
   static constexpr int UNR = UNIT && D <= 4 ? (D <= 3 ? 4 : 2) : 1;   // UNIT: short body, unroll the column loop
   static constexpr bool kClampable = false, kSets = UNIT;
+  static constexpr int CS = 1;
   using Params = LscvScalarParams;
   f2 xr[D];
   f2 a1[NB], a2[NB];
@@ -327,6 +334,50 @@ __global__ void __launch_bounds__(F::NT, F::MINB) pair_kernel(const Args a,
   }
   __syncthreads();
 
+  if constexpr (F::CS > 1) {
+  // column-split tiles: work unit u = (tile tb + u / CS, chunk u % CS)
+  constexpr int CS = F::CS;
+  const int64_t units = (a.tile_end - a.tile_begin) * CS;
+  auto issue = [&](int64_t u, int buf) {
+    int64_t l, q;
+    tile_coords(a.tile_begin + u / CS, l, q);
+    float* dst = cols + buf * D * T;
+    mbar_expect_tx(&bar[buf], (uint32_t)(D * T * sizeof(float)));
+#pragma unroll
+    for (int d = 0; d < D; ++d)
+      tma_load_1d(dst + d * T, a.X + d * a.ld + l * T, (uint32_t)(T * sizeof(float)), &bar[buf]);
+  };
+  const bool clamp = F::kClampable && a.clamp != nullptr && *a.clamp != 0;   // uniform per launch
+  int64_t u = blockIdx.x;
+  if (tid == 0 && u < units) issue(u, 0);
+  uint32_t k = 0;
+  for (; u < units; u += gridDim.x, ++k) {
+    int64_t l, q;
+    tile_coords(a.tile_begin + u / CS, l, q);
+    const int64_t un = u + gridDim.x;
+    if (tid == 0 && un < units) issue(un, (k + 1) & 1);
+
+    F f;
+    f.load_rows(a.X, a.ld, row_origin<F>(q));
+    f.jbase = (int)(u % CS) * F::CW;
+    mbar_wait(&bar[k & 1], (k >> 1) & 1);
+    const float* sc = cols + (k & 1) * D * T;
+    const bool diag = (q == l);
+    const int64_t jl = a.n - l * (int64_t)T;
+    if (clamp) {
+      if (!diag && jl >= T) f.template compute<false, true>(sc, p, false, T);
+      else f.template compute<true, true>(sc, p, diag, (int)(jl < T ? jl : T));
+    } else {
+      if (!diag && jl >= T) f.template compute<false, false>(sc, p, false, T);
+      else f.template compute<true, false>(sc, p, diag, (int)(jl < T ? jl : T));
+    }
+
+    double v[NOUT];
+    f.outputs(v);
+    commit_tile<NOUT, F::NT>(v, red, a.limbs, a.scale_exp);
+  }
+    return;
+  } else {
   auto issue = [&](int64_t tile, int buf) {
     int64_t l, q;
     tile_coords(tile, l, q);
@@ -364,6 +415,7 @@ __global__ void __launch_bounds__(F::NT, F::MINB) pair_kernel(const Args a,
     double v[NOUT];
     f.outputs(v);
     commit_tile<NOUT, F::NT>(v, red, a.limbs, a.scale_exp);
+  }
   }
 }
 
@@ -448,7 +500,7 @@ inline cudaError_t launch_pair(const LaunchCfg& c, const typename F::Params& p) 
     if (e != cudaSuccess) return e;
     occ = o > 0 ? o : 1;
   }
-  const int64_t units = (c.tile_end - c.tile_begin) * c.n_sets;
+  const int64_t units = (c.tile_end - c.tile_begin) * c.n_sets * F::CS;
   int64_t grid = (int64_t)c.sm_count * occ;
   if (grid > units) grid = units;
   Args a{c.X, c.n, c.ld, c.tile_begin, c.tile_end, c.scale_exp, c.limbs, c.clamp, c.n_sets, c.set_stride};

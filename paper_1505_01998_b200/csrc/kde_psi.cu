@@ -38,12 +38,26 @@ int cand_per_launch(Kind k, int d) {
   return 1;
 }
 
+// Small n (fewer tiles of 512 than ~2 waves of 64-thread CTAs, 16 per SM): split each tile's
+// columns into 8 work units of 64, so the launch fills the GPU.
+static bool psi_split(const LaunchCfg& c) {
+  static const char* dbg = getenv("KDE_DEBUG_PSI_SPLIT");   // diagnostics only
+  if (dbg) return c.tile == 512 && atoi(dbg) == 1;
+  const int64_t nb = (c.n + c.tile - 1) / c.tile;
+  return c.tile == 512 && nb * (nb + 1) / 2 < 2 * 16 * (int64_t)c.sm_count;
+}
+
+template <int R>
+static cudaError_t launch_psi_r(const LaunchCfg& c, const PsiParams& p) {
+  if (c.tile == 2048) return launch_pair<FPsi<R, 256>>(c, p);
+  return psi_split(c) ? launch_pair<FPsi<R, 64, 8>>(c, p) : launch_pair<FPsi<R, 64>>(c, p);
+}
+
 cudaError_t launch_psi(int r, const LaunchCfg& c, const PsiParams& p) {
-  const bool big = c.tile == 2048;
   switch (r) {
-    case 4: return big ? launch_pair<FPsi<4, 256>>(c, p) : launch_pair<FPsi<4, 64>>(c, p);
-    case 6: return big ? launch_pair<FPsi<6, 256>>(c, p) : launch_pair<FPsi<6, 64>>(c, p);
-    case 8: return big ? launch_pair<FPsi<8, 256>>(c, p) : launch_pair<FPsi<8, 64>>(c, p);
+    case 4: return launch_psi_r<4>(c, p);
+    case 6: return launch_psi_r<6>(c, p);
+    case 8: return launch_psi_r<8>(c, p);
   }
   return cudaErrorInvalidValue;
 }
