@@ -45,6 +45,7 @@ struct LaunchCfg {
 
 // Launchers (kde_psi.cu, kde_lscv_scalar.cu, kde_lscv_matrix.cu).  Return cudaSuccess or the launch error.
 cudaError_t launch_psi(int r, const LaunchCfg& c, const PsiParams& p);
+cudaError_t prepare_psi(int r, const LaunchCfg& c);   // one-time setup of launch_psi's kernel
 cudaError_t launch_lscv_scalar(int d, int nb, const LaunchCfg& c, const LscvScalarParams& p);
 // LSCV_H with per-candidate whitened data (one candidate per set, c.n_sets sets).
 cudaError_t launch_lscv_white(int d, const LaunchCfg& c);

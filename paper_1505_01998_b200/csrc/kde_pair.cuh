@@ -484,11 +484,12 @@ __global__ void __launch_bounds__(F::NT, F::MINB) pair_kernel_sets(const Args a,
   }
 }
 
+// One-time per-instantiation setup (shared-memory opt-in, resident CTAs per SM).  Not allowed
+// inside a stream capture, so graph users call it before capturing (prepare_* below).
 template <class F>
-inline cudaError_t launch_pair(const LaunchCfg& c, const typename F::Params& p) {
-  if (c.tile_end <= c.tile_begin) return cudaSuccess;
-  const size_t smem = 2 * F::D * F::T * sizeof(float) + (F::NT / 32) * F::NOUT * sizeof(double) + 16;
-  static int occ = -1;   // per-instantiation: resident CTAs per SM
+inline cudaError_t pair_occupancy(int* occ_out) {
+  constexpr size_t smem = 2 * F::D * F::T * sizeof(float) + (F::NT / 32) * F::NOUT * sizeof(double) + 16;
+  static int occ = -1;
   if (occ < 0) {
     const void* kern;
     if constexpr (F::kSets) kern = (const void*)pair_kernel_sets<F>;
@@ -500,6 +501,17 @@ inline cudaError_t launch_pair(const LaunchCfg& c, const typename F::Params& p) 
     if (e != cudaSuccess) return e;
     occ = o > 0 ? o : 1;
   }
+  *occ_out = occ;
+  return cudaSuccess;
+}
+
+template <class F>
+inline cudaError_t launch_pair(const LaunchCfg& c, const typename F::Params& p) {
+  if (c.tile_end <= c.tile_begin) return cudaSuccess;
+  constexpr size_t smem = 2 * F::D * F::T * sizeof(float) + (F::NT / 32) * F::NOUT * sizeof(double) + 16;
+  int occ = 1;
+  cudaError_t e = pair_occupancy<F>(&occ);
+  if (e != cudaSuccess) return e;
   const int64_t units = (c.tile_end - c.tile_begin) * c.n_sets * F::CS;
   int64_t grid = (int64_t)c.sm_count * occ;
   if (grid > units) grid = units;
@@ -508,6 +520,5 @@ inline cudaError_t launch_pair(const LaunchCfg& c, const typename F::Params& p) 
   else pair_kernel<F><<<(unsigned)grid, F::NT, smem, c.stream>>>(a, p);
   return cudaGetLastError();
 }
-
 
 }  // namespace kde

@@ -53,6 +53,22 @@ static cudaError_t launch_psi_r(const LaunchCfg& c, const PsiParams& p) {
   return psi_split(c) ? launch_pair<FPsi<R, 64, 8>>(c, p) : launch_pair<FPsi<R, 64>>(c, p);
 }
 
+template <int R>
+static cudaError_t prepare_psi_r(const LaunchCfg& c) {
+  int occ;
+  if (c.tile == 2048) return pair_occupancy<FPsi<R, 256>>(&occ);
+  return psi_split(c) ? pair_occupancy<FPsi<R, 64, 8>>(&occ) : pair_occupancy<FPsi<R, 64>>(&occ);
+}
+
+cudaError_t prepare_psi(int r, const LaunchCfg& c) {
+  switch (r) {
+    case 4: return prepare_psi_r<4>(c);
+    case 6: return prepare_psi_r<6>(c);
+    case 8: return prepare_psi_r<8>(c);
+  }
+  return cudaErrorInvalidValue;
+}
+
 cudaError_t launch_psi(int r, const LaunchCfg& c, const PsiParams& p) {
   switch (r) {
     case 4: return launch_psi_r<4>(c, p);

@@ -291,3 +291,23 @@ def test_lscv_H_many_candidates_span_launches(ctx):
     g = ctx.lscv_H_scores(Xd, cands[[0, 256, 299]])
     for v, c in zip(g, cands[[0, 256, 299]]):
         assert rel(v, oracle.lscv_H_score(X, c)) < RTOL
+
+
+def test_plugin_graph_replay_follows_the_data(ctx):
+    # kde_plugin_h replays a captured CUDA graph while (pointer, n) are unchanged: new data in the
+    # same buffer must give that data's bandwidth, and errors must still be reported.
+    a = datagen.sample_mixture("skewed", 3000, 51)
+    b = datagen.sample_mixture("bimodal", 3000, 52)
+    xd = dev(a)
+    ha = ctx.plugin_h(xd)
+    xd.copy_(torch.from_numpy(b).cuda())
+    hb = ctx.plugin_h(xd)
+    fresh = kb.Context()
+    assert hb == fresh.plugin_h(dev(b)) and ha == fresh.plugin_h(dev(a))
+    fresh.close()
+    xd.fill_(1.5)
+    with pytest.raises(kb.KDEError) as e:
+        ctx.plugin_h(xd)
+    assert e.value.status == "KDE_E_DEGENERATE"
+    xd.copy_(torch.from_numpy(a).cuda())
+    assert ctx.plugin_h(xd) == ha
