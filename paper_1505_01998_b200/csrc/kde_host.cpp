@@ -1203,7 +1203,8 @@ static kde_status plugin_impl(kde_ctx* c, const double* x, int64_t n, kde_plugin
                                       (uintptr_t)c->h_limbs, (uintptr_t)c->profiling, (uintptr_t)c->comm};
   // The first call with a given key runs directly (and does any lazy module loading and library
   // setup outside a capture); a second call with the same key captures, later ones replay.
-  if (!c->graphs || (key != c->plug_seen && !(c->plug_exec && key == c->plug_key))) {
+  // (single-GPU contexts only: with a communicator the all-reduces stay plain stream operations)
+  if (!c->graphs || c->comm || (key != c->plug_seen && !(c->plug_exec && key == c->plug_key))) {
     TRY(plugin_enqueue(c, x, n, T, ld, w));
     c->plug_seen = key;
   } else {
