@@ -7,9 +7,13 @@
 
 namespace kde {
 
+// d <= 4: 8 candidates per pair visit at 3 CTAs/SM, a quarter of the exponentials in software on
+// the FMA pipe (measured on C2: 478 ms vs 490 ms for 16 candidates, all on MUFU); d > 4: the
+// per-pair work dominates, 16 candidates on MUFU.
 template <int D>
 static cudaError_t lscv_scalar_d(const LaunchCfg& c, const LscvScalarParams& p) {
-  return launch_pair<FLscvScalar<D, 256, nb_scalar(D)>>(c, p);
+  if constexpr (D <= 4) return launch_pair<FLscvScalar<D, 256, nb_scalar(D), false, true, 3>>(c, p);
+  else return launch_pair<FLscvScalar<D, 256, nb_scalar(D)>>(c, p);
 }
 
 cudaError_t launch_lscv_scalar(int d, int nb, const LaunchCfg& c, const LscvScalarParams& p) {

@@ -27,7 +27,7 @@
 namespace kde {
 
 // Candidates per launch: chosen so that no instantiation spills at 128 registers (2 CTAs/SM).
-constexpr int nb_scalar(int d) { return d <= 12 ? 16 : 8; }
+constexpr int nb_scalar(int d) { return d <= 4 ? 8 : (d <= 12 ? 16 : 8); }
 
 
 // ------------------------------------------------------------------ small device helpers
@@ -221,11 +221,13 @@ struct FPsi {
 // UNIT (LSCV_H, one candidate per data set): the data are whitened by the candidate itself,
 // x' = sqrt(log2 e / 4) L_c^-1 (x - mean) with H_c = L_c L_c^T, so s = (log2 e / 4) v^T H_c^-1 v
 // and e = 2^-s (the negation is a MUFU operand modifier): 2d + 2 FP32 ops per eval.
-template <int D_, int NT_, int NB_, bool UNIT = false>
+// SWC (LSCV_h): the exponentials of the 4th column of every 4 come from exp2_sw2 on the FMA pipe
+// instead of MUFU.EX2 (chosen by column, so a candidate's sum does not depend on its batch).
+template <int D_, int NT_, int NB_, bool UNIT = false, bool SWC = false, int MINB_ = 0>
 struct FLscvScalar {
   static_assert(!UNIT || NB_ == 1, "UNIT sets carry one candidate");
   static constexpr int NT = NT_, D = D_, R = 2, T = NT_ * 2, NB = NB_, NOUT = 2 * NB_;
-  static constexpr int MINB = (UNIT && D <= 4 ? 1024 : 512) / NT_;   // UNIT d<=4: 4 CTAs of 256, 64 regs
+  static constexpr int MINB = MINB_ > 0 ? MINB_ : (UNIT && D <= 4 ? 1024 : 512) / NT_;   // UNIT d<=4: 4 CTAs of 256
   static constexpr int UNR = UNIT && D <= 4 ? (D <= 3 ? 4 : 2) : 1;   // UNIT: short body, unroll the column loop
   static constexpr bool kClampable = false, kSets = UNIT;
   static constexpr int CS = 1;
@@ -281,9 +283,15 @@ struct FLscvScalar {
         } else {
 #pragma unroll
           for (int c = 0; c < NB; ++c) {
-            float q0, q1;
-            upk(mul2(s, pk(p.kappa[c], p.kappa[c])), q0, q1);
-            const f2 e = pk(ex2(q0), ex2(q1));
+            const f2 q = mul2(s, pk(p.kappa[c], p.kappa[c]));
+            f2 e;
+            if (SWC && k == 3) {
+              e = exp2_sw2(q);
+            } else {
+              float q0, q1;
+              upk(q, q0, q1);
+              e = pk(ex2(q0), ex2(q1));
+            }
             a1[c] = add2(a1[c], e);
             a2[c] = fma2(e, e, a2[c]);
           }
