@@ -236,20 +236,6 @@ std::vector<double> tri_lower_inverse(const std::vector<double>& L, int d) {
   return M;
 }
 
-// SPD inverse from its Cholesky factor: A^-1 = L^-T L^-1.
-std::vector<double> spd_inverse(const std::vector<double>& L, int d) {
-  std::vector<double> Li = tri_lower_inverse(L, d), R((size_t)d * d, 0.0);
-  for (int i = 0; i < d; ++i)
-    for (int j = 0; j < d; ++j) {
-      double s = 0.0;
-      for (int k = std::max(i, j); k < d; ++k) s += Li[k * d + i] * Li[k * d + j];
-      R[i * d + j] = s;
-    }
-  for (int i = 0; i < d; ++i)
-    for (int j = 0; j < i; ++j) R[i * d + j] = R[j * d + i] = 0.5 * (R[i * d + j] + R[j * d + i]);
-  return R;
-}
-
 // Principal square root of an SPD matrix by the Denman–Beavers iteration (the paper used
 // ALGLIB; reading Z9).  Y_{k+1} = (Y_k + Z_k^-1)/2, Z_{k+1} = (Z_k + Y_k^-1)/2.
 bool gen_inverse(const std::vector<double>& A, int d, std::vector<double>& R) {

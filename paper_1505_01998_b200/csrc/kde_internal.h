@@ -33,7 +33,7 @@ struct LaunchCfg {
   int tile;                // tile edge T (rows = columns)
   int scale_exp;           // fixed-point exponent S
   unsigned long long* limbs;   // [n_out][3] accumulators, device
-  int n_out;               // outputs written by this launch (<= 2*kMaxCand)
+  int n_out;               // outputs written per data set by this launch
   cudaStream_t stream;
   int sm_count;
   const unsigned long long* clamp = nullptr;   // Psi: device flag "some |x'| > 3e4"
