@@ -142,7 +142,7 @@ struct FPsi {
     const f2 mk = pk(-K, -K);
     f2 o[NP];
 #pragma unroll
-    for (int q = 0; q < NP; ++q) o[q] = pk(p.o[2 * q], p.o[2 * q + 1]);
+    for (int q = 0; q < NP; ++q) o[q] = reinterpret_cast<const f2*>(p.o)[q];   // 64-bit constant loads
     const int J0 = CS > 1 ? jbase : 0, J1 = CS > 1 ? jbase + CW : T;
     for (int jc = J0; jc < J1; jc += CH) {
       if (MASK && jc >= jlim) break;
