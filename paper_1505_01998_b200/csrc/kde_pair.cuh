@@ -99,7 +99,7 @@ struct Args {
 // so a launch over few tiles still spreads over the GPU (the split is fixed by n: deterministic).
 template <int RORD, int NT_, int CS_ = 1>
 struct FPsi {
-  static constexpr int NT = NT_, D = 1, R = 8, T = NT_ * 8, NOUT = 1, MINB = 1024 / NT_;
+  static constexpr int NT = NT_, D = 1, R = 8, T = NT_ * 8, NOUT = 1, MINB = 768 / NT_;
   static constexpr int CS = CS_, CW = T / CS_;                     // column chunks per tile, width
   static constexpr int CH = CS_ > 1 ? CW : (T < 1024 ? T : 1024);  // columns per fp64 flush
   static constexpr int NP = R / 2;   // row pairs (r = 2p, 2p+1) packed into fp32x2 lanes
