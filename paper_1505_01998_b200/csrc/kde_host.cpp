@@ -404,11 +404,10 @@ kde_status gpu_prep_into(kde_ctx* c, const double* X, int64_t n, int d, const st
                          const std::vector<double>& mean, int64_t ld, Ws& w, float* Y,
                          double clamp_thresh = 0.0) {
   Range r("kde.prep");
-  double* mean_dev = w.small;
-  double* W_dev = w.small + 16;
-  CUDA_TRY(c, cudaMemcpyAsync(mean_dev, mean.data(), d * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-  CUDA_TRY(c, cudaMemcpyAsync(W_dev, W.data(), (size_t)d * d * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-  CUDA_TRY(c, kde::launch_prep(X, n, d, W_dev, mean_dev, Y, ld, c->stream, 0.f, w.flag(), clamp_thresh));
+  kde::PrepParams pp;                      // W and mean travel in the kernel parameters
+  std::copy(W.begin(), W.begin() + (size_t)d * d, pp.W);
+  std::copy(mean.begin(), mean.begin() + d, pp.mean);
+  CUDA_TRY(c, kde::launch_prep_params(X, n, d, pp, Y, ld, c->stream, 0.f, w.flag(), clamp_thresh));
   c->prof_all += 1;
   return KDE_OK;
 }
@@ -1397,13 +1396,12 @@ kde_status kde_evaluate(kde_ctx* c, const double* X, int64_t n, int32_t d, const
     if (!std::isfinite(hs[a])) return fail(c, KDE_E_INVALID, "non-finite sample values");
     mean[a] = hs[a] / (double)n;
   }
-  double* mean_dev = w.small;
-  double* W_dev = w.small + 16;
-  CUDA_TRY(c, cudaMemcpyAsync(mean_dev, mean.data(), d * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-  CUDA_TRY(c, cudaMemcpyAsync(W_dev, W.data(), (size_t)d * d * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  kde::PrepParams pp;
+  std::copy(W.begin(), W.begin() + (size_t)d * d, pp.W);
+  std::copy(mean.begin(), mean.begin() + d, pp.mean);
   CUDA_TRY(c, cudaMemsetAsync(w.flag(), 0, sizeof(unsigned long long), c->stream));
-  CUDA_TRY(c, kde::launch_prep(X, n, d, W_dev, mean_dev, Xw, ldn, c->stream, __int_as_float_host(0x7f800000), w.flag()));
-  CUDA_TRY(c, kde::launch_prep(Y, m, d, W_dev, mean_dev, Yw, ldm, c->stream, 0.f, w.flag()));
+  CUDA_TRY(c, kde::launch_prep_params(X, n, d, pp, Xw, ldn, c->stream, __int_as_float_host(0x7f800000), w.flag()));
+  CUDA_TRY(c, kde::launch_prep_params(Y, m, d, pp, Yw, ldm, c->stream, 0.f, w.flag()));
   kde::EvalLaunch el;
   el.Y = Yw; el.X = Xw; el.m = m; el.ldm = ldm; el.ldn = ldn; el.part = part; el.part_capacity = parts;
   el.scale = std::pow(2.0 * kPi, -0.5 * d) / std::sqrt(det) / (double)n;

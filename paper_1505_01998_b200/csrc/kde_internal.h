@@ -59,6 +59,13 @@ cudaError_t launch_moments2(const double* X, int64_t n, int d, const double* mea
                             double* part, int nblk, cudaStream_t s);
 cudaError_t launch_reduce_parts(const double* part, int nblk, int width, double* out,
                                 cudaStream_t s);
+struct PrepParams {
+  double W[kMaxDim * kMaxDim];   // row-major d x d
+  double mean[kMaxDim];
+};
+cudaError_t launch_prep_params(const double* X, int64_t n, int d, const PrepParams& pp, float* Y, int64_t ld,
+                               cudaStream_t s, float pad = 0.f, unsigned long long* overflow_flag = nullptr,
+                               double clamp_thresh = 0.0);
 cudaError_t launch_prep(const double* X, int64_t n, int d, const double* W_dev,
                         const double* mean_dev, float* Y, int64_t ld, cudaStream_t s,
                         float pad = 0.f, unsigned long long* overflow_flag = nullptr,

@@ -162,12 +162,12 @@ cudaError_t launch_reduce_parts(const double* part, int nblk, int width, double*
   return cudaGetLastError();
 }
 
-// Data prep (row a1 of SURVEY §8(a)): y_a = fp32( sum_b W_ab (x_b - mean_b) ), zero padding.
-__global__ void prep_kernel(const double* __restrict__ X, int64_t n, int d,
-                            const double* __restrict__ W, const double* __restrict__ mean,
-                            float* __restrict__ Y, int64_t ld, float pad,
-                            unsigned long long* __restrict__ flag, double clamp_thresh) {
-  // flag[0]: some scaled value beyond 1e18 (error); flag[1]: some beyond clamp_thresh (> 0)
+// Data prep (row a1 of SURVEY §8(a)): y_a = fp32( sum_b W_ab (x_b - mean_b) ), padding `pad`.
+// flag[0]: some scaled value beyond 1e18 (error); flag[1]: some beyond clamp_thresh (> 0).
+__device__ __forceinline__ void prep_body(const double* __restrict__ X, int64_t n, int d,
+                                          const double* W, const double* mean,
+                                          float* __restrict__ Y, int64_t ld, float pad,
+                                          unsigned long long* __restrict__ flag, double clamp_thresh) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   bool bad = false, big = false;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ld; i += stride) {
@@ -189,12 +189,36 @@ __global__ void prep_kernel(const double* __restrict__ X, int64_t n, int d,
   if (big && flag) atomicOr(flag + 1, 1ull);
 }
 
+// W and mean in device memory (the device-resident PLUGIN chain writes them).
+__global__ void prep_kernel(const double* __restrict__ X, int64_t n, int d, const double* __restrict__ W,
+                            const double* __restrict__ mean, float* __restrict__ Y, int64_t ld, float pad,
+                            unsigned long long* __restrict__ flag, double clamp_thresh) {
+  prep_body(X, n, d, W, mean, Y, ld, pad, flag, clamp_thresh);
+}
+
+// W and mean passed by value in the kernel parameters (no host-to-device copy per prep).
+__global__ void prep_kernel_p(const double* __restrict__ X, int64_t n, int d, const __grid_constant__ PrepParams pp,
+                              float* __restrict__ Y, int64_t ld, float pad, unsigned long long* __restrict__ flag,
+                              double clamp_thresh) {
+  prep_body(X, n, d, pp.W, pp.mean, Y, ld, pad, flag, clamp_thresh);
+}
+
+static unsigned prep_blocks(int64_t ld) {
+  int64_t blocks = (ld + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  return (unsigned)blocks;
+}
+
 cudaError_t launch_prep(const double* X, int64_t n, int d, const double* W_dev,
                         const double* mean_dev, float* Y, int64_t ld, cudaStream_t s, float pad,
                         unsigned long long* flag, double clamp_thresh) {
-  int64_t blocks = (ld + 255) / 256;
-  if (blocks > 148 * 16) blocks = 148 * 16;
-  prep_kernel<<<(unsigned)blocks, 256, 0, s>>>(X, n, d, W_dev, mean_dev, Y, ld, pad, flag, clamp_thresh);
+  prep_kernel<<<prep_blocks(ld), 256, 0, s>>>(X, n, d, W_dev, mean_dev, Y, ld, pad, flag, clamp_thresh);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_prep_params(const double* X, int64_t n, int d, const PrepParams& pp, float* Y, int64_t ld,
+                               cudaStream_t s, float pad, unsigned long long* flag, double clamp_thresh) {
+  prep_kernel_p<<<prep_blocks(ld), 256, 0, s>>>(X, n, d, pp, Y, ld, pad, flag, clamp_thresh);
   return cudaGetLastError();
 }
 
