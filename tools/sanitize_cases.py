@@ -26,3 +26,6 @@ print("select h refine", ctx.select_bandwidth(kb.LSCV_h, X, n_grid=20, refine_st
 print("plugin host input", ctx.plugin_h(datagen.sample_mixture("skewed", 1500, 1))[0])
 print("psi shards", [kb.fixed_value(f) for r in range(3) for f in ctx.raw_sums(kb.SUM_PSI6, x, [0.3], shard=(r, 3))])
 print("select plugin", ctx.select_bandwidth(kb.PLUGIN, x)["h"])
+print("lscv_H 300 candidates (two launches)", ctx.lscv_H_scores(X, np.tile([[0.05, 0.01, 0.04]], (300, 1)))[[0, 299]])
+xs = kb.to_device(datagen.sample_mixture("skewed", 700, 3))
+print("plugin x3 (graph capture + replay)", [ctx.plugin_h(xs)[0] for _ in range(3)])
