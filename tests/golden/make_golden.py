@@ -3,7 +3,7 @@
 Calls only oracle/ (and datagen for the seeded inputs).  Each JSON file records the workload,
 the oracle outputs and the PAPER.md passages they follow.  Run (CPU, all cores, ~1 h):
 
-    python tests/golden/make_golden.py [C4] [C2] [C3] [C5]
+    python tests/golden/make_golden.py [C1] [C4] [C2] [C3] [C5]
 """
 from __future__ import annotations
 
@@ -27,6 +27,16 @@ THREADS = len(os.sched_getaffinity(0))
 def dump(name, obj):
     with open(os.path.join(HERE, name), "w") as f:
         json.dump(obj, f, indent=1)
+
+
+def c1():
+    x = datagen.config_data("C1")[0]
+    t0 = time.time()
+    tr = oracle.plugin(x)
+    dump("C1_plugin.json", {
+        "config": "C1", "workload": "PLUGIN, n=1000, N(0,1), datagen seed 1",
+        "cite": "PAPER.md P:203-256 (Sec. 4.4.1 steps 1-8, Eq. 11-18), reading Z1 for Eq. 15/17",
+        "trace": tr, "oracle_seconds": time.time() - t0, "threads": 1})
 
 
 def c4():
@@ -93,7 +103,7 @@ def c5():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["C4", "C2", "C3", "C5"]
+    which = sys.argv[1:] or ["C1", "C4", "C2", "C3", "C5"]
     for w in which:
         print("golden", w, flush=True)
-        {"C4": c4, "C2": c2, "C3": c3, "C5": c5}[w]()
+        {"C1": c1, "C4": c4, "C2": c2, "C3": c3, "C5": c5}[w]()

@@ -1,10 +1,13 @@
-"""Time every BASELINE.json config through the public API (1 GPU), one JSON line each.
+"""Time every BASELINE.json config through the public API (1 GPU), one JSON line each
+(SURVEY §8(d) d8 report).
 
-  python tools/bench_configs.py [C1 C2 C3 C4 C5] [--reps 3]
+  python tools/bench_configs.py [C1 C2 C3 C4 C5 ...] [--reps 3]
 
 evals = algorithmic pair-kernel evaluations (pairs i<j x candidates); pair_ms = device time of
 the pair-kernel launches (library events); wall_ms = host wall time of the call (time to
 bandwidth / to scores, X resident on the device).  MUFU peak = 16 EX2/clk/SM x SMs x 1965 MHz.
+`parity` compares with the fp64 oracle's stored values in tests/golden/*.json (written by
+tests/golden/make_golden.py, which calls only oracle/; this tool never runs the oracle).
 """
 from __future__ import annotations
 
@@ -41,9 +44,30 @@ def timed(fn, reps):
     return best
 
 
+GOLD = os.path.join(ROOT, "tests", "golden")
+
+
+def gold(name):
+    return json.load(open(os.path.join(GOLD, name)))
+
+
+def relerr(a, b):
+    return abs(a - b) / abs(b)
+
+
+def sm_clock():
+    try:
+        import subprocess
+        out = subprocess.run(["nvidia-smi", "-i", "0", "--query-gpu=clocks.sm", "--format=csv,noheader,nounits"],
+                             capture_output=True, text=True, timeout=10).stdout.strip()
+        return float(out.split()[0])
+    except Exception:
+        return None
+
+
 def line(cfg, what, dt, prof, extra=None):
     ev = prof["pair_evals"]
-    d = {"config": cfg, "what": what, "wall_ms": dt * 1e3, "pair_ms": prof["pair_ms"],
+    d = {"config": cfg, "what": what, "gpus": 1, "sm_clock_mhz": sm_clock(), "wall_ms": dt * 1e3, "pair_ms": prof["pair_ms"],
          "pair_launches": prof["pair_launches"], "evals": ev,
          "evals_per_s_pair": ev / (prof["pair_ms"] / 1e3) if prof["pair_ms"] > 0 else None,
          "frac_mufu_peak": (ev / (prof["pair_ms"] / 1e3)) / PEAK if prof["pair_ms"] > 0 else None}
@@ -59,11 +83,17 @@ def run(cfg, reps):
     if cfg == "C1":
         x = kb.to_device(datagen.config_data("C1"))
         dt, prof, out = timed(lambda: ctx.plugin_h(x), reps)
-        line(cfg, "plugin_h n=1000", dt, prof, {"h": out[0]})
+        g = gold("C1_plugin.json")["trace"]
+        line(cfg, "plugin_h n=1000", dt, prof, {"n": 1000, "d": 1, "n_cand": 2, "h": out[0],
+             "parity": {"reference": "tests/golden/C1_plugin.json (fp64 oracle)",
+                        "rel_err": {k: relerr(out[1][k], g[k]) for k in ("psi6", "psi4", "h")}}})
     elif cfg == "C4":
         x = kb.to_device(datagen.config_data("C4"))
         dt, prof, out = timed(lambda: ctx.plugin_h(x), reps)
-        line(cfg, "plugin_h n=2^20", dt, prof, {"h": out[0], "trace": out[1]})
+        g = gold("C4_plugin.json")["trace"]
+        line(cfg, "plugin_h n=2^20", dt, prof, {"n": 1 << 20, "d": 1, "n_cand": 2, "h": out[0], "trace": out[1],
+             "parity": {"reference": "tests/golden/C4_plugin.json (fp64 oracle)",
+                        "rel_err": {k: relerr(out[1][k], g[k]) for k in ("psi6", "psi4", "h")}}})
     elif cfg == "C2":
         X = datagen.config_data("C2")
         Xd = kb.to_device(X)
@@ -73,14 +103,26 @@ def run(cfg, reps):
         dt, prof, g = timed(lambda: ctx.lscv_h_scores(Xd, grid), reps)
         line(cfg, "lscv_h_scores 1024 h, n=65536", dt, prof, {"argmin": int(np.argmin(g)), "g_min": float(g.min())})
         dt, prof, r = timed(lambda: ctx.select_bandwidth(kb.LSCV_h, Xd, n_grid=1024), 1)
-        line(cfg, "select LSCV_h (1024-point grid)", dt, prof, {"h": r["h"], "index": r["iterations"]})
+        gd = gold("C2_lscv_h.json")
+        gs = ctx.lscv_h_scores(Xd, gd["h"])
+        line(cfg, "select LSCV_h (1024-point grid)", dt, prof, {"n": n, "d": 1, "n_cand": 1024, "h": r["h"],
+             "index": r["iterations"],
+             "parity": {"reference": "tests/golden/C2_lscv_h.json (fp64 oracle, 81 grid points)",
+                        "max_rel_err": float(np.max(np.abs(gs - np.array(gd["g"])) / np.abs(gd["g"]))),
+                        "argmin_match": r["iterations"] == gd["argmin_index_among_evaluated"]}})
     elif cfg == "C3":
         X = datagen.config_data("C3")
         Xd = kb.to_device(X)
         dt, prof, r = timed(lambda: ctx.select_bandwidth(kb.LSCV_H, Xd), reps)
+        gd = gold("C3_lscv_H.json")
+        Hg, Ho = datagen.unvech(r["vechH"], 2), datagen.unvech(np.array(gd["vechH"]), 2)
         line(cfg, "select LSCV_H (Nelder-Mead, default serial rounds)", dt, prof,
-             {"vechH": r["vechH"].tolist(), "objective": r["objective"], "iterations": r["iterations"],
-              "evaluations": r["evaluations"], "stop": r["stop_reason"]})
+             {"n": X.shape[1], "d": 2, "vechH": r["vechH"].tolist(), "objective": r["objective"],
+              "iterations": r["iterations"], "evaluations": r["evaluations"], "stop": r["stop_reason"],
+              "parity": {"reference": "tests/golden/C3_lscv_H.json (fp64 oracle Nelder-Mead)",
+                         "same_iterations": r["iterations"] == gd["iterations"],
+                         "H_rel_diff": float(np.max(np.abs(Hg - Ho)) / np.max(np.diag(Ho))),
+                         "objective_rel_diff": relerr(r["objective"], gd["f"])}})
     elif cfg == "F3":
         # the paper's two-phase LSCV_h on the C2 workload: HBM-bound phase 2 at 1 h per pass
         X = datagen.config_data("C2")
@@ -148,8 +190,13 @@ def run(cfg, reps):
         # (tools/pipes.cu)
         fma_peak = 125.0 / (2 * 4 + 2) * SMS * 1965e6
         ev = prof["pair_evals"] / (prof["pair_ms"] / 1e3)
-        line(cfg, f"lscv_H_scores {len(cands)} H, d=4, n=2^18", dt, prof,
-             {"g_first": g[:4].tolist(), "fma_bound_evals_per_s": fma_peak, "frac_fma_bound": ev / fma_peak})
+        extra = {"n": n, "d": 4, "n_cand": len(cands), "g_first": g[:4].tolist(),
+                 "fma_bound_evals_per_s": fma_peak, "frac_fma_bound": ev / fma_peak}
+        if cfg == "C5":
+            gd = gold("C5_lscv_H.json")
+            extra["parity"] = {"reference": "tests/golden/C5_lscv_H.json (fp64 oracle, 8 of 256 candidates)",
+                               "max_rel_err": float(np.max(np.abs(g[gd["indices"]] - np.array(gd["g"])) / np.abs(gd["g"])))}
+        line(cfg, f"lscv_H_scores {len(cands)} H, d=4, n=2^18", dt, prof, extra)
 
 
 if __name__ == "__main__":
