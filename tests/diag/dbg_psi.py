@@ -1,6 +1,6 @@
 import math, sys, time, os
 import numpy as np
-sys.path.insert(0, '.')
+sys.path.insert(0, os.getcwd())
 import datagen, oracle
 import paper_1505_01998_b200 as kb
 ctx = kb.Context()
