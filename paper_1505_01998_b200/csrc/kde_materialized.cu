@@ -21,7 +21,7 @@ namespace kde {
 
 constexpr int kMatT = 256;   // tile edge
 constexpr int kP2Threads = 256;
-constexpr int kP2Vec = 16;   // float4 per thread per chunk
+constexpr int kP2Vec = 64;   // float4 per thread per chunk (one 256x256 tile: epilogue every 256 KB)
 constexpr int64_t kP2Chunk = (int64_t)kP2Threads * kP2Vec * 4;
 
 int mat_tile() { return kMatT; }

@@ -139,7 +139,7 @@ def run(cfg, reps):
             gbs = buf_bytes * passes / (prof["pair_ms"] / 1e3) / 1e9
             line(cfg, f"materialised S(v) LSCV_h, 1024 h, {B} h per pass", dt, prof,
                  {"phase1_ms": ctx.last_aux_ms(), "buffer_GB": buf_bytes / 1e9, "phase2_hbm_GBps": gbs,
-                  "hbm_frac_of_measured_6547": gbs / 6547.5, "argmin": int(np.argmin(g))})
+                  "hbm_frac_of_measured_copy": gbs / 6552.0, "hbm_frac_of_nominal_7700": gbs / 7700.0, "argmin": int(np.argmin(g))})
     elif cfg == "F1":
         # LSCV_h for d > 1 (whitened scalar h, row f1): n = 65536, 1024 h, d = 2 and 4
         for d in (2, 4):
