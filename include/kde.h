@@ -103,9 +103,17 @@ typedef struct {
  * legacy default stream).  For world > 1, `nccl_unique_id` points to the 128-byte ncclUniqueId
  * rank 0 obtained from kde_nccl_unique_id() and broadcast to all ranks; the library creates its
  * own NCCL communicator (NCCL is loaded at run time, libnccl.so.2).  world == 1 with a non-NULL
- * id creates a single-rank communicator, so the collective path runs (used by the tests). */
+ * id creates a single-rank communicator, so the collective path runs (used by the tests); world > 1
+ * without an id needs kde_set_host_allreduce before any call that sums pairs. */
 kde_status kde_create(kde_ctx **out, int device, void *cuda_stream, const void *nccl_unique_id,
                       int rank, int world);
+/* Test transport for world > 1 without NCCL (e.g. several ranks sharing one GPU, where NCCL refuses
+ * to run): the library copies each pass's int64 partial sums to pinned host memory and calls
+ * fn(data, count, user), which must replace data[] by its element-wise sum over all ranks (e.g. a
+ * gloo all-reduce) and return 0; the sums are then copied back.  Only for a context created with
+ * world > 1 and no NCCL id.  Production multi-GPU runs use NCCL. */
+typedef int (*kde_host_allreduce_fn)(int64_t *data, size_t count, void *user);
+kde_status kde_set_host_allreduce(kde_ctx *ctx, kde_host_allreduce_fn fn, void *user);
 void kde_destroy(kde_ctx *ctx);
 const char *kde_last_error(const kde_ctx *ctx);
 /* Fill a 128-byte buffer with a fresh ncclUniqueId (rank 0 only). */

@@ -35,7 +35,7 @@ EXPORTS = ["kde_create", "kde_destroy", "kde_last_error", "kde_nccl_unique_id",
            "kde_plugin_h", "kde_lscv_h_scores", "kde_lscv_H_scores", "kde_select_bandwidth",
            "kde_raw_sums", "kde_fixed_value", "kde_fixed_add", "kde_tile_coords",
            "kde_last_profile", "kde_set_profiling", "kde_shard_tiles", "kde_evaluate", "kde_aqp_1d",
-           "kde_lscv_h_scores_materialized", "kde_last_aux_ms"]
+           "kde_lscv_h_scores_materialized", "kde_last_aux_ms", "kde_set_host_allreduce"]
 
 
 class KDEError(RuntimeError):
@@ -78,6 +78,9 @@ class Fixed(ctypes.Structure):
 
 _lib = None
 
+# int (*)(int64_t* data, size_t count, void* user): the test transport's all-reduce callback
+HOST_ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.POINTER(ctypes.c_int64), ctypes.c_size_t, ctypes.c_void_p)
+
 
 def lib():
     """Load libkde_b200.so (raises if it has not been built: no fallback path exists)."""
@@ -118,6 +121,8 @@ def lib():
     L.kde_lscv_h_scores_materialized.restype = ctypes.c_int
     L.kde_last_aux_ms.argtypes = [vp]
     L.kde_last_aux_ms.restype = f64
+    L.kde_set_host_allreduce.argtypes = [vp, HOST_ALLREDUCE_FN, vp]
+    L.kde_set_host_allreduce.restype = ctypes.c_int
     for f in ("kde_create", "kde_nccl_unique_id", "kde_set_workspace", "kde_psi_r", "kde_plugin_h",
               "kde_lscv_h_scores", "kde_lscv_H_scores", "kde_select_bandwidth", "kde_raw_sums",
               "kde_last_profile", "kde_set_profiling"):
@@ -249,6 +254,30 @@ class Context:
             dist.broadcast_object_list(obj, src=0)
         return cls(device=device, rank=rank, world=world, nccl_id=obj[0] if world > 1 else None,
                    profiling=profiling)
+
+    @classmethod
+    def distributed_host(cls, device: int | None = None, profiling: bool = False):
+        """SPMD context whose per-pass partial sums are summed with torch.distributed on the host
+        (any backend, e.g. gloo): a test transport for several ranks sharing one GPU, where NCCL
+        refuses to run.  All compute stays on the GPU; only the int64 partial sums (24 bytes per
+        output) travel through host memory."""
+        import torch
+        import torch.distributed as dist
+        rank, world = dist.get_rank(), dist.get_world_size()
+        ctx = cls(device=device, rank=rank, world=world, profiling=profiling)
+
+        def _allreduce(ptr, count, _user):
+            try:
+                arr = np.ctypeslib.as_array(ptr, shape=(count,))
+                t = torch.from_numpy(arr)          # shares the pinned staging buffer
+                dist.all_reduce(t, op=dist.ReduceOp.SUM)
+                return 0
+            except Exception:
+                return 1
+
+        ctx._har = HOST_ALLREDUCE_FN(_allreduce)  # keep the callback alive
+        ctx._check(lib().kde_set_host_allreduce(ctx._h, ctx._har, None))
+        return ctx
 
     def close(self):
         if getattr(self, "_h", None):

@@ -87,6 +87,11 @@ struct kde_ctx {
   // pinned host staging for limbs
   long long* h_limbs = nullptr;
   size_t h_limbs_cap = 0;
+  // host-staged collective (test transport for world > 1 without NCCL, kde_set_host_allreduce)
+  kde_host_allreduce_fn har_fn = nullptr;
+  void* har_user = nullptr;
+  long long* har_buf = nullptr;
+  size_t har_cap = 0;
   // CUDA graph of the PLUGIN chain, replayed while its key (pointers, n, mode) is unchanged
   bool graphs = true;
   cudaStream_t cap_stream = nullptr;          // capture stream (the caller's may be the legacy one)
@@ -491,6 +496,33 @@ struct SumLaunch {
   int64_t set_stride = 0;
 };
 
+// Sum `count` int64 limbs in device memory across the ranks: NCCL on the context stream, or (test
+// transport, no NCCL) staged through pinned host memory and the caller's all-reduce callback.
+kde_status allreduce_limbs(kde_ctx* c, unsigned long long* limbs, size_t count) {
+  if (c->comm) {
+    Range ra("kde.allreduce");
+    NcclApi& api = nccl();
+    ncclResult_t r = api.AllReduce(limbs, limbs, count, kNcclInt64, kNcclSum, c->comm, c->stream);
+    if (r != 0) return fail(c, KDE_E_NCCL, "ncclAllReduce: %s", api.GetErrorString ? api.GetErrorString(r) : "?");
+    return KDE_OK;
+  }
+  if (c->world <= 1) return KDE_OK;
+  if (!c->har_fn) return fail(c, KDE_E_NCCL, "world > 1 without a collective (NCCL id or host all-reduce)");
+  Range ra("kde.allreduce_host");
+  if (c->har_cap < count) {
+    if (c->har_buf) cudaFreeHost(c->har_buf);
+    c->har_buf = nullptr;
+    CUDA_TRY(c, cudaMallocHost(&c->har_buf, count * sizeof(long long)));
+    c->har_cap = count;
+  }
+  CUDA_TRY(c, cudaMemcpyAsync(c->har_buf, limbs, count * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  if (c->har_fn(reinterpret_cast<int64_t*>(c->har_buf), count, c->har_user) != 0)
+    return fail(c, KDE_E_NCCL, "host all-reduce callback failed");
+  CUDA_TRY(c, cudaMemcpyAsync(limbs, c->har_buf, count * sizeof(long long), cudaMemcpyHostToDevice, c->stream));
+  return KDE_OK;
+}
+
 // Launch the given pair kernels over shard tiles, all-reduce (if requested), fetch fixed-point
 // outputs.  Data must already be prepared in w.Y with leading dimension ld.
 kde_status run_sums(kde_ctx* c, int d, int64_t n, int64_t ld, int T, int scale, Ws& w,
@@ -526,13 +558,7 @@ kde_status run_sums(kde_ctx* c, int d, int64_t n, int64_t ld, int T, int scale, 
       c->prof_evals += pairs * (double)L.nb * (double)L.n_sets;
     }
   }
-  if (allreduce && c->comm) {
-    Range ra("kde.allreduce");
-    NcclApi& api = nccl();
-    ncclResult_t r = api.AllReduce(w.limbs, w.limbs, (size_t)n_out * kde::kLimbs, kNcclInt64, kNcclSum,
-                                   c->comm, c->stream);
-    if (r != 0) return fail(c, KDE_E_NCCL, "ncclAllReduce: %s", api.GetErrorString ? api.GetErrorString(r) : "?");
-  }
+  if (allreduce) TRY(allreduce_limbs(c, w.limbs, (size_t)n_out * kde::kLimbs));
   size_t need = (size_t)n_out * kde::kLimbs;
   if (c->h_limbs_cap < need) {
     if (c->h_limbs) cudaFreeHost(c->h_limbs);
@@ -964,7 +990,8 @@ kde_status kde_create(kde_ctx** out, int device, void* stream, const void* nccl_
     delete c;
     return KDE_E_CUDA;
   }
-  if (world > 1 || nccl_id) {   // world == 1 with an id: single-rank communicator (tests)
+  if (nccl_id) {   // world == 1 with an id: single-rank communicator (tests); world > 1 without an
+                   // id: no transport until kde_set_host_allreduce (test transport)
     NcclApi& api = nccl();
     if (!nccl_id || !api.ok) { delete c; return KDE_E_NCCL; }
     ncclUniqueId id;
@@ -990,6 +1017,7 @@ void kde_destroy(kde_ctx* c) {
   for (void* p : c->in_ws)
     if (p) cudaFree(p);
   if (c->h_limbs) cudaFreeHost(c->h_limbs);
+  if (c->har_buf) cudaFreeHost(c->har_buf);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   delete c;
 }
@@ -1006,6 +1034,14 @@ kde_status kde_set_workspace(kde_ctx* c, void* p, size_t bytes) {
   if (!c) return KDE_E_INVALID;
   c->ext_ws = p;
   c->ext_bytes = p ? bytes : 0;
+  return KDE_OK;
+}
+
+kde_status kde_set_host_allreduce(kde_ctx* c, kde_host_allreduce_fn fn, void* user) {
+  if (!c) return KDE_E_INVALID;
+  if (c->comm) return fail(c, KDE_E_INVALID, "context already has an NCCL communicator");
+  c->har_fn = fn;
+  c->har_user = user;
   return KDE_OK;
 }
 
@@ -1110,12 +1146,7 @@ static kde_status plugin_pass(kde_ctx* c, int r, int64_t n, int64_t ld, int T, i
     c->prof_launches++;
     c->prof_evals += pairs;
   }
-  if (c->comm) {
-    Range ra("kde.allreduce");
-    NcclApi& api = nccl();
-    ncclResult_t rc = api.AllReduce(limbs, limbs, kde::kLimbs, kNcclInt64, kNcclSum, c->comm, c->stream);
-    if (rc != 0) return fail(c, KDE_E_NCCL, "ncclAllReduce: %s", api.GetErrorString ? api.GetErrorString(rc) : "?");
-  }
+  TRY(allreduce_limbs(c, limbs, kde::kLimbs));
   return KDE_OK;
 }
 
@@ -1189,7 +1220,7 @@ static kde_status plugin_impl(kde_ctx* c, const double* x, int64_t n, kde_plugin
   // The first call with a given key runs directly (and does any lazy module loading and library
   // setup outside a capture); a second call with the same key captures, later ones replay.
   // (single-GPU contexts only: with a communicator the all-reduces stay plain stream operations)
-  if (!c->graphs || c->comm || (key != c->plug_seen && !(c->plug_exec && key == c->plug_key))) {
+  if (!c->graphs || c->comm || c->world > 1 || (key != c->plug_seen && !(c->plug_exec && key == c->plug_key))) {
     TRY(plugin_enqueue(c, x, n, T, ld, w));
     c->plug_seen = key;
   } else {
@@ -1513,11 +1544,7 @@ kde_status kde_lscv_h_scores_materialized(kde_ctx* c, const double* X, int64_t n
       c->prof_evals += pairs * B;
     }
   }
-  if (c->comm) {
-    NcclApi& api = nccl();
-    if (api.AllReduce(w.limbs, w.limbs, (size_t)n_out * kde::kLimbs, kNcclInt64, kNcclSum, c->comm, c->stream) != 0)
-      return fail(c, KDE_E_NCCL, "ncclAllReduce failed");
-  }
+  TRY(allreduce_limbs(c, w.limbs, (size_t)n_out * kde::kLimbs));
   std::vector<long long> hl((size_t)n_out * kde::kLimbs);
   CUDA_TRY(c, cudaMemcpyAsync(hl.data(), w.limbs, hl.size() * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
   unsigned long long overflow = 0;
