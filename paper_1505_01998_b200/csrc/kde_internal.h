@@ -19,8 +19,8 @@ enum class Kind : int { Psi4 = 4, Psi6 = 6, Psi8 = 8, LscvScalar = 1, LscvMatrix
 // Per-launch parameters (copied into the kernel parameter space = constant bank).
 struct PsiParams {
   // He_r coefficients are compile-time; see FPsi (kde_pair.cuh) for the exponent scheme.
-  double fac[8];     // 2^((r-1) c0 - o_k), exact in fp64 (applied at the fp64 flush)
-  float o[8];        // per accumulator class k: o_k = fp32((r-1) c0 - 16 - k/8); 8-byte aligned pairs
+  double fac[16];    // 2^((r-1) c0 - o_k), exact in fp64 (applied at the fp64 flush)
+  float o[16];       // class k = 8 * (tile parity) + row slot: o_k = fp32((r-1) c0 - 16 - k/16); aligned pairs
   float c0;          // fp32(-log2(e)/2): exp(-s/2) = 2^(s c0)
 };
 struct LscvScalarParams {

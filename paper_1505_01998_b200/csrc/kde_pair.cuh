@@ -87,16 +87,15 @@ struct Args {
 // and t comes from the difference in one FFMA, t = fma(d, d, -K): one FP32 op per eval fewer
 // than Horner in s (r = 6: 6 instead of 7).  exp(-s/2) = 2^(s c0), c0 = -log2(e)/2, is taken
 // from MUFU.EX2 as
-//     2^(s c0) = ex2(t c0 + o_k) * 2^(K c0 - o_k),   o_k = fp32(K c0 - 16 - k/8),
-// k = accumulator class (the row slot), with the factor 2^(K c0 - o_k) applied exactly in fp64
-// at the flush.  The MUFU input is then s c0 - (16 + k/8) up to one rounding: MUFU.EX2's
-// relative error has a near-constant bias (-5.1e-8) only for inputs in [-32,-16), and a
-// different, input-dependent one on (-1, 0] where the dominant near pairs live; the sums of
-// Psi_r cancel 1000-5000x at the PLUGIN bandwidths, so that bias pattern alone cost 2e-5..5e-5
-// relative.  Offsetting into one binade and averaging over 8 fractional shifts brings the error
-// to ~2e-10 of sum|t| at no per-eval cost (measured by tools/term_error.cu).
-// CS_ > 1 (small n): each tile's columns are split into CS_ chunks that are separate work units,
-// so a launch over few tiles still spreads over the GPU (the split is fixed by n: deterministic).
+//     2^(s c0) = ex2(t c0 + o_k) * 2^(K c0 - o_k),   o_k = fp32(K c0 - 16 - r/8 - p/16),
+// k = (p, r) = accumulator class: r = the row slot (0..7), p = the tile-id parity, 16 classes;
+// the factor 2^(K c0 - o_k) is applied exactly in fp64 at the flush.  The MUFU input is then
+// s c0 - 16 - k/16 up to one rounding: MUFU.EX2's relative error has a near-constant bias
+// (-5.1e-8) only for inputs in [-32,-16), and a different, input-dependent one on (-1, 0] where
+// the dominant near pairs live; the sums of Psi_r cancel 1000-5000x at the PLUGIN bandwidths, so
+// that bias pattern alone cost 2e-5..5e-5 relative.  Offsetting into one binade and averaging
+// over 16 fractional shifts brings Psi-hat to ~1e-6 at C4 at no per-eval cost (measured against
+// the oracle: 8 shifts 2.7e-6, 16 shifts 5.4e-7, 32 shifts 8.9e-7).
 template <int RORD, int NT_, int CS_ = 1>
 struct FPsi {
   static constexpr int NT = NT_, D = 1, R = 8, T = NT_ * 8, NOUT = 1, MINB = 768 / NT_;
@@ -110,9 +109,11 @@ struct FPsi {
   f2 xr[NP];
   double acc;
   int jbase;   // first column of this work unit's chunk (CS > 1)
+  int par;     // tile-id parity: second index of the MUFU offset class (16 classes)
 
   // Rows are interleaved: thread t owns rows q*T + 8t + r, r = 0..7.  The data are sorted
-  // (kde_host.cpp), so the 8 accumulator classes r see statistically identical distances.
+  // (kde_host.cpp), so the 8 row classes r see statistically identical distances; the tile-id
+  // parity p doubles the classes across tiles.
   __device__ __forceinline__ void load_rows(const float* __restrict__ X, int64_t ld,
                                             int64_t i0) {
     const float4* p = reinterpret_cast<const float4*>(X + i0);
@@ -142,7 +143,7 @@ struct FPsi {
     const f2 mk = pk(-K, -K);
     f2 o[NP];
 #pragma unroll
-    for (int q = 0; q < NP; ++q) o[q] = reinterpret_cast<const f2*>(p.o)[q];   // 64-bit constant loads
+    for (int q = 0; q < NP; ++q) o[q] = reinterpret_cast<const f2*>(p.o + 8 * par)[q];   // 64-bit constant loads
     const int J0 = CS > 1 ? jbase : 0, J1 = CS > 1 ? jbase + CW : T;
     for (int jc = J0; jc < J1; jc += CH) {
       if (MASK && jc >= jlim) break;
@@ -204,8 +205,8 @@ struct FPsi {
         float a0, a1, c0_, c1_;
         upk(a[q], a0, a1);
         upk(cmp[q], c0_, c1_);
-        s += ((double)a0 + (double)c0_) * p.fac[2 * q];
-        s += ((double)a1 + (double)c1_) * p.fac[2 * q + 1];
+        s += ((double)a0 + (double)c0_) * p.fac[8 * par + 2 * q];
+        s += ((double)a1 + (double)c1_) * p.fac[8 * par + 2 * q + 1];
       }
       acc += s;
     }
@@ -234,6 +235,7 @@ struct FLscvScalar {
   using Params = LscvScalarParams;
   f2 xr[D];
   f2 a1[NB], a2[NB];
+  int par;   // unused (interface shared with FPsi)
 
   __device__ __forceinline__ void load_rows(const float* __restrict__ X, int64_t ld,
                                             int64_t i0) {
@@ -368,6 +370,7 @@ __global__ void __launch_bounds__(F::NT, F::MINB) pair_kernel(const Args a,
     F f;
     f.load_rows(a.X, a.ld, row_origin<F>(q));
     f.jbase = (int)(u % CS) * F::CW;
+    f.par = (int)((a.tile_begin + u / CS) & 1);
     mbar_wait(&bar[k & 1], (k >> 1) & 1);
     const float* sc = cols + (k & 1) * D * T;
     const bool diag = (q == l);
@@ -408,6 +411,7 @@ __global__ void __launch_bounds__(F::NT, F::MINB) pair_kernel(const Args a,
 
     F f;
     f.load_rows(a.X, a.ld, row_origin<F>(q));
+    f.par = (int)(t & 1);
     mbar_wait(&bar[k & 1], (k >> 1) & 1);
     const float* sc = cols + (k & 1) * D * T;
     const bool diag = (q == l);
