@@ -311,3 +311,24 @@ def test_plugin_graph_replay_follows_the_data(ctx):
     assert e.value.status == "KDE_E_DEGENERATE"
     xd.copy_(torch.from_numpy(a).cuda())
     assert ctx.plugin_h(xd) == ha
+
+
+def test_empty_and_too_small_inputs_are_rejected(ctx):
+    # every entry point rejects n = 0 (and the selectors n = 1) with a status, never a crash
+    empty1, empty2 = np.zeros((1, 0)), np.zeros((2, 0))
+    cases = [
+        (lambda: ctx.psi_r(empty1, 4, [0.5]), "KDE_E_INVALID"),
+        (lambda: ctx.plugin_h(empty1), "KDE_E_INVALID"),
+        (lambda: ctx.lscv_h_scores(empty2, [0.5]), "KDE_E_INVALID"),
+        (lambda: ctx.lscv_H_scores(empty2, [[0.1, 0.0, 0.1]]), "KDE_E_INVALID"),
+        (lambda: ctx.select_bandwidth(kb.LSCV_H, empty2), "KDE_E_INVALID"),
+        (lambda: ctx.lscv_h_scores(np.zeros((2, 1)), [0.5]), "KDE_E_INSUFFICIENT_SAMPLES"),
+        (lambda: ctx.select_bandwidth(kb.PLUGIN, np.zeros((2, 5))), "KDE_E_NOT_UNIVARIATE"),
+        (lambda: ctx.lscv_H_scores(np.ones((2, 10)), [[0.1, 0.0]]), "KDE_E_DIM_MISMATCH"),
+    ]
+    for fn, status in cases:
+        with pytest.raises(kb.KDEError) as e:
+            fn()
+        assert e.value.status == status
+    # an empty query set is valid: no output
+    assert ctx.evaluate(dev(datagen.sample_mixture("C3", 50, 1)), np.zeros((2, 0)), [0.1, 0.0, 0.1]).size == 0
