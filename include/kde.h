@@ -237,6 +237,12 @@ kde_status kde_shard_tiles(kde_sum_kind kind, int64_t n, int32_t d, int32_t rank
  * evaluations they performed (pairs i<j on this rank x candidates). */
 kde_status kde_last_profile(const kde_ctx *ctx, int32_t *launches, double *pair_ms,
                             double *evals, int32_t *all_launches);
+/* Term precision of the Psi_r sums (kde_psi_r, kde_plugin_h, KDE_SUM_PSI* raw sums): 0 (default)
+ * fp32 terms with fp64/exact accumulation, the throughput path (parity ~1e-6 at the PLUGIN
+ * bandwidths); 1 = fp64 terms (libdevice exp, fp64 Horner in u^2), ~20x slower, for
+ * bandwidths far below the PLUGIN pilots where the sums cancel by more than ~10^4.
+ * Results stay deterministic and partition-invariant in either mode. */
+kde_status kde_set_precision(kde_ctx *ctx, int32_t fp64_terms);
 /* Turn per-launch event timing on/off (default off; adds an event pair per launch). */
 kde_status kde_set_profiling(kde_ctx *ctx, int32_t on);
 

@@ -35,7 +35,7 @@ EXPORTS = ["kde_create", "kde_destroy", "kde_last_error", "kde_nccl_unique_id",
            "kde_plugin_h", "kde_lscv_h_scores", "kde_lscv_H_scores", "kde_select_bandwidth",
            "kde_raw_sums", "kde_fixed_value", "kde_fixed_add", "kde_tile_coords",
            "kde_last_profile", "kde_set_profiling", "kde_shard_tiles", "kde_evaluate", "kde_aqp_1d",
-           "kde_lscv_h_scores_materialized", "kde_last_aux_ms", "kde_set_host_allreduce"]
+           "kde_lscv_h_scores_materialized", "kde_last_aux_ms", "kde_set_host_allreduce", "kde_set_precision"]
 
 
 class KDEError(RuntimeError):
@@ -121,6 +121,8 @@ def lib():
     L.kde_lscv_h_scores_materialized.restype = ctypes.c_int
     L.kde_last_aux_ms.argtypes = [vp]
     L.kde_last_aux_ms.restype = f64
+    L.kde_set_precision.argtypes = [vp, i32]
+    L.kde_set_precision.restype = ctypes.c_int
     L.kde_set_host_allreduce.argtypes = [vp, HOST_ALLREDUCE_FN, vp]
     L.kde_set_host_allreduce.restype = ctypes.c_int
     for f in ("kde_create", "kde_nccl_unique_id", "kde_set_workspace", "kde_psi_r", "kde_plugin_h",
@@ -300,6 +302,10 @@ class Context:
         self._ws = buf
         self._check(lib().kde_set_workspace(self._h, ctypes.c_void_p(buf.data_ptr()),
                                             buf.numel() * buf.element_size()))
+
+    def set_precision(self, fp64_terms: bool):
+        """fp64 terms for the Psi_r sums (slow, exact-parity mode) or the fp32-term default."""
+        self._check(lib().kde_set_precision(self._h, 1 if fp64_terms else 0))
 
     def set_profiling(self, on: bool):
         self._check(lib().kde_set_profiling(self._h, 1 if on else 0))

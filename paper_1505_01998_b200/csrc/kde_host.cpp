@@ -87,6 +87,10 @@ struct kde_ctx {
   // pinned host staging for limbs
   long long* h_limbs = nullptr;
   size_t h_limbs_cap = 0;
+  // fp64-term Psi mode (kde_set_precision) and its fp64 scaled-sample buffer, context-owned
+  bool fp64 = false;
+  void* y64 = nullptr;
+  size_t y64_bytes = 0;
   // host-staged collective (test transport for world > 1 without NCCL, kde_set_host_allreduce)
   kde_host_allreduce_fn har_fn = nullptr;
   void* har_user = nullptr;
@@ -594,6 +598,26 @@ double he_at_zero(int r) { return r == 4 ? 3.0 : (r == 6 ? -15.0 : 105.0); }
 
 Kind psi_kind(int r) { return r == 4 ? Kind::Psi4 : (r == 6 ? Kind::Psi6 : Kind::Psi8); }
 
+// fp64-term mode: one Psi_r pass over this rank's 256-tiles of the fp64 scaled samples y, into
+// `limbs` (3 int64), then the all-reduce.
+kde_status psi64_pass(kde_ctx* c, int r, const double* y, int64_t n, int S, unsigned long long* limbs) {
+  Range rr("kde.pair_pass_fp64");
+  int64_t tb, te;
+  shard_range(n_tiles(n, kde::kPsi64Tile), c->rank, c->world, &tb, &te);
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  const unsigned rec = (c->cap_stream && c->stream == c->cap_stream) ? cudaEventRecordExternal : cudaEventRecordDefault;
+  if (c->profiling) { e0 = next_event(c); e1 = next_event(c); CUDA_TRY(c, cudaEventRecordWithFlags(e0, c->stream, rec)); }
+  CUDA_TRY(c, kde::launch_psi64(r, y, n, tb, te, S, limbs, c->sm_count, c->stream));
+  if (tb < te) c->prof_all += 1;
+  if (c->profiling) {
+    CUDA_TRY(c, cudaEventRecordWithFlags(e1, c->stream, rec));
+    c->prof_launches++;
+    c->prof_evals += pairs_in_range(n, kde::kPsi64Tile, tb, te);
+  }
+  TRY(allreduce_limbs(c, limbs, kde::kLimbs));
+  return KDE_OK;
+}
+
 // Raw Psi sums S_r(g) = sum_{i<j} He_r(u) e^{-u^2/2} for each g (one prep + one launch per g).
 kde_status psi_raw(kde_ctx* c, const double* x, int64_t n, int r, const double* g, int ng,
                    const Moments& m, int shard_rank, int shard_world, bool allreduce,
@@ -609,6 +633,28 @@ kde_status psi_raw(kde_ctx* c, const double* x, int64_t n, int r, const double* 
     x = xs;
   }
   out.clear();
+  if (c->fp64) {                       // fp64-term mode (kde_set_precision)
+    TRY(grow(c, &c->y64, &c->y64_bytes, (size_t)std::max<int64_t>(n, 1) * sizeof(double)));
+    double* y = static_cast<double*>(c->y64);
+    for (int k = 0; k < ng; ++k) {
+      const double hv[2] = {m.mean[0], 1.0 / g[k]};
+      CUDA_TRY(c, cudaMemcpyAsync(w.small, hv, sizeof(hv), cudaMemcpyHostToDevice, c->stream));
+      CUDA_TRY(c, kde::launch_scale64(x, n, w.small, w.small + 1, y, c->stream));
+      CUDA_TRY(c, cudaMemsetAsync(w.limbs, 0, kde::kLimbs * sizeof(long long), c->stream));
+      if (allreduce) {
+        TRY(psi64_pass(c, r, y, n, S, w.limbs));
+      } else {                         // one shard, no collective
+        int64_t tb, te;
+        shard_range(n_tiles(n, kde::kPsi64Tile), shard_rank, shard_world, &tb, &te);
+        CUDA_TRY(c, kde::launch_psi64(r, y, n, tb, te, S, w.limbs, c->sm_count, c->stream));
+      }
+      long long hl[kde::kLimbs];
+      CUDA_TRY(c, cudaMemcpyAsync(hl, w.limbs, sizeof(hl), cudaMemcpyDeviceToHost, c->stream));
+      CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+      out.push_back(limbs_to_fixed(hl, S));
+    }
+    return KDE_OK;
+  }
   for (int k = 0; k < ng; ++k) {
     std::vector<double> W = {1.0 / g[k]};
     TRY(gpu_prep(c, x, n, 1, W, m.mean, ld, w, 3.0e4));
@@ -1012,6 +1058,7 @@ void kde_destroy(kde_ctx* c) {
   if (c->own_ws) cudaFree(c->own_ws);
   if (c->sort_ws) cudaFree(c->sort_ws);
   if (c->white_ws) cudaFree(c->white_ws);
+  if (c->y64) cudaFree(c->y64);
   if (c->ev_ws) cudaFree(c->ev_ws);
   if (c->mat_ws) cudaFree(c->mat_ws);
   for (void* p : c->in_ws)
@@ -1034,6 +1081,12 @@ kde_status kde_set_workspace(kde_ctx* c, void* p, size_t bytes) {
   if (!c) return KDE_E_INVALID;
   c->ext_ws = p;
   c->ext_bytes = p ? bytes : 0;
+  return KDE_OK;
+}
+
+kde_status kde_set_precision(kde_ctx* c, int32_t fp64_terms) {
+  if (!c) return KDE_E_INVALID;
+  c->fp64 = fp64_terms != 0;
   return KDE_OK;
 }
 
@@ -1178,11 +1231,20 @@ static kde_status plugin_enqueue(kde_ctx* c, const double* x, int64_t n, int T, 
   const double pairs = c->profiling ? pairs_in_range(n, T, tb, te) : 0.0;
   const int S6 = scale_exp_for(2.0 * 15.0, n), S4 = scale_exp_for(2.0 * 3.0, n);
   CUDA_TRY(c, cudaMemsetAsync(w.limbs, 0, 2 * kde::kLimbs * sizeof(long long), st));
-  CUDA_TRY(c, kde::launch_prep(xs, n, 1, dv.W, dv.mean, w.Y, ld, st, 0.f, w.flag(), 3.0e4));   // x/g1
-  TRY(plugin_pass(c, 6, n, ld, T, S6, w, w.limbs, tb, te, pairs));                     // step 5
-  CUDA_TRY(c, kde::launch_plugin_chain(2, n, w.small, w.limbs, S6, st));               // Psi6, g2
-  CUDA_TRY(c, kde::launch_prep(xs, n, 1, dv.W, dv.mean, w.Y, ld, st, 0.f, w.flag(), 3.0e4));   // x/g2
-  TRY(plugin_pass(c, 4, n, ld, T, S4, w, w.limbs + kde::kLimbs, tb, te, pairs));       // step 7
+  if (c->fp64) {                                                                       // fp64 terms
+    double* y = static_cast<double*>(c->y64);
+    CUDA_TRY(c, kde::launch_scale64(xs, n, dv.mean, dv.W, y, st));                     // x/g1
+    TRY(psi64_pass(c, 6, y, n, S6, w.limbs));                                          // step 5
+    CUDA_TRY(c, kde::launch_plugin_chain(2, n, w.small, w.limbs, S6, st));             // Psi6, g2
+    CUDA_TRY(c, kde::launch_scale64(xs, n, dv.mean, dv.W, y, st));                     // x/g2
+    TRY(psi64_pass(c, 4, y, n, S4, w.limbs + kde::kLimbs));                            // step 7
+  } else {
+    CUDA_TRY(c, kde::launch_prep(xs, n, 1, dv.W, dv.mean, w.Y, ld, st, 0.f, w.flag(), 3.0e4));   // x/g1
+    TRY(plugin_pass(c, 6, n, ld, T, S6, w, w.limbs, tb, te, pairs));                   // step 5
+    CUDA_TRY(c, kde::launch_plugin_chain(2, n, w.small, w.limbs, S6, st));             // Psi6, g2
+    CUDA_TRY(c, kde::launch_prep(xs, n, 1, dv.W, dv.mean, w.Y, ld, st, 0.f, w.flag(), 3.0e4));   // x/g2
+    TRY(plugin_pass(c, 4, n, ld, T, S4, w, w.limbs + kde::kLimbs, tb, te, pairs));     // step 7
+  }
   CUDA_TRY(c, kde::launch_plugin_chain(3, n, w.small, w.limbs + kde::kLimbs, S4, st)); // Psi4, h
   c->prof_all += 4;
   CUDA_TRY(c, cudaMemcpyAsync(c->h_limbs, w.flag(), (kde::kSmallDoubles - 408) * sizeof(double),
@@ -1202,6 +1264,7 @@ static kde_status plugin_impl(kde_ctx* c, const double* x, int64_t n, kde_plugin
   Ws w;
   TRY(get_ws(c, ld, 1, 2, &w));                   // everything the chain touches exists before
   TRY(ensure_sort_ws(c, n));                      // a capture starts
+  if (c->fp64) TRY(grow(c, &c->y64, &c->y64_bytes, (size_t)n * sizeof(double)));
   const size_t cnt = kde::kSmallDoubles - 408;    // flags, trace, status
   if (c->h_limbs_cap < cnt) {
     if (c->h_limbs) cudaFreeHost(c->h_limbs);
@@ -1216,7 +1279,8 @@ static kde_status plugin_impl(kde_ctx* c, const double* x, int64_t n, kde_plugin
   }
   cudaStream_t st = c->stream;
   const std::vector<uintptr_t> key = {(uintptr_t)x, (uintptr_t)n, (uintptr_t)w.Y, (uintptr_t)c->sort_ws,
-                                      (uintptr_t)c->h_limbs, (uintptr_t)c->profiling, (uintptr_t)c->comm};
+                                      (uintptr_t)c->h_limbs, (uintptr_t)c->profiling, (uintptr_t)c->comm,
+                                      (uintptr_t)c->fp64, (uintptr_t)c->y64};
   // The first call with a given key runs directly (and does any lazy module loading and library
   // setup outside a capture); a second call with the same key captures, later ones replay.
   // (single-GPU contexts only: with a communicator the all-reduces stay plain stream operations)

@@ -46,6 +46,12 @@ struct LaunchCfg {
 // Launchers (kde_psi.cu, kde_lscv_scalar.cu, kde_lscv_matrix.cu).  Return cudaSuccess or the launch error.
 cudaError_t launch_psi(int r, const LaunchCfg& c, const PsiParams& p);
 cudaError_t prepare_psi(int r, const LaunchCfg& c);   // one-time setup of launch_psi's kernel
+// fp64-term Psi mode (kde_set_precision): y = (x - mean[0]) * w[0] in fp64, then 256-tiles of fp64 terms.
+constexpr int kPsi64Tile = 256;
+cudaError_t launch_scale64(const double* x, int64_t n, const double* mean_dev, const double* w_dev, double* y,
+                           cudaStream_t s);
+cudaError_t launch_psi64(int r, const double* y, int64_t n, int64_t tile_begin, int64_t tile_end, int S,
+                         unsigned long long* limbs, int sm_count, cudaStream_t s);
 cudaError_t launch_lscv_scalar(int d, int nb, const LaunchCfg& c, const LscvScalarParams& p);
 // LSCV_H with per-candidate whitened data (one candidate per set, c.n_sets sets).
 cudaError_t launch_lscv_white(int d, const LaunchCfg& c);

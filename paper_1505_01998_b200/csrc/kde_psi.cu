@@ -222,6 +222,75 @@ cudaError_t launch_prep_params(const double* X, int64_t n, int d, const PrepPara
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ fp64-term Psi mode
+// kde_set_precision(ctx, 1): every term in fp64 (libdevice exp, Horner in s with the integer
+// coefficients of He_r, fp64 tile sums), for bandwidths far below the PLUGIN pilots where the
+// cancellation exceeds what fp32 terms carry.  ~20x slower than the fp32 path;
+// same tile map (256-tiles), fixed-point limbs and multi-GPU partition.
+__global__ void scale64_kernel(const double* __restrict__ x, int64_t n, const double* __restrict__ mean,
+                               const double* __restrict__ w, double* __restrict__ y) {
+  const double m = mean[0], s = w[0];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = (x[i] - m) * s;
+}
+
+cudaError_t launch_scale64(const double* x, int64_t n, const double* mean_dev, const double* w_dev, double* y,
+                           cudaStream_t s) {
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  scale64_kernel<<<(unsigned)(blocks > 0 ? blocks : 1), 256, 0, s>>>(x, n, mean_dev, w_dev, y);
+  return cudaGetLastError();
+}
+
+template <int R>
+__device__ __forceinline__ double he64(double s) {   // He_r(u) in s = u^2
+  if (R == 4) return (s - 6.0) * s + 3.0;
+  if (R == 6) return ((s - 15.0) * s + 45.0) * s - 15.0;
+  return (((s - 28.0) * s + 210.0) * s - 420.0) * s + 105.0;
+}
+
+template <int R>
+__global__ void __launch_bounds__(kPsi64Tile) psi64_kernel(const double* __restrict__ y, int64_t n, int64_t tb,
+                                                           int64_t te, int S, unsigned long long* __restrict__ limbs) {
+  __shared__ double cs[kPsi64Tile];
+  __shared__ double red[kPsi64Tile / 32];
+  const int tid = threadIdx.x;
+  for (int64_t t = tb + blockIdx.x; t < te; t += gridDim.x) {
+    int64_t l, q;
+    tile_coords(t, l, q);
+    const int64_t jc = l * kPsi64Tile + tid, i = q * kPsi64Tile + tid;
+    __syncthreads();
+    cs[tid] = jc < n ? y[jc] : 0.0;
+    __syncthreads();
+    const int jlim = (int)(n - l * kPsi64Tile < kPsi64Tile ? n - l * kPsi64Tile : kPsi64Tile);
+    double acc = 0.0;
+    if (i < n) {
+      const double xi = y[i];
+      for (int j = (q == l ? tid + 1 : 0); j < jlim; ++j) {
+        const double u = xi - cs[j];
+        const double s = u * u;
+        acc += he64<R>(s) * exp(-0.5 * s);
+      }
+    }
+    double v[1] = {acc};
+    commit_tile<1, kPsi64Tile>(v, red, limbs, S);
+  }
+}
+
+cudaError_t launch_psi64(int r, const double* y, int64_t n, int64_t tb, int64_t te, int S,
+                         unsigned long long* limbs, int sm_count, cudaStream_t s) {
+  if (te <= tb) return cudaSuccess;
+  int64_t grid = te - tb;
+  if (grid > (int64_t)sm_count * 8) grid = (int64_t)sm_count * 8;
+  switch (r) {
+    case 4: psi64_kernel<4><<<(unsigned)grid, kPsi64Tile, 0, s>>>(y, n, tb, te, S, limbs); break;
+    case 6: psi64_kernel<6><<<(unsigned)grid, kPsi64Tile, 0, s>>>(y, n, tb, te, S, limbs); break;
+    case 8: psi64_kernel<8><<<(unsigned)grid, kPsi64Tile, 0, s>>>(y, n, tb, te, S, limbs); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ device-resident PLUGIN chain
 // The scalar steps of Sec. 4.4.1 (Eq. 11-18) run in single-thread kernels between the
 // O(n) and O(n^2) kernels, so kde_plugin_h enqueues the whole chain without a host round trip
