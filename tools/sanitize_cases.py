@@ -29,3 +29,6 @@ print("select plugin", ctx.select_bandwidth(kb.PLUGIN, x)["h"])
 print("lscv_H 300 candidates (two launches)", ctx.lscv_H_scores(X, np.tile([[0.05, 0.01, 0.04]], (300, 1)))[[0, 299]])
 xs = kb.to_device(datagen.sample_mixture("skewed", 700, 3))
 print("plugin x3 (graph capture + replay)", [ctx.plugin_h(xs)[0] for _ in range(3)])
+ctx.set_precision(True)
+print("fp64 psi + plugin", ctx.psi_r(x, 6, [0.3]), ctx.plugin_h(x)[0])
+ctx.set_precision(False)
