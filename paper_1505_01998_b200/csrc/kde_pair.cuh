@@ -6,11 +6,14 @@
 // visit.  Design:
 //  * work unit = one T x T tile (l, q), q <= l, of the upper-triangular pair matrix,
 //    numbered column by column and mapped back with Eq. 42-43 + an integer fix-up;
+//    variants: a column chunk of a tile (small-n Psi, CS > 1) or a (data set, tile) pair
+//    (LSCV_H: one whitened data set per candidate, pair_kernel_sets);
 //  * persistent CTAs stride over their rank's contiguous tile range;
 //  * the T column samples (D rows) of the next tile are staged in shared memory by TMA bulk
 //    copies (cp.async.bulk + mbarrier, double-buffered); the T row samples sit in registers
 //    (R per thread); columns are read back with broadcast LDS.128;
-//  * per eval: FP32 difference / quadratic form, one MUFU.EX2, Horner or accumulate FMAs;
+//  * per eval: FP32 difference and square (sum of squares), one MUFU.EX2 (or, for a quarter of
+//    the LSCV_h terms, a software exp2 on the FMA pipe), Horner or accumulate FMAs;
 //  * every tile's partial is reduced in a fixed order (fp32 per thread -> fp64 warp butterfly ->
 //    fixed cross-warp order) and added as exact fixed-point limbs with integer atomics, so the
 //    result is independent of grid size, tile-to-CTA assignment, batch composition and GPU count.
@@ -26,7 +29,8 @@
 
 namespace kde {
 
-// Candidates per launch: chosen so that no instantiation spills at 128 registers (2 CTAs/SM).
+// LSCV_h candidates per pair visit: d <= 4: 8 at 3 CTAs/SM (80 registers); larger d: 16, then 8,
+// so that no instantiation spills.
 constexpr int nb_scalar(int d) { return d <= 4 ? 8 : (d <= 12 ? 16 : 8); }
 
 
