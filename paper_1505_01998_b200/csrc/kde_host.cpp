@@ -563,20 +563,22 @@ kde_status run_sums(kde_ctx* c, int d, int64_t n, int64_t ld, int T, int scale, 
     }
   }
   if (allreduce) TRY(allreduce_limbs(c, w.limbs, (size_t)n_out * kde::kLimbs));
-  size_t need = (size_t)n_out * kde::kLimbs;
+  // one device-to-host copy of [prep flags .. limbs): the workspace places the limbs right after
+  // the fixed-size block that holds the flags (get_ws)
+  const size_t gap = (size_t)(reinterpret_cast<const char*>(w.limbs) - reinterpret_cast<const char*>(w.flag())) /
+                     sizeof(long long);
+  const size_t need = gap + (size_t)n_out * kde::kLimbs;
   if (c->h_limbs_cap < need) {
     if (c->h_limbs) cudaFreeHost(c->h_limbs);
     c->h_limbs = nullptr;
     CUDA_TRY(c, cudaMallocHost(&c->h_limbs, need * sizeof(long long)));
     c->h_limbs_cap = need;
   }
-  CUDA_TRY(c, cudaMemcpyAsync(c->h_limbs, w.limbs, need * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
-  unsigned long long overflow = 0;
-  CUDA_TRY(c, cudaMemcpyAsync(&overflow, w.flag(), sizeof(overflow), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(c->h_limbs, w.flag(), need * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-  if (overflow) return fail(c, KDE_E_INVALID, "scaled sample differences exceed 1e18 (outliers vs. bandwidth)");
+  if (c->h_limbs[0]) return fail(c, KDE_E_INVALID, "scaled sample differences exceed 1e18 (outliers vs. bandwidth)");
   out.resize(n_out);
-  for (int k = 0; k < n_out; ++k) out[k] = limbs_to_fixed(c->h_limbs + (size_t)k * kde::kLimbs, scale);
+  for (int k = 0; k < n_out; ++k) out[k] = limbs_to_fixed(c->h_limbs + gap + (size_t)k * kde::kLimbs, scale);
   return KDE_OK;
 }
 
