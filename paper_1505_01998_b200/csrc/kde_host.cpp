@@ -531,9 +531,10 @@ kde_status allreduce_limbs(kde_ctx* c, unsigned long long* limbs, size_t count) 
 // outputs.  Data must already be prepared in w.Y with leading dimension ld.
 kde_status run_sums(kde_ctx* c, int d, int64_t n, int64_t ld, int T, int scale, Ws& w,
                     const std::vector<SumLaunch>& launches, int n_out, int shard_rank,
-                    int shard_world, bool allreduce, std::vector<kde_fixed>& out) {
+                    int shard_world, bool allreduce, std::vector<kde_fixed>& out, bool limbs_zeroed = false) {
   Range rr("kde.pair_pass");
-  CUDA_TRY(c, cudaMemsetAsync(w.limbs, 0, (size_t)n_out * kde::kLimbs * sizeof(long long), c->stream));
+  if (!limbs_zeroed)
+    CUDA_TRY(c, cudaMemsetAsync(w.limbs, 0, (size_t)n_out * kde::kLimbs * sizeof(long long), c->stream));
   int64_t tiles = n_tiles(n, T), tb, te;
   shard_range(tiles, shard_rank, shard_world, &tb, &te);
   const double pairs = c->profiling ? pairs_in_range(n, T, tb, te) : 0.0;
@@ -767,7 +768,10 @@ kde_status lscv_H_raw(kde_ctx* c, const double* X, int64_t n, int d, const std::
     const int cnt = std::min(per_launch, nc - b0);
     TRY(grow(c, &c->white_ws, &c->white_bytes, (size_t)cnt * set_floats * sizeof(float)));
     float* Yw = static_cast<float*>(c->white_ws);
-    CUDA_TRY(c, cudaMemsetAsync(w.flag(), 0, 2 * sizeof(unsigned long long), c->stream));
+    // prep flags and this launch's limbs are one contiguous span of the workspace (get_ws): one memset
+    const size_t span = (size_t)(reinterpret_cast<char*>(w.limbs + (size_t)2 * cnt * kde::kLimbs) -
+                                 reinterpret_cast<char*>(w.flag()));
+    CUDA_TRY(c, cudaMemsetAsync(w.flag(), 0, span, c->stream));
     for (int j = 0; j < cnt; ++j) {
       std::vector<double> W = tri_lower_inverse(cands[b0 + j].L, d);
       for (double& v : W) v *= std::sqrt(kLog2e / 4.0);
@@ -777,7 +781,8 @@ kde_status lscv_H_raw(kde_ctx* c, const double* X, int64_t n, int d, const std::
     L.kind = Kind::LscvMatrix; L.nb = 1; L.out_offset = 0; L.n_out = 2 * cnt;
     L.X = Yw; L.n_sets = cnt; L.set_stride = set_floats;
     std::vector<kde_fixed> o;
-    TRY(run_sums(c, d, n, ld, T, scale_exp_for(1.0, n), w, {L}, 2 * cnt, shard_rank, shard_world, allreduce, o));
+    TRY(run_sums(c, d, n, ld, T, scale_exp_for(1.0, n), w, {L}, 2 * cnt, shard_rank, shard_world, allreduce, o,
+                 /*limbs_zeroed=*/true));
     out.insert(out.end(), o.begin(), o.end());
   }
   return KDE_OK;
