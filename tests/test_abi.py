@@ -79,6 +79,10 @@ def test_null_context_is_rejected():
     g = ctypes.c_double(1.0)
     assert L.kde_psi_r(None, None, 10, 4, ctypes.byref(g), 1, ctypes.byref(out)) == 1
     assert L.kde_last_error(None) == b"null context"
+    # the mode setters reject a null context too (no GPU needed)
+    assert L.kde_set_precision(None, 1) == 1
+    assert L.kde_set_profiling(None, 1) == 1
+    assert L.kde_set_host_allreduce(None, kb.HOST_ALLREDUCE_FN(lambda p, n, u: 0), None) == 1
 
 
 def test_binding_marshals_host_and_rejects_other_dtypes():
