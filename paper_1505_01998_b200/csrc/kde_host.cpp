@@ -590,7 +590,7 @@ kde_status run_sums(kde_ctx* c, int d, int64_t n, int64_t ld, int T, int scale, 
 void psi_coeffs(int r, kde::PsiParams& p) {
   std::memset(&p, 0, sizeof(p));
   p.c0 = (float)(-kLog2e / 2.0);
-  const double Kc0 = (double)(r - 1) * (double)p.c0;             // exact in fp64
+  const double Kc0 = (double)(r == 8 ? 0 : r - 1) * (double)p.c0;   // K of FPsi; exact in fp64
   for (int k = 0; k < 16; ++k) {   // k = 8 * (tile parity) + row slot; shift (row slot)/8 + parity/16
     p.o[k] = (float)(Kc0 - (16.0 + (k % 8) / 8.0 + (k / 8) / 16.0));
     p.fac[k] = std::exp2(Kc0 - (double)p.o[k]);                    // exponent exact in fp64

@@ -87,9 +87,10 @@ struct Args {
 // He_r is a polynomial in s with integer coefficients.  Shifting by the mean of
 // its roots, t = s - K with K = r - 1, removes the next-to-leading term and keeps the
 // coefficients exact integers (depressed form; expand (t+K) to recover P:231/P:247):
-//     He_4 = t^2 - 6,   He_6 = t (t^2 - 30) - 40,   He_8 = ((t^2 - 84) t - 224) t + 252,
+//     He_4 = t^2 - 6,   He_6 = t (t^2 - 30) - 40,
 // and t comes from the difference in one FFMA, t = fma(d, d, -K): one FP32 op per eval fewer
-// than Horner in s (r = 6: 6 instead of 7).  exp(-s/2) = 2^(s c0), c0 = -log2(e)/2, is taken
+// than Horner in s (r = 6: 6 instead of 7).  He_8 stays Horner in s (its depressed form
+// ((t^2 - 84) t - 224) t + 252 cancels 40x near s = 0).  exp(-s/2) = 2^(s c0), c0 = -log2(e)/2, is taken
 // from MUFU.EX2 as
 //     2^(s c0) = ex2(t c0 + o_k) * 2^(K c0 - o_k),   o_k = fp32(K c0 - 16 - r/8 - p/16),
 // k = (p, r) = accumulator class: r = the row slot (0..7), p = the tile-id parity, 16 classes;
@@ -107,7 +108,10 @@ struct FPsi {
   static constexpr int CH = CS_ > 1 ? CW : (T < 1024 ? T : 1024);  // columns per fp64 flush
   static constexpr int NP = R / 2;   // row pairs (r = 2p, 2p+1) packed into fp32x2 lanes
   static constexpr int G = 16;       // columns per compensated group
-  static constexpr float K = (float)(RORD - 1);
+  // K: the shift of the depressed form (r = 4, 6); r = 8 keeps Horner in s = u^2 (K = 0): its depressed
+  // form cancels 40x at s = 0 (2401 - 4116 + 1568 + 252 = 105) and measured 1.3e-5 worst case
+  // (tests/diag/fuzz_wide.py, 300 cases) against 1.1e-6 for Horner in s.
+  static constexpr float K = RORD == 8 ? 0.f : (float)(RORD - 1);
   static constexpr bool kClampable = true, kSets = false;
   using Params = PsiParams;
   f2 xr[NP];
@@ -127,11 +131,12 @@ struct FPsi {
   }
   static __device__ __forceinline__ int64_t row0(int64_t q) { return q * T + 8 * (int64_t)threadIdx.x; }
 
-  // He_r(t + K) in the depressed form, two lanes at once.
+  // He_r(t + K): depressed form for r = 4, 6; Horner in s for r = 8 (K = 0); two lanes at once.
   __device__ __forceinline__ f2 poly(f2 t) const {
     if (RORD == 4) return fma2(t, t, pk(-6.f, -6.f));
     if (RORD == 6) return fma2(fma2(t, t, pk(-30.f, -30.f)), t, pk(-40.f, -40.f));
-    return fma2(fma2(fma2(t, t, pk(-84.f, -84.f)), t, pk(-224.f, -224.f)), t, pk(252.f, 252.f));
+    return fma2(fma2(fma2(add2(t, pk(-28.f, -28.f)), t, pk(210.f, 210.f)), t, pk(-420.f, -420.f)), t,
+                pk(105.f, 105.f));   // r = 8: Horner in s (t = s)
   }
 
   // Accumulation: the G = 16 terms of one column group of a row are summed in

@@ -1,0 +1,60 @@
+"""Extended seeded fuzz (GPU vs oracle), the same checks as tests/test_gpu_fuzz.py on many more
+random (n, d, bandwidth scale) cases; prints the worst relative errors per family and every case
+over the 1e-5 contract.  Usage: python tests/diag/fuzz_wide.py [cases] [seed]"""
+import os
+import sys
+
+sys.path.insert(0, os.getcwd())
+import numpy as np  # noqa: E402
+
+import datagen  # noqa: E402
+import oracle  # noqa: E402
+import paper_1505_01998_b200 as kb  # noqa: E402
+
+
+def _data(n, d, seed):
+    r = np.random.default_rng(seed)
+    A = r.normal(size=(d, d)) / np.sqrt(d) + np.eye(d)
+    X = A @ r.standard_t(5, size=(d, n))
+    return X + r.normal(size=(d, 1)) * 3
+
+
+def main():
+    cases = int(sys.argv[1]) if len(sys.argv) > 1 else 200
+    rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 7)
+    ctx = kb.Context()
+    worst = {"psi": 0.0, "lscv_h": 0.0, "lscv_H": 0.0}
+    bad = []
+    for c in range(cases):
+        n = int(rng.integers(2, 4000))
+        d = int(rng.integers(1, 7))
+        scale = float(10 ** rng.uniform(-1.3, 0.3))
+        X = _data(n, d, 1000 + c)
+        x1 = np.ascontiguousarray(X[:1])
+        g = scale * max(np.std(x1), 1e-3)
+        for r in (4, 6, 8):
+            got = ctx.psi_r(kb.to_device(x1), r, [g])[0]
+            ref = oracle.psi_r(x1[0], r, g)
+            e = abs(got - ref) / abs(ref)
+            worst["psi"] = max(worst["psi"], e)
+            if e > 1e-5:
+                bad.append(("psi", n, d, r, scale, e))
+        _, S = oracle.mean_cov(X)
+        if n < 3 or np.linalg.cond(S) > 1e8:
+            continue
+        Xd = kb.to_device(X)
+        hs = np.array([0.5, 1.0, 2.0]) * scale
+        for fam, got, ref in (("lscv_h", ctx.lscv_h_scores(Xd, hs), oracle.lscv_h_scores(X, hs)),
+                              ("lscv_H", ctx.lscv_H_scores(Xd, [datagen.vech(h * h * S) for h in hs]),
+                               [oracle.lscv_H_score(X, datagen.vech(h * h * S)) for h in hs])):
+            e = float(np.max(np.abs(np.asarray(got) - ref) / np.abs(ref)))
+            worst[fam] = max(worst[fam], e)
+            if e > 1e-5:
+                bad.append((fam, n, d, scale, e))
+    print("cases", cases, "worst", worst)
+    for b in bad:
+        print("OVER 1e-5:", b)
+
+
+if __name__ == "__main__":
+    main()
