@@ -47,7 +47,10 @@ def main():
         for fam, got, ref in (("lscv_h", ctx.lscv_h_scores(Xd, hs), oracle.lscv_h_scores(X, hs)),
                               ("lscv_H", ctx.lscv_H_scores(Xd, [datagen.vech(h * h * S) for h in hs]),
                                [oracle.lscv_H_score(X, datagen.vech(h * h * S)) for h in hs])):
-            e = float(np.max(np.abs(np.asarray(got) - ref) / np.abs(ref)))
+            # relative to the curve's scale: an objective can cross zero between grid points
+            # (case 28 of seed 7: g = 7.4e-8 between 3.0e-3 and -9.0e-5), where a pointwise
+            # relative error says nothing about the kernel
+            e = float(np.max(np.abs(np.asarray(got) - ref)) / np.max(np.abs(ref)))
             worst[fam] = max(worst[fam], e)
             if e > 1e-5:
                 bad.append((fam, n, d, scale, e))
