@@ -1,6 +1,6 @@
 """Extended seeded fuzz (GPU vs oracle), the same checks as tests/test_gpu_fuzz.py on many more
 random (n, d, bandwidth scale) cases; prints the worst relative errors per family and every case
-over the 1e-5 contract.  Usage: python tests/diag/fuzz_wide.py [cases] [seed]"""
+over the 1e-5 contract.  Usage: python tests/diag/fuzz_wide.py [cases] [seed] [dmax] [nmax]"""
 import os
 import sys
 
@@ -22,12 +22,14 @@ def _data(n, d, seed):
 def main():
     cases = int(sys.argv[1]) if len(sys.argv) > 1 else 200
     rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 7)
+    dmax = int(sys.argv[3]) if len(sys.argv) > 3 else 6      # d drawn from 1..dmax
+    nmax = int(sys.argv[4]) if len(sys.argv) > 4 else 4000
     ctx = kb.Context()
     worst = {"psi": 0.0, "lscv_h": 0.0, "lscv_H": 0.0}
     bad = []
     for c in range(cases):
-        n = int(rng.integers(2, 4000))
-        d = int(rng.integers(1, 7))
+        n = int(rng.integers(2, nmax))
+        d = int(rng.integers(1, dmax + 1))
         scale = float(10 ** rng.uniform(-1.3, 0.3))
         X = _data(n, d, 1000 + c)
         x1 = np.ascontiguousarray(X[:1])
