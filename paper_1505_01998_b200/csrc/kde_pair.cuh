@@ -237,8 +237,10 @@ template <int D_, int NT_, int NB_, bool UNIT = false, bool SWC = false, int MIN
 struct FLscvScalar {
   static_assert(!UNIT || NB_ == 1, "UNIT sets carry one candidate");
   static constexpr int NT = NT_, D = D_, R = 2, T = NT_ * 2, NB = NB_, NOUT = 2 * NB_;
-  static constexpr int MINB = MINB_ > 0 ? MINB_ : (UNIT && D <= 4 ? 1024 : 512) / NT_;   // UNIT d<=4: 4 CTAs of 256
-  static constexpr int UNR = UNIT && D <= 4 ? (D <= 3 ? 4 : 2) : 1;   // UNIT: short body, unroll the column loop
+  // UNIT (LSCV_H sets): d <= 3 at 4 CTAs of 256 (64 registers); d = 4 at 3 CTAs with the column loop
+  // unrolled x4 (C5 2.81 s vs 2.87 s at 4 CTAs; the same change costs C3 (d = 2) 4.5%)
+  static constexpr int MINB = MINB_ > 0 ? MINB_ : (UNIT && D <= 3 ? 1024 : (UNIT && D == 4 ? 768 : 512)) / NT_;
+  static constexpr int UNR = UNIT && D <= 4 ? 4 : 1;   // UNIT: short body, unroll the column loop
   static constexpr bool kClampable = false, kSets = UNIT;
   static constexpr int CS = 1;
   using Params = LscvScalarParams;
