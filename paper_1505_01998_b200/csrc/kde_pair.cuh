@@ -240,8 +240,9 @@ struct FLscvScalar {
   // UNIT (LSCV_H sets): d <= 3 at 4 CTAs of 256 (64 registers); d = 4 at 3 CTAs with the column loop
   // unrolled x4 (C5 2.81 s vs 2.87 s at 4 CTAs; the same change costs C3 (d = 2) 4.5%)
   static constexpr int MINB = MINB_ > 0 ? MINB_ : (UNIT && D <= 3 ? 1024 : (UNIT && D == 4 ? 768 : 512)) / NT_;
-  // column-loop unroll: UNIT d <= 4 x4; LSCV_h with software-exp columns x2 (C2 469 vs 477 ms)
-  static constexpr int UNR = UNIT && D <= 4 ? 4 : (SWC ? 2 : 1);
+  // column-loop unroll: UNIT d <= 2 x8 (C3 pair time 15.64 -> 15.37 ms), d = 3, 4 x4 (no spills);
+  // LSCV_h with software-exp columns x2 (C2 469 vs 477 ms)
+  static constexpr int UNR = UNIT && D <= 2 ? 8 : (UNIT && D <= 4 ? 4 : (SWC ? 2 : 1));
   static constexpr bool kClampable = false, kSets = UNIT;
   static constexpr int CS = 1;
   using Params = LscvScalarParams;
