@@ -184,6 +184,8 @@ kde_status get_ws(kde_ctx* c, int64_t ld, int32_t d, int32_t n_out, Ws* w) {
       size_t cap = need + need / 4;
       CUDA_TRY(c, cudaMalloc(&c->own_ws, cap));
       c->own_bytes = cap;
+      // defined contents once: run_sums copies [prep flags .. limbs) in one transfer, gap included
+      CUDA_TRY(c, cudaMemsetAsync(c->own_ws, 0, cap, c->stream));
     }
     base = (char*)c->own_ws;
   }
