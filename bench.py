@@ -227,7 +227,7 @@ def main():
         x_pin = torch.from_numpy(x_host).pin_memory()
         barrier()
         ee = []
-        for _ in range(max(1, min(args.steps, 3))):
+        for _ in range(max(1, min(args.steps, 10))):
             flush.random_(0, 255)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
