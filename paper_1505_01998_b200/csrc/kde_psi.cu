@@ -21,8 +21,15 @@ int tile_for(Kind k, int d, int64_t n) {
     }
     case Kind::LscvScalar: return 512;
     case Kind::LscvMatrix: {
-      // 512-row tiles unless that leaves fewer than ~20 tiles per resident CTA (wave tail)
-      const int64_t nb = (n + 511) / 512;
+      // the largest of 1024 (d <= 4: 512 threads, 2 CTAs/SM), 512 and 256-row tiles that leaves
+      // ~20 tiles per resident CTA (wave tail).  1024 halves the per-unit barrier/epilogue share
+      // at the same 32 resident warps: C5 2.81 -> 2.71 s.
+      static const char* dbg = getenv("KDE_DEBUG_LSCVH_TILE");   // tests / diagnostics only
+      const int force = dbg ? atoi(dbg) : 0;
+      if (force == 1024 && d <= 4) return 1024;
+      if (force == 256 || force == 512) return force;
+      const int64_t nb2 = (n + 1023) / 1024, nb = (n + 511) / 512;
+      if (d <= 4 && nb2 * (nb2 + 1) / 2 >= 6000) return 1024;
       return nb * (nb + 1) / 2 >= 6000 ? 512 : 256;
     }
   }

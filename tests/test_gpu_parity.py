@@ -332,3 +332,38 @@ def test_empty_and_too_small_inputs_are_rejected(ctx):
         assert e.value.status == status
     # an empty query set is valid: no output
     assert ctx.evaluate(dev(datagen.sample_mixture("C3", 50, 1)), np.zeros((2, 0)), [0.1, 0.0, 0.1]).size == 0
+
+
+_TILE1024 = r"""
+import sys, numpy as np
+sys.path.insert(0, ".")
+import datagen, oracle
+import paper_1505_01998_b200 as kb
+ctx = kb.Context()
+worst = 0.0
+for d, n in [(1, 1025), (2, 2100), (3, 1500), (4, 3071)]:
+    X = datagen.sample_mixture("C5", n, 17 + n)[:d]
+    rng = np.random.default_rng(d)
+    cands = []
+    for _ in range(3):
+        A = rng.normal(size=(d, d))
+        cands.append(datagen.vech(0.2 * (A @ A.T / d + 0.3 * np.eye(d))))
+    got = ctx.lscv_H_scores(kb.to_device(X), np.array(cands))
+    for v, c in zip(got, cands):
+        ref = oracle.lscv_H_score(X, c)
+        worst = max(worst, abs(v - ref) / abs(ref))
+print(worst)
+"""
+
+
+def test_lscv_H_tile1024_ragged_matches_oracle():
+    # the 1024-row tile (512 threads) that large-n LSCV_H uses for d <= 4, forced at small ragged n
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, KDE_DEBUG_LSCVH_TILE="1024")
+    r = subprocess.run([sys.executable, "-c", _TILE1024], cwd=root, env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert float(r.stdout.strip().splitlines()[-1]) < RTOL

@@ -93,7 +93,7 @@ def full(rep, prefix, expected):
             try:
                 dur = float(d["gpu__time_duration.sum"]["value"].replace(",", ""))
                 unit = d["gpu__time_duration.sum"]["unit"]
-                sec = dur * {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1}[unit]
+                sec = dur * {"nsecond": 1e-9, "ns": 1e-9, "usecond": 1e-6, "us": 1e-6, "msecond": 1e-3, "ms": 1e-3, "second": 1, "s": 1}[unit]
                 md.append(f"| algorithmic evals / duration | {float(expected[n]) / sec:.4e} evals/s |")
             except Exception:
                 pass
