@@ -9,7 +9,10 @@ here in plain Python floats (IEEE fp64), each following the cited passage of PAP
 
 Parity status: every function below is pinned by tests/test_oracle_*.py against something
 other than itself (quadrature identities, library routines, closed forms, invariants, MC
-expectations); nelder_mead is pinned step for step to scipy's Nelder–Mead.  The GPU selector's
+expectations); nelder_mead is pinned step for step to scipy's Nelder–Mead.  The PLUGIN chain
+(every step of Eq. 11-18) is pinned to the mpmath X=[1,2,3] trace, lscv_h0 at d = 1, 2, 3 to
+Eq. 25 simplified by hand, initial_simplex to hand-written vertices (reading Z8) and the
+nm_starts 4^-k scaling to the evaluation trace (tests/test_paper_examples.py).  The GPU selector's
 NM decision path is checked against this one by replay (tests/test_gpu_nm_replay.py: identical
 decisions on seeded inputs); where an fp32-term objective could legitimately flip a near-tie
 comparison, the SURVEY §8(c) c5 tie rule applies.

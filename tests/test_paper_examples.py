@@ -40,6 +40,57 @@ def test_h0_and_H_start():
     assert Hs == pytest.approx(EX["H_start_d1"]["H"] * 2 ** -0.2 * math.sqrt(2.0), rel=1e-9)
 
 
+def test_plugin_x123_worked_trace():
+    # Every step of the PLUGIN chain (Eq. 11-18) against the independently computed mpmath trace:
+    # a wrong root (1/9, 1/7, 1/5), a dropped -2 or mu2 factor, or a wrong K^(r)(0) fails here.
+    e = EX["plugin_x123_trace"]
+    t = oracle.plugin(np.array(e["x"]))
+    for k in ("V_hat", "sigma_hat", "psi8_ns", "g1", "psi6", "g2", "psi4", "h"):
+        assert t[k] == pytest.approx(e[k], rel=1e-12), k
+
+
+def test_lscv_h0_hand_values_d_gt_1():
+    # Eq. 25 as written, reading Z3: h0 = (4/(d^3 (d+2) n))^{1/(d+4)} by hand.
+    for c in EX["lscv_h0_hand"]["cases"]:
+        d, n = c["d"], c["n"]
+        ref = c["h0"] if "h0" in c else (c["num"] / (c["den"] * n)) ** (1.0 / (d + 4))
+        assert oracle.lscv_h0(n, d) == pytest.approx(ref, rel=1e-13), (d, n)
+    # the grid is bracketed by it (Eq. 27)
+    hs = oracle.lscv_h_grid(32768, 2, 5)
+    assert list(hs) == pytest.approx([0.125 / 4, 0.125 / 4 + 0.125 * 3.75 / 4 * 1, 0.125 / 4 + 0.125 * 3.75 / 4 * 2,
+                                      0.125 / 4 + 0.125 * 3.75 / 4 * 3, 0.5], rel=1e-14)
+
+
+@pytest.mark.parametrize("case", ["d2", "d3"])
+def test_initial_simplex_hand_vertices(case):
+    # Reading Z8: an off-diagonal entry that is 0 still gets a nonzero step 0.1*sqrt(H_aa H_bb).
+    e = EX["nm_initial_simplex_hand"][case]
+    d = 2 if case == "d2" else 3
+    sim = oracle.initial_simplex(np.array(e["x0"]), d)
+    assert len(sim) == len(e["vertices"])
+    for v, ref in zip(sim, e["vertices"]):
+        np.testing.assert_allclose(v, ref, rtol=1e-15, atol=1e-15)
+
+
+def test_nm_starts_scale_the_initial_simplex_by_powers_of_4():
+    # Row f4 multi-start: run k starts from the initial simplex scaled by 4^-k; the best run
+    # (ties -> earlier) is returned.  Checked on the evaluation trace: run 2's first m+1
+    # evaluations are the hand-scaled vertices x_k / 4.
+    X = np.array([[0.0, 0.4, 1.1, 1.5, 2.6, 3.0, 3.2, 4.4], [0.3, -0.2, 0.9, 0.1, 1.7, 1.2, 2.5, 2.1]])
+    t1, t2 = [], []
+    r1 = oracle.lscv_H_select(X, max_iter=30, trace=t1)
+    r2 = oracle.lscv_H_select(X, max_iter=30, trace=t2, nm_starts=2)
+    L = len(t1)
+    for a, b in zip(t1, t2[:L]):
+        np.testing.assert_array_equal(a[0], b[0])
+    sim0 = oracle.initial_simplex(oracle.vech(r1["H_start"]), 2)
+    for k, v in enumerate(sim0):
+        np.testing.assert_allclose(t2[L + k][0], v / 4.0, rtol=1e-15)
+    run2 = [f for _, f in t2[L:]]
+    assert r2["f"] == min(r1["f"], r2["f"]) and r2["f"] <= r1["f"]
+    assert r2["f"] in run2 or r2["f"] == r1["f"]
+
+
 def test_toy_data_plugin_is_finite_and_equivariant():
     x = np.array(EX["toy_data"]["x"])
     t = oracle.plugin(x)
