@@ -11,12 +11,18 @@ timed events.  `e2e` repeats the step through the public API from pinned host me
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
   torchrun --nproc-per-node N bench.py --gpus N ...
+
+`--gpus N` with N > 1 outside torchrun re-executes itself under `torch.distributed.run`
+(127.0.0.1, a free port), so both launch forms run N ranks; under torchrun the world size must
+equal --gpus.  `--dry-run` runs the same multi-rank plumbing on CPU (gloo, no kernels): every rank
+reports its tile range of the pair partition, rank 0 prints one JSON line (tests/test_bench_cli.py).
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -104,7 +110,7 @@ def cpu_baseline_sample(x: np.ndarray, g: tuple, seconds: float = 12.0):
         pairs += 2 * sum((n - 1 - i) for a, b in chunks for i in range(a, b))
         i0 = hi
     dt = time.perf_counter() - t0
-    return {"value": pairs / dt, "unit": "evals/s", "cores": cores, "kind": "oracle",
+    return {"value": pairs / dt, "unit": "evals/s", "cores": cores, "kind": "oracle", "evals": pairs,
             "sample": f"rows 0..{i0} of C4 (all j>i), Psi6(g1)+Psi4(g2) pair sums, {pairs:.3e} evals in {dt:.1f}s"}
 
 
@@ -119,6 +125,9 @@ def load_traffic():
 
 
 def run_reference(args, rank, world):
+    """The reference arm (tier rules): the fp64 oracle as it stands, timed on this box's host
+    cores; each step is a bounded row sample of the C4 workload whose wall time is MEASURED
+    (ms_per_step is that measured time, not an extrapolation to the full step)."""
     if rank != 0:
         return
     import datagen
@@ -128,20 +137,70 @@ def run_reference(args, rank, world):
     # pair sums on a bounded row sample at those bandwidths.
     tr = json.load(open(os.path.join(ROOT, "tests", "golden", "C4_plugin.json")))["trace"]
     g1, g2 = tr["g1"], tr["g2"]
-    times, vals = [], []
+    times, vals, evals = [], [], []
+    per_step_s = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
     for s in range(args.warmup + args.steps):
-        r = cpu_baseline_sample(x, (g1, g2), seconds=max(2.0, 20.0 / max(1, args.steps)))
+        t0 = time.perf_counter()
+        r = cpu_baseline_sample(x, (g1, g2), seconds=per_step_s)
+        dt = time.perf_counter() - t0
         if s >= args.warmup:
             vals.append(r["value"])
-            times.append(evals_per_step(x.size) / r["value"] * 1e3)
-    v = statistics.median(vals)
+            times.append(dt * 1e3)
+            evals.append(r["evals"])
+    v = sum(evals) / (sum(times) / 1e3)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "evals/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": statistics.median(times),
+            "ms_per_step_basis": "measured wall time of one bounded-sample step (oracle on host cores)",
+            "full_step_ms_extrapolated": evals_per_step(x.size) / v * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": "C4 PLUGIN n=2^20 skewed mixture (MW#2)", "n": x.size},
+            "data": "synthetic", "config": {"workload": "C4 PLUGIN n=2^20 skewed mixture (MW#2)", "n": x.size,
+                                            "sample_evals_per_step": statistics.median(evals)},
             "cpu_baseline": {"value": v, "unit": "evals/s", "cores": r["cores"], "kind": "oracle", "sample": r["sample"]},
             "e2e": {"value": v, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def _free_port() -> int:
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch_under_torchrun(n: int):
+    """`python bench.py --gpus N` (N > 1) outside torchrun: become `torch.distributed.run` with N
+    ranks on this node (the driver's own launch form), so N really is the world size."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
+
+
+def run_dry(args, rank, world):
+    """CPU check of the N-rank plumbing (gloo): rendezvous, each rank's contiguous tile range of
+    the C4 pair partition (the library's own kde_shard_tiles), barrier and max-over-ranks
+    reduction as in the timed path; rank 0 prints the JSON line.  No kernels run."""
+    import torch
+    import torch.distributed as dist
+    import paper_1505_01998_b200 as kb
+    if world > 1:
+        dist.init_process_group("gloo")
+    T, total, tb, te = kb.shard_tiles(kb.SUM_PSI6, args.n, 1, rank, world)
+    t = torch.tensor([float(te - tb), float(rank)], dtype=torch.float64)
+    ranges = [None] * world
+    if world > 1:
+        dist.barrier()
+        dist.all_gather_object(ranges, (tb, te))
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    else:
+        ranges = [(tb, te)]
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": None, "unit": "evals/s", "n_gpus": world, "steps": 0,
+                          "warmup": 0, "dry_run": True, "scaling": "strong",
+                          "config": {"workload": "C4 PLUGIN n=2^20 skewed mixture (MW#2), seed 4", "n": args.n,
+                                     "parallelism": f"pair-range x{world}", "tile": T, "tiles": total,
+                                     "rank_tiles": ranges, "max_rank_tiles": float(t[0])}}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def main():
@@ -153,11 +212,19 @@ def main():
     ap.add_argument("--n", type=int, default=N_C4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dry-run", action="store_true", help="CPU check of the N-rank plumbing (gloo, no kernels)")
     args = ap.parse_args()
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_under_torchrun(args.gpus)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.dry_run:
+        run_dry(args, rank, world)
+        return
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -211,6 +278,10 @@ def main():
         kernel_launches += prof["kernel_launches"]
     barrier()
     clocks = sampler.stop()
+    clocks_per_rank = [clocks]
+    if world > 1:
+        clocks_per_rank = [None] * world
+        dist.all_gather_object(clocks_per_rank, {k: clocks.get(k) for k in ("sm_mhz", "sm_max_mhz", "reasons")})
     total_ms = sum(step_ms)
     t = torch.tensor([total_ms, pair_ms], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -258,8 +329,11 @@ def main():
                          "peak_basis": "16 MUFU.EX2/clk/SM x SMs x 1965 MHz (guide unit counts; tools/peaks.cu measured 4.646e12/s)"},
             "clocks": clocks,
             "gpu_launches": kernel_launches,
+            "pair_ms_per_launch": per_launch_ms,
             "e2e": e2e,
         }
+        if world > 1:
+            line["clocks_per_rank"] = clocks_per_rank
         if not args.no_cpu_baseline and world == 1:
             line["cpu_baseline"] = cpu_baseline_sample(x_host[0], (tr["g1"], tr["g2"]))
         print(json.dumps(line), flush=True)

@@ -73,7 +73,9 @@ class Fixed(ctypes.Structure):
                 ("scale_exp", ctypes.c_int32), ("pad_", ctypes.c_int32)]
 
     def key(self):
-        return (self.hi, self.mid, self.lo, self.scale_exp)
+        """Exact identity of the value: the integer hi 2^80 + mid 2^40 + lo and the scale (limb
+        layouts that differ only by carries, e.g. a sum of shards, compare equal)."""
+        return (self.hi * (1 << 80) + self.mid * (1 << 40) + self.lo, self.scale_exp)
 
 
 _lib = None

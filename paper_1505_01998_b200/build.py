@@ -16,8 +16,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I" + os.path.join(ROOT, "include")]
 SOURCES = ["kde_psi.cu", "kde_lscv_scalar.cu", "kde_lscv_matrix.cu", "kde_eval.cu", "kde_materialized.cu",
-           "kde_host.cpp"]
-HEADERS = ["kde_internal.h", "kde_device.cuh", "kde_pair.cuh", os.path.join("..", "..", "include", "kde.h")]
+           "kde_runtime.cpp", "kde_linalg.cpp", "kde_nm.cpp", "kde_selectors.cpp", "kde_extras.cpp"]
+HEADERS = ["kde_internal.h", "kde_host.h", "kde_device.cuh", "kde_pair.cuh", "kde_tiles.cuh", os.path.join("..", "..", "include", "kde.h")]
 
 
 def _newer(target: str, deps) -> bool:

@@ -100,7 +100,10 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// Exact fixed-point split of v * 2^S (|v| 2^S < 2^120): sign-magnitude limbs of 40 bits.
+// Exact fixed-point split of v * 2^S (|v| 2^S < 2^120): sign-magnitude limbs of 40 bits.  The
+// lo limb is an unsigned mod-2^64 accumulator; its carry-outs minus the borrows of negative
+// addends go to the carry limb (dst[3], units of 2^64), so (unsigned) lo + 2^64 carry is the exact
+// sum whatever the number and order of the commits (the difference true - lo is order-free).
 __device__ __forceinline__ void add_limbs(double v, int S, unsigned long long* dst) {
   double a = fabs(ldexp(v, S));
   double h = floor(ldexp(a, -80));
@@ -111,7 +114,16 @@ __device__ __forceinline__ void add_limbs(double v, int S, unsigned long long* d
   if (v < 0) { H = -H; M = -M; L = -L; }
   atomicAdd(dst + 0, (unsigned long long)H);
   atomicAdd(dst + 1, (unsigned long long)M);
-  atomicAdd(dst + 2, (unsigned long long)L);
+  const unsigned long long u = (unsigned long long)L;
+  const unsigned long long old = atomicAdd(dst + 2, u);
+  const long long c = (long long)(old + u < old) - (long long)(L < 0);
+  if (c != 0) atomicAdd(dst + 3, (unsigned long long)c);
+}
+
+// Value of one output's limbs (device side of the host's limbs_to_fixed / fixed_value).
+__device__ __forceinline__ __int128 limbs_total(const unsigned long long* l) {
+  return (__int128)(long long)l[0] * ((__int128)1 << 80) + (__int128)(long long)l[1] * ((__int128)1 << 40) +
+         (__int128)l[2] + (__int128)(long long)l[3] * ((__int128)1 << 64);
 }
 
 }  // namespace kde

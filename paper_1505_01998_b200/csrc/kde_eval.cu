@@ -129,10 +129,11 @@ int eval_rows_per_block() { return kEvRows; }
 int eval_cols_per_tile() { return kEvTC; }
 
 template <int D>
-static cudaError_t launch_eval_d(const EvalLaunch& c) {
+static cudaError_t eval_occupancy(int* occ_out) {
   const size_t smem = 2 * D * kEvTC * sizeof(float) + 16;
-  static int occ = -1;
-  if (occ < 0) {
+  static int occ_dev[kMaxDevices];   // 0 = not yet set up on that device (the opt-in is per device)
+  int& occ = occ_dev[current_device()];
+  if (occ <= 0) {
     cudaError_t e = cudaFuncSetAttribute(eval_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int o = 0;
@@ -140,17 +141,43 @@ static cudaError_t launch_eval_d(const EvalLaunch& c) {
     if (e != cudaSuccess) return e;
     occ = o > 0 ? o : 1;
   }
+  *occ_out = occ;
+  return cudaSuccess;
+}
+
+// Columns are split so that there are >= 2 waves of (row block, split) units (deterministic for a
+// given m, n and SM count); returns the number of splits actually used.
+static int eval_split_count(int sm_count, int occ, int64_t ldm, int64_t ldn, int* tiles_per_split) {
+  const int row_blocks = (int)(ldm / kEvRows), n_tiles = (int)(ldn / kEvTC);
+  const int target = 2 * sm_count * occ;
+  int splits = (target + row_blocks - 1) / row_blocks;
+  if (splits > n_tiles) splits = n_tiles;
+  if (splits < 1) splits = 1;
+  const int tps = (n_tiles + splits - 1) / splits;
+  if (tiles_per_split) *tiles_per_split = tps;
+  return (n_tiles + tps - 1) / tps;
+}
+
+template <int D>
+static cudaError_t eval_splits_d(int sm_count, int64_t ldm, int64_t ldn, int* splits) {
+  int occ = 1;
+  cudaError_t e = eval_occupancy<D>(&occ);
+  if (e != cudaSuccess) return e;
+  *splits = eval_split_count(sm_count, occ, ldm, ldn, nullptr);
+  return cudaSuccess;
+}
+
+template <int D>
+static cudaError_t launch_eval_d(const EvalLaunch& c) {
+  const size_t smem = 2 * D * kEvTC * sizeof(float) + 16;
+  int occ = 1;
+  cudaError_t e0 = eval_occupancy<D>(&occ);
+  if (e0 != cudaSuccess) return e0;
   EvalArgs a;
   a.Y = c.Y; a.X = c.X; a.m = c.m; a.ldm = c.ldm; a.ldn = c.ldn;
   a.row_blocks = (int)(c.ldm / kEvRows);
   a.n_tiles = (int)(c.ldn / kEvTC);
-  // split the columns so that there are >= 2 waves of units (deterministic for given m, n, SMs)
-  const int target = 2 * c.sm_count * occ;
-  int splits = (target + a.row_blocks - 1) / a.row_blocks;
-  if (splits > a.n_tiles) splits = a.n_tiles;
-  if (splits < 1) splits = 1;
-  a.tiles_per_split = (a.n_tiles + splits - 1) / splits;
-  a.splits = (a.n_tiles + a.tiles_per_split - 1) / a.tiles_per_split;
+  a.splits = eval_split_count(c.sm_count, occ, c.ldm, c.ldn, &a.tiles_per_split);
   a.part = c.part;
   if ((size_t)a.splits * (size_t)c.ldm > c.part_capacity) return cudaErrorInvalidValue;
   const int units = a.row_blocks * a.splits;
@@ -166,7 +193,20 @@ static cudaError_t launch_eval_d(const EvalLaunch& c) {
   return cudaGetLastError();
 }
 
-int eval_max_splits(int sm_count) { return 2 * sm_count * 8; }
+
+cudaError_t eval_splits(int d, int sm_count, int64_t ldm, int64_t ldn, int* splits) {
+  switch (d) {
+    case 1: return eval_splits_d<1>(sm_count, ldm, ldn, splits);   case 2: return eval_splits_d<2>(sm_count, ldm, ldn, splits);
+    case 3: return eval_splits_d<3>(sm_count, ldm, ldn, splits);   case 4: return eval_splits_d<4>(sm_count, ldm, ldn, splits);
+    case 5: return eval_splits_d<5>(sm_count, ldm, ldn, splits);   case 6: return eval_splits_d<6>(sm_count, ldm, ldn, splits);
+    case 7: return eval_splits_d<7>(sm_count, ldm, ldn, splits);   case 8: return eval_splits_d<8>(sm_count, ldm, ldn, splits);
+    case 9: return eval_splits_d<9>(sm_count, ldm, ldn, splits);   case 10: return eval_splits_d<10>(sm_count, ldm, ldn, splits);
+    case 11: return eval_splits_d<11>(sm_count, ldm, ldn, splits); case 12: return eval_splits_d<12>(sm_count, ldm, ldn, splits);
+    case 13: return eval_splits_d<13>(sm_count, ldm, ldn, splits); case 14: return eval_splits_d<14>(sm_count, ldm, ldn, splits);
+    case 15: return eval_splits_d<15>(sm_count, ldm, ldn, splits); case 16: return eval_splits_d<16>(sm_count, ldm, ldn, splits);
+  }
+  return cudaErrorInvalidValue;
+}
 
 cudaError_t launch_eval(int d, const EvalLaunch& c) {
   switch (d) {
@@ -200,9 +240,9 @@ __device__ __forceinline__ double phi_diff(double al, double be) {
 __global__ void __launch_bounds__(kAqpThreads) aqp_kernel(const double* __restrict__ x, int64_t n,
                                                           double h, const double* __restrict__ lo,
                                                           const double* __restrict__ hi,
-                                                          double* __restrict__ part) {
+                                                          double* __restrict__ part, int q0) {
   __shared__ double red[kAqpThreads / 32][2];
-  const int q = blockIdx.y;
+  const int q = q0 + blockIdx.y;
   const double a = lo[q], b = hi[q], ih = 1.0 / h;
   const double k = 0.39894228040143267794;   // 1/sqrt(2 pi)
   double c = 0.0, s = 0.0;
@@ -244,10 +284,12 @@ int aqp_blocks(int64_t n) {
 
 cudaError_t launch_aqp(const double* x, int64_t n, double h, const double* lo, const double* hi, int nq,
                        double* part, int nblk, double* out, cudaStream_t s) {
-  dim3 grid(nblk, nq);
-  aqp_kernel<<<grid, kAqpThreads, 0, s>>>(x, n, h, lo, hi, part);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
+  for (int q0 = 0; q0 < nq; q0 += 65535) {   // gridDim.y <= 65535: intervals in chunks
+    const int cnt = nq - q0 < 65535 ? nq - q0 : 65535;
+    aqp_kernel<<<dim3(nblk, cnt), kAqpThreads, 0, s>>>(x, n, h, lo, hi, part, q0);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
   aqp_reduce_kernel<<<(nq + 127) / 128, 128, 0, s>>>(part, nblk, nq, out);
   return cudaGetLastError();
 }

@@ -10,8 +10,21 @@ constexpr int kThreads = 256;          // threads per CTA of every pair kernel
 constexpr int kMaxCand = 32;           // candidates per pair-kernel launch (upper bound)
 constexpr int kMaxDim = 16;
 
-// Fixed-point limbs of one output value: value*2^S = hi*2^80 + mid*2^40 + lo.
-constexpr int kLimbs = 3;
+// Fixed-point limbs of one output value on the device: value*2^S = hi*2^80 + mid*2^40 +
+// (unsigned) lo + carry*2^64.  Every tile commit adds |hi|, |mid|, |lo| < 2^40 (sign-magnitude
+// split); hi and mid stay far from overflow because the a-priori bound caps the sum of |commits|
+// at 2^100, and lo's unsigned wrap-arounds are counted in the carry limb (add_limbs), so the
+// value is exact for any number of commits (n up to 2^31).  Readers fold the carry; before a
+// cross-rank sum each rank's limbs are normalised (normalize_limbs) so the int64 sums cannot wrap.
+constexpr int kLimbs = 4;
+constexpr int kMaxDevices = 64;   // per-device caches of one-time kernel setup
+
+// Current CUDA device (per-device caches: the dynamic shared-memory opt-in is a device attribute).
+inline int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d < 0 || d >= kMaxDevices ? 0 : d;
+}
 
 // Which functor a launch runs.
 enum class Kind : int { Psi4 = 4, Psi6 = 6, Psi8 = 8, LscvScalar = 1, LscvMatrix = 2 };
@@ -103,7 +116,9 @@ struct EvalLaunch {
 cudaError_t launch_eval(int d, const EvalLaunch& c);
 int eval_rows_per_block();
 int eval_cols_per_tile();
-int eval_max_splits(int sm_count);
+// Column splits eval_kernel<d> uses for an m x n problem (the launch and the host's scratch
+// sizing share this): scratch = splits * ldm doubles.
+cudaError_t eval_splits(int d, int sm_count, int64_t ldm, int64_t ldn, int* splits);
 // The paper's two-phase LSCV_h (kde_materialized.cu).
 int mat_tile();
 int64_t mat_chunk();
@@ -117,6 +132,9 @@ cudaError_t launch_aqp(const double* x, int64_t n, double h, const double* lo, c
                        double* part, int nblk, double* out, cudaStream_t s);
 int moments_blocks(int64_t n);
 size_t sort_temp_bytes(int64_t n);
+// Canonical form of `count` outputs' limbs (hi, mid in [0,2^40), lo in [0,2^40), carry 0) so
+// that a sum over ranks of int64 limbs cannot wrap.
+cudaError_t launch_normalize_limbs(unsigned long long* limbs, int count, cudaStream_t s);
 cudaError_t launch_sort(const double* in, double* out, int64_t n, void* temp, size_t temp_bytes,
                         cudaStream_t s);
 

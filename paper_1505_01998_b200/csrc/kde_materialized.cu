@@ -16,6 +16,7 @@
 
 #include "kde_device.cuh"
 #include "kde_internal.h"
+#include "kde_tiles.cuh"
 
 namespace kde {
 
@@ -27,16 +28,6 @@ constexpr int64_t kP2Chunk = (int64_t)kP2Threads * kP2Vec * 4;
 int mat_tile() { return kMatT; }
 int64_t mat_chunk() { return kP2Chunk; }
 
-__host__ __device__ inline void mat_tile_coords(int64_t bx, int64_t& l, int64_t& q) {
-  double s = sqrt(8.0 * (double)bx + 9.0);
-  int64_t L = (int64_t)ceil((s - 3.0) * 0.5);
-  if (L < 0) L = 0;
-  while (L > 0 && L * (L + 1) / 2 > bx) --L;
-  while ((L + 1) * (L + 2) / 2 <= bx) ++L;
-  l = L;
-  q = bx - L * (L + 1) / 2;
-}
-
 template <int D>
 __global__ void __launch_bounds__(kMatT) mat_write_kernel(const float* __restrict__ X, int64_t n, int64_t ld,
                                                           int64_t tb, int64_t te, float* __restrict__ buf) {
@@ -44,7 +35,7 @@ __global__ void __launch_bounds__(kMatT) mat_write_kernel(const float* __restric
   const int tid = threadIdx.x;
   for (int64_t t = tb + blockIdx.x; t < te; t += gridDim.x) {
     int64_t l, q;
-    mat_tile_coords(t, l, q);
+    tile_coords(t, l, q);
     __syncthreads();
 #pragma unroll
     for (int d = 0; d < D; ++d) cs[d][tid] = X[d * ld + l * kMatT + tid];

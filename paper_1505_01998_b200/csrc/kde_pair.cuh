@@ -26,6 +26,7 @@
 
 #include "kde_device.cuh"
 #include "kde_internal.h"
+#include "kde_tiles.cuh"
 
 namespace kde {
 
@@ -35,19 +36,6 @@ constexpr int nb_scalar(int d) { return d <= 4 ? 8 : (d <= 12 ? 16 : 8); }
 
 
 // ------------------------------------------------------------------ small device helpers
-
-__host__ __device__ inline void tile_coords(int64_t bx, int64_t& l, int64_t& q) {
-  // Eq. 42: l = ceil((sqrt(8 bx + 9) - 3) / 2);  Eq. 43: q = bx - l(l+1)/2.  The fp64 sqrt is
-  // exact enough to land within +-1 of l for bx < 2^62; the loops make it exact (reading Z13).
-  double s = sqrt(8.0 * (double)bx + 9.0);
-  int64_t L = (int64_t)ceil((s - 3.0) * 0.5);
-  if (L < 0) L = 0;
-  while (L > 0 && L * (L + 1) / 2 > bx) --L;
-  while ((L + 1) * (L + 2) / 2 <= bx) ++L;
-  l = L;
-  q = bx - L * (L + 1) / 2;
-}
-
 
 // Per-tile epilogue: fixed-order reduction of NOUT per-thread values, then limb atomics.
 template <int NOUT, int NT>
@@ -514,8 +502,9 @@ __global__ void __launch_bounds__(F::NT, F::MINB) pair_kernel_sets(const Args a,
 template <class F>
 inline cudaError_t pair_occupancy(int* occ_out) {
   constexpr size_t smem = 2 * F::D * F::T * sizeof(float) + (F::NT / 32) * F::NOUT * sizeof(double) + 16;
-  static int occ = -1;
-  if (occ < 0) {
+  static int occ_dev[kMaxDevices];   // 0 = not yet set up on that device
+  int& occ = occ_dev[current_device()];
+  if (occ <= 0) {
     const void* kern;
     if constexpr (F::kSets) kern = (const void*)pair_kernel_sets<F>;
     else kern = (const void*)pair_kernel<F>;

@@ -303,9 +303,7 @@ cudaError_t launch_psi64(int r, const double* y, int64_t n, int64_t tb, int64_t 
 // O(n) and O(n^2) kernels, so kde_plugin_h enqueues the whole chain without a host round trip
 // (one synchronisation at the end).  State in the workspace's `small` block (PluginDev layout).
 __device__ __forceinline__ double limbs_value_dev(const unsigned long long* l, int S) {
-  const __int128 T = (__int128)(long long)l[0] * ((__int128)1 << 80) +
-                     (__int128)(long long)l[1] * ((__int128)1 << 40) + (__int128)(long long)l[2];
-  return ldexp((double)T, -S);
+  return ldexp((double)limbs_total(l), -S);
 }
 
 __device__ __forceinline__ void set_status(double* st, int code) {
@@ -352,6 +350,26 @@ __global__ void plugin_chain_kernel(int stage, int64_t n, double* small, const u
 cudaError_t launch_plugin_chain(int stage, int64_t n, double* small, const unsigned long long* limbs, int S,
                                 cudaStream_t s) {
   plugin_chain_kernel<<<1, 1, 0, s>>>(stage, n, small, limbs, S);
+  return cudaGetLastError();
+}
+
+// Canonical limbs before a cross-rank int64 sum (kde_internal.h): total = hi 2^80 + mid 2^40 + lo
+// with mid, lo in [0, 2^40), carry 0.
+__global__ void normalize_limbs_kernel(unsigned long long* limbs, int count) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < count; k += gridDim.x * blockDim.x) {
+    unsigned long long* l = limbs + (size_t)k * kLimbs;
+    const __int128 T = limbs_total(l);
+    const __int128 m40 = ((__int128)1 << 40) - 1;
+    l[0] = (unsigned long long)(long long)(T >> 80);
+    l[1] = (unsigned long long)(long long)((T >> 40) & m40);
+    l[2] = (unsigned long long)(long long)(T & m40);
+    l[3] = 0ull;
+  }
+}
+
+cudaError_t launch_normalize_limbs(unsigned long long* limbs, int count, cudaStream_t s) {
+  if (count <= 0) return cudaSuccess;
+  normalize_limbs_kernel<<<(count + 255) / 256, 256, 0, s>>>(limbs, count);
   return cudaGetLastError();
 }
 

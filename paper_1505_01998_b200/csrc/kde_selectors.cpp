@@ -1,0 +1,667 @@
+// kde_selectors.cpp — the three bandwidth selectors of Sec. 4.4 on top of the pair
+// kernels: Psi_r sums and the device-resident PLUGIN chain (Eq. 11-18), LSCV_h (Eq. 19-28) and
+// LSCV_H (Eq. 29-35) with Nelder–Mead; ABI calls kde_psi_r, kde_plugin_h, kde_lscv_h_scores,
+// kde_lscv_H_scores, kde_raw_sums, kde_select_bandwidth.  P:NNN = PAPER.md line NNN.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "kde_host.h"
+
+using kde::Kind;
+using namespace kde::host;
+
+namespace kde {
+namespace host {
+
+// ------------------------------------------------------------------ Psi_r
+// The kernel evaluates He_r in t = u^2 - (r-1) with exact integer coefficients; the parameters
+// are the exponent scale c0 and, per accumulator class k, the MUFU offset o_k and the exact
+// fp64 factor that undoes it: 2^(u^2 c0) = 2^(t c0 + o_k) * 2^((r-1) c0 - o_k).
+void psi_coeffs(int r, kde::PsiParams& p) {
+  std::memset(&p, 0, sizeof(p));
+  p.c0 = (float)(-kLog2e / 2.0);
+  const double Kc0 = (double)(r == 8 ? 0 : r - 1) * (double)p.c0;   // K of FPsi; exact in fp64
+  for (int k = 0; k < 16; ++k) {   // k = 8 * (tile parity) + row slot; shift (row slot)/8 + parity/16
+    p.o[k] = (float)(Kc0 - (16.0 + (k % 8) / 8.0 + (k / 8) / 16.0));
+    p.fac[k] = std::exp2(Kc0 - (double)p.o[k]);                    // exponent exact in fp64
+  }
+}
+
+double he_at_zero(int r) { return r == 4 ? 3.0 : (r == 6 ? -15.0 : 105.0); }
+
+Kind psi_kind(int r) { return r == 4 ? Kind::Psi4 : (r == 6 ? Kind::Psi6 : Kind::Psi8); }
+
+// fp64-term mode: one Psi_r pass over this rank's 256-tiles of the fp64 scaled samples y, into
+// `limbs` (3 int64), then the all-reduce.
+kde_status psi64_pass(kde_ctx* c, int r, const double* y, int64_t n, int S, unsigned long long* limbs) {
+  Range rr("kde.pair_pass_fp64");
+  int64_t tb, te;
+  shard_range(n_tiles(n, kde::kPsi64Tile), c->rank, c->world, &tb, &te);
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  const unsigned rec = (c->cap_stream && c->stream == c->cap_stream) ? cudaEventRecordExternal : cudaEventRecordDefault;
+  if (c->profiling) { e0 = next_event(c); e1 = next_event(c); CUDA_TRY(c, cudaEventRecordWithFlags(e0, c->stream, rec)); }
+  CUDA_TRY(c, kde::launch_psi64(r, y, n, tb, te, S, limbs, c->sm_count, c->stream));
+  if (tb < te) c->prof_all += 1;
+  if (c->profiling) {
+    CUDA_TRY(c, cudaEventRecordWithFlags(e1, c->stream, rec));
+    c->prof_launches++;
+    c->prof_evals += pairs_in_range(n, kde::kPsi64Tile, tb, te);
+  }
+  TRY(allreduce_limbs(c, limbs, kde::kLimbs));
+  return KDE_OK;
+}
+
+// Raw Psi sums S_r(g) = sum_{i<j} He_r(u) e^{-u^2/2} for each g (one prep + one launch per g).
+kde_status psi_raw(kde_ctx* c, const double* x, int64_t n, int r, const double* g, int ng,
+                   const Moments& m, int shard_rank, int shard_world, bool allreduce,
+                   std::vector<kde_fixed>& out, bool presorted = false) {
+  const int T = kde::tile_for(psi_kind(r), 1, n);
+  const int64_t ld = (n + T - 1) / T * T;
+  Ws w;
+  TRY(get_ws(c, ld, 1, 1, &w));
+  const int S = scale_exp_for(2.0 * std::fabs(he_at_zero(r)), n);
+  if (!presorted) {
+    const double* xs = nullptr;
+    TRY(gpu_sorted(c, x, n, &xs));
+    x = xs;
+  }
+  out.clear();
+  if ((c->psi_mode == 1)) {                       // fp64-term mode (kde_set_precision)
+    TRY(grow(c, &c->y64, &c->y64_bytes, (size_t)std::max<int64_t>(n, 1) * sizeof(double)));
+    double* y = static_cast<double*>(c->y64);
+    for (int k = 0; k < ng; ++k) {
+      const double hv[2] = {m.mean[0], 1.0 / g[k]};
+      CUDA_TRY(c, cudaMemcpyAsync(w.small, hv, sizeof(hv), cudaMemcpyHostToDevice, c->stream));
+      CUDA_TRY(c, kde::launch_scale64(x, n, w.small, w.small + 1, y, c->stream));
+      CUDA_TRY(c, cudaMemsetAsync(w.limbs, 0, kde::kLimbs * sizeof(long long), c->stream));
+      if (allreduce) {
+        TRY(psi64_pass(c, r, y, n, S, w.limbs));
+      } else {                         // one shard, no collective
+        int64_t tb, te;
+        shard_range(n_tiles(n, kde::kPsi64Tile), shard_rank, shard_world, &tb, &te);
+        CUDA_TRY(c, kde::launch_psi64(r, y, n, tb, te, S, w.limbs, c->sm_count, c->stream));
+      }
+      long long hl[kde::kLimbs];
+      CUDA_TRY(c, cudaMemcpyAsync(hl, w.limbs, sizeof(hl), cudaMemcpyDeviceToHost, c->stream));
+      CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+      out.push_back(limbs_to_fixed(hl, S));
+    }
+    return KDE_OK;
+  }
+  for (int k = 0; k < ng; ++k) {
+    std::vector<double> W = {1.0 / g[k]};
+    TRY(gpu_prep(c, x, n, 1, W, m.mean, ld, w, 3.0e4));
+    SumLaunch L;
+    L.kind = psi_kind(r); L.r = r; L.nb = 1; L.out_offset = 0; L.n_out = 1;
+    psi_coeffs(r, L.psi);
+    std::vector<kde_fixed> o;
+    TRY(run_sums(c, 1, n, ld, T, S, w, {L}, 1, shard_rank, shard_world, allreduce, o));
+    out.push_back(o[0]);
+  }
+  return KDE_OK;
+}
+
+double psi_finalize(int r, int64_t n, double g, double S) {
+  const double s2p = std::sqrt(2.0 * kPi);
+  const double nn = (double)n;
+  return (2.0 * S / s2p + nn * he_at_zero(r) / s2p) / (nn * nn * std::pow(g, r + 1));
+}
+
+// ------------------------------------------------------------------ LSCV_h
+
+kde_status lscv_h_prepare(kde_ctx* c, const Moments& m, int d, LscvhPrep& p) {
+  if (!cholesky(m.cov, d, p.Lc)) return fail(c, KDE_E_SINGULAR_COV, "covariance matrix is not positive definite");
+  p.det = 1.0;
+  for (int i = 0; i < d; ++i) p.det *= p.Lc[i * d + i] * p.Lc[i * d + i];
+  if (!(p.det > 0.0) || !std::isfinite(p.det)) return fail(c, KDE_E_SINGULAR_COV, "det(Sigma) <= 0");
+  return KDE_OK;
+}
+
+kde_status lscv_h_raw(kde_ctx* c, const double* X, int64_t n, int d, const double* h, int nh,
+                      const Moments& m, const LscvhPrep& pp, int shard_rank, int shard_world,
+                      bool allreduce, std::vector<kde_fixed>& out) {
+  const int T = kde::tile_for(Kind::LscvScalar, d, n);
+  const int nb = kde::cand_per_launch(Kind::LscvScalar, d);
+  const int64_t ld = (n + T - 1) / T * T;
+  const int nbatch = (nh + nb - 1) / nb;
+  const int n_out = 2 * nbatch * nb;
+  Ws w;
+  TRY(get_ws(c, ld, d, n_out, &w));
+  // W = sqrt(log2 e / 4) L^-1  =>  |W v|^2 = (log2 e / 4) v^T Sigma^-1 v
+  std::vector<double> W = tri_lower_inverse(pp.Lc, d);
+  for (double& v : W) v *= std::sqrt(kLog2e / 4.0);
+  TRY(gpu_prep(c, X, n, d, W, m.mean, ld, w));
+  std::vector<SumLaunch> Ls;
+  for (int b = 0; b < nbatch; ++b) {
+    SumLaunch L;
+    L.kind = Kind::LscvScalar; L.nb = nb; L.out_offset = 2 * b * nb; L.n_out = 2 * nb;
+    for (int j = 0; j < kde::kMaxCand; ++j) {
+      int idx = std::min(b * nb + j, nh - 1);   // pad with a valid candidate
+      L.ls.kappa[j] = (float)(-1.0 / (h[idx] * h[idx]));
+    }
+    Ls.push_back(L);
+  }
+  std::vector<kde_fixed> o;
+  TRY(run_sums(c, d, n, ld, T, scale_exp_for(1.0, n), w, Ls, n_out, shard_rank, shard_world, allreduce, o));
+  out.assign(o.begin(), o.begin() + 2 * nh);
+  return KDE_OK;
+}
+
+double lscv_h_finalize(int64_t n, int d, double det, double h, double S1, double S2) {
+  const double nn = (double)n;
+  const double c4 = std::pow(4.0 * kPi, -0.5 * d) / std::sqrt(det);
+  const double c2 = std::pow(2.0 * kPi, -0.5 * d) / std::sqrt(det);
+  return std::pow(h, -d) * (2.0 * (c4 * S1 - 2.0 * c2 * S2) / (nn * nn) + c4 / nn);
+}
+
+// ------------------------------------------------------------------ LSCV_H
+
+HCand h_candidate(const double* vh, int d) {
+  HCand hc;
+  std::vector<double> H = unvech(vh, d), L;
+  if (!cholesky(H, d, L)) return hc;
+  hc.pd = true;
+  hc.det = 1.0;
+  for (int i = 0; i < d; ++i) hc.det *= L[i * d + i] * L[i * d + i];
+  hc.L = std::move(L);
+  return hc;
+}
+
+// Raw LSCV_H sums for PD candidates `cands` (all must be PD).  Each candidate gets its own
+// whitened fp32 copy of the data, x'_c = sqrt(log2 e / 4) L_c^-1 (x - mean) with H_c = L_c L_c^T,
+// so that v^T H_c^-1 v = (4 / log2 e) |x'_ci - x'_cj|^2: the pair kernel then needs no quadratic
+// form (2d + 2 FP32 ops per eval instead of d(d+1)/2 + 2 per candidate plus the monomials), and
+// the sum of squares does not lose accuracy with cond(H).  Candidates are
+// independent work units, so a candidate's sums are bit-identical alone or inside any batch.
+kde_status lscv_H_raw(kde_ctx* c, const double* X, int64_t n, int d, const std::vector<HCand>& cands,
+                      const Moments& m, int shard_rank, int shard_world, bool allreduce,
+                      std::vector<kde_fixed>& out) {
+  const int T = kde::tile_for(Kind::LscvMatrix, d, n);
+  const int64_t ld = (n + T - 1) / T * T;
+  const int64_t set_floats = (int64_t)d * ld;
+  const int nc = (int)cands.size();
+  // sets per launch: up to 256 candidates within ~1 GiB of prepared data
+  const int per_launch = (int)std::max<int64_t>(1, std::min<int64_t>(256, (1LL << 28) / set_floats));
+  Ws w;
+  TRY(get_ws(c, ld, d, 2 * std::min(nc, per_launch), &w));
+  out.clear();
+  for (int b0 = 0; b0 < nc; b0 += per_launch) {
+    const int cnt = std::min(per_launch, nc - b0);
+    TRY(grow(c, &c->white_ws, &c->white_bytes, (size_t)cnt * set_floats * sizeof(float)));
+    float* Yw = static_cast<float*>(c->white_ws);
+    // prep flags and this launch's limbs are one contiguous span of the workspace (get_ws): one memset
+    const size_t span = (size_t)(reinterpret_cast<char*>(w.limbs + (size_t)2 * cnt * kde::kLimbs) -
+                                 reinterpret_cast<char*>(w.flag()));
+    CUDA_TRY(c, cudaMemsetAsync(w.flag(), 0, span, c->stream));
+    for (int j = 0; j < cnt; ++j) {
+      std::vector<double> W = tri_lower_inverse(cands[b0 + j].L, d);
+      for (double& v : W) v *= std::sqrt(kLog2e / 4.0);
+      TRY(gpu_prep_into(c, X, n, d, W, m.mean, ld, w, Yw + (size_t)j * set_floats));
+    }
+    SumLaunch L;
+    L.kind = Kind::LscvMatrix; L.nb = 1; L.out_offset = 0; L.n_out = 2 * cnt;
+    L.X = Yw; L.n_sets = cnt; L.set_stride = set_floats;
+    std::vector<kde_fixed> o;
+    TRY(run_sums(c, d, n, ld, T, scale_exp_for(1.0, n), w, {L}, 2 * cnt, shard_rank, shard_world, allreduce, o,
+                 /*limbs_zeroed=*/true));
+    out.insert(out.end(), o.begin(), o.end());
+  }
+  return KDE_OK;
+}
+
+double lscv_H_finalize(int64_t n, int d, double det, double S1, double S2) {
+  const double nn = (double)n;
+  const double c4 = std::pow(4.0 * kPi, -0.5 * d) / std::sqrt(det);
+  const double c2 = std::pow(2.0 * kPi, -0.5 * d) / std::sqrt(det);
+  return 2.0 * (c4 * S1 - 2.0 * c2 * S2) / (nn * nn) + c4 / nn;
+}
+
+// Evaluate g(H) for a list of vech vectors (non-PD -> penalty); one GPU batch for all PD ones.
+kde_status lscv_H_eval(kde_ctx* c, const double* X, int64_t n, int d, const Moments& m,
+                       const std::vector<std::vector<double>>& vs, double penalty,
+                       std::vector<double>& g, int* evals) {
+  std::vector<HCand> pdc;
+  std::vector<int> idx;
+  g.assign(vs.size(), penalty);
+  for (size_t k = 0; k < vs.size(); ++k) {
+    HCand hc = h_candidate(vs[k].data(), d);
+    if (hc.pd) { pdc.push_back(std::move(hc)); idx.push_back((int)k); }
+  }
+  if (pdc.empty()) return KDE_OK;
+  std::vector<kde_fixed> o;
+  TRY(lscv_H_raw(c, X, n, d, pdc, m, c->rank, c->world, true, o));
+  for (size_t j = 0; j < pdc.size(); ++j)
+    g[idx[j]] = lscv_H_finalize(n, d, pdc[j].det, fixed_value(o[2 * j]), fixed_value(o[2 * j + 1]));
+  if (evals) *evals += (int)pdc.size();
+  return KDE_OK;
+}
+
+}  // namespace host
+}  // namespace kde
+
+extern "C" {
+
+kde_status kde_psi_r(kde_ctx* c, const double* x, int64_t n, int32_t r, const double* g, int32_t ng, double* psi) {
+  TRY(check_ctx(c));
+  prof_reset(c);
+  TRY(validate_X(c, x, n, 1, 1));
+  if (!(r == 4 || r == 6 || r == 8)) return fail(c, KDE_E_INVALID, "r=%d not in {4,6,8}", r);
+  if (!g || !psi || ng < 1) return fail(c, KDE_E_INVALID, "null candidate/output array");
+  for (int k = 0; k < ng; ++k)
+    if (!(g[k] > 0.0) || !std::isfinite(g[k])) return fail(c, KDE_E_NONPOSITIVE_BW, "g[%d] <= 0", k);
+  Ws w;
+  TRY(get_ws(c, (n + 2047) / 2048 * 2048, 1, 2, &w));
+  Moments m;
+  if (n >= 2) {
+    TRY(gpu_moments(c, x, n, 1, w, m));
+  } else {
+    m.mean = {0.0};
+  }
+  std::vector<kde_fixed> o;
+  TRY(psi_raw(c, x, n, r, g, ng, m, c->rank, c->world, true, o));
+  TRY(prof_collect(c));
+  for (int k = 0; k < ng; ++k) psi[k] = psi_finalize(r, n, g[k], fixed_value(o[k]));
+  return KDE_OK;
+}
+
+// One Psi_r pair pass of the device-resident PLUGIN chain: kernel over this rank's tiles into
+// `limbs`, then (world > 1) the all-reduce of the 3 limbs, all enqueued on the context stream.
+static kde_status plugin_pass(kde_ctx* c, int r, int64_t n, int64_t ld, int T, int S, Ws& w,
+                              unsigned long long* limbs, int64_t tb, int64_t te, double pairs) {
+  Range rr("kde.pair_pass");
+  kde::LaunchCfg cfg;
+  cfg.X = w.Y; cfg.n = n; cfg.ld = ld; cfg.tile_begin = tb; cfg.tile_end = te; cfg.tile = T;
+  cfg.scale_exp = S; cfg.limbs = limbs; cfg.n_out = 1; cfg.stream = c->stream; cfg.sm_count = c->sm_count;
+  cfg.clamp = w.flag() + 1;
+  kde::PsiParams p;
+  psi_coeffs(r, p);
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  // external event records: inside a graph capture they become timing event nodes
+  const unsigned rec = (c->cap_stream && c->stream == c->cap_stream) ? cudaEventRecordExternal : cudaEventRecordDefault;
+  if (c->profiling) { e0 = next_event(c); e1 = next_event(c); CUDA_TRY(c, cudaEventRecordWithFlags(e0, c->stream, rec)); }
+  cudaError_t err = kde::launch_psi(r, cfg, p);
+  if (err != cudaSuccess) return fail(c, KDE_E_CUDA, "pair kernel launch: %s", cudaGetErrorString(err));
+  if (tb < te) c->prof_all += 1;
+  if (c->profiling) {
+    CUDA_TRY(c, cudaEventRecordWithFlags(e1, c->stream, rec));
+    c->prof_launches++;
+    c->prof_evals += pairs;
+  }
+  TRY(allreduce_limbs(c, limbs, kde::kLimbs));
+  return KDE_OK;
+}
+
+// PLUGIN (Sec. 4.4.1): moments, sort, prep and the two pair passes, with the scalar
+// steps 1-8 computed by single-thread kernels on the device between them, so the whole chain is
+// enqueued without a host round trip and the call synchronises once.  The steps' formulas are those
+// of the host reading (Z1, Z10, Z11); failures are recorded on the device and reported in order.
+// Enqueue the whole chain on c->stream (no allocation, no synchronisation: capturable).
+static kde_status plugin_enqueue(kde_ctx* c, const double* x, int64_t n, int T, int64_t ld, Ws& w) {
+  kde::PluginDev dv(w.small);
+  const int nblk = kde::moments_blocks(n);
+  cudaStream_t st = c->stream;
+  // flags (2 x u64), trace (8) and status (1) start at zero
+  CUDA_TRY(c, cudaMemsetAsync(w.flag(), 0, (kde::kSmallDoubles - 408) * sizeof(double), st));
+  {
+    Range r("kde.moments");
+    CUDA_TRY(c, kde::launch_moments1(x, n, 1, w.part, nblk, st));
+    CUDA_TRY(c, kde::launch_reduce_parts(w.part, nblk, 1, dv.sums, st));
+    CUDA_TRY(c, kde::launch_plugin_chain(0, n, w.small, nullptr, 0, st));             // mean
+    CUDA_TRY(c, kde::launch_moments2(x, n, 1, dv.mean, w.part, nblk, st));
+    CUDA_TRY(c, kde::launch_reduce_parts(w.part, nblk, 1, dv.sums, st));
+    CUDA_TRY(c, kde::launch_plugin_chain(1, n, w.small, nullptr, 0, st));             // steps 1-4
+    c->prof_all += 6;
+  }
+  const double* xs = nullptr;                                                          // sorted once (§3)
+  TRY(gpu_sorted(c, x, n, &xs));
+  int64_t tb, te;
+  shard_range(n_tiles(n, T), c->rank, c->world, &tb, &te);
+  const double pairs = c->profiling ? pairs_in_range(n, T, tb, te) : 0.0;
+  const int S6 = scale_exp_for(2.0 * 15.0, n), S4 = scale_exp_for(2.0 * 3.0, n);
+  CUDA_TRY(c, cudaMemsetAsync(w.limbs, 0, 2 * kde::kLimbs * sizeof(long long), st));
+  if ((c->psi_mode == 1)) {                                                                       // fp64 terms
+    double* y = static_cast<double*>(c->y64);
+    CUDA_TRY(c, kde::launch_scale64(xs, n, dv.mean, dv.W, y, st));                     // x/g1
+    TRY(psi64_pass(c, 6, y, n, S6, w.limbs));                                          // step 5
+    CUDA_TRY(c, kde::launch_plugin_chain(2, n, w.small, w.limbs, S6, st));             // Psi6, g2
+    CUDA_TRY(c, kde::launch_scale64(xs, n, dv.mean, dv.W, y, st));                     // x/g2
+    TRY(psi64_pass(c, 4, y, n, S4, w.limbs + kde::kLimbs));                            // step 7
+  } else {
+    CUDA_TRY(c, kde::launch_prep(xs, n, 1, dv.W, dv.mean, w.Y, ld, st, 0.f, w.flag(), 3.0e4));   // x/g1
+    TRY(plugin_pass(c, 6, n, ld, T, S6, w, w.limbs, tb, te, pairs));                   // step 5
+    CUDA_TRY(c, kde::launch_plugin_chain(2, n, w.small, w.limbs, S6, st));             // Psi6, g2
+    CUDA_TRY(c, kde::launch_prep(xs, n, 1, dv.W, dv.mean, w.Y, ld, st, 0.f, w.flag(), 3.0e4));   // x/g2
+    TRY(plugin_pass(c, 4, n, ld, T, S4, w, w.limbs + kde::kLimbs, tb, te, pairs));     // step 7
+  }
+  CUDA_TRY(c, kde::launch_plugin_chain(3, n, w.small, w.limbs + kde::kLimbs, S4, st)); // Psi4, h
+  c->prof_all += 4;
+  CUDA_TRY(c, cudaMemcpyAsync(c->h_limbs, w.flag(), (kde::kSmallDoubles - 408) * sizeof(double),
+                              cudaMemcpyDeviceToHost, st));
+  return KDE_OK;
+}
+
+// PLUGIN (Sec. 4.4.1): moments, sort, prep and the two pair passes, with the scalar
+// steps 1-8 computed by single-thread kernels on the device between them, so the whole chain is
+// enqueued without a host round trip and the call synchronises once.  The chain is captured once
+// as a CUDA graph and replayed while its inputs (pointers, n, mode) are unchanged.  The steps'
+// formulas are those of the host reading (Z1, Z10, Z11); failures are recorded on the device and
+// reported in order.
+static kde_status plugin_impl(kde_ctx* c, const double* x, int64_t n, kde_plugin_trace* tr) {
+  const int T = kde::tile_for(Kind::Psi6, 1, n);
+  const int64_t ld = (n + T - 1) / T * T;
+  Ws w;
+  TRY(get_ws(c, ld, 1, 2, &w));                   // everything the chain touches exists before
+  TRY(ensure_sort_ws(c, n));                      // a capture starts
+  if ((c->psi_mode == 1)) TRY(grow(c, &c->y64, &c->y64_bytes, (size_t)n * sizeof(double)));
+  const size_t cnt = kde::kSmallDoubles - 408;    // flags, trace, status
+  if (c->h_limbs_cap < cnt) {
+    if (c->h_limbs) cudaFreeHost(c->h_limbs);
+    c->h_limbs = nullptr;
+    CUDA_TRY(c, cudaMallocHost(&c->h_limbs, cnt * sizeof(long long)));
+    c->h_limbs_cap = cnt;
+  }
+  for (int r : {6, 4}) {                          // kernel attributes: not settable while capturing
+    kde::LaunchCfg cfg;
+    cfg.n = n; cfg.tile = T; cfg.sm_count = c->sm_count;
+    CUDA_TRY(c, kde::prepare_psi(r, cfg));
+  }
+  cudaStream_t st = c->stream;
+  const std::vector<uintptr_t> key = {(uintptr_t)x, (uintptr_t)n, (uintptr_t)w.Y, (uintptr_t)c->sort_ws,
+                                      (uintptr_t)c->h_limbs, (uintptr_t)c->profiling, (uintptr_t)c->comm,
+                                      (uintptr_t)(c->psi_mode == 1), (uintptr_t)c->y64};
+  // The first call with a given key runs directly (and does any lazy module loading and library
+  // setup outside a capture); a second call with the same key captures, later ones replay.
+  // (single-GPU contexts only: with a communicator the all-reduces stay plain stream operations)
+  if (!c->graphs || c->comm || c->world > 1 || (key != c->plug_seen && !(c->plug_exec && key == c->plug_key))) {
+    TRY(plugin_enqueue(c, x, n, T, ld, w));
+    c->plug_seen = key;
+  } else {
+    if (!(c->plug_exec && key == c->plug_key)) {
+      Range r("kde.capture");
+      if (!c->cap_stream) CUDA_TRY(c, cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+      if (c->plug_exec) { cudaGraphExecDestroy(c->plug_exec); c->plug_exec = nullptr; }
+      CUDA_TRY(c, cudaStreamSynchronize(st));
+      cudaGetLastError();
+      CUDA_TRY(c, cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeRelaxed));
+      c->stream = c->cap_stream;
+      const int32_t l0 = c->prof_launches, a0 = c->prof_all;
+      const double e0 = c->prof_evals;
+      const kde_status es = plugin_enqueue(c, x, n, T, ld, w);
+      c->stream = st;
+      cudaGraph_t g = nullptr;
+      const cudaError_t ce = cudaStreamEndCapture(c->cap_stream, &g);
+      if (es != KDE_OK) { if (g) cudaGraphDestroy(g); return es; }
+      if (ce != cudaSuccess) return fail(c, KDE_E_CUDA, "graph capture: %s", cudaGetErrorString(ce));
+      const cudaError_t ie = cudaGraphInstantiate(&c->plug_exec, g, 0);
+      cudaGraphDestroy(g);
+      if (ie != cudaSuccess) { c->plug_exec = nullptr; return fail(c, KDE_E_CUDA, "graph instantiate: %s", cudaGetErrorString(ie)); }
+      c->plug_key = key;
+      c->plug_prof_launches = c->prof_launches - l0;
+      c->plug_prof_all = c->prof_all - a0;
+      c->plug_prof_evals = c->prof_evals - e0;
+      c->plug_ev_used = c->ev_used;
+    } else {
+      c->prof_launches += c->plug_prof_launches;
+      c->prof_all += c->plug_prof_all;
+      c->prof_evals += c->plug_prof_evals;
+      c->ev_used = c->plug_ev_used;   // the graph records the same pool events
+    }
+    CUDA_TRY(c, cudaGraphLaunch(c->plug_exec, st));
+  }
+  CUDA_TRY(c, cudaStreamSynchronize(st));
+  const unsigned long long* flags = reinterpret_cast<const unsigned long long*>(c->h_limbs);
+  double res[9];
+  std::memcpy(res, c->h_limbs + 2, sizeof(res));
+  const int status = (int)res[8];
+  if (status == KDE_E_INVALID) return fail(c, KDE_E_INVALID, "non-finite sample values");
+  if (status == KDE_E_DEGENERATE) return fail(c, KDE_E_DEGENERATE, "variance estimate <= 0");
+  if (flags[0]) return fail(c, KDE_E_INVALID, "scaled sample differences exceed 1e18 (outliers vs. bandwidth)");
+  if (status == KDE_E_NUMERIC)
+    return fail(c, KDE_E_NUMERIC, !(res[4] < 0.0) ? "Psi6-hat >= 0" : "Psi4-hat <= 0");
+  kde_plugin_trace t;
+  t.V_hat = res[0]; t.sigma_hat = res[1]; t.psi8_ns = res[2]; t.g1 = res[3];
+  t.psi6 = res[4]; t.g2 = res[5]; t.psi4 = res[6]; t.h = res[7];
+  *tr = t;
+  return KDE_OK;
+}
+
+kde_status kde_plugin_h(kde_ctx* c, const double* x, int64_t n, double* h, kde_plugin_trace* tr) {
+  TRY(check_ctx(c));
+  prof_reset(c);
+  TRY(validate_X(c, x, n, 1, 2));
+  if (!h) return fail(c, KDE_E_INVALID, "null output");
+  kde_plugin_trace t;
+  TRY(plugin_impl(c, x, n, &t));
+  TRY(prof_collect(c));
+  *h = t.h;
+  if (tr) *tr = t;
+  return KDE_OK;
+}
+
+static kde_status lscv_h_scores_impl(kde_ctx* c, const double* X, int64_t n, int d, const double* h,
+                                     int nh, double* g) {
+  Ws w;
+  TRY(get_ws(c, (n + 2047) / 2048 * 2048, d, 2, &w));
+  Moments m;
+  TRY(gpu_moments(c, X, n, d, w, m));
+  LscvhPrep pp;
+  TRY(lscv_h_prepare(c, m, d, pp));
+  std::vector<kde_fixed> o;
+  TRY(lscv_h_raw(c, X, n, d, h, nh, m, pp, c->rank, c->world, true, o));
+  for (int k = 0; k < nh; ++k)
+    g[k] = lscv_h_finalize(n, d, pp.det, h[k], fixed_value(o[2 * k]), fixed_value(o[2 * k + 1]));
+  return KDE_OK;
+}
+
+kde_status kde_lscv_h_scores(kde_ctx* c, const double* X, int64_t n, int32_t d, const double* h,
+                             int32_t nh, double* g) {
+  TRY(check_ctx(c));
+  prof_reset(c);
+  TRY(validate_X(c, X, n, d, 2));
+  if (!h || !g || nh < 1) return fail(c, KDE_E_INVALID, "null candidate/output array");
+  for (int k = 0; k < nh; ++k)
+    if (!(h[k] > 0.0) || !std::isfinite(h[k])) return fail(c, KDE_E_NONPOSITIVE_BW, "h[%d] <= 0", k);
+  std::vector<double> tmp(nh);
+  TRY(lscv_h_scores_impl(c, X, n, d, h, nh, tmp.data()));
+  TRY(prof_collect(c));
+  std::copy(tmp.begin(), tmp.end(), g);
+  return KDE_OK;
+}
+
+kde_status kde_lscv_H_scores(kde_ctx* c, const double* X, int64_t n, int32_t d, const double* vh,
+                             int32_t nH, double penalty, double* g) {
+  TRY(check_ctx(c));
+  prof_reset(c);
+  TRY(validate_X(c, X, n, d, 2));
+  if (!vh || !g || nH < 1) return fail(c, KDE_E_INVALID, "null candidate/output array");
+  if (std::isnan(penalty)) penalty = 1e300;
+  const int P = d * (d + 1) / 2;
+  Ws w;
+  TRY(get_ws(c, (n + 2047) / 2048 * 2048, d, 2, &w));
+  Moments m;
+  TRY(gpu_moments(c, X, n, d, w, m));
+  std::vector<std::vector<double>> vs;
+  for (int k = 0; k < nH; ++k) vs.emplace_back(vh + (size_t)k * P, vh + (size_t)(k + 1) * P);
+  std::vector<double> out;
+  TRY(lscv_H_eval(c, X, n, d, m, vs, penalty, out, nullptr));
+  TRY(prof_collect(c));
+  std::copy(out.begin(), out.end(), g);
+  return KDE_OK;
+}
+
+kde_status kde_raw_sums(kde_ctx* c, kde_sum_kind kind, const double* X, int64_t n, int32_t d,
+                        const double* cand, int32_t nc, int32_t srank, int32_t sworld, kde_fixed* out) {
+  TRY(check_ctx(c));
+  prof_reset(c);
+  TRY(validate_X(c, X, n, d, 1));
+  if (!cand || !out || nc < 1) return fail(c, KDE_E_INVALID, "null candidate/output array");
+  bool allreduce = sworld == 0;
+  if (sworld == 0) { srank = c->rank; sworld = c->world; }
+  if (srank < 0 || srank >= sworld) return fail(c, KDE_E_INVALID, "bad shard");
+  Ws w;
+  TRY(get_ws(c, (n + 2047) / 2048 * 2048, d, 2, &w));
+  Moments m;
+  if (n >= 2) {
+    TRY(gpu_moments(c, X, n, d, w, m));
+  } else {
+    m.mean.assign(d, 0.0);
+    m.cov.assign((size_t)d * d, 0.0);
+  }
+  std::vector<kde_fixed> o;
+  if (kind == KDE_SUM_PSI4 || kind == KDE_SUM_PSI6 || kind == KDE_SUM_PSI8) {
+    if (d != 1) return fail(c, KDE_E_NOT_UNIVARIATE, "Psi sums need d = 1");
+    for (int k = 0; k < nc; ++k)
+      if (!(cand[k] > 0.0)) return fail(c, KDE_E_NONPOSITIVE_BW, "g <= 0");
+    TRY(psi_raw(c, X, n, (int)kind, cand, nc, m, srank, sworld, allreduce, o));
+  } else if (kind == KDE_SUM_LSCV_h) {
+    if (n < 2) return fail(c, KDE_E_INSUFFICIENT_SAMPLES, "n < 2");
+    for (int k = 0; k < nc; ++k)
+      if (!(cand[k] > 0.0)) return fail(c, KDE_E_NONPOSITIVE_BW, "h <= 0");
+    LscvhPrep pp;
+    TRY(lscv_h_prepare(c, m, d, pp));
+    TRY(lscv_h_raw(c, X, n, d, cand, nc, m, pp, srank, sworld, allreduce, o));
+  } else if (kind == KDE_SUM_LSCV_H) {
+    const int P = d * (d + 1) / 2;
+    std::vector<HCand> hc;
+    for (int k = 0; k < nc; ++k) {
+      hc.push_back(h_candidate(cand + (size_t)k * P, d));
+      if (!hc.back().pd) return fail(c, KDE_E_INVALID, "candidate %d is not positive definite", k);
+    }
+    if (n < 2) m.mean.assign(d, 0.0);
+    TRY(lscv_H_raw(c, X, n, d, hc, m, srank, sworld, allreduce, o));
+  } else {
+    return fail(c, KDE_E_INVALID, "unknown sum kind");
+  }
+  TRY(prof_collect(c));
+  std::copy(o.begin(), o.end(), out);
+  return KDE_OK;
+}
+
+kde_status kde_select_bandwidth(kde_ctx* c, kde_method method, const double* X, int64_t n, int32_t d,
+                                const kde_select_opts* opts_in, kde_bandwidth* out) {
+  TRY(check_ctx(c));
+  prof_reset(c);
+  if (!out) return fail(c, KDE_E_INVALID, "null output");
+  kde_select_opts o;
+  kde_default_opts(&o);
+  if (opts_in) o = *opts_in;
+  TRY(validate_X(c, X, n, d, 2));
+  kde_bandwidth r;
+  std::memset(&r, 0, sizeof(r));
+  r.method = method;
+  r.d = d;
+  if (method == KDE_PLUGIN) {
+    if (d != 1) return fail(c, KDE_E_NOT_UNIVARIATE, "PLUGIN is univariate (P:196)");
+    TRY(plugin_impl(c, X, n, &r.trace));
+    r.h = r.trace.h;
+    r.evaluations = 2;
+  } else if (method == KDE_LSCV_h) {
+    if (o.n_grid < 2 || !(o.range_factor > 1.0)) return fail(c, KDE_E_INVALID, "bad grid options");
+    // Eq. 25 as written (reading Z3): R(K)/mu2^2 = 1/(2^d pi^{d/2} d^2), R(f'') = d(d+2)/(2^{d+2} pi^{d/2})
+    const double dd = d;
+    const double ratio = 1.0 / (std::pow(2.0, dd) * std::pow(kPi, dd / 2) * dd * dd);
+    const double Rf2 = dd * (dd + 2) / (std::pow(2.0, dd + 2) * std::pow(kPi, dd / 2));
+    const double h0 = std::pow(ratio / (Rf2 * (double)n), 1.0 / (dd + 4));
+    const double lo = h0 / o.range_factor, hi = h0 * o.range_factor;       // Eq. 27
+    std::vector<double> hs(o.n_grid), gs(o.n_grid);
+    for (int k = 0; k < o.n_grid; ++k) hs[k] = lo + k * (hi - lo) / (o.n_grid - 1);
+    TRY(lscv_h_scores_impl(c, X, n, d, hs.data(), o.n_grid, gs.data()));
+    int best = 0;
+    for (int k = 1; k < o.n_grid; ++k)
+      if (gs[k] < gs[best]) best = k;                                    // ties -> smaller h
+    r.h = hs[best];
+    r.objective = gs[best];
+    r.iterations = best;
+    r.evaluations = o.n_grid;
+    // Optional refinement (f4): bracket = the grid neighbours of the argmin; each step scores
+    // 16 equally spaced interior points in one pass and re-brackets around the best known point
+    // (ties -> smaller h).  A batched form of the section search the paper suggests.
+    if (o.refine_steps > 0) {
+      std::vector<std::pair<double, double>> pts;   // (h, g) known inside the bracket, sorted by h
+      pts.push_back({hs[best > 0 ? best - 1 : 0], gs[best > 0 ? best - 1 : 0]});
+      if (best > 0) pts.push_back({hs[best], gs[best]});
+      if (best + 1 < o.n_grid) pts.push_back({hs[best + 1], gs[best + 1]});
+      int steps = 0;
+      while (steps < o.refine_steps) {
+        const double a = pts.front().first, b = pts.back().first;
+        if (!(b - a > o.refine_tol * r.h)) break;
+        std::vector<double> hh(16), gg(16);
+        for (int k = 0; k < 16; ++k) hh[k] = a + (k + 1) * (b - a) / 17.0;
+        TRY(lscv_h_scores_impl(c, X, n, d, hh.data(), 16, gg.data()));
+        r.evaluations += 16;
+        for (int k = 0; k < 16; ++k) pts.push_back({hh[k], gg[k]});
+        std::sort(pts.begin(), pts.end());
+        size_t bi = 0;
+        for (size_t k = 1; k < pts.size(); ++k)
+          if (pts[k].second < pts[bi].second) bi = k;
+        r.h = pts[bi].first;
+        r.objective = pts[bi].second;
+        const size_t lo_i = bi > 0 ? bi - 1 : 0, hi_i = bi + 1 < pts.size() ? bi + 1 : bi;
+        std::vector<std::pair<double, double>> nb(pts.begin() + lo_i, pts.begin() + hi_i + 1);
+        pts.swap(nb);
+        ++steps;
+      }
+      r.stop_reason = steps;
+    }
+  } else if (method == KDE_LSCV_H) {
+    Ws w;
+    TRY(get_ws(c, (n + 2047) / 2048 * 2048, d, 2, &w));
+    Moments m;
+    TRY(gpu_moments(c, X, n, d, w, m));
+    std::vector<double> Lc, root;
+    if (!cholesky(m.cov, d, Lc)) return fail(c, KDE_E_SINGULAR_COV, "covariance not positive definite");
+    if (!spd_sqrt(m.cov, d, root)) return fail(c, KDE_E_SINGULAR_COV, "matrix square root failed");
+    // Eq. 35 as written: H_start = (4/(d+2))^{1/(d+4)} n^{-1/(d+4)} Sigma^{1/2}
+    const double f = std::pow(4.0 / (d + 2), 1.0 / (d + 4)) * std::pow((double)n, -1.0 / (d + 4));
+    for (double& v : root) v *= f;
+    const int P = d * (d + 1) / 2;
+    std::vector<double> x0(P);
+    vech(root, d, x0.data());
+    std::vector<std::vector<double>> sim = {x0};
+    int t = 0;
+    for (int b = 0; b < d; ++b)
+      for (int a = b; a < d; ++a) {
+        const double delta = 0.1 * (a == b ? root[a * d + a] : std::sqrt(root[a * d + a] * root[b * d + b]));
+        std::vector<double> v = x0;
+        v[t] += delta;
+        sim.push_back(v);
+        ++t;
+      }
+    // start k of o.nm_starts: vech(H_start) scaled by 4^-k (the paper's Eq. 35 start first)
+    std::vector<std::vector<std::vector<double>>> sims;
+    const int K = std::max(1, o.nm_starts);
+    for (int k = 0; k < K; ++k) {
+      const double sc = std::pow(4.0, -k);
+      std::vector<std::vector<double>> sk;
+      for (const auto& v : sim) {
+        std::vector<double> w(v);
+        for (double& e : w) e *= sc;
+        sk.push_back(w);
+      }
+      sims.push_back(sk);
+    }
+    NMResult nm;
+    TRY(nelder_mead_multi(c, X, n, d, m, sims, o.max_iter, o.tol_rel, o.penalty, o.speculative != 0, nm, nullptr));
+    if (!(nm.f < o.penalty)) return fail(c, KDE_E_NO_FEASIBLE, "no positive-definite H found");
+    for (int k = 0; k < P; ++k) r.vechH[k] = nm.x[k];
+    r.objective = nm.f;
+    r.iterations = nm.iterations;
+    r.evaluations = nm.evals;
+    r.stop_reason = nm.stop;
+  } else {
+    return fail(c, KDE_E_INVALID, "unknown method");
+  }
+  TRY(prof_collect(c));
+  *out = r;
+  return KDE_OK;
+}
+
+}  // extern "C"

@@ -367,3 +367,22 @@ def test_lscv_H_tile1024_ragged_matches_oracle():
                        timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     assert float(r.stdout.strip().splitlines()[-1]) < RTOL
+
+
+def test_limb_carry_beyond_2_23_commits(ctx):
+    # every tile commit adds up to 2^40 to the lo limb, so past ~2^23 commits per output
+    # an int64 lo limb wraps.  The carry limb (kde_device.cuh add_limbs) keeps the sum exact: at
+    # n = 3.2e6 (LSCV_h, 512-tiles: 19.5M commits per output, all positive) the full sum equals the
+    # exact sum of 4 shards (each < 2^23 commits), value for value.
+    X = datagen.sample_mixture("bimodal", 3_200_000, 21)
+    Xd = dev(X)
+    cand = [0.05]
+    full = ctx.raw_sums(kb.SUM_LSCV_h, Xd, cand)
+    acc = None
+    for r in range(4):
+        part = ctx.raw_sums(kb.SUM_LSCV_h, Xd, cand, shard=(r, 4))
+        acc = part if acc is None else [kb.fixed_add(a, b) for a, b in zip(acc, part)]
+    assert [f.key() for f in acc] == [f.key() for f in full]
+    # and the value is the right order of magnitude (the sum of e over n(n-1)/2 pairs, e <= 1)
+    n = X.shape[1]
+    assert 0 < kb.fixed_value(full[0]) < n * (n - 1) / 2
