@@ -69,6 +69,9 @@ MIXTURES = {
                 [np.array([[4.0 / 9.0]]), np.array([[4.0 / 9.0]])]),
     "skewed": ([0.2, 0.2, 0.6], [np.array([0.0]), np.array([0.5]), np.array([13.0 / 12.0])],
                [np.array([[1.0]]), np.array([[4.0 / 9.0]]), np.array([[25.0 / 81.0]])]),
+    # Marron–Wand #4 kurtotic unimodal: ⅔N(0,1) + ⅓N(0,(1/10)²) (second n=2^20 PLUGIN golden)
+    "kurtotic": ([2.0 / 3.0, 1.0 / 3.0], [np.array([0.0]), np.array([0.0])],
+                 [np.array([[1.0]]), np.array([[0.01]])]),
     "C3": ([0.5, 0.5], [np.array([-1.0, -1.0]), np.array([1.0, 1.0])],
            [4.0 / 9.0 * np.array([[1.0, 0.7], [0.7, 1.0]]),
             4.0 / 9.0 * np.array([[1.0, -0.5], [-0.5, 1.0]])]),

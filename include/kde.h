@@ -75,6 +75,11 @@ typedef struct {
   double refine_tol;     /* LSCV_h: stop refining when the bracket is narrower than tol * h; 1e-9 */
   int32_t nm_starts;     /* LSCV_H: independent Nelder-Mead runs from vech(H_start) * 4^-k,
                             k < nm_starts, evaluated together in one GPU batch per round; 1 */
+  int32_t nm_loop;       /* LSCV_H: 0 = the serial single-start loop runs device-resident on one
+                            GPU (one CUDA graph with a conditional WHILE node: decide, whiten,
+                            pair kernel per round, no host round trip; same decisions as the host
+                            loop); 1 = host loop (one synchronisation per round).  Multi-start,
+                            speculative and multi-rank selections always use the host loop; 0 */
 } kde_select_opts;
 
 typedef struct {
@@ -237,12 +242,21 @@ kde_status kde_shard_tiles(kde_sum_kind kind, int64_t n, int32_t d, int32_t rank
  * evaluations they performed (pairs i<j on this rank x candidates). */
 kde_status kde_last_profile(const kde_ctx *ctx, int32_t *launches, double *pair_ms,
                             double *evals, int32_t *all_launches);
-/* Term precision of the Psi_r sums (kde_psi_r, kde_plugin_h, KDE_SUM_PSI* raw sums): 0 (default)
- * fp32 terms with fp64/exact accumulation, the throughput path (parity ~1e-6 at the PLUGIN
- * bandwidths); 1 = fp64 terms (libdevice exp, fp64 Horner in u^2), ~20x slower, for
- * bandwidths far below the PLUGIN pilots where the sums cancel by more than ~10^4.
- * Results stay deterministic and partition-invariant in either mode. */
+/* Term precision of the Psi_r sums (kde_psi_r, kde_plugin_h, KDE_SUM_PSI* raw sums; Eq. 15/17,
+ * P:227-247):
+ *   0 (default) automatic: every pass runs with fp32 terms (fp64/exact accumulation, tile-local
+ *     centring) and also yields a cancellation estimate kappa = 2A/|2S + n He_r(0)| (A ~ sum|t|);
+ *     a pass with kappa > 1e4 is re-run with fp64 terms (for kde_plugin_h the decision is taken on
+ *     the device, inside the chain), so Psi-hat stays within 1e-5 for any g > 0.
+ *     Shard-only raw sums (shard_world > 0) are never re-run (the decision needs the full sum).
+ *   1 = fp64 terms for every pass (libdevice exp, fp64 Horner in u^2), the exact-parity mode.
+ *  -1 = fp32 terms only (diagnostics).
+ * Results stay deterministic and partition-invariant in every mode. */
 kde_status kde_set_precision(kde_ctx *ctx, int32_t fp64_terms);
+/* Number of Psi passes of the last call that the automatic precision re-ran with fp64 terms, and
+ * the largest cancellation estimate kappa of its fp32-term Psi passes (diagnostics). */
+int32_t kde_last_fp64_passes(const kde_ctx *ctx);
+double kde_last_psi_kappa(const kde_ctx *ctx);
 /* Turn per-launch event timing on/off (default off; adds an event pair per launch). */
 kde_status kde_set_profiling(kde_ctx *ctx, int32_t on);
 

@@ -35,7 +35,8 @@ EXPORTS = ["kde_create", "kde_destroy", "kde_last_error", "kde_nccl_unique_id",
            "kde_plugin_h", "kde_lscv_h_scores", "kde_lscv_H_scores", "kde_select_bandwidth",
            "kde_raw_sums", "kde_fixed_value", "kde_fixed_add", "kde_tile_coords",
            "kde_last_profile", "kde_set_profiling", "kde_shard_tiles", "kde_evaluate", "kde_aqp_1d",
-           "kde_lscv_h_scores_materialized", "kde_last_aux_ms", "kde_set_host_allreduce", "kde_set_precision"]
+           "kde_lscv_h_scores_materialized", "kde_last_aux_ms", "kde_set_host_allreduce", "kde_set_precision",
+           "kde_last_fp64_passes", "kde_last_psi_kappa"]
 
 
 class KDEError(RuntimeError):
@@ -58,7 +59,7 @@ class SelectOpts(ctypes.Structure):
                 ("max_iter", ctypes.c_int32), ("tol_rel", ctypes.c_double),
                 ("penalty", ctypes.c_double), ("speculative", ctypes.c_int32),
                 ("refine_steps", ctypes.c_int32), ("refine_tol", ctypes.c_double),
-                ("nm_starts", ctypes.c_int32)]
+                ("nm_starts", ctypes.c_int32), ("nm_loop", ctypes.c_int32)]
 
 
 class Bandwidth(ctypes.Structure):
@@ -125,6 +126,10 @@ def lib():
     L.kde_last_aux_ms.restype = f64
     L.kde_set_precision.argtypes = [vp, i32]
     L.kde_set_precision.restype = ctypes.c_int
+    L.kde_last_fp64_passes.argtypes = [vp]
+    L.kde_last_fp64_passes.restype = i32
+    L.kde_last_psi_kappa.argtypes = [vp]
+    L.kde_last_psi_kappa.restype = f64
     L.kde_set_host_allreduce.argtypes = [vp, HOST_ALLREDUCE_FN, vp]
     L.kde_set_host_allreduce.restype = ctypes.c_int
     for f in ("kde_create", "kde_nccl_unique_id", "kde_set_workspace", "kde_psi_r", "kde_plugin_h",
@@ -305,9 +310,20 @@ class Context:
         self._check(lib().kde_set_workspace(self._h, ctypes.c_void_p(buf.data_ptr()),
                                             buf.numel() * buf.element_size()))
 
-    def set_precision(self, fp64_terms: bool):
-        """fp64 terms for the Psi_r sums (slow, exact-parity mode) or the fp32-term default."""
-        self._check(lib().kde_set_precision(self._h, 1 if fp64_terms else 0))
+    def set_precision(self, fp64_terms):
+        """Psi_r term precision (kde_set_precision): True / 1 = fp64 terms (exact-parity mode),
+        False / 0 = automatic (fp32 terms, fp64 re-run of a pass that cancels too much),
+        -1 = fp32 terms only (diagnostics)."""
+        mode = int(fp64_terms) if not isinstance(fp64_terms, bool) else (1 if fp64_terms else 0)
+        self._check(lib().kde_set_precision(self._h, mode))
+
+    def last_fp64_passes(self) -> int:
+        """Psi passes of the last call re-run with fp64 terms by the automatic precision."""
+        return int(lib().kde_last_fp64_passes(self._h))
+
+    def last_psi_kappa(self) -> float:
+        """Largest cancellation estimate 2A/|2S + n He_r(0)| of the last call's fp32 Psi passes."""
+        return float(lib().kde_last_psi_kappa(self._h))
 
     def set_profiling(self, on: bool):
         self._check(lib().kde_set_profiling(self._h, 1 if on else 0))

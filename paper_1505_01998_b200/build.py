@@ -16,8 +16,10 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I" + os.path.join(ROOT, "include")]
 SOURCES = ["kde_psi.cu", "kde_lscv_scalar.cu", "kde_lscv_matrix.cu", "kde_eval.cu", "kde_materialized.cu",
-           "kde_runtime.cpp", "kde_linalg.cpp", "kde_nm.cpp", "kde_selectors.cpp", "kde_extras.cpp"]
-HEADERS = ["kde_internal.h", "kde_host.h", "kde_device.cuh", "kde_pair.cuh", "kde_tiles.cuh", os.path.join("..", "..", "include", "kde.h")]
+           "kde_nm_dev.cu", "kde_runtime.cpp", "kde_linalg.cpp", "kde_nm.cpp", "kde_selectors.cpp", "kde_extras.cpp"]
+# the device Nelder-Mead makes the host loop's decisions only without FMA contraction (kde_nm.cuh)
+EXTRA = {"kde_nm_dev.cu": ["-fmad=false"]}
+HEADERS = ["kde_internal.h", "kde_host.h", "kde_nm.cuh", "kde_device.cuh", "kde_pair.cuh", "kde_tiles.cuh", os.path.join("..", "..", "include", "kde.h")]
 
 
 def _newer(target: str, deps) -> bool:
@@ -35,7 +37,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         obj = os.path.join(CSRC, s + ".o")
         objs.append(obj)
         if force or _newer(obj, [src] + hdrs):
-            cmd = [NVCC] + ARCH + FLAGS + ["-c", src, "-o", obj]
+            cmd = [NVCC] + ARCH + FLAGS + EXTRA.get(s, []) + ["-c", src, "-o", obj]
             if s.endswith(".cu") and verbose:
                 cmd += ["-Xptxas", "-v"]
             cmds.append(cmd)

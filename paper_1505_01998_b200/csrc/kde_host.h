@@ -56,8 +56,11 @@ struct kde_ctx {
   // estimate says fp32 terms cannot carry 1e-5), 1 = always fp64 terms (kde_set_precision),
   // -1 = always fp32 terms (diagnostics).  The fp64 scaled-sample buffer is context-owned.
   int psi_mode = 0;
-  void* y64 = nullptr;
-  size_t y64_bytes = 0;
+  // PLUGIN chain: event-pair index and evals of each gated fp64 re-run (profiling), pairs to leave
+  // out of the pair time (a gated pass that did not run)
+  int gate_pair[2] = {-1, -1};
+  double gate_evals[2] = {0.0, 0.0};
+  std::vector<char> ev_excl;
   // host-staged collective (test transport for world > 1 without NCCL, kde_set_host_allreduce)
   kde_host_allreduce_fn har_fn = nullptr;
   void* har_user = nullptr;
@@ -71,20 +74,22 @@ struct kde_ctx {
   int32_t plug_prof_launches = 0, plug_prof_all = 0;
   double plug_prof_evals = 0.0;
   size_t plug_ev_used = 0;
-  // device-resident Nelder–Mead (kde_nm_dev.cu): state block and its instantiated graph
+  // device-resident Nelder–Mead (kde_nm_dev.cu): state block, its graph, pinned staging
   void* nm_ws = nullptr;
   size_t nm_bytes = 0;
   cudaGraphExec_t nm_exec = nullptr;
   std::vector<uintptr_t> nm_key;
-  bool device_nm = true;
+  void* nm_host = nullptr;
+  size_t nm_host_cap = 0;
   // profiling
   bool profiling = false;
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
   int32_t prof_launches = 0, prof_all = 0;
   double prof_ms = 0.0, prof_evals = 0.0;
-  // sum of per-pass fp64 re-runs taken by the automatic Psi precision (diagnostics)
+  // Psi passes re-run with fp64 terms by the automatic precision during the last call
   int32_t psi_escalations = 0;
+  double psi_kappa_max = 0.0;   // largest cancellation estimate of the last call's fp32 Psi passes
 };
 
 namespace kde {
@@ -181,6 +186,8 @@ struct SumLaunch {
   const float* X = nullptr;         // prepared data if not the workspace's Y (LSCV_H sets)
   const double* Y64 = nullptr;      // Psi: fp64 scaled rows (tile-local centring)
   const float* centres = nullptr;   // Psi: per-column-tile centres
+  unsigned long long* skipped = nullptr;   // Psi: skipped-pair counter
+  double skip_gap = kPsiSkipGap32;         // Psi: exact-zero tile skip threshold
   int n_sets = 1;                   // LSCV_H: candidates (one data set each), n_out per set
   int64_t set_stride = 0;
 };
@@ -195,7 +202,7 @@ kde_status validate_X(kde_ctx* c, const double*& X, int64_t n, int32_t d, int64_
 struct HCand {
   bool pd = false;
   double det = 0.0;
-  std::vector<double> L;      // Cholesky factor of H (row-major lower), fp64
+  std::vector<double> W;      // whitening sqrt(log2 e / 4) L^-1 (row-major), H = L L^T, fp64
 };
 HCand h_candidate(const double* vh, int d);
 double lscv_H_finalize(int64_t n, int d, double det, double S1, double S2);
@@ -218,6 +225,10 @@ struct NMResult {
 kde_status nelder_mead_multi(kde_ctx* c, const double* X, int64_t n, int d, const Moments& m,
                              const std::vector<std::vector<std::vector<double>>>& sims, int max_iter,
                              double tol, double penalty, bool speculative, NMResult& best, int* total_evals);
+// The same serial NM as one CUDA graph with a device-side loop (kde_nm_dev.cu): single GPU, one start.
+kde_status nelder_mead_device(kde_ctx* c, const double* X, int64_t n, int d, const Moments& m,
+                              const std::vector<std::vector<double>>& sim, int max_iter, double tol,
+                              double penalty, NMResult& best);
 
 }  // namespace host
 }  // namespace kde

@@ -39,6 +39,13 @@ struct PsiParams {
 struct LscvScalarParams {
   float kappa[kMaxCand];   // -1/h_c^2 (data pre-scaled by sqrt(log2 e / 4) L^-1)
 };
+// Tiles whose sorted gap min|y_i - y_j| exceeds these contribute exactly 0 and are skipped:
+// fp32 path: MUFU input <= -0.72 s - 16 < -126 (flushed to 0) for s > 152.5; fp64: exp(-s/2)
+// underflows to 0 for s > 1490.4.
+constexpr double kPsiSkipGap32 = 13.0, kPsiSkipGap64 = 40.0;
+// (KDE_DEBUG_PSI_NOSKIP=1 in the environment disables the skip: results are bit-identical.)
+double psi_skip_gap(bool fp64);
+
 struct LaunchCfg {
   const float* X;          // D rows of ld floats (fp32, prepared), device
   int64_t n, ld;           // samples, padded row length (multiple of the tile)
@@ -54,20 +61,37 @@ struct LaunchCfg {
   // X + s * set_stride and writes outputs [s * n_out, (s + 1) * n_out); work unit = (set, tile).
   int n_sets = 1;
   int64_t set_stride = 0;  // floats
+  // Psi (tile-local centring): X holds fp32(y_j - c_l) per column tile l, Y64 the
+  // fp64 scaled sorted samples y (rows are formed as fp32(y_i - c_l) per tile), centres[l] = c_l.
+  const double* Y64 = nullptr;
+  const float* centres = nullptr;
+  unsigned long long* skipped = nullptr;   // Psi: pairs of skipped (exactly zero) tiles, or null
+  double skip_gap = kPsiSkipGap32;         // Psi: skip tiles whose sorted gap exceeds this (inf: never)
+  // Sets whose count is decided on the device (the device-resident Nelder–Mead): the kernel reads
+  // *n_sets_dev (<= n_sets, which sizes the grid).
+  const int* n_sets_dev = nullptr;
 };
 
 // Launchers (kde_psi.cu, kde_lscv_scalar.cu, kde_lscv_matrix.cu).  Return cudaSuccess or the launch error.
 cudaError_t launch_psi(int r, const LaunchCfg& c, const PsiParams& p);
 cudaError_t prepare_psi(int r, const LaunchCfg& c);   // one-time setup of launch_psi's kernel
-// fp64-term Psi mode (kde_set_precision): y = (x - mean[0]) * w[0] in fp64, then 256-tiles of fp64 terms.
+// Psi data prep: sorted x -> y = (x - mean[0]) * w[0] (fp64, ld entries, zero padded), the
+// per-column-tile centres c_l = fp32(y[min(l T + T/2, n-1)]) and Yc = fp32(y - c_l) (tile T).
+cudaError_t launch_psi_prep(const double* x, int64_t n, const double* mean_dev, const double* w_dev, int T,
+                            double* Y64, float* Yc, float* centres, int64_t ld, cudaStream_t s,
+                            unsigned long long* flag, double clamp_thresh);
+// fp64-term Psi pass over 256-tiles of y (Y64 of launch_psi_prep): kde_set_precision(ctx, 1), or the
+// automatic re-run of a pass whose cancellation estimate exceeds what fp32 terms carry.  With a
+// non-null `gate` the kernel returns at once unless *gate != 0 (device-side decision).
 constexpr int kPsi64Tile = 256;
-cudaError_t launch_scale64(const double* x, int64_t n, const double* mean_dev, const double* w_dev, double* y,
-                           cudaStream_t s);
 cudaError_t launch_psi64(int r, const double* y, int64_t n, int64_t tile_begin, int64_t tile_end, int S,
-                         unsigned long long* limbs, int sm_count, cudaStream_t s);
+                         unsigned long long* limbs, int sm_count, cudaStream_t s,
+                         const unsigned long long* gate = nullptr, double skip_gap = kPsiSkipGap64);
+
 cudaError_t launch_lscv_scalar(int d, int nb, const LaunchCfg& c, const LscvScalarParams& p);
 // LSCV_H with per-candidate whitened data (one candidate per set, c.n_sets sets).
 cudaError_t launch_lscv_white(int d, const LaunchCfg& c);
+cudaError_t prepare_lscv_white(int d, const LaunchCfg& c);   // one-time setup (before a graph capture)
 int tile_for(Kind k, int d, int64_t n);       // tile edge the launcher uses
 int cand_per_launch(Kind k, int d);           // B
 
@@ -82,6 +106,11 @@ struct PrepParams {
   double W[kMaxDim * kMaxDim];   // row-major d x d
   double mean[kMaxDim];
 };
+// One prepared data set per PrepParams entry, set s into Y + s * set_stride, for the first
+// *n_sets_dev of max_sets entries (count decided on the device).
+cudaError_t launch_prep_sets(const double* X, int64_t n, int d, const PrepParams* pp_dev, const int* n_sets_dev,
+                             int max_sets, float* Y, int64_t set_stride, int64_t ld, cudaStream_t s,
+                             unsigned long long* flag);
 cudaError_t launch_prep_params(const double* X, int64_t n, int d, const PrepParams& pp, float* Y, int64_t ld,
                                cudaStream_t s, float pad = 0.f, unsigned long long* overflow_flag = nullptr,
                                double clamp_thresh = 0.0);
@@ -92,14 +121,27 @@ cudaError_t launch_prep(const double* X, int64_t n, int d, const double* W_dev,
 
 // Device-resident PLUGIN chain (kde_psi.cu).  Layout of the workspace's `small` block (doubles):
 // mean[16] | W[256] | sums[136] | flags (2 x u64) | trace[8] | status.
+// mean[16] | W[256] | sums[136] | flags (2 x u64) | trace[8] | status | gate (2 x u64: the Psi6 /
+// Psi4 pass needs its fp64-term re-run) | kappa (2: the passes' cancellation estimates) | skipped
+// (u64: pairs in tiles the fp32 kernel skipped as exactly zero, kPluginSkipped).  Limbs of the chain: [Psi6 S, Psi6 A, Psi4 S, Psi4 A,
+// Psi6 S fp64, Psi4 S fp64] (kPluginOuts outputs).
 struct PluginDev {
   double *mean, *W, *sums, *trace, *status;
+  unsigned long long* gate;
   __host__ __device__ explicit PluginDev(double* small)
-      : mean(small), W(small + 16), sums(small + 272), trace(small + 410), status(small + 418) {}
+      : mean(small), W(small + 16), sums(small + 272), trace(small + 410), status(small + 418),
+        gate(reinterpret_cast<unsigned long long*>(small + 419)) {}
 };
+constexpr int kPluginOuts = 6;
+constexpr int kSkippedSlot = 423;   // small + 423: skipped-pair counter (PLUGIN chain and psi_raw)
 constexpr int kSmallDoubles = 424;
 cudaError_t launch_plugin_chain(int stage, int64_t n, double* small, const unsigned long long* limbs, int S,
-                                cudaStream_t s);
+                                cudaStream_t s, int psi_mode = 0);
+// Automatic Psi precision: an fp32-term pass (S = sum t, A ~ sum |t| at 16-column-group level) is
+// re-run with fp64 terms when kappa = 2A / |2S + n He_r(0)| exceeds kPsiKappaMax.
+// Calibrated (profiles/r02_psi_kappa.jsonl): fp32-term error <= ~3e-10 kappa for kappa > 10^3, so
+// 1e4 keeps the fp32 path within ~3e-6; the C4 passes have kappa <= 5.8e3 and stay on fp32 terms.
+constexpr double kPsiKappaMax = 1.0e4;
 
 // KDE evaluation on an m x n rectangle (kde_eval.cu).
 struct EvalLaunch {

@@ -67,6 +67,11 @@ struct Args {
   const unsigned long long* clamp;   // device flag set by the prep kernel (Psi only), or null
   int n_sets;                        // data sets (work unit = (set, tile)), set s at X + s*set_stride
   int64_t set_stride;
+  const double* Y64;                 // Psi: fp64 scaled sorted samples (rows), or null
+  const float* centres;              // Psi: per-column-tile centres c_l
+  unsigned long long* skipped;       // Psi: counter of pairs in skipped tiles, or null
+  const int* n_sets_dev;             // sets: the count in device memory (device-resident loops), or null
+  double skip_gap;                   // Psi: tiles with a larger sorted gap are exactly zero
 };
 
 // ------------------------------------------------------------------ functors
@@ -91,7 +96,7 @@ struct Args {
 // the oracle: 8 shifts 2.7e-6, 16 shifts 5.4e-7, 32 shifts 8.9e-7).
 template <int RORD, int NT_, int CS_ = 1>
 struct FPsi {
-  static constexpr int NT = NT_, D = 1, R = 8, T = NT_ * 8, NOUT = 1, MINB = 768 / NT_;
+  static constexpr int NT = NT_, D = 1, R = 8, T = NT_ * 8, NOUT = 2, MINB = 768 / NT_;
   static constexpr int CS = CS_, CW = T / CS_;                     // column chunks per tile, width
   static constexpr int CH = CS_ > 1 ? CW : (T < 1024 ? T : 1024);  // columns per fp64 flush
   static constexpr int NP = R / 2;   // row pairs (r = 2p, 2p+1) packed into fp32x2 lanes
@@ -100,22 +105,31 @@ struct FPsi {
   // form cancels 40x at s = 0 (2401 - 4116 + 1568 + 252 = 105) and measured 1.3e-5 worst case
   // (tests/diag/fuzz_wide.py, 300 cases) against 1.1e-6 for Horner in s.
   static constexpr float K = RORD == 8 ? 0.f : (float)(RORD - 1);
-  static constexpr bool kClampable = true, kSets = false;
+  static constexpr bool kClampable = true, kSets = false, kCentred = true;
   using Params = PsiParams;
   f2 xr[NP];
-  double acc;
+  double acc, accA;
   int jbase;   // first column of this work unit's chunk (CS > 1)
   int par;     // tile-id parity: second index of the MUFU offset class (16 classes)
 
   // Rows are interleaved: thread t owns rows q*T + 8t + r, r = 0..7.  The data are sorted
-  // (kde_host.cpp), so the 8 row classes r see statistically identical distances; the tile-id
-  // parity p doubles the classes across tiles.
-  __device__ __forceinline__ void load_rows(const float* __restrict__ X, int64_t ld,
-                                            int64_t i0) {
-    const float4* p = reinterpret_cast<const float4*>(X + i0);
-    const float4 u = __ldg(p), v = __ldg(p + 1);
-    xr[0] = pk(u.x, u.y); xr[1] = pk(u.z, u.w); xr[2] = pk(v.x, v.y); xr[3] = pk(v.z, v.w);
+  // (kde_selectors.cpp), so the 8 row classes r see statistically identical distances; the
+  // tile-id parity p doubles the classes across tiles.
+  // Tile-local centring: the columns of tile column l arrive as fp32(y_j - c_l)
+  // and the rows are formed here as fp32(y_i - c_l) from the fp64 y, so a difference carries the
+  // fp32 rounding of |y - c_l| (about |u| plus the tile's span on sorted data) instead of |y|:
+  // for small bandwidths |y| = |x - mean|/g reaches 10^2..10^3 and that input rounding alone
+  // cost 2.3e-5 relative at n = 40 000, g = 0.02 (emulated; measured 2.4e-5 on the GPU).
+  __device__ __forceinline__ void load_rows_c(const double* __restrict__ Y64, int64_t i0, float c) {
+    const double2* p = reinterpret_cast<const double2*>(Y64 + i0);
+    const double cc = (double)c;
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      const double2 u = __ldg(p + q);
+      xr[q] = pk(__double2float_rn(u.x - cc), __double2float_rn(u.y - cc));
+    }
     acc = 0.0;
+    accA = 0.0;
   }
   static __device__ __forceinline__ int64_t row0(int64_t q) { return q * T + 8 * (int64_t)threadIdx.x; }
 
@@ -145,6 +159,7 @@ struct FPsi {
     for (int jc = J0; jc < J1; jc += CH) {
       if (MASK && jc >= jlim) break;
       f2 a[NP], cmp[NP];
+      float aabs = 0.f;
 #pragma unroll
       for (int q = 0; q < NP; ++q) a[q] = cmp[q] = pk(0.f, 0.f);
 #pragma unroll 2   // two 16-column groups per iteration (C4 step 250.1 -> 247.1 ms; x4: 258 ms)
@@ -194,6 +209,10 @@ struct FPsi {
           const f2 z = sub2(s2, a[q]);
           cmp[q] = add2(cmp[q], sub2(grp[q], z));
           a[q] = s2;
+          float g0, g1;                                     // cancellation estimate: sum of
+          upk(grp[q], g0, g1);                              // |16-column group sums| (FADD |.|)
+          aabs = __fadd_rn(aabs, fabsf(g0));
+          aabs = __fadd_rn(aabs, fabsf(g1));
         }
       }
       double s = 0.0;
@@ -206,10 +225,16 @@ struct FPsi {
         s += ((double)a1 + (double)c1_) * p.fac[8 * par + 2 * q + 1];
       }
       acc += s;
+      accA += (double)aabs;
     }
   }
 
-  __device__ __forceinline__ void outputs(double (&v)[NOUT]) const { v[0] = acc; }
+  // v[0] = the tile's sum; v[1] = its cancellation estimate A (sum of |group sums|, scaled by the
+  // middle offset class's factor: an estimate within 2^(+-7/16) of the exact scaling).
+  __device__ __forceinline__ void outputs(double (&v)[NOUT], const Params& p) const {
+    v[0] = acc;
+    v[1] = accA * p.fac[8 * par + 4];
+  }
 };
 
 // LSCV_h (any d): data pre-whitened and scaled, x' = sqrt(log2 e / 4) L^-1 (x - mean) with
@@ -303,7 +328,7 @@ struct FLscvScalar {
     }
   }
 
-  __device__ __forceinline__ void outputs(double (&v)[NOUT]) const {
+  __device__ __forceinline__ void outputs(double (&v)[NOUT], const Params&) const {
 #pragma unroll
     for (int c = 0; c < NB; ++c) {
       float x0, x1, y0, y1;
@@ -328,10 +353,61 @@ __device__ __forceinline__ int64_t row_origin(int64_t q) {
   else return q * F::T + threadIdx.x;
 }
 
+// Functors with tile-local centring (FPsi) read their rows from the fp64 samples; the others from X.
+template <class F, class = void>
+struct IsCentred : std::false_type {};
+template <class F>
+struct IsCentred<F, std::enable_if_t<F::kCentred>> : std::true_type {};
+
+// Evaluate one work unit (tile (l, q), column chunk `chunk` when F::CS > 1) whose column samples
+// are in shared memory at `sc`, and commit its outputs.  Sorted Psi data: a tile whose smallest
+// pair distance exceeds kPsiSkipGap32 contributes exactly 0 (every MUFU input underflows) and is
+// skipped, so small bandwidths cost only the tiles near the diagonal.
+template <class F>
+__device__ __forceinline__ void pair_unit(const Args& a, const typename F::Params& p, int64_t tile,
+                                          int64_t l, int64_t q, int chunk, const float* sc, double* red,
+                                          unsigned long long* limbs, bool clamp, uint64_t* bar, uint32_t parity) {
+  constexpr int T = F::T, NOUT = F::NOUT;
+  F f;
+  if constexpr (IsCentred<F>::value) {
+    if (q < l && a.Y64[l * T] - a.Y64[q * T + T - 1] > a.skip_gap) {   // uniform per CTA
+      if (threadIdx.x == 0 && a.skipped != nullptr) {   // pairs of this unit, for the profile
+        int64_t c0 = 0, c1 = a.n - l * (int64_t)T;
+        if (F::CS > 1) c0 = (int64_t)chunk * (T / F::CS), c1 = c1 < c0 + T / F::CS ? c1 : c0 + T / F::CS;
+        else c1 = c1 < T ? c1 : T;
+        if (c1 > c0) atomicAdd(a.skipped, (unsigned long long)(T * (c1 - c0)));
+      }
+      mbar_wait(bar, parity);   // a skipped unit still consumes its buffer's phase
+      return;
+    }
+    f.load_rows_c(a.Y64, row_origin<F>(q), a.centres[l]);
+  } else {
+    f.load_rows(a.X, a.ld, row_origin<F>(q));
+  }
+  mbar_wait(bar, parity);      // the row loads above overlap the column chunk's TMA
+  if constexpr (F::CS > 1) f.jbase = chunk * F::CW;
+  f.par = (int)(tile & 1);
+  const bool diag = (q == l);
+  const int64_t jl = a.n - l * (int64_t)T;
+  if (clamp) {
+    if (!diag && jl >= T) f.template compute<false, true>(sc, p, false, T);
+    else f.template compute<true, true>(sc, p, diag, (int)(jl < T ? jl : T));
+  } else {
+    if (!diag && jl >= T) f.template compute<false, false>(sc, p, false, T);
+    else f.template compute<true, false>(sc, p, diag, (int)(jl < T ? jl : T));
+  }
+  double v[NOUT];
+  f.outputs(v, p);
+  commit_tile<NOUT, F::NT>(v, red, limbs, a.scale_exp);
+}
+
+// Work unit u of the rank's range: tile tile_begin + u / CS, column chunk u % CS (CS = 1: whole
+// tiles).  Persistent CTAs stride over the units; the next unit's column chunk is staged by TMA
+// into the other buffer while the current one is evaluated.
 template <class F>
 __global__ void __launch_bounds__(F::NT, F::MINB) pair_kernel(const Args a,
                                                         const __grid_constant__ typename F::Params p) {
-  constexpr int T = F::T, D = F::D, NOUT = F::NOUT, NW = F::NT / 32;
+  constexpr int T = F::T, D = F::D, NOUT = F::NOUT, NW = F::NT / 32, CS = F::CS;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* cols = reinterpret_cast<float*>(smem_raw);                 // [2][D][T]
   double* red = reinterpret_cast<double*>(cols + 2 * D * T);        // [NW][NOUT]
@@ -345,9 +421,6 @@ __global__ void __launch_bounds__(F::NT, F::MINB) pair_kernel(const Args a,
   }
   __syncthreads();
 
-  if constexpr (F::CS > 1) {
-  // column-split tiles: work unit u = (tile tb + u / CS, chunk u % CS)
-  constexpr int CS = F::CS;
   const int64_t units = (a.tile_end - a.tile_begin) * CS;
   auto issue = [&](int64_t u, int buf) {
     int64_t l, q;
@@ -363,72 +436,13 @@ __global__ void __launch_bounds__(F::NT, F::MINB) pair_kernel(const Args a,
   if (tid == 0 && u < units) issue(u, 0);
   uint32_t k = 0;
   for (; u < units; u += gridDim.x, ++k) {
-    int64_t l, q;
-    tile_coords(a.tile_begin + u / CS, l, q);
-    const int64_t un = u + gridDim.x;
-    if (tid == 0 && un < units) issue(un, (k + 1) & 1);
-
-    F f;
-    f.load_rows(a.X, a.ld, row_origin<F>(q));
-    f.jbase = (int)(u % CS) * F::CW;
-    f.par = (int)((a.tile_begin + u / CS) & 1);
-    mbar_wait(&bar[k & 1], (k >> 1) & 1);
-    const float* sc = cols + (k & 1) * D * T;
-    const bool diag = (q == l);
-    const int64_t jl = a.n - l * (int64_t)T;
-    if (clamp) {
-      if (!diag && jl >= T) f.template compute<false, true>(sc, p, false, T);
-      else f.template compute<true, true>(sc, p, diag, (int)(jl < T ? jl : T));
-    } else {
-      if (!diag && jl >= T) f.template compute<false, false>(sc, p, false, T);
-      else f.template compute<true, false>(sc, p, diag, (int)(jl < T ? jl : T));
-    }
-
-    double v[NOUT];
-    f.outputs(v);
-    commit_tile<NOUT, F::NT>(v, red, a.limbs, a.scale_exp);
-  }
-    return;
-  } else {
-  auto issue = [&](int64_t tile, int buf) {
+    const int64_t tile = a.tile_begin + u / CS;
     int64_t l, q;
     tile_coords(tile, l, q);
-    float* dst = cols + buf * D * T;
-    mbar_expect_tx(&bar[buf], (uint32_t)(D * T * sizeof(float)));
-#pragma unroll
-    for (int d = 0; d < D; ++d)
-      tma_load_1d(dst + d * T, a.X + d * a.ld + l * T, (uint32_t)(T * sizeof(float)), &bar[buf]);
-  };
-
-  const bool clamp = F::kClampable && a.clamp != nullptr && *a.clamp != 0;   // uniform per launch
-  int64_t t = a.tile_begin + blockIdx.x;
-  if (tid == 0 && t < a.tile_end) issue(t, 0);
-  uint32_t k = 0;
-  for (; t < a.tile_end; t += gridDim.x, ++k) {
-    int64_t l, q;
-    tile_coords(t, l, q);
-    const int64_t tn = t + gridDim.x;
-    if (tid == 0 && tn < a.tile_end) issue(tn, (k + 1) & 1);
-
-    F f;
-    f.load_rows(a.X, a.ld, row_origin<F>(q));
-    f.par = (int)(t & 1);
-    mbar_wait(&bar[k & 1], (k >> 1) & 1);
-    const float* sc = cols + (k & 1) * D * T;
-    const bool diag = (q == l);
-    const int64_t jl = a.n - l * (int64_t)T;
-    if (clamp) {
-      if (!diag && jl >= T) f.template compute<false, true>(sc, p, false, T);
-      else f.template compute<true, true>(sc, p, diag, (int)(jl < T ? jl : T));
-    } else {
-      if (!diag && jl >= T) f.template compute<false, false>(sc, p, false, T);
-      else f.template compute<true, false>(sc, p, diag, (int)(jl < T ? jl : T));
-    }
-
-    double v[NOUT];
-    f.outputs(v);
-    commit_tile<NOUT, F::NT>(v, red, a.limbs, a.scale_exp);
-  }
+    const int64_t un = u + gridDim.x;
+    if (tid == 0 && un < units) issue(un, (k + 1) & 1);
+    pair_unit<F>(a, p, tile, l, q, (int)(u % CS), cols + (k & 1) * D * T, red, a.limbs, clamp, &bar[k & 1],
+                 (k >> 1) & 1);
   }
 }
 
@@ -453,7 +467,7 @@ __global__ void __launch_bounds__(F::NT, F::MINB) pair_kernel_sets(const Args a,
   // Work units u in [0, n_sets * tiles): set = u / tiles, tile = tile_begin + u % tiles (set-major,
   // so consecutive CTAs share a set's data in L2).
   const int64_t per = a.tile_end - a.tile_begin;
-  const int64_t units = per * a.n_sets;
+  const int64_t units = per * (a.n_sets_dev != nullptr ? *a.n_sets_dev : a.n_sets);
   auto issue = [&](int64_t u, int buf) {
     const int64_t set = u / per;
     int64_t l, q;
@@ -472,28 +486,15 @@ __global__ void __launch_bounds__(F::NT, F::MINB) pair_kernel_sets(const Args a,
   uint32_t k = 0;
   for (; u < units; u += gridDim.x, ++k) {
     const int64_t set = u / per;
+    const int64_t tile = a.tile_begin + (u - set * per);
     int64_t l, q;
-    tile_coords(a.tile_begin + (u - set * per), l, q);
+    tile_coords(tile, l, q);
     const int64_t un = u + gridDim.x;
     if (tid == 0 && un < units) issue(un, (k + 1) & 1);
-
-    F f;
-    f.load_rows(a.X + set * a.set_stride, a.ld, row_origin<F>(q));
-    mbar_wait(&bar[k & 1], (k >> 1) & 1);
-    const float* sc = cols + (k & 1) * D * T;
-    const bool diag = (q == l);
-    const int64_t jl = a.n - l * (int64_t)T;
-    if (clamp) {
-      if (!diag && jl >= T) f.template compute<false, true>(sc, p, false, T);
-      else f.template compute<true, true>(sc, p, diag, (int)(jl < T ? jl : T));
-    } else {
-      if (!diag && jl >= T) f.template compute<false, false>(sc, p, false, T);
-      else f.template compute<true, false>(sc, p, diag, (int)(jl < T ? jl : T));
-    }
-
-    double v[NOUT];
-    f.outputs(v);
-    commit_tile<NOUT, F::NT>(v, red, a.limbs + set * NOUT * kLimbs, a.scale_exp);
+    Args as = a;
+    as.X = a.X + set * a.set_stride;
+    pair_unit<F>(as, p, tile, l, q, 0, cols + (k & 1) * D * T, red, a.limbs + set * NOUT * kLimbs, clamp,
+                 &bar[k & 1], (k >> 1) & 1);
   }
 }
 
@@ -529,7 +530,8 @@ inline cudaError_t launch_pair(const LaunchCfg& c, const typename F::Params& p) 
   const int64_t units = (c.tile_end - c.tile_begin) * c.n_sets * F::CS;
   int64_t grid = (int64_t)c.sm_count * occ;
   if (grid > units) grid = units;
-  Args a{c.X, c.n, c.ld, c.tile_begin, c.tile_end, c.scale_exp, c.limbs, c.clamp, c.n_sets, c.set_stride};
+  Args a{c.X, c.n, c.ld, c.tile_begin, c.tile_end, c.scale_exp, c.limbs, c.clamp, c.n_sets, c.set_stride,
+         c.Y64, c.centres, c.skipped, c.n_sets_dev, c.skip_gap};
   if constexpr (F::kSets) pair_kernel_sets<F><<<(unsigned)grid, F::NT, smem, c.stream>>>(a, p);
   else pair_kernel<F><<<(unsigned)grid, F::NT, smem, c.stream>>>(a, p);
   return cudaGetLastError();

@@ -10,6 +10,12 @@ namespace kde {
 
 void tile_coords_host(int64_t bx, int64_t* l, int64_t* q) { tile_coords(bx, *l, *q); }
 
+double psi_skip_gap(bool fp64) {
+  const char* e = getenv("KDE_DEBUG_PSI_NOSKIP");   // tests / diagnostics: read at every call
+  if (e && atoi(e) == 1) return INFINITY;
+  return fp64 ? kPsiSkipGap64 : kPsiSkipGap32;
+}
+
 // ------------------------------------------------------------------ dispatch
 
 int tile_for(Kind k, int d, int64_t n) {
@@ -210,6 +216,15 @@ __global__ void prep_kernel_p(const double* __restrict__ X, int64_t n, int d, co
   prep_body(X, n, d, pp.W, pp.mean, Y, ld, pad, flag, clamp_thresh);
 }
 
+// Several sets, parameters in device memory, the set count decided on the device (blockIdx.y = set).
+__global__ void prep_sets_kernel(const double* __restrict__ X, int64_t n, int d, const PrepParams* __restrict__ pp,
+                                 const int* __restrict__ n_sets, float* __restrict__ Y, int64_t set_stride,
+                                 int64_t ld, unsigned long long* __restrict__ flag) {
+  const int set = blockIdx.y;
+  if (set >= *n_sets) return;
+  prep_body(X, n, d, pp[set].W, pp[set].mean, Y + (int64_t)set * set_stride, ld, 0.f, flag, 0.0);
+}
+
 static unsigned prep_blocks(int64_t ld) {
   int64_t blocks = (ld + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
@@ -223,32 +238,66 @@ cudaError_t launch_prep(const double* X, int64_t n, int d, const double* W_dev,
   return cudaGetLastError();
 }
 
+cudaError_t launch_prep_sets(const double* X, int64_t n, int d, const PrepParams* pp_dev, const int* n_sets_dev,
+                             int max_sets, float* Y, int64_t set_stride, int64_t ld, cudaStream_t s,
+                             unsigned long long* flag) {
+  unsigned bx = prep_blocks(ld);
+  const unsigned per = (148u * 16u + (unsigned)max_sets - 1) / (unsigned)max_sets;   // ~16 blocks/SM overall
+  if (bx > per) bx = per > 0 ? per : 1;
+  prep_sets_kernel<<<dim3(bx, (unsigned)max_sets), 256, 0, s>>>(X, n, d, pp_dev, n_sets_dev, Y, set_stride, ld, flag);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_prep_params(const double* X, int64_t n, int d, const PrepParams& pp, float* Y, int64_t ld,
                                cudaStream_t s, float pad, unsigned long long* flag, double clamp_thresh) {
   prep_kernel_p<<<prep_blocks(ld), 256, 0, s>>>(X, n, d, pp, Y, ld, pad, flag, clamp_thresh);
   return cudaGetLastError();
 }
 
-// ------------------------------------------------------------------ fp64-term Psi mode
-// kde_set_precision(ctx, 1): every term in fp64 (libdevice exp, Horner in s with the integer
-// coefficients of He_r, fp64 tile sums), for bandwidths far below the PLUGIN pilots where the
-// cancellation exceeds what fp32 terms carry.  ~20x slower than the fp32 path;
-// same tile map (256-tiles), fixed-point limbs and multi-GPU partition.
-__global__ void scale64_kernel(const double* __restrict__ x, int64_t n, const double* __restrict__ mean,
-                               const double* __restrict__ w, double* __restrict__ y) {
+// Psi data prep (rows a1 of SURVEY §8(a) + tile-local centring): sorted x ->
+// y = (x - mean) * w in fp64 (Y64, zero padded to ld), per column tile l the centre
+// c_l = fp32(y[min(l T + T/2, n - 1)]) and Yc = fp32(y - c_l) (padding 0).  Flags as prep_body:
+// flag[0] some |y| > 1e18 (error), flag[1] some |y| > clamp_thresh.
+__global__ void psi_prep_kernel(const double* __restrict__ x, int64_t n, const double* __restrict__ mean,
+                                const double* __restrict__ w, int T, double* __restrict__ Y64,
+                                float* __restrict__ Yc, float* __restrict__ centres, int64_t ld,
+                                unsigned long long* __restrict__ flag, double clamp_thresh) {
   const double m = mean[0], s = w[0];
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    y[i] = (x[i] - m) * s;
+  bool bad = false, big = false;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ld; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t l = i / T;
+    int64_t mid = l * T + T / 2;
+    if (mid > n - 1) mid = n - 1;
+    const float c = __double2float_rn((x[mid] - m) * s);   // the same expression as y[mid]
+    if (i == l * T) centres[l] = c;
+    if (i < n) {
+      const double y = (x[i] - m) * s;
+      bad |= !(fabs(y) <= 1.0e18);
+      big |= fabs(y) > clamp_thresh;
+      Y64[i] = y;
+      Yc[i] = __double2float_rn(y - (double)c);
+    } else {
+      Y64[i] = 0.0;
+      Yc[i] = 0.f;
+    }
+  }
+  if (bad && flag) atomicOr(flag, 1ull);
+  if (big && flag) atomicOr(flag + 1, 1ull);
 }
 
-cudaError_t launch_scale64(const double* x, int64_t n, const double* mean_dev, const double* w_dev, double* y,
-                           cudaStream_t s) {
-  int64_t blocks = (n + 255) / 256;
-  if (blocks > 148 * 16) blocks = 148 * 16;
-  scale64_kernel<<<(unsigned)(blocks > 0 ? blocks : 1), 256, 0, s>>>(x, n, mean_dev, w_dev, y);
+cudaError_t launch_psi_prep(const double* x, int64_t n, const double* mean_dev, const double* w_dev, int T,
+                            double* Y64, float* Yc, float* centres, int64_t ld, cudaStream_t s,
+                            unsigned long long* flag, double clamp_thresh) {
+  psi_prep_kernel<<<prep_blocks(ld), 256, 0, s>>>(x, n, mean_dev, w_dev, T, Y64, Yc, centres, ld, flag, clamp_thresh);
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ fp64-term Psi mode
+// Every term in fp64 (libdevice exp, Horner in s with the integer coefficients of He_r, fp64 tile
+// sums) on the fp64 scaled samples of psi_prep_kernel: kde_set_precision(ctx, 1), or the automatic
+// re-run of a pass whose cancellation estimate exceeds what fp32 terms carry.
+// Same tile map (256-tiles), fixed-point limbs and multi-GPU partition as the fp32 path; sorted
+// data: tiles whose smallest pair distance exceeds kPsiSkipGap64 add exactly 0 and are skipped.
 template <int R>
 __device__ __forceinline__ double he64(double s) {   // He_r(u) in s = u^2
   if (R == 4) return (s - 6.0) * s + 3.0;
@@ -258,13 +307,17 @@ __device__ __forceinline__ double he64(double s) {   // He_r(u) in s = u^2 (P:23
 
 template <int R>
 __global__ void __launch_bounds__(kPsi64Tile) psi64_kernel(const double* __restrict__ y, int64_t n, int64_t tb,
-                                                           int64_t te, int S, unsigned long long* __restrict__ limbs) {
+                                                           int64_t te, int S, unsigned long long* __restrict__ limbs,
+                                                           const unsigned long long* __restrict__ gate,
+                                                           double skip_gap) {
   __shared__ double cs[kPsi64Tile];
   __shared__ double red[kPsi64Tile / 32];
   const int tid = threadIdx.x;
+  if (gate != nullptr && *gate == 0) return;   // device-side decision: the fp32 pass sufficed
   for (int64_t t = tb + blockIdx.x; t < te; t += gridDim.x) {
     int64_t l, q;
     tile_coords(t, l, q);
+    if (q < l && y[l * kPsi64Tile] - y[q * kPsi64Tile + kPsi64Tile - 1] > skip_gap) continue;   // exact 0
     const int64_t jc = l * kPsi64Tile + tid, i = q * kPsi64Tile + tid;
     __syncthreads();
     cs[tid] = jc < n ? y[jc] : 0.0;
@@ -285,14 +338,15 @@ __global__ void __launch_bounds__(kPsi64Tile) psi64_kernel(const double* __restr
 }
 
 cudaError_t launch_psi64(int r, const double* y, int64_t n, int64_t tb, int64_t te, int S,
-                         unsigned long long* limbs, int sm_count, cudaStream_t s) {
+                         unsigned long long* limbs, int sm_count, cudaStream_t s, const unsigned long long* gate,
+                         double skip_gap) {
   if (te <= tb) return cudaSuccess;
   int64_t grid = te - tb;
   if (grid > (int64_t)sm_count * 8) grid = (int64_t)sm_count * 8;
   switch (r) {
-    case 4: psi64_kernel<4><<<(unsigned)grid, kPsi64Tile, 0, s>>>(y, n, tb, te, S, limbs); break;
-    case 6: psi64_kernel<6><<<(unsigned)grid, kPsi64Tile, 0, s>>>(y, n, tb, te, S, limbs); break;
-    case 8: psi64_kernel<8><<<(unsigned)grid, kPsi64Tile, 0, s>>>(y, n, tb, te, S, limbs); break;
+    case 4: psi64_kernel<4><<<(unsigned)grid, kPsi64Tile, 0, s>>>(y, n, tb, te, S, limbs, gate, skip_gap); break;
+    case 6: psi64_kernel<6><<<(unsigned)grid, kPsi64Tile, 0, s>>>(y, n, tb, te, S, limbs, gate, skip_gap); break;
+    case 8: psi64_kernel<8><<<(unsigned)grid, kPsi64Tile, 0, s>>>(y, n, tb, te, S, limbs, gate, skip_gap); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
@@ -311,9 +365,12 @@ __device__ __forceinline__ void set_status(double* st, int code) {
 }
 
 // stage 0: mean = sum / n.  stage 1: V-hat, sigma-hat, Psi8^NS, g1 (steps 1-4), W = 1/g1.
-// stage 2: Psi6-hat(g1) (step 5), g2 (step 6), W = 1/g2.  stage 3: Psi4-hat(g2) (step 7), h (8).
+// stage 4 (5): after the fp32-term Psi6 (Psi4) pass, decide whether it is re-run with fp64 terms
+// (gate): psi_mode 1 always, 0 when kappa = 2A / |2S + n He_r(0)| > kPsiKappaMax, -1 never.
+// stage 2: Psi6-hat(g1) (step 5) from the fp64 or fp32 sum, g2 (step 6), W = 1/g2.
+// stage 3: Psi4-hat(g2) (step 7), h (step 8).  `limbs` = the chain's kPluginOuts outputs.
 __global__ void plugin_chain_kernel(int stage, int64_t n, double* small, const unsigned long long* limbs,
-                                    int S) {
+                                    int S, int psi_mode) {
   PluginDev dv(small);
   const double nn = (double)n, pi = 3.14159265358979323846, s2p = sqrt(2.0 * pi);
   double* t = dv.trace;   // V_hat, sigma_hat, psi8_ns, g1, psi6, g2, psi4, h
@@ -331,15 +388,22 @@ __global__ void plugin_chain_kernel(int stage, int64_t n, double* small, const u
     const double K6_0 = -15.0 / s2p;
     t[3] = pow(-2.0 * K6_0 / (t[2] * nn), 1.0 / 9.0);                      // Eq. 14
     dv.W[0] = 1.0 / t[3];
+  } else if (stage == 4 || stage == 5) {
+    const int k = stage - 4;                                               // 0: Psi6, 1: Psi4
+    const unsigned long long* L = limbs + (size_t)(2 * k) * kLimbs;
+    const double Sr = limbs_value_dev(L, S), A = limbs_value_dev(L + kLimbs, S);
+    const double kappa = 2.0 * A / fabs(2.0 * Sr + nn * (k == 0 ? -15.0 : 3.0));
+    dv.gate[k] = psi_mode > 0 || (psi_mode == 0 && !(kappa <= kPsiKappaMax)) ? 1ull : 0ull;
+    small[421 + k] = kappa;                                                // reported (kde_last_psi_kappa)
   } else if (stage == 2) {
-    const double Sr = limbs_value_dev(limbs, S);
+    const double Sr = limbs_value_dev(limbs + (size_t)(dv.gate[0] ? 4 : 0) * kLimbs, S);
     t[4] = (2.0 * Sr / s2p + nn * -15.0 / s2p) / (nn * nn * pow(t[3], 7.0));   // Eq. 15, reading Z1
     if (!(t[4] < 0.0)) set_status(dv.status, 8);                           // KDE_E_NUMERIC
     const double K4_0 = 3.0 / s2p;
     t[5] = pow(-2.0 * K4_0 / (t[4] * nn), 1.0 / 7.0);                      // Eq. 16
     dv.W[0] = 1.0 / t[5];
   } else {
-    const double Sr = limbs_value_dev(limbs, S);
+    const double Sr = limbs_value_dev(limbs + (size_t)(dv.gate[1] ? 5 : 2) * kLimbs, S);
     t[6] = (2.0 * Sr / s2p + nn * 3.0 / s2p) / (nn * nn * pow(t[5], 5.0));     // Eq. 17
     if (!(t[6] > 0.0)) set_status(dv.status, 8);
     const double RK = 1.0 / (2.0 * sqrt(pi));
@@ -348,8 +412,8 @@ __global__ void plugin_chain_kernel(int stage, int64_t n, double* small, const u
 }
 
 cudaError_t launch_plugin_chain(int stage, int64_t n, double* small, const unsigned long long* limbs, int S,
-                                cudaStream_t s) {
-  plugin_chain_kernel<<<1, 1, 0, s>>>(stage, n, small, limbs, S);
+                                cudaStream_t s, int psi_mode) {
+  plugin_chain_kernel<<<1, 1, 0, s>>>(stage, n, small, limbs, S, psi_mode);
   return cudaGetLastError();
 }
 

@@ -273,6 +273,9 @@ cudaEvent_t next_event(kde_ctx* c) {
 
 void prof_reset(kde_ctx* c) {
   c->ev_used = 0;
+  c->ev_excl.clear();
+  c->psi_escalations = 0;
+  c->psi_kappa_max = 0.0;
   c->prof_launches = 0;
   c->prof_all = 0;
   c->prof_ms = 0.0;
@@ -284,6 +287,7 @@ kde_status prof_collect(kde_ctx* c) {
   if (!c->profiling) return KDE_OK;
   double ms = 0.0;
   for (size_t k = 0; k + 1 < c->ev_used; k += 2) {
+    if (k / 2 < c->ev_excl.size() && c->ev_excl[k / 2]) continue;
     float x = 0.f;
     CUDA_TRY(c, cudaEventElapsedTime(&x, c->ev_pool[k], c->ev_pool[k + 1]));
     ms += x;
@@ -342,6 +346,10 @@ kde_status run_sums(kde_ctx* c, int d, int64_t n, int64_t ld, int T, int scale, 
     if (L.X) cfg.X = L.X;
     cfg.n_sets = L.n_sets;
     cfg.set_stride = L.set_stride;
+    cfg.Y64 = L.Y64;
+    cfg.centres = L.centres;
+    cfg.skipped = L.skipped;
+    cfg.skip_gap = L.skip_gap;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (c->profiling) { e0 = next_event(c); e1 = next_event(c); cudaEventRecord(e0, c->stream); }
     cudaError_t err = cudaSuccess;
@@ -425,6 +433,7 @@ void kde_default_opts(kde_select_opts* o) {
   o->refine_steps = 0;
   o->refine_tol = 1e-9;
   o->nm_starts = 1;
+  o->nm_loop = 0;           // device-resident Nelder-Mead where it applies
 }
 
 kde_status kde_nccl_unique_id(void* out128) {
@@ -469,12 +478,14 @@ void kde_destroy(kde_ctx* c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream); else cudaDeviceSynchronize();
   if (c->plug_exec) cudaGraphExecDestroy(c->plug_exec);
+  if (c->nm_exec) cudaGraphExecDestroy(c->nm_exec);
+  if (c->nm_ws) cudaFree(c->nm_ws);
+  if (c->nm_host) cudaFreeHost(c->nm_host);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   if (c->comm) nccl().CommDestroy(c->comm);
   if (c->own_ws) cudaFree(c->own_ws);
   if (c->sort_ws) cudaFree(c->sort_ws);
   if (c->white_ws) cudaFree(c->white_ws);
-  if (c->y64) cudaFree(c->y64);
   if (c->ev_ws) cudaFree(c->ev_ws);
   if (c->mat_ws) cudaFree(c->mat_ws);
   for (void* p : c->in_ws)
@@ -513,6 +524,10 @@ kde_status kde_set_host_allreduce(kde_ctx* c, kde_host_allreduce_fn fn, void* us
   c->har_user = user;
   return KDE_OK;
 }
+
+int32_t kde_last_fp64_passes(const kde_ctx* c) { return c ? c->psi_escalations : 0; }
+
+double kde_last_psi_kappa(const kde_ctx* c) { return c ? c->psi_kappa_max : 0.0; }
 
 kde_status kde_set_profiling(kde_ctx* c, int32_t on) {
   if (!c) return KDE_E_INVALID;

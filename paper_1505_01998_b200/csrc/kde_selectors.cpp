@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "kde_host.h"
+#include "kde_nm.cuh"
 
 using kde::Kind;
 using namespace kde::host;
@@ -39,34 +40,67 @@ double he_at_zero(int r) { return r == 4 ? 3.0 : (r == 6 ? -15.0 : 105.0); }
 
 Kind psi_kind(int r) { return r == 4 ? Kind::Psi4 : (r == 6 ? Kind::Psi6 : Kind::Psi8); }
 
-// fp64-term mode: one Psi_r pass over this rank's 256-tiles of the fp64 scaled samples y, into
-// `limbs` (3 int64), then the all-reduce.
-kde_status psi64_pass(kde_ctx* c, int r, const double* y, int64_t n, int S, unsigned long long* limbs) {
+// Psi workspace: Yc (fp32 tile-centred columns, ld) | Y64 (fp64 scaled samples, ld) | centres
+// (ld / T): get_ws with d = 4 rows of ld floats.
+struct PsiBufs {
+  float* Yc;
+  double* Y64;
+  float* centres;
+};
+PsiBufs psi_bufs(const Ws& w, int64_t ld) {
+  return PsiBufs{w.Y, reinterpret_cast<double*>(w.Y + ld), w.Y + 3 * ld};
+}
+
+// Cancellation of an fp32-term Psi pass as seen by Psi-hat: kappa = 2A / |2S + n He_r(0)| with
+// S = sum t and A ~ sum |t| (the kernel's group-level estimate); Psi-hat's error is ~kappa times
+// the terms' systematic error.
+double psi_kappa(int r, int64_t n, double S, double A) {
+  return 2.0 * A / std::fabs(2.0 * S + (double)n * he_at_zero(r));
+}
+
+// One fp64-term Psi_r pass over this rank's 256-tiles of Y64 into `limbs`, then the all-reduce.
+// gate != null (PLUGIN chain): the kernel runs only if the device decided so; its profiling events
+// are kept aside (slot) and counted after the chain if it ran.
+kde_status psi64_pass(kde_ctx* c, int r, const double* y, int64_t n, int S, unsigned long long* limbs,
+                      const unsigned long long* gate = nullptr, int slot = -1) {
   Range rr("kde.pair_pass_fp64");
   int64_t tb, te;
   shard_range(n_tiles(n, kde::kPsi64Tile), c->rank, c->world, &tb, &te);
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   const unsigned rec = (c->cap_stream && c->stream == c->cap_stream) ? cudaEventRecordExternal : cudaEventRecordDefault;
-  if (c->profiling) { e0 = next_event(c); e1 = next_event(c); CUDA_TRY(c, cudaEventRecordWithFlags(e0, c->stream, rec)); }
-  CUDA_TRY(c, kde::launch_psi64(r, y, n, tb, te, S, limbs, c->sm_count, c->stream));
+  if (c->profiling) {
+    if (gate) c->gate_pair[slot] = (int)(c->ev_used / 2);
+    e0 = next_event(c); e1 = next_event(c);
+    CUDA_TRY(c, cudaEventRecordWithFlags(e0, c->stream, rec));
+  }
+  CUDA_TRY(c, kde::launch_psi64(r, y, n, tb, te, S, limbs, c->sm_count, c->stream, gate, kde::psi_skip_gap(true)));
   if (tb < te) c->prof_all += 1;
   if (c->profiling) {
     CUDA_TRY(c, cudaEventRecordWithFlags(e1, c->stream, rec));
-    c->prof_launches++;
-    c->prof_evals += pairs_in_range(n, kde::kPsi64Tile, tb, te);
+    const double pairs = pairs_in_range(n, kde::kPsi64Tile, tb, te);
+    if (gate) {
+      c->gate_evals[slot] = pairs;
+    } else {
+      c->prof_launches++;
+      c->prof_evals += pairs;
+    }
   }
   TRY(allreduce_limbs(c, limbs, kde::kLimbs));
   return KDE_OK;
 }
 
-// Raw Psi sums S_r(g) = sum_{i<j} He_r(u) e^{-u^2/2} for each g (one prep + one launch per g).
+// Raw Psi sums S_r(g) = sum_{i<j} He_r(u) e^{-u^2/2} for each g: sort once, then per g the prep
+// (fp64 y, tile centres, centred fp32 columns) and the fp32-term pass, whose cancellation
+// estimate decides (psi_mode 0, full sums only) whether the pass is re-run with fp64 terms;
+// psi_mode 1 runs fp64 terms only, -1 fp32 terms only.
 kde_status psi_raw(kde_ctx* c, const double* x, int64_t n, int r, const double* g, int ng,
                    const Moments& m, int shard_rank, int shard_world, bool allreduce,
                    std::vector<kde_fixed>& out, bool presorted = false) {
   const int T = kde::tile_for(psi_kind(r), 1, n);
   const int64_t ld = (n + T - 1) / T * T;
   Ws w;
-  TRY(get_ws(c, ld, 1, 1, &w));
+  TRY(get_ws(c, ld, 4, 2, &w));
+  const PsiBufs b = psi_bufs(w, ld);
   const int S = scale_exp_for(2.0 * std::fabs(he_at_zero(r)), n);
   if (!presorted) {
     const double* xs = nullptr;
@@ -74,37 +108,52 @@ kde_status psi_raw(kde_ctx* c, const double* x, int64_t n, int r, const double* 
     x = xs;
   }
   out.clear();
-  if ((c->psi_mode == 1)) {                       // fp64-term mode (kde_set_precision)
-    TRY(grow(c, &c->y64, &c->y64_bytes, (size_t)std::max<int64_t>(n, 1) * sizeof(double)));
-    double* y = static_cast<double*>(c->y64);
-    for (int k = 0; k < ng; ++k) {
-      const double hv[2] = {m.mean[0], 1.0 / g[k]};
-      CUDA_TRY(c, cudaMemcpyAsync(w.small, hv, sizeof(hv), cudaMemcpyHostToDevice, c->stream));
-      CUDA_TRY(c, kde::launch_scale64(x, n, w.small, w.small + 1, y, c->stream));
-      CUDA_TRY(c, cudaMemsetAsync(w.limbs, 0, kde::kLimbs * sizeof(long long), c->stream));
-      if (allreduce) {
-        TRY(psi64_pass(c, r, y, n, S, w.limbs));
-      } else {                         // one shard, no collective
-        int64_t tb, te;
-        shard_range(n_tiles(n, kde::kPsi64Tile), shard_rank, shard_world, &tb, &te);
-        CUDA_TRY(c, kde::launch_psi64(r, y, n, tb, te, S, w.limbs, c->sm_count, c->stream));
-      }
-      long long hl[kde::kLimbs];
-      CUDA_TRY(c, cudaMemcpyAsync(hl, w.limbs, sizeof(hl), cudaMemcpyDeviceToHost, c->stream));
-      CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-      out.push_back(limbs_to_fixed(hl, S));
-    }
-    return KDE_OK;
-  }
   for (int k = 0; k < ng; ++k) {
-    std::vector<double> W = {1.0 / g[k]};
-    TRY(gpu_prep(c, x, n, 1, W, m.mean, ld, w, 3.0e4));
-    SumLaunch L;
-    L.kind = psi_kind(r); L.r = r; L.nb = 1; L.out_offset = 0; L.n_out = 1;
-    psi_coeffs(r, L.psi);
-    std::vector<kde_fixed> o;
-    TRY(run_sums(c, 1, n, ld, T, S, w, {L}, 1, shard_rank, shard_world, allreduce, o));
-    out.push_back(o[0]);
+    const double hv[2] = {m.mean[0], 1.0 / g[k]};
+    CUDA_TRY(c, cudaMemcpyAsync(w.small, hv, sizeof(hv), cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(c, cudaMemsetAsync(w.flag(), 0, (kde::kSmallDoubles - 408) * sizeof(double), c->stream));
+    CUDA_TRY(c, kde::launch_psi_prep(x, n, w.small, w.small + 1, T, b.Y64, b.Yc, b.centres, ld, c->stream,
+                                     w.flag(), 3.0e4));
+    c->prof_all += 1;
+    if (c->psi_mode != 1) {
+      SumLaunch L;
+      L.kind = psi_kind(r); L.r = r; L.nb = 1; L.out_offset = 0; L.n_out = 2;
+      L.X = b.Yc; L.Y64 = b.Y64; L.centres = b.centres;
+      L.skipped = reinterpret_cast<unsigned long long*>(w.small + kde::kSkippedSlot);
+      L.skip_gap = kde::psi_skip_gap(false);
+      psi_coeffs(r, L.psi);
+      std::vector<kde_fixed> o;
+      TRY(run_sums(c, 1, n, ld, T, S, w, {L}, 2, shard_rank, shard_world, allreduce, o));
+      if (c->profiling) {   // run_sums copied the small block's tail with the limbs
+        unsigned long long sk = 0;
+        std::memcpy(&sk, c->h_limbs + (kde::kSkippedSlot - 408), sizeof(sk));
+        c->prof_evals -= (double)sk;
+      }
+      const double kappa = psi_kappa(r, n, fixed_value(o[0]), fixed_value(o[1]));
+      if (allreduce) c->psi_kappa_max = std::max(c->psi_kappa_max, kappa);
+      const bool escalate = allreduce && c->psi_mode == 0 && !(kappa <= kde::kPsiKappaMax);
+      if (!escalate) {
+        out.push_back(o[0]);
+        continue;
+      }
+      c->psi_escalations++;
+    }
+    CUDA_TRY(c, cudaMemsetAsync(w.limbs, 0, kde::kLimbs * sizeof(long long), c->stream));
+    if (allreduce) {
+      TRY(psi64_pass(c, r, b.Y64, n, S, w.limbs));
+    } else {                         // one shard, no collective
+      int64_t tb, te;
+      shard_range(n_tiles(n, kde::kPsi64Tile), shard_rank, shard_world, &tb, &te);
+      CUDA_TRY(c, kde::launch_psi64(r, b.Y64, n, tb, te, S, w.limbs, c->sm_count, c->stream, nullptr,
+                                    kde::psi_skip_gap(true)));
+      if (tb < te) c->prof_all += 1;
+    }
+    long long hl[2 + kde::kLimbs];   // prep flags, then the limbs
+    CUDA_TRY(c, cudaMemcpyAsync(hl, w.flag(), 2 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(hl + 2, w.limbs, kde::kLimbs * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    if (hl[0]) return fail(c, KDE_E_INVALID, "scaled sample differences exceed 1e18 (outliers vs. bandwidth)");
+    out.push_back(limbs_to_fixed(hl + 2, S));
   }
   return KDE_OK;
 }
@@ -164,14 +213,16 @@ double lscv_h_finalize(int64_t n, int d, double det, double h, double S1, double
 
 // ------------------------------------------------------------------ LSCV_H
 
+// PD test, |H| and the whitening W = sqrt(log2 e / 4) L^-1 of one candidate, with the arithmetic the
+// device-resident Nelder–Mead uses too (kde_nm.cuh), so both loops prepare identical data sets.
 HCand h_candidate(const double* vh, int d) {
   HCand hc;
-  std::vector<double> H = unvech(vh, d), L;
-  if (!cholesky(H, d, L)) return hc;
+  double L[kde::kMaxDim * kde::kMaxDim], det = 0.0;
+  if (!kde::nm_cholesky_vech(vh, d, L, &det)) return hc;
   hc.pd = true;
-  hc.det = 1.0;
-  for (int i = 0; i < d; ++i) hc.det *= L[i * d + i] * L[i * d + i];
-  hc.L = std::move(L);
+  hc.det = det;
+  hc.W.assign((size_t)d * d, 0.0);
+  kde::nm_whitening(L, d, std::sqrt(kLog2e / 4.0), hc.W.data());
   return hc;
 }
 
@@ -201,11 +252,8 @@ kde_status lscv_H_raw(kde_ctx* c, const double* X, int64_t n, int d, const std::
     const size_t span = (size_t)(reinterpret_cast<char*>(w.limbs + (size_t)2 * cnt * kde::kLimbs) -
                                  reinterpret_cast<char*>(w.flag()));
     CUDA_TRY(c, cudaMemsetAsync(w.flag(), 0, span, c->stream));
-    for (int j = 0; j < cnt; ++j) {
-      std::vector<double> W = tri_lower_inverse(cands[b0 + j].L, d);
-      for (double& v : W) v *= std::sqrt(kLog2e / 4.0);
-      TRY(gpu_prep_into(c, X, n, d, W, m.mean, ld, w, Yw + (size_t)j * set_floats));
-    }
+    for (int j = 0; j < cnt; ++j)
+      TRY(gpu_prep_into(c, X, n, d, cands[b0 + j].W, m.mean, ld, w, Yw + (size_t)j * set_floats));
     SumLaunch L;
     L.kind = Kind::LscvMatrix; L.nb = 1; L.out_offset = 0; L.n_out = 2 * cnt;
     L.X = Yw; L.n_sets = cnt; L.set_stride = set_floats;
@@ -218,10 +266,7 @@ kde_status lscv_H_raw(kde_ctx* c, const double* X, int64_t n, int d, const std::
 }
 
 double lscv_H_finalize(int64_t n, int d, double det, double S1, double S2) {
-  const double nn = (double)n;
-  const double c4 = std::pow(4.0 * kPi, -0.5 * d) / std::sqrt(det);
-  const double c2 = std::pow(2.0 * kPi, -0.5 * d) / std::sqrt(det);
-  return 2.0 * (c4 * S1 - 2.0 * c2 * S2) / (nn * nn) + c4 / nn;
+  return kde::nm_lscv_H_finalize((double)n, std::pow(4.0 * kPi, -0.5 * d), std::pow(2.0 * kPi, -0.5 * d), det, S1, S2);
 }
 
 // Evaluate g(H) for a list of vech vectors (non-PD -> penalty); one GPU batch for all PD ones.
@@ -272,15 +317,18 @@ kde_status kde_psi_r(kde_ctx* c, const double* x, int64_t n, int32_t r, const do
   return KDE_OK;
 }
 
-// One Psi_r pair pass of the device-resident PLUGIN chain: kernel over this rank's tiles into
-// `limbs`, then (world > 1) the all-reduce of the 3 limbs, all enqueued on the context stream.
-static kde_status plugin_pass(kde_ctx* c, int r, int64_t n, int64_t ld, int T, int S, Ws& w,
-                              unsigned long long* limbs, int64_t tb, int64_t te, double pairs) {
+// One fp32-term Psi_r pair pass of the device-resident PLUGIN chain: kernel over this rank's
+// tiles into `limbs` (S, A), then (world > 1) the all-reduce, all enqueued on the context stream.
+static kde_status plugin_pass(kde_ctx* c, int r, int64_t n, int64_t ld, int T, int S, const PsiBufs& b,
+                              unsigned long long* clamp, unsigned long long* limbs, int64_t tb, int64_t te,
+                              double pairs, unsigned long long* skipped) {
   Range rr("kde.pair_pass");
   kde::LaunchCfg cfg;
-  cfg.X = w.Y; cfg.n = n; cfg.ld = ld; cfg.tile_begin = tb; cfg.tile_end = te; cfg.tile = T;
-  cfg.scale_exp = S; cfg.limbs = limbs; cfg.n_out = 1; cfg.stream = c->stream; cfg.sm_count = c->sm_count;
-  cfg.clamp = w.flag() + 1;
+  cfg.X = b.Yc; cfg.n = n; cfg.ld = ld; cfg.tile_begin = tb; cfg.tile_end = te; cfg.tile = T;
+  cfg.scale_exp = S; cfg.limbs = limbs; cfg.n_out = 2; cfg.stream = c->stream; cfg.sm_count = c->sm_count;
+  cfg.clamp = clamp; cfg.Y64 = b.Y64; cfg.centres = b.centres;
+  cfg.skipped = skipped;
+  cfg.skip_gap = kde::psi_skip_gap(false);
   kde::PsiParams p;
   psi_coeffs(r, p);
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -295,20 +343,23 @@ static kde_status plugin_pass(kde_ctx* c, int r, int64_t n, int64_t ld, int T, i
     c->prof_launches++;
     c->prof_evals += pairs;
   }
-  TRY(allreduce_limbs(c, limbs, kde::kLimbs));
+  TRY(allreduce_limbs(c, limbs, 2 * kde::kLimbs));
   return KDE_OK;
 }
 
 // PLUGIN (Sec. 4.4.1): moments, sort, prep and the two pair passes, with the scalar
 // steps 1-8 computed by single-thread kernels on the device between them, so the whole chain is
-// enqueued without a host round trip and the call synchronises once.  The steps' formulas are those
-// of the host reading (Z1, Z10, Z11); failures are recorded on the device and reported in order.
+// enqueued without a host round trip and the call synchronises once.  Each Psi pass runs with
+// fp32 terms; a device-side decision (stage 4 / 5: the pass's cancellation estimate, or the
+// precision mode) gates an fp64-term re-run of that pass on the same fp64 samples, and the next
+// stage reads whichever sum is valid.  Failures are recorded on the device and reported in order.
 // Enqueue the whole chain on c->stream (no allocation, no synchronisation: capturable).
 static kde_status plugin_enqueue(kde_ctx* c, const double* x, int64_t n, int T, int64_t ld, Ws& w) {
   kde::PluginDev dv(w.small);
+  const PsiBufs b = psi_bufs(w, ld);
   const int nblk = kde::moments_blocks(n);
   cudaStream_t st = c->stream;
-  // flags (2 x u64), trace (8) and status (1) start at zero
+  // flags (2 x u64), trace (8), status (1) and gates (2) start at zero
   CUDA_TRY(c, cudaMemsetAsync(w.flag(), 0, (kde::kSmallDoubles - 408) * sizeof(double), st));
   {
     Range r("kde.moments");
@@ -326,42 +377,36 @@ static kde_status plugin_enqueue(kde_ctx* c, const double* x, int64_t n, int T, 
   shard_range(n_tiles(n, T), c->rank, c->world, &tb, &te);
   const double pairs = c->profiling ? pairs_in_range(n, T, tb, te) : 0.0;
   const int S6 = scale_exp_for(2.0 * 15.0, n), S4 = scale_exp_for(2.0 * 3.0, n);
-  CUDA_TRY(c, cudaMemsetAsync(w.limbs, 0, 2 * kde::kLimbs * sizeof(long long), st));
-  if ((c->psi_mode == 1)) {                                                                       // fp64 terms
-    double* y = static_cast<double*>(c->y64);
-    CUDA_TRY(c, kde::launch_scale64(xs, n, dv.mean, dv.W, y, st));                     // x/g1
-    TRY(psi64_pass(c, 6, y, n, S6, w.limbs));                                          // step 5
-    CUDA_TRY(c, kde::launch_plugin_chain(2, n, w.small, w.limbs, S6, st));             // Psi6, g2
-    CUDA_TRY(c, kde::launch_scale64(xs, n, dv.mean, dv.W, y, st));                     // x/g2
-    TRY(psi64_pass(c, 4, y, n, S4, w.limbs + kde::kLimbs));                            // step 7
-  } else {
-    CUDA_TRY(c, kde::launch_prep(xs, n, 1, dv.W, dv.mean, w.Y, ld, st, 0.f, w.flag(), 3.0e4));   // x/g1
-    TRY(plugin_pass(c, 6, n, ld, T, S6, w, w.limbs, tb, te, pairs));                   // step 5
-    CUDA_TRY(c, kde::launch_plugin_chain(2, n, w.small, w.limbs, S6, st));             // Psi6, g2
-    CUDA_TRY(c, kde::launch_prep(xs, n, 1, dv.W, dv.mean, w.Y, ld, st, 0.f, w.flag(), 3.0e4));   // x/g2
-    TRY(plugin_pass(c, 4, n, ld, T, S4, w, w.limbs + kde::kLimbs, tb, te, pairs));     // step 7
+  const int mode = c->psi_mode;
+  unsigned long long* L = w.limbs;                       // [S6, A6, S4, A4, S6 fp64, S4 fp64]
+  CUDA_TRY(c, cudaMemsetAsync(L, 0, kde::kPluginOuts * kde::kLimbs * sizeof(long long), st));
+  const int Ss[2] = {S6, S4};
+  for (int k = 0; k < 2; ++k) {                                                        // Psi6(g1), Psi4(g2)
+    const int r = k == 0 ? 6 : 4;
+    CUDA_TRY(c, kde::launch_psi_prep(xs, n, dv.mean, dv.W, T, b.Y64, b.Yc, b.centres, ld, st, w.flag(), 3.0e4));
+    if (mode != 1)
+      TRY(plugin_pass(c, r, n, ld, T, Ss[k], b, w.flag() + 1, L + (size_t)(2 * k) * kde::kLimbs, tb, te, pairs,
+                      reinterpret_cast<unsigned long long*>(w.small + kde::kSkippedSlot)));
+    CUDA_TRY(c, kde::launch_plugin_chain(4 + k, n, w.small, L, Ss[k], st, mode));     // fp64 re-run?
+    TRY(psi64_pass(c, r, b.Y64, n, Ss[k], L + (size_t)(4 + k) * kde::kLimbs, dv.gate + k, k));
+    CUDA_TRY(c, kde::launch_plugin_chain(k == 0 ? 2 : 3, n, w.small, L, Ss[k], st));  // steps 5-6 / 7-8
+    c->prof_all += 3;
   }
-  CUDA_TRY(c, kde::launch_plugin_chain(3, n, w.small, w.limbs + kde::kLimbs, S4, st)); // Psi4, h
-  c->prof_all += 4;
   CUDA_TRY(c, cudaMemcpyAsync(c->h_limbs, w.flag(), (kde::kSmallDoubles - 408) * sizeof(double),
                               cudaMemcpyDeviceToHost, st));
   return KDE_OK;
 }
 
-// PLUGIN (Sec. 4.4.1): moments, sort, prep and the two pair passes, with the scalar
-// steps 1-8 computed by single-thread kernels on the device between them, so the whole chain is
-// enqueued without a host round trip and the call synchronises once.  The chain is captured once
-// as a CUDA graph and replayed while its inputs (pointers, n, mode) are unchanged.  The steps'
-// formulas are those of the host reading (Z1, Z10, Z11); failures are recorded on the device and
-// reported in order.
+// PLUGIN (Sec. 4.4.1): the chain above, captured once as a CUDA graph and replayed while
+// its inputs (pointers, n, mode) are unchanged.  The steps' formulas are those of the host reading
+// (Z1, Z10, Z11); failures are recorded on the device and reported in order.
 static kde_status plugin_impl(kde_ctx* c, const double* x, int64_t n, kde_plugin_trace* tr) {
   const int T = kde::tile_for(Kind::Psi6, 1, n);
   const int64_t ld = (n + T - 1) / T * T;
   Ws w;
-  TRY(get_ws(c, ld, 1, 2, &w));                   // everything the chain touches exists before
+  TRY(get_ws(c, ld, 4, kde::kPluginOuts, &w));    // everything the chain touches exists before
   TRY(ensure_sort_ws(c, n));                      // a capture starts
-  if ((c->psi_mode == 1)) TRY(grow(c, &c->y64, &c->y64_bytes, (size_t)n * sizeof(double)));
-  const size_t cnt = kde::kSmallDoubles - 408;    // flags, trace, status
+  const size_t cnt = kde::kSmallDoubles - 408;    // flags, trace, status, gates
   if (c->h_limbs_cap < cnt) {
     if (c->h_limbs) cudaFreeHost(c->h_limbs);
     c->h_limbs = nullptr;
@@ -376,7 +421,7 @@ static kde_status plugin_impl(kde_ctx* c, const double* x, int64_t n, kde_plugin
   cudaStream_t st = c->stream;
   const std::vector<uintptr_t> key = {(uintptr_t)x, (uintptr_t)n, (uintptr_t)w.Y, (uintptr_t)c->sort_ws,
                                       (uintptr_t)c->h_limbs, (uintptr_t)c->profiling, (uintptr_t)c->comm,
-                                      (uintptr_t)(c->psi_mode == 1), (uintptr_t)c->y64};
+                                      (uintptr_t)(c->psi_mode + 1)};
   // The first call with a given key runs directly (and does any lazy module loading and library
   // setup outside a capture); a second call with the same key captures, later ones replay.
   // (single-GPU contexts only: with a communicator the all-reduces stay plain stream operations)
@@ -420,6 +465,24 @@ static kde_status plugin_impl(kde_ctx* c, const double* x, int64_t n, kde_plugin
   const unsigned long long* flags = reinterpret_cast<const unsigned long long*>(c->h_limbs);
   double res[9];
   std::memcpy(res, c->h_limbs + 2, sizeof(res));
+  const unsigned long long* gates = flags + 11;
+  double kap[2];                                  // small[421..422]
+  std::memcpy(kap, c->h_limbs + 13, sizeof(kap));
+  if (c->psi_mode != 1) c->psi_kappa_max = std::max(kap[0], kap[1]);
+  if (c->profiling) {                             // pairs of exactly-zero tiles the kernels skipped
+    unsigned long long sk = 0;
+    std::memcpy(&sk, c->h_limbs + (kde::kSkippedSlot - 408), sizeof(sk));
+    c->prof_evals -= (double)sk;
+  }
+  for (int k = 0; k < 2; ++k) {                   // fp64 re-runs that actually ran
+    if (gates[k]) {
+      if (c->psi_mode == 0) c->psi_escalations++;
+      if (c->profiling) { c->prof_launches++; c->prof_evals += c->gate_evals[k]; }
+    } else if (c->profiling && c->gate_pair[k] >= 0) {
+      if (c->ev_excl.size() <= (size_t)c->gate_pair[k]) c->ev_excl.resize(c->gate_pair[k] + 1, 0);
+      c->ev_excl[c->gate_pair[k]] = 1;            // its (empty) launch is not a pair pass
+    }
+  }
   const int status = (int)res[8];
   if (status == KDE_E_INVALID) return fail(c, KDE_E_INVALID, "non-finite sample values");
   if (status == KDE_E_DEGENERATE) return fail(c, KDE_E_DEGENERATE, "variance estimate <= 0");
@@ -649,7 +712,14 @@ kde_status kde_select_bandwidth(kde_ctx* c, kde_method method, const double* X, 
       sims.push_back(sk);
     }
     NMResult nm;
-    TRY(nelder_mead_multi(c, X, n, d, m, sims, o.max_iter, o.tol_rel, o.penalty, o.speculative != 0, nm, nullptr));
+    // device-resident loop: one GPU, one start, serial rounds, whitened sets within ~1 GiB
+    const int64_t Tm = kde::tile_for(Kind::LscvMatrix, d, n), ldT = (n + Tm - 1) / Tm * Tm;
+    const bool dev_loop = o.nm_loop == 0 && K == 1 && o.speculative == 0 && c->world == 1 && !c->comm &&
+                          !c->har_fn && (double)(P + 1) * d * (double)ldT * 4.0 <= (double)(1LL << 30);
+    if (dev_loop)
+      TRY(nelder_mead_device(c, X, n, d, m, sims[0], o.max_iter, o.tol_rel, o.penalty, nm));
+    else
+      TRY(nelder_mead_multi(c, X, n, d, m, sims, o.max_iter, o.tol_rel, o.penalty, o.speculative != 0, nm, nullptr));
     if (!(nm.f < o.penalty)) return fail(c, KDE_E_NO_FEASIBLE, "no positive-definite H found");
     for (int k = 0; k < P; ++k) r.vechH[k] = nm.x[k];
     r.objective = nm.f;

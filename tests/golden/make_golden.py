@@ -3,7 +3,7 @@
 Calls only oracle/ (and datagen for the seeded inputs).  Each JSON file records the workload,
 the oracle outputs and the PAPER.md passages they follow.  Run (CPU, all cores, ~1 h):
 
-    python tests/golden/make_golden.py [C1] [C4] [C2] [C3] [C5]
+    python tests/golden/make_golden.py [C1] [C4] [C2] [C3] [C5] [C4b] [T2048] [C5small] [ESC]
 """
 from __future__ import annotations
 
@@ -102,8 +102,67 @@ def c5():
         "oracle_seconds": time.time() - t0, "threads": THREADS})
 
 
+def c4b():
+    """A second n = 2^20 PLUGIN data set (MW#4 kurtotic, seed 14): the Psi-hat margin at C4 size
+    on another shape (the C4 Psi4 error rested on one seed and one mixture)."""
+    x = datagen.sample_mixture("kurtotic", 1 << 20, 14)[0]
+    t0 = time.time()
+    tr = oracle.plugin(x, threads=THREADS)
+    dump("C4b_plugin.json", {
+        "config": "C4b", "workload": "PLUGIN, n=2^20, Marron-Wand #4 kurtotic mixture, datagen seed 14",
+        "cite": "PAPER.md P:203-256 (Sec. 4.4.1 steps 1-8, Eq. 11-18), reading Z1 for Eq. 15/17",
+        "trace": tr, "oracle_seconds": time.time() - t0, "threads": THREADS})
+
+
+def t2048():
+    """Raw Psi_r pair sums on ragged n that the library evaluates with 2048-row tiles
+    (n >= 128 x 2048): n = 2^18 + 37 (r = 4, 6, 8) and n = 300001 (r = 6), skewed mixture seed 8."""
+    xs = datagen.sample_mixture("skewed", 300001, 8)[0]
+    out = []
+    t0 = time.time()
+    for n, r, g in [((1 << 18) + 37, 4, 0.12), ((1 << 18) + 37, 6, 0.2), ((1 << 18) + 37, 8, 0.3),
+                    (300001, 6, 0.18)]:
+        S = oracle.psi_pairsum(xs[:n], r, g, threads=THREADS)
+        out.append({"n": n, "r": r, "g": g, "S": S})
+        print(out[-1], flush=True)
+    dump("T2048_psi.json", {
+        "config": "T2048", "workload": "raw Psi_r sums sum_{i<j} He_r(u) exp(-u^2/2), u = (x_i - x_j)/g, "
+        "first n samples of datagen.sample_mixture('skewed', 300001, 8)",
+        "cite": "PAPER.md P:227-247 (Eq. 15, 17 pair sums); tiling P:539-566", "cases": out,
+        "oracle_seconds": time.time() - t0, "threads": THREADS})
+
+
+def esc():
+    """Raw Psi sums for the automatic-precision decision tests: skewed seed 7, n = 131109 at
+    (r, g) = (8, 0.2) (kappa ~ 4e4: the fp32-term pass is re-run in fp64) and (6, 0.2) (kappa ~ 8e3:
+    it is not)."""
+    xs = datagen.sample_mixture("skewed", 131109, 7)[0]
+    out = []
+    t0 = time.time()
+    for r, g in [(8, 0.2), (6, 0.2)]:
+        out.append({"n": 131109, "r": r, "g": g, "S": oracle.psi_pairsum(xs, r, g, threads=THREADS)})
+    dump("ESC_psi.json", {
+        "config": "ESC", "workload": "raw Psi_r sums, datagen.sample_mixture('skewed', 131109, 7)",
+        "cite": "PAPER.md P:227-247 (Eq. 15, 17 pair sums)", "cases": out,
+        "oracle_seconds": time.time() - t0, "threads": THREADS})
+
+
+def c5small():
+    """All 256 C5 candidates at n = 4096."""
+    n = 4096
+    X = datagen.config_data("C5", n=n)
+    cands = datagen.c5_candidates(n, 256)
+    t0 = time.time()
+    g = [oracle.lscv_H_score(X, c, threads=THREADS) for c in cands]
+    dump("C5small_lscv_H.json", {
+        "config": "C5small", "workload": "LSCV_H d=4, n=4096 (datagen.config_data('C5', n=4096)), all 256 "
+        "candidates datagen.c5_candidates(4096, 256)", "cite": "PAPER.md P:368-389 (Eq. 30-34)",
+        "g": g, "oracle_seconds": time.time() - t0, "threads": THREADS})
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["C1", "C4", "C2", "C3", "C5"]
     for w in which:
         print("golden", w, flush=True)
-        {"C1": c1, "C4": c4, "C2": c2, "C3": c3, "C5": c5}[w]()
+        {"C1": c1, "C4": c4, "C2": c2, "C3": c3, "C5": c5, "C4b": c4b, "T2048": t2048,
+         "C5small": c5small, "ESC": esc}[w]()

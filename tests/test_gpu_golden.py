@@ -110,3 +110,40 @@ def test_c3_lscv_H_nelder_mead_full_size(ctx):
     close = np.max(np.abs(Hg - Hor)) / np.max(np.diag(Hor)) < 1e-4
     tie = g_or_at_gpu <= gold["f"] + max(2 * eps, 1e-7) * abs(gold["f"])
     assert close or tie, (sel["vechH"], gold["vechH"], g_or_at_gpu, gold["f"])
+
+
+def test_c4b_plugin_second_full_size_dataset(ctx):
+    # A second n = 2^20 PLUGIN workload (MW#4 kurtotic, seed 14): the Psi-hat margin at full size
+    # on another shape, in the default (automatic-precision) mode.
+    gold = load("C4b_plugin.json")["trace"]
+    x = datagen.sample_mixture("kurtotic", 1 << 20, 14)
+    h, tr = ctx.plugin_h(kb.to_device(x))
+    for k in ("V_hat", "sigma_hat", "psi8_ns", "g1"):
+        assert rel(tr[k], gold[k]) < 1e-12, k
+    assert rel(tr["psi6"], gold["psi6"]) < 1e-5, (tr["psi6"], gold["psi6"])
+    assert rel(tr["psi4"], gold["psi4"]) < 1e-5, (tr["psi4"], gold["psi4"])
+    assert rel(h, gold["h"]) < 1e-4
+
+
+@pytest.mark.parametrize("case", range(4))
+def test_psi_2048_row_tiles_ragged_n(ctx, case):
+    # n >= 128 x 2048 runs the 2048-row tiles (FPsi<r, 256>); n = 2^18 + 37 and 300001 leave a
+    # ragged last column block.  Raw sums vs the oracle's (T2048 golden).
+    gold = load("T2048_psi.json")
+    c = gold["cases"][case]
+    x = datagen.sample_mixture("skewed", 300001, 8)[:, :c["n"]]
+    kind = {4: kb.SUM_PSI4, 6: kb.SUM_PSI6, 8: kb.SUM_PSI8}[c["r"]]
+    T, _, _, _ = kb.shard_tiles(kind, c["n"], 1, 0, 1)
+    assert T == 2048
+    got = kb.fixed_value(ctx.raw_sums(kind, kb.to_device(x), [c["g"]])[0]) / math.sqrt(2 * math.pi)
+    n, he0 = c["n"], {4: 3.0, 6: -15.0, 8: 105.0}[c["r"]]
+    # Psi-hat's relative error (the diagonal n K(0) term included, Eq. 15/17)
+    assert abs(2 * (got - c["S"])) / abs(2 * c["S"] + n * he0) < 1e-5, (c, got)
+
+
+def test_c5_all_256_candidates_small_n(ctx):
+    # every one of the 256 C5 candidates at n = 4096 against the oracle.
+    gold = load("C5small_lscv_H.json")
+    X = datagen.config_data("C5", n=4096)
+    got = ctx.lscv_H_scores(kb.to_device(X), datagen.c5_candidates(4096, 256))
+    np.testing.assert_allclose(got, gold["g"], rtol=1e-5)

@@ -69,3 +69,35 @@ def test_multistart_nm_on_dirty_caller_workspace():
     got = c.select_bandwidth(kb.LSCV_H, X, max_iter=60, nm_starts=4)
     c.close()
     assert np.array_equal(got["vechH"], ref["vechH"]) and got["objective"] == ref["objective"]
+
+
+@pytest.mark.parametrize("name,n,d,seed,max_iter", [("C3", 3000, 2, 41, 500), ("C3", 700, 2, 42, 40),
+                                                     ("C5", 1200, 3, 43, 500), ("C5", 900, 4, 44, 200),
+                                                     ("bimodal", 800, 1, 45, 500), ("C3", 50, 2, 46, 500),
+                                                     ("C3", 5, 2, 47, 500)])
+def test_device_nm_loop_equals_host_loop(ctx, name, n, d, seed, max_iter):
+    # The device-resident Nelder-Mead (one CUDA graph, conditional WHILE node) runs the state
+    # machine of kde_nm.cuh without FMA contraction, so on the same objective values it must take
+    # exactly the host loop's decisions: identical H bits, objective, iterations, evaluations.
+    X = datagen.sample_mixture(name, n, seed)[:d]
+    Xd = kb.to_device(X)
+    dev = ctx.select_bandwidth(kb.LSCV_H, Xd, max_iter=max_iter, nm_loop=0)
+    host = ctx.select_bandwidth(kb.LSCV_H, Xd, max_iter=max_iter, nm_loop=1)
+    assert np.array_equal(dev["vechH"], host["vechH"])
+    assert dev["objective"] == host["objective"]
+    for k in ("iterations", "evaluations", "stop_reason"):
+        assert dev[k] == host[k], k
+    # replayed graph on a second call (same key) gives the same result
+    again = ctx.select_bandwidth(kb.LSCV_H, Xd, max_iter=max_iter, nm_loop=0)
+    assert np.array_equal(again["vechH"], dev["vechH"]) and again["evaluations"] == dev["evaluations"]
+
+
+def test_device_nm_with_non_pd_proposals(ctx):
+    # A huge penalty-side start (max_iter small, near-singular data) makes the simplex propose
+    # non-PD matrices: those get the penalty on the device exactly as on the host.
+    t = np.linspace(0.0, 1.0, 400)
+    X = np.vstack([t, t + 1e-3 * np.sin(37.0 * t)])
+    Xd = kb.to_device(X)
+    dev = ctx.select_bandwidth(kb.LSCV_H, Xd, max_iter=200, nm_loop=0)
+    host = ctx.select_bandwidth(kb.LSCV_H, Xd, max_iter=200, nm_loop=1)
+    assert np.array_equal(dev["vechH"], host["vechH"]) and dev["evaluations"] == host["evaluations"]

@@ -104,12 +104,19 @@ def test_lscv_h_scores_match_oracle(ctx, d, n):
     np.testing.assert_allclose(got, ref, rtol=RTOL)
 
 
-def test_lscv_h_select_matches_oracle(ctx):
-    X = datagen.sample_mixture("bimodal", 3000, 21)
+@pytest.mark.parametrize("d", [1, 2, 3])
+def test_lscv_h_select_matches_oracle(ctx, d):
+    # d > 1 exercises Eq. 25's h0 as written (reading Z3) and the Sigma-sphered grid (row f1)
+    X = datagen.sample_mixture("bimodal", 3000, 21) if d == 1 else datagen.sample_mixture(
+        "C3" if d == 2 else "C5", 2500, 30 + d)[:d]
     got = ctx.select_bandwidth(kb.LSCV_h, dev(X), n_grid=150)
-    ref = oracle.lscv_h_select(X, n_grid=150)
+    threads = len(__import__("os").sched_getaffinity(0))
+    ref = oracle.lscv_h_select(X, n_grid=150, threads=threads)
     g_at_gpu = ref["scores"][got["iterations"]]
     eps = max(abs(g - r) / abs(r) for g, r in zip(ctx.lscv_h_scores(dev(X), ref["grid"]), ref["scores"]))
+    assert eps <= RTOL
+    # the grid brackets the same h0 (first grid point = h0 / 4)
+    assert rel(ref["grid"][0], oracle.lscv_h0(X.shape[1], d) / 4) < 1e-14
     # same grid index, or a tie within the demonstrated objective error
     assert got["iterations"] == ref["index"] or g_at_gpu - ref["scores"][ref["index"]] <= 2 * eps * abs(ref["scores"][ref["index"]])
     assert rel(got["h"], ref["h"]) < 1e-4 or got["iterations"] != ref["index"]
@@ -205,7 +212,7 @@ def test_profiled_pair_counts_partition_all_pairs(ctx, n, world):
     x = dev(datagen.sample_mixture("skewed", n, 4))
     tot = 0.0
     for r in range(world):
-        ctx.raw_sums(kb.SUM_PSI6, x, [0.3], shard=(r, world))
+        ctx.raw_sums(kb.SUM_PSI6, x, [5.0], shard=(r, world))   # g large: no tile is skipped
         tot += ctx.last_profile()["pair_evals"]
     assert tot == n * (n - 1) / 2
 
@@ -386,3 +393,70 @@ def test_limb_carry_beyond_2_23_commits(ctx):
     # and the value is the right order of magnitude (the sum of e over n(n-1)/2 pairs, e <= 1)
     n = X.shape[1]
     assert 0 < kb.fixed_value(full[0]) < n * (n - 1) / 2
+
+
+# ----------------------------------------------------------------------------- Psi at small g
+@pytest.fixture(scope="module")
+def skewed40k():
+    return datagen.sample_mixture("skewed", 40000, 7)
+
+
+@pytest.mark.parametrize("r,g", [(6, "0.01sigma"), (6, 0.02), (6, 0.05), (4, 0.02), (8, 0.05)])
+def test_psi_default_mode_small_bandwidth(ctx, skewed40k, r, g):
+    # Psi-hat(g) is defined for any g > 0 (Eq. 15/17).  At bandwidths far below the
+    # PLUGIN pilots the pair sums cancel by 10^4..10^6; the default (automatic) precision must
+    # still meet 1e-5: tile-local centring plus the fp64 re-run of passes whose kappa > 2e4.
+    X = skewed40k
+    if g == "0.01sigma":
+        g = 0.01 * float(np.std(X[0], ddof=1))
+    ctx.set_precision(0)
+    got = ctx.psi_r(dev(X), r, [g])[0]
+    ref = oracle.psi_r(X[0], r, g, threads=len(__import__("os").sched_getaffinity(0)))
+    assert rel(got, ref) <= RTOL, (r, g, got, ref, ctx.last_psi_kappa(), ctx.last_fp64_passes())
+
+
+def test_psi_automatic_precision_decisions(ctx):
+    # kappa = 2A/|2S + n He_r(0)| decides whether an fp32-term pass is re-run with fp64 terms
+    # (threshold 1e4, calibrated in profiles/r02_psi_kappa.jsonl).  Skewed mixture, n = 131109:
+    # (r, g) = (8, 0.2) has kappa ~ 4e4 and is re-run; (6, 0.2) has kappa ~ 8e3 and is not; both
+    # are within 1e-5 of the oracle's sums (ESC golden, tests/golden/make_golden.py).
+    import json, os
+    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "ESC_psi.json")
+    if not os.path.exists(p):
+        pytest.skip("ESC golden not generated")
+    gold = json.load(open(p))["cases"]
+    X = datagen.sample_mixture("skewed", 131109, 7)
+    Xd = dev(X)
+    n = X.shape[1]
+    ctx.set_precision(0)
+    for c, escalated in zip(gold, (1, 0)):
+        psi = ctx.psi_r(Xd, c["r"], [c["g"]])[0]
+        assert ctx.last_fp64_passes() == escalated, (c, ctx.last_psi_kappa())
+        assert (ctx.last_psi_kappa() > 1e4) == bool(escalated)
+        he0 = {4: 3.0, 6: -15.0, 8: 105.0}[c["r"]]
+        ref = (2 * c["S"] + n * he0) / math.sqrt(2 * math.pi) / (n * n * c["g"] ** (c["r"] + 1))
+        assert rel(psi, ref) <= RTOL, (c, psi, ref)
+
+
+@pytest.mark.parametrize("mode", [-1, 1])
+def test_psi_far_tile_skip_is_exact(ctx, mode):
+    # Sorted data: a tile whose smallest pair distance exceeds the skip gap has every term exactly
+    # 0 (fp32: the MUFU input underflows; fp64: exp underflows), so skipping it changes no bit.
+    import os
+    X = dev(datagen.sample_mixture("skewed", 131109 if mode < 0 else 20000, 7))
+    ctx.set_precision(mode)
+    try:
+        for kind in (kb.SUM_PSI4, kb.SUM_PSI6, kb.SUM_PSI8):
+            a = ctx.raw_sums(kind, X, [0.03, 0.2])
+            evaluated = ctx.last_profile()["pair_evals"]
+            os.environ["KDE_DEBUG_PSI_NOSKIP"] = "1"
+            try:
+                b = ctx.raw_sums(kind, X, [0.03, 0.2])
+                full = ctx.last_profile()["pair_evals"]
+            finally:
+                del os.environ["KDE_DEBUG_PSI_NOSKIP"]
+            assert [f.key() for f in a] == [f.key() for f in b]
+            if mode < 0:
+                assert evaluated < full   # g = 0.03: most tiles are skipped
+    finally:
+        ctx.set_precision(0)
