@@ -58,6 +58,30 @@ __device__ __forceinline__ f2 exp2_sw2(f2 q) {
             q1 >= -125.f ? __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23)) : 0.f);
 }
 
+// As exp2_sw2 without the zero select: the argument is clamped to >= -125, so arguments below
+// return 2^-125 (~2.4e-38, an absolute error far below any term that matters) instead of 0.  One
+// FMNMX per lane plus the magic-number split, the degree-5 polynomial and one LEA per lane: no
+// compare, no predication.  Callers mask invalid pairs themselves.
+__device__ __forceinline__ f2 exp2_sw2_fast(f2 q) {
+  float q0, q1;
+  upk(q, q0, q1);
+  const f2 a = pk(fmaxf(q0, -125.f), fmaxf(q1, -125.f));
+  const f2 magic = pk(12582912.f, 12582912.f);   // 1.5 * 2^23
+  const f2 t = add2(a, magic);
+  const f2 fr = sub2(a, sub2(t, magic));
+  f2 p = fma2(pk(1.3276472454890609e-03f, 1.3276472454890609e-03f), fr,
+              pk(9.675540961325169e-03f, 9.675540961325169e-03f));
+  p = fma2(p, fr, pk(5.550713092088699e-02f, 5.550713092088699e-02f));
+  p = fma2(p, fr, pk(2.4022120237350464e-01f, 2.4022120237350464e-01f));
+  p = fma2(p, fr, pk(6.931469440460205e-01f, 6.931469440460205e-01f));
+  p = fma2(p, fr, pk(1.0000001192092896f, 1.0000001192092896f));
+  float t0, t1, p0, p1;
+  upk(t, t0, t1);
+  upk(p, p0, p1);
+  return pk(__int_as_float(__float_as_int(p0) + (__float_as_int(t0) << 23)),
+            __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23)));
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

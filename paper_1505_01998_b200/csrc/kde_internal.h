@@ -18,6 +18,7 @@ constexpr int kMaxDim = 16;
 // cross-rank sum each rank's limbs are normalised (normalize_limbs) so the int64 sums cannot wrap.
 constexpr int kLimbs = 4;
 constexpr int kMaxDevices = 64;   // per-device caches of one-time kernel setup
+constexpr int kWorkCounters = 1024;   // dynamic-scheduling counters the workspace holds after the limbs
 
 // Current CUDA device (per-device caches: the dynamic shared-memory opt-in is a device attribute).
 inline int current_device() {
@@ -67,6 +68,9 @@ struct LaunchCfg {
   const float* centres = nullptr;
   unsigned long long* skipped = nullptr;   // Psi: pairs of skipped (exactly zero) tiles, or null
   double skip_gap = kPsiSkipGap32;         // Psi: skip tiles whose sorted gap exceeds this (inf: never)
+  // Dynamic tile scheduling: a unit counter that is 0 when the launch starts (the caller zeroes it
+  // with the limbs), or null for the static stride.
+  unsigned long long* work = nullptr;
   // Sets whose count is decided on the device (the device-resident Nelder–Mead): the kernel reads
   // *n_sets_dev (<= n_sets, which sizes the grid).
   const int* n_sets_dev = nullptr;

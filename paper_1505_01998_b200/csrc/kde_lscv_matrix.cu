@@ -12,7 +12,7 @@ template <int D>
 static cudaError_t lscv_white_d(const LaunchCfg& c) {
   LscvScalarParams p{};
   if constexpr (D <= 4)   // large n: 1024-row tiles, 512 threads at 2 CTAs/SM (tile_for)
-    if (c.tile == 1024) return launch_pair<FLscvScalar<D, 512, 1, true, false, 2>>(c, p);
+    if (c.tile == 1024) return launch_pair<FLscvScalar<D, 512, 1, true, 0u, 2>>(c, p);
   return c.tile == 256 ? launch_pair<FLscvScalar<D, 128, 1, true>>(c, p)
                        : launch_pair<FLscvScalar<D, 256, 1, true>>(c, p);
 }
@@ -21,7 +21,7 @@ template <int D>
 static cudaError_t prepare_white_d(const LaunchCfg& c) {
   int occ;
   if constexpr (D <= 4)
-    if (c.tile == 1024) return pair_occupancy<FLscvScalar<D, 512, 1, true, false, 2>>(&occ);
+    if (c.tile == 1024) return pair_occupancy<FLscvScalar<D, 512, 1, true, 0u, 2>>(&occ);
   return c.tile == 256 ? pair_occupancy<FLscvScalar<D, 128, 1, true>>(&occ)
                        : pair_occupancy<FLscvScalar<D, 256, 1, true>>(&occ);
 }

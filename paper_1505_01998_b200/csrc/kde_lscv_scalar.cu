@@ -10,9 +10,31 @@ namespace kde {
 // d <= 4: 8 candidates per pair visit at 3 CTAs/SM, a quarter of the exponentials in software on
 // the FMA pipe (measured on C2: 478 ms vs 490 ms for 16 candidates, all on MUFU); d > 4: the
 // per-pair work dominates, 16 candidates on MUFU.
+// Software-exp column masks (bit j mod 16): KDE_DEBUG_LSCVh_SW selects an A/B variant for d = 1
+// (diagnostics only; results stay deterministic for each setting).
+constexpr unsigned kSwDefault = 0x8888u;   // columns 3, 7, 11, 15 of every 16: a quarter
+
+static int sw_variant() {
+  static const char* e = getenv("KDE_DEBUG_LSCVh_SW");
+  return e ? atoi(e) : 0;
+}
+
 template <int D>
 static cudaError_t lscv_scalar_d(const LaunchCfg& c, const LscvScalarParams& p) {
-  if constexpr (D <= 4) return launch_pair<FLscvScalar<D, 256, nb_scalar(D), false, true, 3>>(c, p);
+  if constexpr (D == 1) {
+    switch (sw_variant()) {
+      case 1: return launch_pair<FLscvScalar<1, 256, 8, false, 0x8888u, 3, true>>(c, p);   // round-1 kernel
+      case 2: return launch_pair<FLscvScalar<1, 256, 8, false, 0x888Au, 3>>(c, p);         // 5/16
+      case 3: return launch_pair<FLscvScalar<1, 256, 8, false, 0x0888u, 3>>(c, p);         // 3/16
+      case 4: return launch_pair<FLscvScalar<1, 256, 8, false, 0x8A8Au, 3>>(c, p);         // 6/16
+      case 5: return launch_pair<FLscvScalar<1, 256, 8, false, 0x0808u, 3>>(c, p);         // 2/16
+      case 6: return launch_pair<FLscvScalar<1, 256, 8, false, 0x4210u, 3>>(c, p);         // 3/16 spread
+      case 7: return launch_pair<FLscvScalar<1, 256, 8, false, 0x1248u, 3>>(c, p);         // 4/16 spread
+      case 8: return launch_pair<FLscvScalar<1, 256, 8, false, 0x0888u, 3, true>>(c, p);   // 3/16, select exp
+      default: break;
+    }
+  }
+  if constexpr (D <= 4) return launch_pair<FLscvScalar<D, 256, nb_scalar(D), false, kSwDefault, 3>>(c, p);
   else return launch_pair<FLscvScalar<D, 256, nb_scalar(D)>>(c, p);
 }
 

@@ -26,15 +26,33 @@ namespace kde {
 
 constexpr int kNMMaxP = kMaxDim * (kMaxDim + 1) / 2;   // 136 parameters at d = 16
 
-struct NMState {
+// PMAX = capacity in parameters: kNMMaxP for the host / the global device block, small for the
+// device's shared-memory working copy (d <= 4); the arithmetic does not depend on PMAX.
+template <int PMAX>
+struct NMStateT {
   enum Phase { INIT = 0, STEP = 1, SERIAL_R = 2, SERIAL_1 = 3, SHRINK = 4, DONE = 5 };
   int P = 0;                    // parameters (vertices P + 1)
   int phase = INIT, it = 0, max_iter = 500, stop = 2, serial_pick = 0, speculative = 0;
   double tol = 1e-7, fr = 0.0;
-  double sim[kNMMaxP + 1][kNMMaxP];
-  double fs[kNMMaxP + 1];
-  double xbar[kNMMaxP], xr[kNMMaxP], xe[kNMMaxP], xc[kNMMaxP], xcc[kNMMaxP];
+  double sim[PMAX + 1][PMAX];
+  double fs[PMAX + 1];
+  double xbar[PMAX], xr[PMAX], xe[PMAX], xc[PMAX], xcc[PMAX];
 };
+using NMState = NMStateT<kNMMaxP>;
+
+// Copy the used part of one state into another of a different capacity.
+template <int A, int B>
+KDE_HD inline void nm_state_copy(NMStateT<A>& d, const NMStateT<B>& s) {
+  d.P = s.P; d.phase = s.phase; d.it = s.it; d.max_iter = s.max_iter; d.stop = s.stop;
+  d.serial_pick = s.serial_pick; d.speculative = s.speculative; d.tol = s.tol; d.fr = s.fr;
+  for (int v = 0; v <= s.P; ++v) {
+    d.fs[v] = s.fs[v];
+    for (int k = 0; k < s.P; ++k) d.sim[v][k] = s.sim[v][k];
+  }
+  for (int k = 0; k < s.P; ++k) {
+    d.xbar[k] = s.xbar[k]; d.xr[k] = s.xr[k]; d.xe[k] = s.xe[k]; d.xc[k] = s.xc[k]; d.xcc[k] = s.xcc[k];
+  }
+}
 
 // r = a + s (b - c), component by component (the one combination formula of the method)
 KDE_HD inline void nm_comb(double* r, const double* a, double s, const double* b, const double* c, int P) {
@@ -46,7 +64,8 @@ KDE_HD inline void nm_copy(double* d, const double* s, int P) {
 }
 
 // Sort (stable, by f then vertex index), test the stopping rule, prepare the trial points.
-KDE_HD inline void nm_begin_iteration(NMState& s) {
+template <class St>
+KDE_HD inline void nm_begin_iteration(St& s) {
   const int M = s.P;
   for (int i = 1; i <= M; ++i) {               // insertion sort: stable, the order of std::stable_sort
     int j = i;
@@ -56,8 +75,8 @@ KDE_HD inline void nm_begin_iteration(NMState& s) {
       --j;
     }
   }
-  if (s.fs[M] - s.fs[0] <= s.tol * fabs(s.fs[0])) { s.stop = 1; s.phase = NMState::DONE; return; }
-  if (s.it >= s.max_iter) { s.stop = 2; s.phase = NMState::DONE; return; }
+  if (s.fs[M] - s.fs[0] <= s.tol * fabs(s.fs[0])) { s.stop = 1; s.phase = St::DONE; return; }
+  if (s.it >= s.max_iter) { s.stop = 2; s.phase = St::DONE; return; }
   ++s.it;
   for (int k = 0; k < s.P; ++k) s.xbar[k] = 0.0;
   for (int v = 0; v < M; ++v)
@@ -67,26 +86,27 @@ KDE_HD inline void nm_begin_iteration(NMState& s) {
   nm_comb(s.xe, s.xbar, 2.0, s.xr, s.xbar, s.P);
   nm_comb(s.xc, s.xbar, 0.5, s.xr, s.xbar, s.P);
   nm_comb(s.xcc, s.xbar, 0.5, s.sim[M], s.xbar, s.P);
-  s.phase = s.speculative ? NMState::STEP : NMState::SERIAL_R;
+  s.phase = s.speculative ? St::STEP : St::SERIAL_R;
 }
 
-// Points needed next, written row by row (stride kNMMaxP) into out; returns how many.
-KDE_HD inline int nm_propose(const NMState& s, double (*out)[kNMMaxP]) {
+// Points needed next, written row by row (stride OUT) into out; returns how many.
+template <class St, int OUT>
+KDE_HD inline int nm_propose(const St& s, double (*out)[OUT]) {
   switch (s.phase) {
-    case NMState::INIT:
+    case St::INIT:
       for (int v = 0; v <= s.P; ++v) nm_copy(out[v], s.sim[v], s.P);
       return s.P + 1;
-    case NMState::STEP:
+    case St::STEP:
       nm_copy(out[0], s.xr, s.P); nm_copy(out[1], s.xe, s.P);
       nm_copy(out[2], s.xc, s.P); nm_copy(out[3], s.xcc, s.P);
       return 4;
-    case NMState::SERIAL_R:
+    case St::SERIAL_R:
       nm_copy(out[0], s.xr, s.P);
       return 1;
-    case NMState::SERIAL_1:
+    case St::SERIAL_1:
       nm_copy(out[0], s.serial_pick == 1 ? s.xe : (s.serial_pick == 2 ? s.xc : s.xcc), s.P);
       return 1;
-    case NMState::SHRINK:
+    case St::SHRINK:
       for (int v = 1; v <= s.P; ++v) nm_comb(out[v - 1], s.sim[0], 0.5, s.sim[v], s.sim[0], s.P);
       return s.P;
     default:
@@ -95,41 +115,43 @@ KDE_HD inline int nm_propose(const NMState& s, double (*out)[kNMMaxP]) {
 }
 
 // Decide with f_r known and (speculatively or not) the one follow-up value.
-KDE_HD inline void nm_decide(NMState& s, double fr, bool have_follow, double fe, double fc, double fcc) {
+template <class St>
+KDE_HD inline void nm_decide(St& s, double fr, bool have_follow, double fe, double fc, double fcc) {
   const int M = s.P;
   if (fr < s.fs[0]) {
-    if (!have_follow) { s.serial_pick = 1; s.fr = fr; s.phase = NMState::SERIAL_1; return; }
+    if (!have_follow) { s.serial_pick = 1; s.fr = fr; s.phase = St::SERIAL_1; return; }
     if (fe < fr) { nm_copy(s.sim[M], s.xe, s.P); s.fs[M] = fe; } else { nm_copy(s.sim[M], s.xr, s.P); s.fs[M] = fr; }
     nm_begin_iteration(s);
     return;
   }
   if (fr < s.fs[M - 1]) { nm_copy(s.sim[M], s.xr, s.P); s.fs[M] = fr; nm_begin_iteration(s); return; }
   if (fr < s.fs[M]) {
-    if (!have_follow) { s.serial_pick = 2; s.fr = fr; s.phase = NMState::SERIAL_1; return; }
+    if (!have_follow) { s.serial_pick = 2; s.fr = fr; s.phase = St::SERIAL_1; return; }
     if (fc <= fr) { nm_copy(s.sim[M], s.xc, s.P); s.fs[M] = fc; nm_begin_iteration(s); return; }
   } else {
-    if (!have_follow) { s.serial_pick = 3; s.fr = fr; s.phase = NMState::SERIAL_1; return; }
+    if (!have_follow) { s.serial_pick = 3; s.fr = fr; s.phase = St::SERIAL_1; return; }
     if (fcc < s.fs[M]) { nm_copy(s.sim[M], s.xcc, s.P); s.fs[M] = fcc; nm_begin_iteration(s); return; }
   }
-  s.phase = NMState::SHRINK;
+  s.phase = St::SHRINK;
 }
 
 // Values g[0 .. count) of the points nm_propose() listed.
-KDE_HD inline void nm_accept(NMState& s, const double* g) {
+template <class St>
+KDE_HD inline void nm_accept(St& s, const double* g) {
   switch (s.phase) {
-    case NMState::INIT:
+    case St::INIT:
       for (int v = 0; v <= s.P; ++v) s.fs[v] = g[v];
       nm_begin_iteration(s);
       break;
-    case NMState::STEP: nm_decide(s, g[0], true, g[1], g[2], g[3]); break;
-    case NMState::SERIAL_R: nm_decide(s, g[0], false, 0.0, 0.0, 0.0); break;
-    case NMState::SERIAL_1: {
+    case St::STEP: nm_decide(s, g[0], true, g[1], g[2], g[3]); break;
+    case St::SERIAL_R: nm_decide(s, g[0], false, 0.0, 0.0, 0.0); break;
+    case St::SERIAL_1: {
       const double v = g[0];
       nm_decide(s, s.fr, true, s.serial_pick == 1 ? v : 0.0, s.serial_pick == 2 ? v : 0.0,
                 s.serial_pick == 3 ? v : 0.0);
       break;
     }
-    case NMState::SHRINK:
+    case St::SHRINK:
       for (int v = 1; v <= s.P; ++v) {
         nm_comb(s.sim[v], s.sim[0], 0.5, s.sim[v], s.sim[0], s.P);
         s.fs[v] = g[v - 1];

@@ -31,6 +31,7 @@ struct NMDevHeader {
   double nn, pow4, pow2, penalty, wscale;
   double mean[kMaxDim];
   unsigned long long* limbs;   // 2 outputs (sum e, sum e^2) x kLimbs per set
+  unsigned long long* work;    // the pair kernel's dynamic-scheduling counter
   PrepParams* pp;              // max_sets entries
 };
 
@@ -48,50 +49,75 @@ __device__ __forceinline__ double limbs_value(const unsigned long long* l, int S
   return ldexp((double)limbs_total(l), -S);
 }
 
-__global__ void nm_decide_kernel(NMDevBlock* b, cudaGraphConditionalHandle cond) {
-  NMDevHeader& h = b->h;
-  NMState& s = b->st;
+// One decision step (see the file comment) on a state `s` of any capacity.
+template <class St, int OUT>
+__device__ void decide_body(NMDevHeader& h, St& s, double (*prop)[OUT], double* g, double* det, int* slot,
+                            double* L, cudaGraphConditionalHandle cond) {
   if (h.pending) {                                   // the previous round's values
     for (int i = 0; i < h.n_prop; ++i) {
-      const int k = b->slot[i];
-      b->g[i] = k < 0 ? h.penalty
-                      : nm_lscv_H_finalize(h.nn, h.pow4, h.pow2, b->det[i],
-                                           limbs_value(h.limbs + (size_t)(2 * k) * kLimbs, h.S),
-                                           limbs_value(h.limbs + (size_t)(2 * k + 1) * kLimbs, h.S));
+      const int k = slot[i];
+      g[i] = k < 0 ? h.penalty
+                   : nm_lscv_H_finalize(h.nn, h.pow4, h.pow2, det[i],
+                                        limbs_value(h.limbs + (size_t)(2 * k) * kLimbs, h.S),
+                                        limbs_value(h.limbs + (size_t)(2 * k + 1) * kLimbs, h.S));
     }
     h.evals += h.n_sets;
-    nm_accept(s, b->g);
+    nm_accept(s, g);
     h.pending = 0;
   }
   while (true) {
-    if (s.phase == NMState::DONE) {
+    if (s.phase == St::DONE) {
       h.n_sets = 0;
       cudaGraphSetConditional(cond, 0);
       return;
     }
-    h.n_prop = nm_propose(s, b->prop);
+    h.n_prop = nm_propose(s, prop);
     h.n_sets = 0;
     for (int i = 0; i < h.n_prop; ++i) {
-      double det = 0.0;
-      if (nm_cholesky_vech(b->prop[i], h.d, b->L, &det)) {
+      double dt = 0.0;
+      if (nm_cholesky_vech(prop[i], h.d, L, &dt)) {
         const int k = h.n_sets++;
-        b->slot[i] = k;
-        b->det[i] = det;
-        nm_whitening(b->L, h.d, h.wscale, h.pp[k].W);
+        slot[i] = k;
+        det[i] = dt;
+        nm_whitening(L, h.d, h.wscale, h.pp[k].W);
         for (int a = 0; a < h.d; ++a) h.pp[k].mean[a] = h.mean[a];
       } else {
-        b->slot[i] = -1;
+        slot[i] = -1;
       }
     }
     if (h.n_sets == 0) {                             // every proposal non-PD: no GPU pass needed
-      for (int i = 0; i < h.n_prop; ++i) b->g[i] = h.penalty;
-      nm_accept(s, b->g);
+      for (int i = 0; i < h.n_prop; ++i) g[i] = h.penalty;
+      nm_accept(s, g);
       continue;
     }
     for (size_t k = 0; k < (size_t)2 * h.n_sets * kLimbs; ++k) h.limbs[k] = 0ull;
+    *h.work = 0ull;
     h.pending = 1;
     ++h.rounds;
     return;
+  }
+}
+
+// d <= 4 (P <= 10): the decision runs on a shared-memory copy of the state (one thread; global
+// memory latency would otherwise dominate the step); larger d works on the global block.
+constexpr int kSmallP = 10;
+
+__global__ void nm_decide_kernel(NMDevBlock* b, cudaGraphConditionalHandle cond) {
+  if (b->st.P <= kSmallP) {
+    __shared__ alignas(16) unsigned char sbuf[sizeof(NMStateT<kSmallP>)];
+    __shared__ double sprop[kSmallP + 1][kSmallP], sg[kSmallP + 1], sdet[kSmallP + 1], sL[kMaxDim * kMaxDim];
+    __shared__ int sslot[kSmallP + 1];
+    __shared__ NMDevHeader sh;
+    NMStateT<kSmallP>& ss = *reinterpret_cast<NMStateT<kSmallP>*>(sbuf);
+    sh = b->h;
+    nm_state_copy(ss, b->st);
+    for (int i = 0; i <= kSmallP; ++i) { sdet[i] = b->det[i]; sslot[i] = b->slot[i]; }
+    decide_body(sh, ss, sprop, sg, sdet, sslot, sL, cond);
+    nm_state_copy(b->st, ss);
+    for (int i = 0; i <= kSmallP; ++i) { b->det[i] = sdet[i]; b->slot[i] = sslot[i]; }
+    b->h = sh;
+  } else {
+    decide_body(b->h, b->st, b->prop, b->g, b->det, b->slot, b->L, cond);
   }
 }
 
@@ -136,6 +162,7 @@ kde_status nelder_mead_device(kde_ctx* c, const double* X, int64_t n, int d, con
   h.penalty = penalty; h.wscale = std::sqrt(kLog2e / 4.0);
   for (int a = 0; a < d; ++a) h.mean[a] = m.mean[a];
   h.limbs = w.limbs; h.pp = pp;
+  h.work = w.limbs + (size_t)2 * max_sets * kLimbs;
   NMState& s = hb->st;
   s.P = P; s.max_iter = max_iter; s.tol = tol; s.speculative = 0; s.phase = NMState::INIT; s.it = 0; s.stop = 2;
   for (int v = 0; v <= P; ++v)
@@ -176,6 +203,7 @@ kde_status nelder_mead_device(kde_ctx* c, const double* X, int64_t n, int d, con
         cfg.X = Yw; cfg.n = n; cfg.ld = ld; cfg.tile = T; cfg.scale_exp = h.S; cfg.limbs = w.limbs;
         cfg.n_out = 2; cfg.stream = c->cap_stream; cfg.sm_count = c->sm_count; cfg.clamp = nullptr;
         cfg.n_sets = max_sets; cfg.set_stride = set_floats; cfg.n_sets_dev = &dblk->h.n_sets;
+        cfg.work = w.limbs + (size_t)2 * max_sets * kLimbs;
         shard_range(n_tiles(n, T), 0, 1, &cfg.tile_begin, &cfg.tile_end);
         le = kde::launch_lscv_white(d, cfg);
       }

@@ -72,7 +72,20 @@ struct Args {
   unsigned long long* skipped;       // Psi: counter of pairs in skipped tiles, or null
   const int* n_sets_dev;             // sets: the count in device memory (device-resident loops), or null
   double skip_gap;                   // Psi: tiles with a larger sorted gap are exactly zero
+  unsigned long long* work;          // dynamic scheduling: unit counter (zero at launch), or null
 };
+
+// Work distribution.  Static: CTA b takes units b, b + grid, ...  Dynamic (a.work != null): CTA b
+// starts with unit b and then takes grid + atomicAdd(work, 1) one unit ahead (so the next unit's TMA
+// still overlaps the current one), broadcast through shared memory; units whose cost varies
+// (skipped exact-zero tiles, diagonal tiles, ragged tails) then cannot leave a CTA behind.  The
+// result is independent of the assignment (exact limbs), so both are deterministic.
+__device__ __forceinline__ int64_t next_unit_issue(const Args& a, int64_t u, int64_t* s_next, uint32_t k) {
+  if (a.work == nullptr) return u + gridDim.x;
+  if (threadIdx.x == 0) s_next[(k + 1) & 1] = (int64_t)gridDim.x + (int64_t)atomicAdd(a.work, 1ull);
+  __syncthreads();
+  return s_next[(k + 1) & 1];
+}
 
 // ------------------------------------------------------------------ functors
 
@@ -244,9 +257,11 @@ struct FPsi {
 // UNIT (LSCV_H, one candidate per data set): the data are whitened by the candidate itself,
 // x' = sqrt(log2 e / 4) L_c^-1 (x - mean) with H_c = L_c L_c^T, so s = (log2 e / 4) v^T H_c^-1 v
 // and e = 2^-s (the negation is a MUFU operand modifier): 2d + 2 FP32 ops per eval.
-// SWC (LSCV_h): the exponentials of the 4th column of every 4 come from exp2_sw2 on the FMA pipe
-// instead of MUFU.EX2 (chosen by column, so a candidate's sum does not depend on its batch).
-template <int D_, int NT_, int NB_, bool UNIT = false, bool SWC = false, int MINB_ = 0>
+// SWM (LSCV_h): a 16-bit column mask; column j takes its exponentials from the software exp2 on the
+// FMA pipe (exp2_sw2_fast) instead of MUFU.EX2 when bit (j mod 16) is set (chosen by column, so a
+// candidate's sum does not depend on its batch).  SWM = 0: MUFU only.  SWSEL: the older exp2_sw2
+// (compare + select to exactly 0 below -125) instead of the clamp-only variant.
+template <int D_, int NT_, int NB_, bool UNIT = false, unsigned SWM = 0, int MINB_ = 0, bool SWSEL = false>
 struct FLscvScalar {
   static_assert(!UNIT || NB_ == 1, "UNIT sets carry one candidate");
   static constexpr int NT = NT_, D = D_, R = 2, T = NT_ * 2, NB = NB_, NOUT = 2 * NB_;
@@ -254,8 +269,10 @@ struct FLscvScalar {
   // unrolled x4 (C5 2.81 s vs 2.87 s at 4 CTAs; the same change costs C3 (d = 2) 4.5%)
   static constexpr int MINB = MINB_ > 0 ? MINB_ : (UNIT && D <= 3 ? 1024 : (UNIT && D == 4 ? 768 : 512)) / NT_;
   // column-loop unroll: UNIT d <= 2 x8 (C3 pair time 15.64 -> 15.37 ms), d = 3, 4 x4 (no spills);
-  // LSCV_h with software-exp columns x2 (C2 469 vs 477 ms)
-  static constexpr int UNR = UNIT && D <= 2 ? 8 : (UNIT && D <= 4 ? 4 : (SWC ? 2 : 1));
+  // LSCV_h with software-exp columns: 16 columns per iteration (the mask period)
+  static constexpr bool SW = SWM != 0;
+  static constexpr int STEP = SW ? 16 : 4;
+  static constexpr int UNR = UNIT && D <= 2 ? 8 : (UNIT && D <= 4 ? 4 : 1);
   static constexpr bool kClampable = false, kSets = UNIT;
   static constexpr int CS = 1;
   using Params = LscvScalarParams;
@@ -275,53 +292,69 @@ struct FLscvScalar {
   __device__ __forceinline__ void compute(const float* __restrict__ sc, const Params& p, bool diag,
                                           int jlim) {
     const int tid = threadIdx.x;
-    const int jend = MASK ? ((jlim + 3) & ~3) : T;
+    const int jend = MASK ? ((jlim + STEP - 1) / STEP) * STEP : T;
 #pragma unroll UNR
-    for (int j = 0; j < jend; j += 4) {
-      float cv[D][4];
+    for (int j0 = 0; j0 < jend; j0 += STEP) {
 #pragma unroll
-      for (int a = 0; a < D; ++a) {
-        const float4 c4 = *reinterpret_cast<const float4*>(sc + a * T + j);
-        cv[a][0] = c4.x; cv[a][1] = c4.y; cv[a][2] = c4.z; cv[a][3] = c4.w;
-      }
+      for (int g4 = 0; g4 < STEP; g4 += 4) {
+        const int j = j0 + g4;
+        float cv[D][4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        f2 dd = sub2(xr[0], pk(cv[0][k], cv[0][k]));
-        f2 s = mul2(dd, dd);
-#pragma unroll
-        for (int a = 1; a < D; ++a) {
-          dd = sub2(xr[a], pk(cv[a][k], cv[a][k]));
-          s = fma2(dd, dd, s);
+        for (int a = 0; a < D; ++a) {
+          const float4 c4 = *reinterpret_cast<const float4*>(sc + a * T + j);
+          cv[a][0] = c4.x; cv[a][1] = c4.y; cv[a][2] = c4.z; cv[a][3] = c4.w;
         }
-        if (MASK) {
-          const int jj = j + k;
-          float s0, s1;
-          upk(s, s0, s1);
-          const float inf = __int_as_float(0x7f800000);   // +inf -> e = 2^-inf = 0
-          const bool ok0 = (jj < jlim) && (!diag || jj > tid);
-          const bool ok1 = (jj < jlim) && (!diag || jj > NT + tid);
-          s = pk(ok0 ? s0 : inf, ok1 ? s1 : inf);
-        }
-        if (UNIT) {
-          float q0, q1;
-          upk(s, q0, q1);
-          const f2 e = pk(ex2(-q0), ex2(-q1));
-          a1[0] = add2(a1[0], e);
-          a2[0] = fma2(e, e, a2[0]);
-        } else {
 #pragma unroll
-          for (int c = 0; c < NB; ++c) {
-            const f2 q = mul2(s, pk(p.kappa[c], p.kappa[c]));
-            f2 e;
-            if (SWC && k == 3) {
-              e = exp2_sw2(q);
-            } else {
-              float q0, q1;
-              upk(q, q0, q1);
-              e = pk(ex2(q0), ex2(q1));
+        for (int k = 0; k < 4; ++k) {
+          f2 dd = sub2(xr[0], pk(cv[0][k], cv[0][k]));
+          f2 s = mul2(dd, dd);
+#pragma unroll
+          for (int a = 1; a < D; ++a) {
+            dd = sub2(xr[a], pk(cv[a][k], cv[a][k]));
+            s = fma2(dd, dd, s);
+          }
+          bool ok0 = true, ok1 = true;
+          if (MASK) {
+            const int jj = j + k;
+            float s0, s1;
+            upk(s, s0, s1);
+            const float inf = __int_as_float(0x7f800000);   // +inf -> e = 2^-inf = 0
+            ok0 = (jj < jlim) && (!diag || jj > tid);
+            ok1 = (jj < jlim) && (!diag || jj > NT + tid);
+            s = pk(ok0 ? s0 : inf, ok1 ? s1 : inf);
+          }
+          if (UNIT) {
+            float q0, q1;
+            upk(s, q0, q1);
+            const f2 e = pk(ex2(-q0), ex2(-q1));
+            a1[0] = add2(a1[0], e);
+            a2[0] = fma2(e, e, a2[0]);
+          } else {
+            constexpr bool dummy = false;
+            (void)dummy;
+#pragma unroll
+            for (int c = 0; c < NB; ++c) {
+              const f2 q = mul2(s, pk(p.kappa[c], p.kappa[c]));
+              f2 e;
+              if (SW && ((SWM >> ((g4 + k) & 15)) & 1u)) {
+                if (SWSEL) {
+                  e = exp2_sw2(q);
+                } else {
+                  e = exp2_sw2_fast(q);
+                  if (MASK) {   // masked lanes: exactly 0 (the clamp would leave 2^-125)
+                    float e0, e1;
+                    upk(e, e0, e1);
+                    e = pk(ok0 ? e0 : 0.f, ok1 ? e1 : 0.f);
+                  }
+                }
+              } else {
+                float q0, q1;
+                upk(q, q0, q1);
+                e = pk(ex2(q0), ex2(q1));
+              }
+              a1[c] = add2(a1[c], e);
+              a2[c] = fma2(e, e, a2[c]);
             }
-            a1[c] = add2(a1[c], e);
-            a2[c] = fma2(e, e, a2[c]);
           }
         }
       }
@@ -432,17 +465,20 @@ __global__ void __launch_bounds__(F::NT, F::MINB) pair_kernel(const Args a,
       tma_load_1d(dst + d * T, a.X + d * a.ld + l * T, (uint32_t)(T * sizeof(float)), &bar[buf]);
   };
   const bool clamp = F::kClampable && a.clamp != nullptr && *a.clamp != 0;   // uniform per launch
+  __shared__ int64_t s_next[2];
   int64_t u = blockIdx.x;
   if (tid == 0 && u < units) issue(u, 0);
   uint32_t k = 0;
-  for (; u < units; u += gridDim.x, ++k) {
+  while (u < units) {
     const int64_t tile = a.tile_begin + u / CS;
     int64_t l, q;
     tile_coords(tile, l, q);
-    const int64_t un = u + gridDim.x;
+    const int64_t un = next_unit_issue(a, u, s_next, k);
     if (tid == 0 && un < units) issue(un, (k + 1) & 1);
     pair_unit<F>(a, p, tile, l, q, (int)(u % CS), cols + (k & 1) * D * T, red, a.limbs, clamp, &bar[k & 1],
                  (k >> 1) & 1);
+    u = un;
+    ++k;
   }
 }
 
@@ -481,20 +517,23 @@ __global__ void __launch_bounds__(F::NT, F::MINB) pair_kernel_sets(const Args a,
   };
 
   const bool clamp = F::kClampable && a.clamp != nullptr && *a.clamp != 0;   // uniform per launch
+  __shared__ int64_t s_next[2];
   int64_t u = blockIdx.x;
   if (tid == 0 && u < units) issue(u, 0);
   uint32_t k = 0;
-  for (; u < units; u += gridDim.x, ++k) {
+  while (u < units) {
     const int64_t set = u / per;
     const int64_t tile = a.tile_begin + (u - set * per);
     int64_t l, q;
     tile_coords(tile, l, q);
-    const int64_t un = u + gridDim.x;
+    const int64_t un = next_unit_issue(a, u, s_next, k);
     if (tid == 0 && un < units) issue(un, (k + 1) & 1);
     Args as = a;
     as.X = a.X + set * a.set_stride;
     pair_unit<F>(as, p, tile, l, q, 0, cols + (k & 1) * D * T, red, a.limbs + set * NOUT * kLimbs, clamp,
                  &bar[k & 1], (k >> 1) & 1);
+    u = un;
+    ++k;
   }
 }
 
@@ -531,7 +570,7 @@ inline cudaError_t launch_pair(const LaunchCfg& c, const typename F::Params& p) 
   int64_t grid = (int64_t)c.sm_count * occ;
   if (grid > units) grid = units;
   Args a{c.X, c.n, c.ld, c.tile_begin, c.tile_end, c.scale_exp, c.limbs, c.clamp, c.n_sets, c.set_stride,
-         c.Y64, c.centres, c.skipped, c.n_sets_dev, c.skip_gap};
+         c.Y64, c.centres, c.skipped, c.n_sets_dev, c.skip_gap, c.work};
   if constexpr (F::kSets) pair_kernel_sets<F><<<(unsigned)grid, F::NT, smem, c.stream>>>(a, p);
   else pair_kernel<F><<<(unsigned)grid, F::NT, smem, c.stream>>>(a, p);
   return cudaGetLastError();

@@ -69,7 +69,8 @@ size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
 
 size_t ws_bytes(int64_t ld, int32_t d, int32_t n_out) {
   return align256((size_t)d * ld * sizeof(float)) +
-         align256((size_t)std::max(n_out, 1) * kde::kLimbs * sizeof(long long)) +
+         align256((size_t)std::max(n_out, 1) * kde::kLimbs * sizeof(long long) +
+                  (size_t)kde::kWorkCounters * sizeof(long long)) +
          align256((size_t)1024 * 136 * sizeof(double)) + align256((16 + 256 + 136 + 16) * sizeof(double));
 }
 
@@ -332,8 +333,11 @@ kde_status run_sums(kde_ctx* c, int d, int64_t n, int64_t ld, int T, int scale, 
                     const std::vector<SumLaunch>& launches, int n_out, int shard_rank,
                     int shard_world, bool allreduce, std::vector<kde_fixed>& out, bool limbs_zeroed) {
   Range rr("kde.pair_pass");
+  // dynamic-scheduling counters (one per launch) follow this run's limbs; zeroed with them
+  unsigned long long* work = w.limbs + (size_t)n_out * kde::kLimbs;
   if (!limbs_zeroed)
-    CUDA_TRY(c, cudaMemsetAsync(w.limbs, 0, (size_t)n_out * kde::kLimbs * sizeof(long long), c->stream));
+    CUDA_TRY(c, cudaMemsetAsync(w.limbs, 0, ((size_t)n_out * kde::kLimbs + launches.size()) * sizeof(long long),
+                                c->stream));
   int64_t tiles = n_tiles(n, T), tb, te;
   shard_range(tiles, shard_rank, shard_world, &tb, &te);
   const double pairs = c->profiling ? pairs_in_range(n, T, tb, te) : 0.0;
@@ -350,6 +354,7 @@ kde_status run_sums(kde_ctx* c, int d, int64_t n, int64_t ld, int T, int scale, 
     cfg.centres = L.centres;
     cfg.skipped = L.skipped;
     cfg.skip_gap = L.skip_gap;
+    cfg.work = work + (&L - launches.data());
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (c->profiling) { e0 = next_event(c); e1 = next_event(c); cudaEventRecord(e0, c->stream); }
     cudaError_t err = cudaSuccess;

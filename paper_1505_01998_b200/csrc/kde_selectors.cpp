@@ -249,8 +249,8 @@ kde_status lscv_H_raw(kde_ctx* c, const double* X, int64_t n, int d, const std::
     TRY(grow(c, &c->white_ws, &c->white_bytes, (size_t)cnt * set_floats * sizeof(float)));
     float* Yw = static_cast<float*>(c->white_ws);
     // prep flags and this launch's limbs are one contiguous span of the workspace (get_ws): one memset
-    const size_t span = (size_t)(reinterpret_cast<char*>(w.limbs + (size_t)2 * cnt * kde::kLimbs) -
-                                 reinterpret_cast<char*>(w.flag()));
+    const size_t span = (size_t)(reinterpret_cast<char*>(w.limbs + (size_t)2 * cnt * kde::kLimbs + 1) -
+                                 reinterpret_cast<char*>(w.flag()));   // + run_sums' one work counter
     CUDA_TRY(c, cudaMemsetAsync(w.flag(), 0, span, c->stream));
     for (int j = 0; j < cnt; ++j)
       TRY(gpu_prep_into(c, X, n, d, cands[b0 + j].W, m.mean, ld, w, Yw + (size_t)j * set_floats));
@@ -321,7 +321,7 @@ kde_status kde_psi_r(kde_ctx* c, const double* x, int64_t n, int32_t r, const do
 // tiles into `limbs` (S, A), then (world > 1) the all-reduce, all enqueued on the context stream.
 static kde_status plugin_pass(kde_ctx* c, int r, int64_t n, int64_t ld, int T, int S, const PsiBufs& b,
                               unsigned long long* clamp, unsigned long long* limbs, int64_t tb, int64_t te,
-                              double pairs, unsigned long long* skipped) {
+                              double pairs, unsigned long long* skipped, unsigned long long* work) {
   Range rr("kde.pair_pass");
   kde::LaunchCfg cfg;
   cfg.X = b.Yc; cfg.n = n; cfg.ld = ld; cfg.tile_begin = tb; cfg.tile_end = te; cfg.tile = T;
@@ -329,6 +329,7 @@ static kde_status plugin_pass(kde_ctx* c, int r, int64_t n, int64_t ld, int T, i
   cfg.clamp = clamp; cfg.Y64 = b.Y64; cfg.centres = b.centres;
   cfg.skipped = skipped;
   cfg.skip_gap = kde::psi_skip_gap(false);
+  cfg.work = work;
   kde::PsiParams p;
   psi_coeffs(r, p);
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -379,14 +380,15 @@ static kde_status plugin_enqueue(kde_ctx* c, const double* x, int64_t n, int T, 
   const int S6 = scale_exp_for(2.0 * 15.0, n), S4 = scale_exp_for(2.0 * 3.0, n);
   const int mode = c->psi_mode;
   unsigned long long* L = w.limbs;                       // [S6, A6, S4, A4, S6 fp64, S4 fp64]
-  CUDA_TRY(c, cudaMemsetAsync(L, 0, kde::kPluginOuts * kde::kLimbs * sizeof(long long), st));
+  unsigned long long* work = L + kde::kPluginOuts * kde::kLimbs;   // one scheduling counter per pass
+  CUDA_TRY(c, cudaMemsetAsync(L, 0, (kde::kPluginOuts * kde::kLimbs + 2) * sizeof(long long), st));
   const int Ss[2] = {S6, S4};
   for (int k = 0; k < 2; ++k) {                                                        // Psi6(g1), Psi4(g2)
     const int r = k == 0 ? 6 : 4;
     CUDA_TRY(c, kde::launch_psi_prep(xs, n, dv.mean, dv.W, T, b.Y64, b.Yc, b.centres, ld, st, w.flag(), 3.0e4));
     if (mode != 1)
       TRY(plugin_pass(c, r, n, ld, T, Ss[k], b, w.flag() + 1, L + (size_t)(2 * k) * kde::kLimbs, tb, te, pairs,
-                      reinterpret_cast<unsigned long long*>(w.small + kde::kSkippedSlot)));
+                      reinterpret_cast<unsigned long long*>(w.small + kde::kSkippedSlot), work + k));
     CUDA_TRY(c, kde::launch_plugin_chain(4 + k, n, w.small, L, Ss[k], st, mode));     // fp64 re-run?
     TRY(psi64_pass(c, r, b.Y64, n, Ss[k], L + (size_t)(4 + k) * kde::kLimbs, dv.gate + k, k));
     CUDA_TRY(c, kde::launch_plugin_chain(k == 0 ? 2 : 3, n, w.small, L, Ss[k], st));  // steps 5-6 / 7-8

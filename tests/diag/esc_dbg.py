@@ -17,3 +17,10 @@ for r, g in [(8, 0.2), (6, 0.2), (8, 0.05)]:
         del os.environ["KDE_DEBUG_PSI_NOSKIP"]
         out[f"mode{mode}_noskip"] = S2
     print(json.dumps(out), flush=True)
+# psi_r (the public call) on the same data, in every mode
+for mode in (-1, 0, 1):
+    ctx.set_precision(mode)
+    for r, g in [(8, 0.2), (6, 0.2)]:
+        v = ctx.psi_r(Xd, r, [g])[0]
+        ref = oracle.psi_r(X[0], r, g, threads=len(os.sched_getaffinity(0)))
+        print(json.dumps({"psi_r": True, "mode": mode, "r": r, "g": g, "got": v, "ref": ref, "passes": ctx.last_fp64_passes()}), flush=True)

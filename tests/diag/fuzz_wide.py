@@ -26,6 +26,8 @@ def main():
     nmax = int(sys.argv[4]) if len(sys.argv) > 4 else 4000
     ctx = kb.Context()
     worst = {"psi": 0.0, "lscv_h": 0.0, "lscv_H": 0.0}
+    worst_pt = {"lscv_h": 0.0, "lscv_H": 0.0}   # pointwise |got - ref| / |ref| (north_star criterion)
+    near_zero = []
     bad = []
     for c in range(cases):
         n = int(rng.integers(2, nmax))
@@ -49,14 +51,24 @@ def main():
         for fam, got, ref in (("lscv_h", ctx.lscv_h_scores(Xd, hs), oracle.lscv_h_scores(X, hs)),
                               ("lscv_H", ctx.lscv_H_scores(Xd, [datagen.vech(h * h * S) for h in hs]),
                                [oracle.lscv_H_score(X, datagen.vech(h * h * S)) for h in hs])):
-            # relative to the curve's scale: an objective can cross zero between grid points
-            # (case 28 of seed 7: g = 7.4e-8 between 3.0e-3 and -9.0e-5), where a pointwise
-            # relative error says nothing about the kernel
-            e = float(np.max(np.abs(np.asarray(got) - ref)) / np.max(np.abs(ref)))
+            # Two measures.  Pointwise relative error (the north_star 1e-5 criterion), reported
+            # in full; and relative to the curve's scale, because an objective can cross zero
+            # between grid points (case 28 of seed 7: g = 7.4e-8 between 3.0e-3 and -9.0e-5),
+            # where the pointwise ratio measures the cancellation of g itself, not the kernel.
+            got, ref = np.asarray(got), np.asarray(ref)
+            pt = np.abs(got - ref) / np.abs(ref)
+            e = float(np.max(np.abs(got - ref)) / np.max(np.abs(ref)))
             worst[fam] = max(worst[fam], e)
+            worst_pt[fam] = max(worst_pt[fam], float(pt.max()))
+            for k in range(len(hs)):
+                if pt[k] > 1e-5:
+                    zc = abs(ref[k]) < 1e-3 * np.max(np.abs(ref))
+                    (near_zero if zc else bad).append((fam, n, d, scale, float(hs[k]), float(ref[k]), float(pt[k])))
             if e > 1e-5:
-                bad.append((fam, n, d, scale, e))
-    print("cases", cases, "worst", worst)
+                bad.append((fam, n, d, scale, "curve-scale", e))
+    print("cases", cases, "worst (curve scale)", worst, "worst (pointwise)", worst_pt)
+    for z in near_zero:
+        print("pointwise > 1e-5 at |g| < 1e-3 max|g| (zero crossing):", z)
     for b in bad:
         print("OVER 1e-5:", b)
 

@@ -137,8 +137,9 @@ def test_psi_2048_row_tiles_ragged_n(ctx, case):
     assert T == 2048
     got = kb.fixed_value(ctx.raw_sums(kind, kb.to_device(x), [c["g"]])[0]) / math.sqrt(2 * math.pi)
     n, he0 = c["n"], {4: 3.0, 6: -15.0, 8: 105.0}[c["r"]]
-    # Psi-hat's relative error (the diagonal n K(0) term included, Eq. 15/17)
-    assert abs(2 * (got - c["S"])) / abs(2 * c["S"] + n * he0) < 1e-5, (c, got)
+    # Psi-hat's relative error (the diagonal n K^(r)(0) term included, Eq. 15/17; the oracle's
+    # pair sums include the kernel's 1/sqrt(2 pi))
+    assert abs(2 * (got - c["S"])) / abs(2 * c["S"] + n * he0 / math.sqrt(2 * math.pi)) < 1e-5, (c, got)
 
 
 def test_c5_all_256_candidates_small_n(ctx):

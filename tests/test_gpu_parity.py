@@ -434,7 +434,8 @@ def test_psi_automatic_precision_decisions(ctx):
         assert ctx.last_fp64_passes() == escalated, (c, ctx.last_psi_kappa())
         assert (ctx.last_psi_kappa() > 1e4) == bool(escalated)
         he0 = {4: 3.0, 6: -15.0, 8: 105.0}[c["r"]]
-        ref = (2 * c["S"] + n * he0) / math.sqrt(2 * math.pi) / (n * n * c["g"] ** (c["r"] + 1))
+        # the oracle's pair sums include the kernel's 1/sqrt(2 pi) (K^(r) = He_r phi)
+        ref = (2 * c["S"] + n * he0 / math.sqrt(2 * math.pi)) / (n * n * c["g"] ** (c["r"] + 1))
         assert rel(psi, ref) <= RTOL, (c, psi, ref)
 
 
