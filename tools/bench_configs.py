@@ -65,12 +65,17 @@ def sm_clock():
         return None
 
 
-def line(cfg, what, dt, prof, extra=None):
+def line(cfg, what, dt, prof, extra=None, alg=None):
+    # evals = evaluated pair-kernel evaluations (the library's profile leaves out the pairs of tiles
+    # skipped as exactly zero); alg = algorithmic evaluations (all pairs x candidates), when known
     ev = prof["pair_evals"]
     d = {"config": cfg, "what": what, "gpus": 1, "sm_clock_mhz": sm_clock(), "wall_ms": dt * 1e3, "pair_ms": prof["pair_ms"],
          "pair_launches": prof["pair_launches"], "evals": ev,
          "evals_per_s_pair": ev / (prof["pair_ms"] / 1e3) if prof["pair_ms"] > 0 else None,
          "frac_mufu_peak": (ev / (prof["pair_ms"] / 1e3)) / PEAK if prof["pair_ms"] > 0 else None}
+    if alg is not None:
+        d.update({"evals_algorithmic": alg, "evaluated_fraction": ev / alg,
+                  "algorithmic_evals_per_s_wall": alg / dt})
     if extra:
         d.update(extra)
     print(json.dumps(d), flush=True)
@@ -91,7 +96,7 @@ def run(cfg, reps):
         x = kb.to_device(datagen.config_data("C4"))
         dt, prof, out = timed(lambda: ctx.plugin_h(x), reps)
         g = gold("C4_plugin.json")["trace"]
-        line(cfg, "plugin_h n=2^20", dt, prof, {"n": 1 << 20, "d": 1, "n_cand": 2, "h": out[0], "trace": out[1],
+        line(cfg, "plugin_h n=2^20", dt, prof, alg=2 * (1 << 20) * ((1 << 20) - 1) / 2, extra={"n": 1 << 20, "d": 1, "n_cand": 2, "h": out[0], "trace": out[1],
              "parity": {"reference": "tests/golden/C4_plugin.json (fp64 oracle)",
                         "rel_err": {k: relerr(out[1][k], g[k]) for k in ("psi6", "psi4", "h")}}})
     elif cfg == "C2":
@@ -101,7 +106,9 @@ def run(cfg, reps):
         h0 = (4.0 / (3.0 * n)) ** 0.2
         grid = np.linspace(h0 / 4, 4 * h0, 1024)
         dt, prof, g = timed(lambda: ctx.lscv_h_scores(Xd, grid), reps)
-        line(cfg, "lscv_h_scores 1024 h, n=65536", dt, prof, {"argmin": int(np.argmin(g)), "g_min": float(g.min())})
+        pairs = n * (n - 1) / 2
+        line(cfg, "lscv_h_scores 1024 h, n=65536", dt, prof, {"argmin": int(np.argmin(g)), "g_min": float(g.min())},
+             alg=pairs * 1024)
         dt, prof, r = timed(lambda: ctx.select_bandwidth(kb.LSCV_h, Xd, n_grid=1024), 1)
         gd = gold("C2_lscv_h.json")
         gs = ctx.lscv_h_scores(Xd, gd["h"])
@@ -109,7 +116,7 @@ def run(cfg, reps):
              "index": r["iterations"],
              "parity": {"reference": "tests/golden/C2_lscv_h.json (fp64 oracle, 81 grid points)",
                         "max_rel_err": float(np.max(np.abs(gs - np.array(gd["g"])) / np.abs(gd["g"]))),
-                        "argmin_match": r["iterations"] == gd["argmin_index_among_evaluated"]}})
+                        "argmin_match": r["iterations"] == gd["argmin_index_among_evaluated"]}}, alg=pairs * 1024)
     elif cfg == "C3":
         X = datagen.config_data("C3")
         Xd = kb.to_device(X)
@@ -129,7 +136,8 @@ def run(cfg, reps):
                                 "same_iterations": r["iterations"] == gd["iterations"],
                                 "H_rel_diff": float(np.max(np.abs(Hg - Ho)) / np.max(np.diag(Ho))),
                                 "objective_rel_diff": relerr(r["objective"], gd["f"])}}
-            line(cfg, f"select LSCV_H (Nelder-Mead, {'device' if loop == 0 else 'host'} loop)", dt, prof, extra)
+            line(cfg, f"select LSCV_H (Nelder-Mead, {'device' if loop == 0 else 'host'} loop)", dt, prof, extra,
+                 alg=r["evaluations"] * X.shape[1] * (X.shape[1] - 1) / 2)
     elif cfg == "F3":
         # the paper's two-phase LSCV_h on the C2 workload: HBM-bound phase 2 at 1 h per pass
         X = datagen.config_data("C2")
@@ -203,7 +211,7 @@ def run(cfg, reps):
             gd = gold("C5_lscv_H.json")
             extra["parity"] = {"reference": "tests/golden/C5_lscv_H.json (fp64 oracle, 8 of 256 candidates)",
                                "max_rel_err": float(np.max(np.abs(g[gd["indices"]] - np.array(gd["g"])) / np.abs(gd["g"])))}
-        line(cfg, f"lscv_H_scores {len(cands)} H, d=4, n=2^18", dt, prof, extra)
+        line(cfg, f"lscv_H_scores {len(cands)} H, d=4, n=2^18", dt, prof, extra, alg=len(cands) * n * (n - 1) / 2)
 
 
 if __name__ == "__main__":
