@@ -82,6 +82,36 @@ __device__ __forceinline__ f2 exp2_sw2_fast(f2 q) {
             __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23)));
 }
 
+// As exp2_sw2_fast for 2^(s kappa) with the product folded into the range reduction: s is clamped to
+// <= smax = 125 / |kappa| (FMNMX), t = fma(s, kappa, magic) rounds s kappa to an integer j in its low
+// bits, -j = magic - t, and f = fma(s, kappa, -j) is the exactly rounded fraction (one FP32 op per
+// lane fewer than forming q = s kappa first).
+__device__ __forceinline__ f2 exp2_sw2_fma(f2 s, float kappa, float smax) {
+  float s0, s1;
+  upk(s, s0, s1);
+  const f2 sc = pk(fminf(s0, smax), fminf(s1, smax));
+  const f2 k2 = pk(kappa, kappa);
+  const f2 magic = pk(12582912.f, 12582912.f);   // 1.5 * 2^23
+  const f2 t = fma2(sc, k2, magic);
+  const f2 fr = fma2(sc, k2, sub2(magic, t));
+  f2 p = fma2(pk(1.3276472454890609e-03f, 1.3276472454890609e-03f), fr,
+              pk(9.675540961325169e-03f, 9.675540961325169e-03f));
+  p = fma2(p, fr, pk(5.550713092088699e-02f, 5.550713092088699e-02f));
+  p = fma2(p, fr, pk(2.4022120237350464e-01f, 2.4022120237350464e-01f));
+  p = fma2(p, fr, pk(6.931469440460205e-01f, 6.931469440460205e-01f));
+  p = fma2(p, fr, pk(1.0000001192092896f, 1.0000001192092896f));
+  float t0, t1, p0, p1;
+  upk(t, t0, t1);
+  upk(p, p0, p1);
+  return pk(__int_as_float(__float_as_int(p0) + (__float_as_int(t0) << 23)),
+            __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23)));
+}
+
+// Programmatic dependent launch: wait until the preceding grid has completed and its memory is visible
+// (a no-op for a kernel launched without the attribute); let the dependent grid start launching.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

@@ -168,6 +168,7 @@ kde_status kde_lscv_h_scores_materialized(kde_ctx* c, const double* X, int64_t n
     for (int j = 0; j < kde::kMaxCand; ++j) {
       const int idx = std::min(b * B + j, nh - 1);
       p.kappa[j] = (float)(-1.0 / (h[idx] * h[idx]));
+      p.smax[j] = (float)(125.0 / -(double)p.kappa[j]);
     }
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (c->profiling) { e0 = next_event(c); e1 = next_event(c); cudaEventRecord(e0, c->stream); }

@@ -46,6 +46,9 @@ struct kde_ctx {
   // sorted copy of univariate samples (+ CUB temp), context-owned
   void* sort_ws = nullptr;
   size_t sort_bytes = 0;
+  // LSCV samples sorted by coordinate 0 (d x n fp64 | keys | perm | CUB temp), context-owned
+  void* rows_ws = nullptr;
+  size_t rows_bytes = 0;
   // device copies of host-resident inputs (slot 0: samples X, slot 1: queries Y), context-owned
   void* in_ws[2] = {nullptr, nullptr};
   size_t in_bytes[2] = {0, 0};
@@ -162,6 +165,12 @@ struct Moments {
 kde_status gpu_moments(kde_ctx* c, const double* X, int64_t n, int d, Ws& w, Moments& m);
 kde_status ensure_sort_ws(kde_ctx* c, int64_t n);
 kde_status gpu_sorted(kde_ctx* c, const double* x, int64_t n, const double** out);
+// LSCV: X (d x n) reordered by ascending coordinate 0 (context-owned copy; X itself if it already is
+// that copy), so that tiles whose pairs are all exactly zero can be skipped (lscv_skip_s).
+kde_status gpu_sorted_rows(kde_ctx* c, const double* X, int64_t n, int d, const double** out);
+// Skip bound on s for LSCV sums: every term exp2(s * kappa) with s * |kappa| > 130 is exactly 0
+// (ex2.approx.ftz flushes results below 2^-126); +inf when KDE_DEBUG_LSCV_NOSKIP=1.
+float lscv_skip_s(double min_abs_kappa);
 kde_status gpu_prep_into(kde_ctx* c, const double* X, int64_t n, int d, const std::vector<double>& W,
                          const std::vector<double>& mean, int64_t ld, Ws& w, float* Y, double clamp_thresh = 0.0);
 kde_status gpu_prep(kde_ctx* c, const double* X, int64_t n, int d, const std::vector<double>& W,
@@ -188,6 +197,7 @@ struct SumLaunch {
   const float* centres = nullptr;   // Psi: per-column-tile centres
   unsigned long long* skipped = nullptr;   // Psi: skipped-pair counter
   double skip_gap = kPsiSkipGap32;         // Psi: exact-zero tile skip threshold
+  float skip_s = __builtin_inff();         // LSCV on sorted data: exact-zero tile skip bound on s
   int n_sets = 1;                   // LSCV_H: candidates (one data set each), n_out per set
   int64_t set_stride = 0;
 };

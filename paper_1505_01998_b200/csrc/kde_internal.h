@@ -39,6 +39,7 @@ struct PsiParams {
 };
 struct LscvScalarParams {
   float kappa[kMaxCand];   // -1/h_c^2 (data pre-scaled by sqrt(log2 e / 4) L^-1)
+  float smax[kMaxCand];    // 125 / |kappa_c|: software-exp clamp on s (exp2_sw2_fma)
 };
 // Tiles whose sorted gap min|y_i - y_j| exceeds these contribute exactly 0 and are skipped:
 // fp32 path: MUFU input <= -0.72 s - 16 < -126 (flushed to 0) for s > 152.5; fp64: exp(-s/2)
@@ -74,6 +75,14 @@ struct LaunchCfg {
   // Sets whose count is decided on the device (the device-resident Nelder–Mead): the kernel reads
   // *n_sets_dev (<= n_sets, which sizes the grid).
   const int* n_sets_dev = nullptr;
+  // LSCV (any d), data sorted by coordinate 0 (launch_sort_rows): skip a tile (l, q), q < l, when
+  // fp32(x_{lT} - x_{qT+T-1})^2 > skip_s, a lower bound on every s of its pairs under which every
+  // term is exactly 0 (lscv_skip_s; +inf = never).  `skipped` then counts the skipped pairs.
+  float skip_s = __builtin_inff();
+  // Programmatic dependent launch (the device-resident Nelder–Mead graph): the kernel may start while
+  // the previous one finishes and waits for it (griddepcontrol.wait) before reading its outputs.
+  bool pdl = false;
+  int reserve_ctas = 0;   // resident CTA slots the persistent grid leaves free (for a programmatic successor)
 };
 
 // Launchers (kde_psi.cu, kde_lscv_scalar.cu, kde_lscv_matrix.cu).  Return cudaSuccess or the launch error.
@@ -114,7 +123,8 @@ struct PrepParams {
 // *n_sets_dev of max_sets entries (count decided on the device).
 cudaError_t launch_prep_sets(const double* X, int64_t n, int d, const PrepParams* pp_dev, const int* n_sets_dev,
                              int max_sets, float* Y, int64_t set_stride, int64_t ld, cudaStream_t s,
-                             unsigned long long* flag);
+                             unsigned long long* flag, unsigned long long* trace = nullptr,
+                             const int* calls = nullptr, bool pdl = false);
 cudaError_t launch_prep_params(const double* X, int64_t n, int d, const PrepParams& pp, float* Y, int64_t ld,
                                cudaStream_t s, float pad = 0.f, unsigned long long* overflow_flag = nullptr,
                                double clamp_thresh = 0.0);
@@ -183,6 +193,11 @@ size_t sort_temp_bytes(int64_t n);
 cudaError_t launch_normalize_limbs(unsigned long long* limbs, int count, cudaStream_t s);
 cudaError_t launch_sort(const double* in, double* out, int64_t n, void* temp, size_t temp_bytes,
                         cudaStream_t s);
+// d x n samples reordered by ascending coordinate 0 (stable, ties by index): Xs = X[:, perm].
+// Scratch: keys (n doubles), idx (2 n ints), CUB temp (sort_rows_temp_bytes).
+size_t sort_rows_temp_bytes(int64_t n);
+cudaError_t launch_sort_rows(const double* X, int64_t n, int d, double* Xs, double* keys, int* idx, void* temp,
+                             size_t temp_bytes, cudaStream_t s);
 
 // Host/device tile map (Eq. 42-43 + integer fix-up).
 void tile_coords_host(int64_t bx, int64_t* l, int64_t* q);

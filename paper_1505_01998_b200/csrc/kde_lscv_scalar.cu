@@ -31,11 +31,24 @@ static cudaError_t lscv_scalar_d(const LaunchCfg& c, const LscvScalarParams& p) 
       case 6: return launch_pair<FLscvScalar<1, 256, 8, false, 0x4210u, 3>>(c, p);         // 3/16 spread
       case 7: return launch_pair<FLscvScalar<1, 256, 8, false, 0x1248u, 3>>(c, p);         // 4/16 spread
       case 8: return launch_pair<FLscvScalar<1, 256, 8, false, 0x0888u, 3, true>>(c, p);   // 3/16, select exp
+      case 12: return launch_pair<FLscvScalar<1, 256, 8, false, 0x888Au, 3, false, true, true>>(c, p);  // 5/16
+      case 14: return launch_pair<FLscvScalar<1, 256, 8, false, 0x8A8Au, 3, false, true, true>>(c, p);  // 6/16
       default: break;
     }
   }
-  if constexpr (D <= 4) return launch_pair<FLscvScalar<D, 256, nb_scalar(D), false, kSwDefault, 3>>(c, p);
-  else return launch_pair<FLscvScalar<D, 256, nb_scalar(D)>>(c, p);
+  if constexpr (D <= 4) {
+    switch (sw_variant()) {
+      case 9: return launch_pair<FLscvScalar<D, 256, 8, false, kSwDefault, 3, false, true, false>>(c, p);    // cand-major
+      case 10: return launch_pair<FLscvScalar<D, 256, 8, false, kSwDefault, 3, false, false, true>>(c, p);   // fma exp
+      case 15: return launch_pair<FLscvScalar<D, 256, 8, false, kSwDefault, 3, false, false, false>>(c, p);  // round-2 kernel
+      default: break;
+    }
+    // default (C2 A/B, profiles/r02_lscv_h_variants2.jsonl): candidate-major order, product folded into
+    // the software exp's range reduction
+    return launch_pair<FLscvScalar<D, 256, nb_scalar(D), false, kSwDefault, 3, false, true, true>>(c, p);
+  } else {
+    return launch_pair<FLscvScalar<D, 256, nb_scalar(D)>>(c, p);
+  }
 }
 
 cudaError_t launch_lscv_scalar(int d, int nb, const LaunchCfg& c, const LscvScalarParams& p) {

@@ -21,6 +21,15 @@
 #ifndef KDE_HD
 #define KDE_HD __host__ __device__
 #endif
+// The device runs this code on one thread per round of the loop (kde_nm_dev.cu), where instruction
+// fetch dominates: unrolled copies of these small loops grew the decide kernel to ~1 MB of SASS and
+// 12.8 us per round (KDE_DEBUG_NM_TRACE; 8.2 us rolled).  Loops stay rolled on the device (no effect on
+// results: the same operations in the same order).
+#if defined(__CUDA_ARCH__)
+#define KDE_ROLLED _Pragma("unroll 1")
+#else
+#define KDE_ROLLED
+#endif
 
 namespace kde {
 
@@ -45,10 +54,13 @@ template <int A, int B>
 KDE_HD inline void nm_state_copy(NMStateT<A>& d, const NMStateT<B>& s) {
   d.P = s.P; d.phase = s.phase; d.it = s.it; d.max_iter = s.max_iter; d.stop = s.stop;
   d.serial_pick = s.serial_pick; d.speculative = s.speculative; d.tol = s.tol; d.fr = s.fr;
+  KDE_ROLLED
   for (int v = 0; v <= s.P; ++v) {
     d.fs[v] = s.fs[v];
+    KDE_ROLLED
     for (int k = 0; k < s.P; ++k) d.sim[v][k] = s.sim[v][k];
   }
+  KDE_ROLLED
   for (int k = 0; k < s.P; ++k) {
     d.xbar[k] = s.xbar[k]; d.xr[k] = s.xr[k]; d.xe[k] = s.xe[k]; d.xc[k] = s.xc[k]; d.xcc[k] = s.xcc[k];
   }
@@ -56,10 +68,12 @@ KDE_HD inline void nm_state_copy(NMStateT<A>& d, const NMStateT<B>& s) {
 
 // r = a + s (b - c), component by component (the one combination formula of the method)
 KDE_HD inline void nm_comb(double* r, const double* a, double s, const double* b, const double* c, int P) {
+  KDE_ROLLED
   for (int k = 0; k < P; ++k) r[k] = a[k] + s * (b[k] - c[k]);
 }
 
 KDE_HD inline void nm_copy(double* d, const double* s, int P) {
+  KDE_ROLLED
   for (int k = 0; k < P; ++k) d[k] = s[k];
 }
 
@@ -67,10 +81,12 @@ KDE_HD inline void nm_copy(double* d, const double* s, int P) {
 template <class St>
 KDE_HD inline void nm_begin_iteration(St& s) {
   const int M = s.P;
+  KDE_ROLLED
   for (int i = 1; i <= M; ++i) {               // insertion sort: stable, the order of std::stable_sort
     int j = i;
     while (j > 0 && s.fs[j] < s.fs[j - 1]) {
       const double tf = s.fs[j]; s.fs[j] = s.fs[j - 1]; s.fs[j - 1] = tf;
+      KDE_ROLLED
       for (int k = 0; k < s.P; ++k) { const double t = s.sim[j][k]; s.sim[j][k] = s.sim[j - 1][k]; s.sim[j - 1][k] = t; }
       --j;
     }
@@ -78,9 +94,13 @@ KDE_HD inline void nm_begin_iteration(St& s) {
   if (s.fs[M] - s.fs[0] <= s.tol * fabs(s.fs[0])) { s.stop = 1; s.phase = St::DONE; return; }
   if (s.it >= s.max_iter) { s.stop = 2; s.phase = St::DONE; return; }
   ++s.it;
+  KDE_ROLLED
   for (int k = 0; k < s.P; ++k) s.xbar[k] = 0.0;
+  KDE_ROLLED
   for (int v = 0; v < M; ++v)
+    KDE_ROLLED
     for (int k = 0; k < s.P; ++k) s.xbar[k] += s.sim[v][k];
+  KDE_ROLLED
   for (int k = 0; k < s.P; ++k) s.xbar[k] /= (double)M;
   nm_comb(s.xr, s.xbar, 1.0, s.xbar, s.sim[M], s.P);
   nm_comb(s.xe, s.xbar, 2.0, s.xr, s.xbar, s.P);
@@ -94,6 +114,7 @@ template <class St, int OUT>
 KDE_HD inline int nm_propose(const St& s, double (*out)[OUT]) {
   switch (s.phase) {
     case St::INIT:
+      KDE_ROLLED
       for (int v = 0; v <= s.P; ++v) nm_copy(out[v], s.sim[v], s.P);
       return s.P + 1;
     case St::STEP:
@@ -107,6 +128,7 @@ KDE_HD inline int nm_propose(const St& s, double (*out)[OUT]) {
       nm_copy(out[0], s.serial_pick == 1 ? s.xe : (s.serial_pick == 2 ? s.xc : s.xcc), s.P);
       return 1;
     case St::SHRINK:
+      KDE_ROLLED
       for (int v = 1; v <= s.P; ++v) nm_comb(out[v - 1], s.sim[0], 0.5, s.sim[v], s.sim[0], s.P);
       return s.P;
     default:
@@ -140,6 +162,7 @@ template <class St>
 KDE_HD inline void nm_accept(St& s, const double* g) {
   switch (s.phase) {
     case St::INIT:
+      KDE_ROLLED
       for (int v = 0; v <= s.P; ++v) s.fs[v] = g[v];
       nm_begin_iteration(s);
       break;
@@ -152,6 +175,7 @@ KDE_HD inline void nm_accept(St& s, const double* g) {
       break;
     }
     case St::SHRINK:
+      KDE_ROLLED
       for (int v = 1; v <= s.P; ++v) {
         nm_comb(s.sim[v], s.sim[0], 0.5, s.sim[v], s.sim[0], s.P);
         s.fs[v] = g[v - 1];
@@ -171,26 +195,34 @@ KDE_HD inline int nm_vech_index(int i, int j, int d) {   // entry (i, j), i >= j
 
 KDE_HD inline bool nm_cholesky_vech(const double* vh, int d, double* L, double* det) {
   double mx = 0.0;
+  KDE_ROLLED
   for (int i = 0; i < d; ++i) {
     const double a = vh[nm_vech_index(i, i, d)];
     if (!isfinite(a)) return false;
     mx = fmax(mx, fabs(a));
   }
+  KDE_ROLLED
   for (int k = 0; k < d * (d + 1) / 2; ++k)
     if (!isfinite(vh[k])) return false;
+  KDE_ROLLED
   for (int i = 0; i < d * d; ++i) L[i] = 0.0;
+  KDE_ROLLED
   for (int j = 0; j < d; ++j) {
     double s = vh[nm_vech_index(j, j, d)];
+    KDE_ROLLED
     for (int k = 0; k < j; ++k) s -= L[j * d + k] * L[j * d + k];
     if (!(s > 1e-12 * mx)) return false;
     L[j * d + j] = sqrt(s);
+    KDE_ROLLED
     for (int i = j + 1; i < d; ++i) {
       double u = vh[nm_vech_index(i, j, d)];
+      KDE_ROLLED
       for (int k = 0; k < j; ++k) u -= L[i * d + k] * L[j * d + k];
       L[i * d + j] = u / L[j * d + j];
     }
   }
   double p = 1.0;
+  KDE_ROLLED
   for (int i = 0; i < d; ++i) p *= L[i * d + i] * L[i * d + i];
   *det = p;
   return true;
@@ -198,12 +230,16 @@ KDE_HD inline bool nm_cholesky_vech(const double* vh, int d, double* L, double* 
 
 // W = sqrt(log2 e / 4) L^-1 (forward substitution), the candidate's whitening.
 KDE_HD inline void nm_whitening(const double* L, int d, double scale, double* W) {
+  KDE_ROLLED
   for (int col = 0; col < d; ++col)
+    KDE_ROLLED
     for (int i = 0; i < d; ++i) {
       double s = (i == col) ? 1.0 : 0.0;
+      KDE_ROLLED
       for (int k = 0; k < i; ++k) s -= L[i * d + k] * W[k * d + col];
       W[i * d + col] = s / L[i * d + i];
     }
+  KDE_ROLLED
   for (int i = 0; i < d * d; ++i) W[i] *= scale;
 }
 

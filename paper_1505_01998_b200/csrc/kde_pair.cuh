@@ -73,6 +73,7 @@ struct Args {
   const int* n_sets_dev;             // sets: the count in device memory (device-resident loops), or null
   double skip_gap;                   // Psi: tiles with a larger sorted gap are exactly zero
   unsigned long long* work;          // dynamic scheduling: unit counter (zero at launch), or null
+  float skip_s;                      // LSCV on coordinate-0-sorted data: skip bound on s (+inf: never)
 };
 
 // Work distribution.  Static: CTA b takes units b, b + grid, ...  Dynamic (a.work != null): CTA b
@@ -261,7 +262,8 @@ struct FPsi {
 // FMA pipe (exp2_sw2_fast) instead of MUFU.EX2 when bit (j mod 16) is set (chosen by column, so a
 // candidate's sum does not depend on its batch).  SWM = 0: MUFU only.  SWSEL: the older exp2_sw2
 // (compare + select to exactly 0 below -125) instead of the clamp-only variant.
-template <int D_, int NT_, int NB_, bool UNIT = false, unsigned SWM = 0, int MINB_ = 0, bool SWSEL = false>
+template <int D_, int NT_, int NB_, bool UNIT = false, unsigned SWM = 0, int MINB_ = 0, bool SWSEL = false,
+          bool CMAJ = false, bool SWFMA = false>
 struct FLscvScalar {
   static_assert(!UNIT || NB_ == 1, "UNIT sets carry one candidate");
   static constexpr int NT = NT_, D = D_, R = 2, T = NT_ * 2, NB = NB_, NOUT = 2 * NB_;
@@ -288,6 +290,30 @@ struct FLscvScalar {
     for (int c = 0; c < NB; ++c) a1[c] = a2[c] = pk(0.f, 0.f);
   }
 
+  // One candidate's term for one column (s = the pair's whitened squared distance, both lanes).
+  template <bool MASK>
+  __device__ __forceinline__ void term(f2 s, int c, int col, bool ok0, bool ok1, const Params& p) {
+    f2 e;
+    if (SW && ((SWM >> (col & 15)) & 1u)) {
+      if (SWSEL) {
+        e = exp2_sw2(mul2(s, pk(p.kappa[c], p.kappa[c])));
+      } else {
+        e = SWFMA ? exp2_sw2_fma(s, p.kappa[c], p.smax[c]) : exp2_sw2_fast(mul2(s, pk(p.kappa[c], p.kappa[c])));
+        if (MASK) {   // masked lanes: exactly 0 (the clamp would leave 2^-125)
+          float e0, e1;
+          upk(e, e0, e1);
+          e = pk(ok0 ? e0 : 0.f, ok1 ? e1 : 0.f);
+        }
+      }
+    } else {
+      float q0, q1;
+      upk(mul2(s, pk(p.kappa[c], p.kappa[c])), q0, q1);
+      e = pk(ex2(q0), ex2(q1));
+    }
+    a1[c] = add2(a1[c], e);
+    a2[c] = fma2(e, e, a2[c]);
+  }
+
   template <bool MASK, bool CLAMP = false>
   __device__ __forceinline__ void compute(const float* __restrict__ sc, const Params& p, bool diag,
                                           int jlim) {
@@ -304,61 +330,58 @@ struct FLscvScalar {
           const float4 c4 = *reinterpret_cast<const float4*>(sc + a * T + j);
           cv[a][0] = c4.x; cv[a][1] = c4.y; cv[a][2] = c4.z; cv[a][3] = c4.w;
         }
+        if (!UNIT && CMAJ) {   // candidate-major: each candidate's software-exp column sits among its MUFU ones
+          f2 sk[4];
+          bool okk0[4], okk1[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          f2 dd = sub2(xr[0], pk(cv[0][k], cv[0][k]));
-          f2 s = mul2(dd, dd);
+          for (int k = 0; k < 4; ++k) sk[k] = dist<MASK>(cv, k, j + k, diag, jlim, tid, okk0[k], okk1[k]);
 #pragma unroll
-          for (int a = 1; a < D; ++a) {
-            dd = sub2(xr[a], pk(cv[a][k], cv[a][k]));
-            s = fma2(dd, dd, s);
-          }
-          bool ok0 = true, ok1 = true;
-          if (MASK) {
-            const int jj = j + k;
-            float s0, s1;
-            upk(s, s0, s1);
-            const float inf = __int_as_float(0x7f800000);   // +inf -> e = 2^-inf = 0
-            ok0 = (jj < jlim) && (!diag || jj > tid);
-            ok1 = (jj < jlim) && (!diag || jj > NT + tid);
-            s = pk(ok0 ? s0 : inf, ok1 ? s1 : inf);
-          }
-          if (UNIT) {
-            float q0, q1;
-            upk(s, q0, q1);
-            const f2 e = pk(ex2(-q0), ex2(-q1));
-            a1[0] = add2(a1[0], e);
-            a2[0] = fma2(e, e, a2[0]);
-          } else {
-            constexpr bool dummy = false;
-            (void)dummy;
+          for (int c = 0; c < NB; ++c)
 #pragma unroll
-            for (int c = 0; c < NB; ++c) {
-              const f2 q = mul2(s, pk(p.kappa[c], p.kappa[c]));
-              f2 e;
-              if (SW && ((SWM >> ((g4 + k) & 15)) & 1u)) {
-                if (SWSEL) {
-                  e = exp2_sw2(q);
-                } else {
-                  e = exp2_sw2_fast(q);
-                  if (MASK) {   // masked lanes: exactly 0 (the clamp would leave 2^-125)
-                    float e0, e1;
-                    upk(e, e0, e1);
-                    e = pk(ok0 ? e0 : 0.f, ok1 ? e1 : 0.f);
-                  }
-                }
-              } else {
-                float q0, q1;
-                upk(q, q0, q1);
-                e = pk(ex2(q0), ex2(q1));
-              }
-              a1[c] = add2(a1[c], e);
-              a2[c] = fma2(e, e, a2[c]);
+            for (int k = 0; k < 4; ++k) term<MASK>(sk[k], c, g4 + k, okk0[k], okk1[k], p);
+        } else {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            bool ok0, ok1;
+            const f2 s = dist<MASK>(cv, k, j + k, diag, jlim, tid, ok0, ok1);
+            if (UNIT) {
+              float q0, q1;
+              upk(s, q0, q1);
+              const f2 e = pk(ex2(-q0), ex2(-q1));
+              a1[0] = add2(a1[0], e);
+              a2[0] = fma2(e, e, a2[0]);
+            } else {
+#pragma unroll
+              for (int c = 0; c < NB; ++c) term<MASK>(s, c, g4 + k, ok0, ok1, p);
             }
           }
         }
       }
     }
+  }
+
+  // Squared whitened distance of the thread's two rows to column k of the staged group (both lanes);
+  // masked lanes (ragged tail, diagonal tile) get s = +inf, so e = 2^-inf = 0.
+  template <bool MASK>
+  __device__ __forceinline__ f2 dist(const float (&cv)[D][4], int k, int jj, bool diag, int jlim, int tid,
+                                     bool& ok0, bool& ok1) const {
+    f2 dd = sub2(xr[0], pk(cv[0][k], cv[0][k]));
+    f2 s = mul2(dd, dd);
+#pragma unroll
+    for (int a = 1; a < D; ++a) {
+      dd = sub2(xr[a], pk(cv[a][k], cv[a][k]));
+      s = fma2(dd, dd, s);
+    }
+    ok0 = ok1 = true;
+    if (MASK) {
+      float s0, s1;
+      upk(s, s0, s1);
+      const float inf = __int_as_float(0x7f800000);
+      ok0 = (jj < jlim) && (!diag || jj > tid);
+      ok1 = (jj < jlim) && (!diag || jj > NT + tid);
+      s = pk(ok0 ? s0 : inf, ok1 ? s1 : inf);
+    }
+    return s;
   }
 
   __device__ __forceinline__ void outputs(double (&v)[NOUT], const Params&) const {
@@ -392,6 +415,20 @@ struct IsCentred : std::false_type {};
 template <class F>
 struct IsCentred<F, std::enable_if_t<F::kCentred>> : std::true_type {};
 
+// LSCV on data sorted by coordinate 0: every pair of tile (l, q), q < l, has |fp32(x_i0 - x_j0)| >= g
+// (rounding is monotone) and s >= fp32(g^2) (the other squares only add), so fp32(g^2) > skip_s makes
+// every term exactly 0.  X = the (set's) prepared data; false for skip_s = +inf and for Psi functors.
+template <class F>
+__device__ __forceinline__ bool lscv_tile_skipped(const Args& a, const float* X, int64_t l, int64_t q) {
+  if constexpr (IsCentred<F>::value) {
+    return false;
+  } else {
+    if (q >= l) return false;
+    const float g = __fsub_rn(X[l * F::T], X[q * F::T + F::T - 1]);
+    return __fmul_rn(g, g) > a.skip_s;
+  }
+}
+
 // Evaluate one work unit (tile (l, q), column chunk `chunk` when F::CS > 1) whose column samples
 // are in shared memory at `sc`, and commit its outputs.  Sorted Psi data: a tile whose smallest
 // pair distance exceeds kPsiSkipGap32 contributes exactly 0 (every MUFU input underflows) and is
@@ -399,7 +436,8 @@ struct IsCentred<F, std::enable_if_t<F::kCentred>> : std::true_type {};
 template <class F>
 __device__ __forceinline__ void pair_unit(const Args& a, const typename F::Params& p, int64_t tile,
                                           int64_t l, int64_t q, int chunk, const float* sc, double* red,
-                                          unsigned long long* limbs, bool clamp, uint64_t* bar, uint32_t parity) {
+                                          unsigned long long* limbs, bool clamp, uint64_t* bar, uint32_t parity,
+                                          bool skip) {
   constexpr int T = F::T, NOUT = F::NOUT;
   F f;
   if constexpr (IsCentred<F>::value) {
@@ -415,6 +453,15 @@ __device__ __forceinline__ void pair_unit(const Args& a, const typename F::Param
     }
     f.load_rows_c(a.Y64, row_origin<F>(q), a.centres[l]);
   } else {
+    if (skip) {   // LSCV far tile (lscv_tile_skipped, decided when the unit's TMA was issued)
+      if (threadIdx.x == 0 && a.skipped != nullptr) {
+        const int64_t c1 = a.n - l * (int64_t)T;
+        atomicAdd(a.skipped, (unsigned long long)(T * (c1 < T ? c1 : T)));
+      }
+      mbar_wait(bar, parity);
+      __syncthreads();   // the unit's skip flag slot is rewritten by the next issue
+      return;
+    }
     f.load_rows(a.X, a.ld, row_origin<F>(q));
   }
   mbar_wait(bar, parity);      // the row loads above overlap the column chunk's TMA
@@ -446,37 +493,40 @@ __global__ void __launch_bounds__(F::NT, F::MINB) pair_kernel(const Args a,
   double* red = reinterpret_cast<double*>(cols + 2 * D * T);        // [NW][NOUT]
   uint64_t* bar = reinterpret_cast<uint64_t*>(red + NW * NOUT);      // [2]
   const int tid = threadIdx.x;
-
-  if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
+  __shared__ int64_t s_next[2];
+  __shared__ int s_skip[2];   // per buffer: the staged unit is an exactly-zero LSCV tile
 
   const int64_t units = (a.tile_end - a.tile_begin) * CS;
+  // thread 0 stages unit u's column chunk into buffer `buf` (TMA) and decides its skip flag
   auto issue = [&](int64_t u, int buf) {
     int64_t l, q;
     tile_coords(a.tile_begin + u / CS, l, q);
+    s_skip[buf] = lscv_tile_skipped<F>(a, a.X, l, q);
     float* dst = cols + buf * D * T;
     mbar_expect_tx(&bar[buf], (uint32_t)(D * T * sizeof(float)));
 #pragma unroll
     for (int d = 0; d < D; ++d)
       tma_load_1d(dst + d * T, a.X + d * a.ld + l * T, (uint32_t)(T * sizeof(float)), &bar[buf]);
   };
-  const bool clamp = F::kClampable && a.clamp != nullptr && *a.clamp != 0;   // uniform per launch
-  __shared__ int64_t s_next[2];
   int64_t u = blockIdx.x;
-  if (tid == 0 && u < units) issue(u, 0);
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (u < units) issue(u, 0);
+  }
+  __syncthreads();
+  const bool clamp = F::kClampable && a.clamp != nullptr && *a.clamp != 0;   // uniform per launch
   uint32_t k = 0;
   while (u < units) {
     const int64_t tile = a.tile_begin + u / CS;
     int64_t l, q;
     tile_coords(tile, l, q);
     const int64_t un = next_unit_issue(a, u, s_next, k);
+    const bool skip = s_skip[k & 1];   // read before the issue below can rewrite the other slot
     if (tid == 0 && un < units) issue(un, (k + 1) & 1);
     pair_unit<F>(a, p, tile, l, q, (int)(u % CS), cols + (k & 1) * D * T, red, a.limbs, clamp, &bar[k & 1],
-                 (k >> 1) & 1);
+                 (k >> 1) & 1, skip);
     u = un;
     ++k;
   }
@@ -492,14 +542,11 @@ __global__ void __launch_bounds__(F::NT, F::MINB) pair_kernel_sets(const Args a,
   double* red = reinterpret_cast<double*>(cols + 2 * D * T);        // [NW][NOUT]
   uint64_t* bar = reinterpret_cast<uint64_t*>(red + NW * NOUT);      // [2]
   const int tid = threadIdx.x;
+  __shared__ int64_t s_next[2];
+  __shared__ int s_skip[2];
 
-  if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-
+  pdl_trigger();   // a programmatic successor (the Nelder–Mead decision) may take its slot right away
+  pdl_wait();      // a programmatic launch (device-resident Nelder–Mead) waits for the whitening here
   // Work units u in [0, n_sets * tiles): set = u / tiles, tile = tile_begin + u % tiles (set-major,
   // so consecutive CTAs share a set's data in L2).
   const int64_t per = a.tile_end - a.tile_begin;
@@ -509,17 +556,22 @@ __global__ void __launch_bounds__(F::NT, F::MINB) pair_kernel_sets(const Args a,
     int64_t l, q;
     tile_coords(a.tile_begin + (u - set * per), l, q);
     const float* Xs = a.X + set * a.set_stride;
+    s_skip[buf] = lscv_tile_skipped<F>(a, Xs, l, q);
     float* dst = cols + buf * D * T;
     mbar_expect_tx(&bar[buf], (uint32_t)(D * T * sizeof(float)));
 #pragma unroll
     for (int d = 0; d < D; ++d)
       tma_load_1d(dst + d * T, Xs + d * a.ld + l * T, (uint32_t)(T * sizeof(float)), &bar[buf]);
   };
-
-  const bool clamp = F::kClampable && a.clamp != nullptr && *a.clamp != 0;   // uniform per launch
-  __shared__ int64_t s_next[2];
   int64_t u = blockIdx.x;
-  if (tid == 0 && u < units) issue(u, 0);
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (u < units) issue(u, 0);
+  }
+  __syncthreads();
+  const bool clamp = F::kClampable && a.clamp != nullptr && *a.clamp != 0;   // uniform per launch
   uint32_t k = 0;
   while (u < units) {
     const int64_t set = u / per;
@@ -527,11 +579,12 @@ __global__ void __launch_bounds__(F::NT, F::MINB) pair_kernel_sets(const Args a,
     int64_t l, q;
     tile_coords(tile, l, q);
     const int64_t un = next_unit_issue(a, u, s_next, k);
+    const bool skip = s_skip[k & 1];
     if (tid == 0 && un < units) issue(un, (k + 1) & 1);
     Args as = a;
     as.X = a.X + set * a.set_stride;
     pair_unit<F>(as, p, tile, l, q, 0, cols + (k & 1) * D * T, red, a.limbs + set * NOUT * kLimbs, clamp,
-                 &bar[k & 1], (k >> 1) & 1);
+                 &bar[k & 1], (k >> 1) & 1, skip);
     u = un;
     ++k;
   }
@@ -567,12 +620,29 @@ inline cudaError_t launch_pair(const LaunchCfg& c, const typename F::Params& p) 
   cudaError_t e = pair_occupancy<F>(&occ);
   if (e != cudaSuccess) return e;
   const int64_t units = (c.tile_end - c.tile_begin) * c.n_sets * F::CS;
-  int64_t grid = (int64_t)c.sm_count * occ;
+  int64_t grid = (int64_t)c.sm_count * occ - c.reserve_ctas;
   if (grid > units) grid = units;
+  if (grid < 1) grid = 1;
   Args a{c.X, c.n, c.ld, c.tile_begin, c.tile_end, c.scale_exp, c.limbs, c.clamp, c.n_sets, c.set_stride,
-         c.Y64, c.centres, c.skipped, c.n_sets_dev, c.skip_gap, c.work};
-  if constexpr (F::kSets) pair_kernel_sets<F><<<(unsigned)grid, F::NT, smem, c.stream>>>(a, p);
-  else pair_kernel<F><<<(unsigned)grid, F::NT, smem, c.stream>>>(a, p);
+         c.Y64, c.centres, c.skipped, c.n_sets_dev, c.skip_gap, c.work, c.skip_s};
+  if constexpr (F::kSets) {
+    if (c.pdl) {
+      cudaLaunchConfig_t lc = {};
+      lc.gridDim = dim3((unsigned)grid);
+      lc.blockDim = dim3(F::NT);
+      lc.dynamicSmemBytes = smem;
+      lc.stream = c.stream;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = 1;
+      lc.attrs = at;
+      lc.numAttrs = 1;
+      return cudaLaunchKernelEx(&lc, pair_kernel_sets<F>, a, p);
+    }
+    pair_kernel_sets<F><<<(unsigned)grid, F::NT, smem, c.stream>>>(a, p);
+  } else {
+    pair_kernel<F><<<(unsigned)grid, F::NT, smem, c.stream>>>(a, p);
+  }
   return cudaGetLastError();
 }
 

@@ -1,5 +1,6 @@
 // kde_psi.cu — Psi_r pair-kernel instantiations, tile/batch policy, O(n) kernels (see kde_pair.cuh).
 #include <cub/device/device_radix_sort.cuh>
+#include <algorithm>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -217,12 +218,28 @@ __global__ void prep_kernel_p(const double* __restrict__ X, int64_t n, int d, co
 }
 
 // Several sets, parameters in device memory, the set count decided on the device (blockIdx.y = set).
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// trace (diagnostics, KDE_DEBUG_NM_TRACE): slot 4 (*calls - 1) + 2 = start of block (0, 0), + 3 = the
+// latest block end (globaltimer ns).
 __global__ void prep_sets_kernel(const double* __restrict__ X, int64_t n, int d, const PrepParams* __restrict__ pp,
                                  const int* __restrict__ n_sets, float* __restrict__ Y, int64_t set_stride,
-                                 int64_t ld, unsigned long long* __restrict__ flag) {
+                                 int64_t ld, unsigned long long* __restrict__ flag, unsigned long long* trace,
+                                 const int* calls) {
+  pdl_wait();   // programmatic launch after the Nelder–Mead decision: its outputs are visible past here
+  pdl_trigger();   // the pair kernel may start launching (it waits for this grid's completion)
   const int set = blockIdx.y;
   if (set >= *n_sets) return;
+  if (trace && threadIdx.x == 0 && blockIdx.x == 0 && set == 0) trace[16 * (*calls - 1) + 2] = global_ns();
   prep_body(X, n, d, pp[set].W, pp[set].mean, Y + (int64_t)set * set_stride, ld, 0.f, flag, 0.0);
+  if (trace) {
+    __syncthreads();
+    if (threadIdx.x == 0) atomicMax(trace + 16 * (*calls - 1) + 3, global_ns());
+  }
 }
 
 static unsigned prep_blocks(int64_t ld) {
@@ -240,11 +257,24 @@ cudaError_t launch_prep(const double* X, int64_t n, int d, const double* W_dev,
 
 cudaError_t launch_prep_sets(const double* X, int64_t n, int d, const PrepParams* pp_dev, const int* n_sets_dev,
                              int max_sets, float* Y, int64_t set_stride, int64_t ld, cudaStream_t s,
-                             unsigned long long* flag) {
+                             unsigned long long* flag, unsigned long long* trace, const int* calls, bool pdl) {
   unsigned bx = prep_blocks(ld);
   const unsigned per = (148u * 16u + (unsigned)max_sets - 1) / (unsigned)max_sets;   // ~16 blocks/SM overall
   if (bx > per) bx = per > 0 ? per : 1;
-  prep_sets_kernel<<<dim3(bx, (unsigned)max_sets), 256, 0, s>>>(X, n, d, pp_dev, n_sets_dev, Y, set_stride, ld, flag);
+  if (pdl) {
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(bx, (unsigned)max_sets);
+    lc.blockDim = dim3(256);
+    lc.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    return cudaLaunchKernelEx(&lc, prep_sets_kernel, X, n, d, pp_dev, n_sets_dev, Y, set_stride, ld, flag, trace, calls);
+  }
+  prep_sets_kernel<<<dim3(bx, (unsigned)max_sets), 256, 0, s>>>(X, n, d, pp_dev, n_sets_dev, Y, set_stride, ld, flag, trace,
+                                                                  calls);
   return cudaGetLastError();
 }
 
@@ -449,6 +479,41 @@ size_t sort_temp_bytes(int64_t n) {
 cudaError_t launch_sort(const double* in, double* out, int64_t n, void* temp, size_t temp_bytes,
                         cudaStream_t s) {
   return cub::DeviceRadixSort::SortKeys(temp, temp_bytes, in, out, (int)n, 0, 64, s);
+}
+
+// LSCV data sorted by coordinate 0 (exact far-tile skip): stable radix sort of
+// (x_0j, j), then a gather of all d rows.  Whitening keeps the order of coordinate 0 (W is lower
+// triangular with W_00 > 0), so every prepared set is sorted by its first coordinate too.
+size_t sort_rows_temp_bytes(int64_t n) {
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const double*)nullptr, (double*)nullptr, (const int*)nullptr,
+                                  (int*)nullptr, (int)n);
+  return bytes;
+}
+
+__global__ void iota_kernel(int* idx, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    idx[i] = (int)i;
+}
+
+__global__ void gather_rows_kernel(const double* __restrict__ X, int64_t n, int d, const int* __restrict__ perm,
+                                   double* __restrict__ Xs) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = perm[i];
+    for (int a = 0; a < d; ++a) Xs[a * n + i] = X[a * n + j];
+  }
+}
+
+cudaError_t launch_sort_rows(const double* X, int64_t n, int d, double* Xs, double* keys, int* idx, void* temp,
+                             size_t temp_bytes, cudaStream_t s) {
+  const unsigned blocks = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 8);
+  iota_kernel<<<blocks, 256, 0, s>>>(idx, n);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  e = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, X, keys, idx, idx + n, (int)n, 0, 64, s);
+  if (e != cudaSuccess) return e;
+  gather_rows_kernel<<<blocks, 256, 0, s>>>(X, n, d, idx + n, Xs);
+  return cudaGetLastError();
 }
 
 

@@ -215,6 +215,33 @@ kde_status gpu_sorted(kde_ctx* c, const double* x, int64_t n, const double** out
   return KDE_OK;
 }
 
+kde_status gpu_sorted_rows(kde_ctx* c, const double* X, int64_t n, int d, const double** out) {
+  if (c->rows_ws && X == static_cast<const double*>(c->rows_ws)) {   // already the sorted copy
+    *out = X;
+    return KDE_OK;
+  }
+  Range r("kde.sort_rows");
+  const size_t tmp = kde::sort_rows_temp_bytes(n);
+  const size_t xs_b = align256((size_t)n * d * sizeof(double)), keys_b = align256((size_t)n * sizeof(double)),
+               idx_b = align256((size_t)2 * n * sizeof(int));
+  TRY(grow(c, &c->rows_ws, &c->rows_bytes, xs_b + keys_b + idx_b + align256(tmp)));
+  char* base = static_cast<char*>(c->rows_ws);
+  double* xs = reinterpret_cast<double*>(base);
+  CUDA_TRY(c, kde::launch_sort_rows(X, n, d, xs, reinterpret_cast<double*>(base + xs_b),
+                                    reinterpret_cast<int*>(base + xs_b + keys_b), base + xs_b + keys_b + idx_b, tmp,
+                                    c->stream));
+  c->prof_all += 12;   // iota, CUB onesweep pairs (histogram, exclusive sum, 8 passes), gather
+  *out = xs;
+  return KDE_OK;
+}
+
+float lscv_skip_s(double min_abs_kappa) {
+  const char* e = getenv("KDE_DEBUG_LSCV_NOSKIP");   // tests / diagnostics: read at every call
+  if ((e && atoi(e) == 1) || !(min_abs_kappa > 0.0)) return __builtin_inff();
+  const double b = 130.0 / min_abs_kappa;
+  return b < 1e30 ? (float)b : __builtin_inff();
+}
+
 // y = fp32(W (x - mean)), padded with zeros to ld, written to Y (default: the workspace's Y).
 // gpu_prep_into does not clear the prep flags (several sets prepared for one launch share them).
 kde_status gpu_prep_into(kde_ctx* c, const double* X, int64_t n, int d, const std::vector<double>& W,
@@ -338,6 +365,12 @@ kde_status run_sums(kde_ctx* c, int d, int64_t n, int64_t ld, int T, int scale, 
   if (!limbs_zeroed)
     CUDA_TRY(c, cudaMemsetAsync(w.limbs, 0, ((size_t)n_out * kde::kLimbs + launches.size()) * sizeof(long long),
                                 c->stream));
+  // LSCV exact-zero tile skip (profiling): pairs of skipped tiles, in the small block's skipped slot (zeroed
+  // here, read back with the limbs below) and left out of the evaluated pairs
+  unsigned long long* lscv_skipped = reinterpret_cast<unsigned long long*>(w.small + kde::kSkippedSlot);
+  bool any_skip = false;
+  for (const SumLaunch& L : launches) any_skip |= L.skip_s < __builtin_inff();
+  if (c->profiling && any_skip) CUDA_TRY(c, cudaMemsetAsync(lscv_skipped, 0, sizeof(unsigned long long), c->stream));
   int64_t tiles = n_tiles(n, T), tb, te;
   shard_range(tiles, shard_rank, shard_world, &tb, &te);
   const double pairs = c->profiling ? pairs_in_range(n, T, tb, te) : 0.0;
@@ -354,6 +387,8 @@ kde_status run_sums(kde_ctx* c, int d, int64_t n, int64_t ld, int T, int scale, 
     cfg.centres = L.centres;
     cfg.skipped = L.skipped;
     cfg.skip_gap = L.skip_gap;
+    cfg.skip_s = L.skip_s;
+    if (c->profiling && L.skip_s < __builtin_inff()) cfg.skipped = lscv_skipped;
     cfg.work = work + (&L - launches.data());
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (c->profiling) { e0 = next_event(c); e1 = next_event(c); cudaEventRecord(e0, c->stream); }
@@ -386,6 +421,11 @@ kde_status run_sums(kde_ctx* c, int d, int64_t n, int64_t ld, int T, int scale, 
   CUDA_TRY(c, cudaMemcpyAsync(c->h_limbs, w.flag(), need * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   if (c->h_limbs[0]) return fail(c, KDE_E_INVALID, "scaled sample differences exceed 1e18 (outliers vs. bandwidth)");
+  if (c->profiling && any_skip) {   // skipped pairs x candidates per pair (the same for every launch here)
+    unsigned long long sk = 0;
+    std::memcpy(&sk, c->h_limbs + (kde::kSkippedSlot - 408), sizeof(sk));
+    c->prof_evals -= (double)sk * (double)launches.front().nb;
+  }
   out.resize(n_out);
   for (int k = 0; k < n_out; ++k) out[k] = limbs_to_fixed(c->h_limbs + gap + (size_t)k * kde::kLimbs, scale);
   return KDE_OK;
@@ -490,6 +530,7 @@ void kde_destroy(kde_ctx* c) {
   if (c->comm) nccl().CommDestroy(c->comm);
   if (c->own_ws) cudaFree(c->own_ws);
   if (c->sort_ws) cudaFree(c->sort_ws);
+  if (c->rows_ws) cudaFree(c->rows_ws);
   if (c->white_ws) cudaFree(c->white_ws);
   if (c->ev_ws) cudaFree(c->ev_ws);
   if (c->mat_ws) cudaFree(c->mat_ws);

@@ -184,23 +184,38 @@ kde_status lscv_h_raw(kde_ctx* c, const double* X, int64_t n, int d, const doubl
   const int n_out = 2 * nbatch * nb;
   Ws w;
   TRY(get_ws(c, ld, d, n_out, &w));
+  // sorted by coordinate 0 (the whitened coordinate 0 keeps that order): far tiles are skipped
+  TRY(gpu_sorted_rows(c, X, n, d, &X));
   // W = sqrt(log2 e / 4) L^-1  =>  |W v|^2 = (log2 e / 4) v^T Sigma^-1 v
   std::vector<double> W = tri_lower_inverse(pp.Lc, d);
   for (double& v : W) v *= std::sqrt(kLog2e / 4.0);
   TRY(gpu_prep(c, X, n, d, W, m.mean, ld, w));
+  // batches of ascending h: each batch's widest h sets its far-tile skip bound (a candidate's sums do not
+  // depend on its batch, so the order only changes how many tiles are skipped)
+  std::vector<int> order(nh);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return h[a] < h[b]; });
   std::vector<SumLaunch> Ls;
   for (int b = 0; b < nbatch; ++b) {
     SumLaunch L;
     L.kind = Kind::LscvScalar; L.nb = nb; L.out_offset = 2 * b * nb; L.n_out = 2 * nb;
+    double kmin = 1e300;
     for (int j = 0; j < kde::kMaxCand; ++j) {
-      int idx = std::min(b * nb + j, nh - 1);   // pad with a valid candidate
+      int idx = order[std::min(b * nb + j, nh - 1)];   // pad with a valid candidate
       L.ls.kappa[j] = (float)(-1.0 / (h[idx] * h[idx]));
+      L.ls.smax[j] = (float)(125.0 / -(double)L.ls.kappa[j]);
+      if (j < nb) kmin = std::min(kmin, -(double)L.ls.kappa[j]);
     }
+    L.skip_s = lscv_skip_s(kmin);   // the batch's widest h bounds every candidate's terms
     Ls.push_back(L);
   }
   std::vector<kde_fixed> o;
   TRY(run_sums(c, d, n, ld, T, scale_exp_for(1.0, n), w, Ls, n_out, shard_rank, shard_world, allreduce, o));
-  out.assign(o.begin(), o.begin() + 2 * nh);
+  out.resize(2 * (size_t)nh);
+  for (int k = 0; k < nh; ++k) {
+    out[2 * (size_t)order[k]] = o[2 * (size_t)k];
+    out[2 * (size_t)order[k] + 1] = o[2 * (size_t)k + 1];
+  }
   return KDE_OK;
 }
 
@@ -243,6 +258,7 @@ kde_status lscv_H_raw(kde_ctx* c, const double* X, int64_t n, int d, const std::
   const int per_launch = (int)std::max<int64_t>(1, std::min<int64_t>(256, (1LL << 28) / set_floats));
   Ws w;
   TRY(get_ws(c, ld, d, 2 * std::min(nc, per_launch), &w));
+  TRY(gpu_sorted_rows(c, X, n, d, &X));   // by coordinate 0 (no-op when X is the sorted copy)
   out.clear();
   for (int b0 = 0; b0 < nc; b0 += per_launch) {
     const int cnt = std::min(per_launch, nc - b0);
@@ -257,6 +273,7 @@ kde_status lscv_H_raw(kde_ctx* c, const double* X, int64_t n, int d, const std::
     SumLaunch L;
     L.kind = Kind::LscvMatrix; L.nb = 1; L.out_offset = 0; L.n_out = 2 * cnt;
     L.X = Yw; L.n_sets = cnt; L.set_stride = set_floats;
+    L.skip_s = lscv_skip_s(1.0);   // e = 2^-s with s = |x'_i - x'_j|^2
     std::vector<kde_fixed> o;
     TRY(run_sums(c, d, n, ld, T, scale_exp_for(1.0, n), w, {L}, 2 * cnt, shard_rank, shard_world, allreduce, o,
                  /*limbs_zeroed=*/true));
@@ -714,6 +731,7 @@ kde_status kde_select_bandwidth(kde_ctx* c, kde_method method, const double* X, 
       sims.push_back(sk);
     }
     NMResult nm;
+    TRY(gpu_sorted_rows(c, X, n, d, &X));   // once for the whole search (far-tile skip)
     // device-resident loop: one GPU, one start, serial rounds, whitened sets within ~1 GiB
     const int64_t Tm = kde::tile_for(Kind::LscvMatrix, d, n), ldT = (n + Tm - 1) / Tm * Tm;
     const bool dev_loop = o.nm_loop == 0 && K == 1 && o.speculative == 0 && c->world == 1 && !c->comm &&

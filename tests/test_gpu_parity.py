@@ -461,3 +461,48 @@ def test_psi_far_tile_skip_is_exact(ctx, mode):
                 assert evaluated < full   # g = 0.03: most tiles are skipped
     finally:
         ctx.set_precision(0)
+
+
+@pytest.mark.parametrize("which", ["h1", "h2", "H2", "H4"])
+def test_lscv_far_tile_skip_is_exact(ctx, which):
+    # LSCV data are sorted by coordinate 0 (whitening keeps that order); a tile whose coordinate-0 gap
+    # bounds every s above the skip bound has every MUFU term exactly 0 (and every software-exp term at
+    # 2^-125, far below the fixed-point resolution), so skipping it changes no output bit.
+    import os
+    if which[0] == "h":
+        d = int(which[1])
+        X = datagen.sample_mixture("bimodal", 20011, 5) if d == 1 else datagen.sample_mixture("C3", 12007, 5)
+        kind, cand = kb.SUM_LSCV_h, list(np.geomspace(0.01, 1.5, 24))
+    else:
+        d = int(which[1])
+        X = datagen.sample_mixture("C3" if d == 2 else "C5", 9001, 6)[:d]
+        kind, cand = kb.SUM_LSCV_H, np.concatenate([_spd_cands(d, 3, 7, s) for s in (1e-4, 1e-3, 0.05)]).ravel()
+    Xd = dev(X)
+    a = ctx.raw_sums(kind, Xd, cand)
+    evaluated = ctx.last_profile()["pair_evals"]
+    os.environ["KDE_DEBUG_LSCV_NOSKIP"] = "1"
+    try:
+        b = ctx.raw_sums(kind, Xd, cand)
+        full = ctx.last_profile()["pair_evals"]
+    finally:
+        del os.environ["KDE_DEBUG_LSCV_NOSKIP"]
+    assert [f.key() for f in a] == [f.key() for f in b]
+    n = X.shape[1]
+    ncand = len(cand) if kind == kb.SUM_LSCV_h else len(cand) // (d * (d + 1) // 2)
+    nb = {1: 8, 2: 8}.get(d, 8) if kind == kb.SUM_LSCV_h else 1
+    assert full == n * (n - 1) / 2 * (-(-ncand // nb) * nb)   # every pair x every candidate slot
+    assert evaluated < 0.9 * full                             # the small bandwidths skip most tiles
+
+
+def test_lscv_h_candidate_order_invariance(ctx):
+    # Candidates are batched in ascending h (the batch's widest h bounds its far-tile skip); each
+    # candidate's sums are the same bits whatever order or company it is given in.
+    X = dev(datagen.sample_mixture("bimodal", 15013, 8))
+    hs = np.geomspace(0.01, 1.2, 21)
+    perm = np.random.default_rng(1).permutation(hs.size)
+    a = ctx.raw_sums(kb.SUM_LSCV_h, X, hs)
+    b = ctx.raw_sums(kb.SUM_LSCV_h, X, hs[perm])
+    for j, k in enumerate(perm):
+        assert [f.key() for f in b[2 * j:2 * j + 2]] == [f.key() for f in a[2 * k:2 * k + 2]]
+    solo = ctx.raw_sums(kb.SUM_LSCV_h, X, hs[3:4])
+    assert [f.key() for f in solo] == [f.key() for f in a[6:8]]
