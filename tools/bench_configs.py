@@ -30,8 +30,18 @@ SMS = torch.cuda.get_device_properties(0).multi_processor_count
 PEAK = 16 * SMS * 1965e6
 
 
-def timed(fn, reps):
+_CLOCKS = {}
+
+
+def timed(fn, reps, warm=True):
+    """Best of `reps` calls (after one untimed warm-up call when warm); the SM clock is sampled by
+    nvidia-smi during the timed calls (bench.ClockSampler) and reported by line()."""
+    from bench import ClockSampler
+    if warm:
+        fn()
     best = None
+    cs = ClockSampler(0)
+    cs.start()
     for _ in range(reps):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -41,6 +51,8 @@ def timed(fn, reps):
         prof = ctx.last_profile()
         if best is None or dt < best[0]:
             best = (dt, prof, out)
+    _CLOCKS.clear()
+    _CLOCKS.update(cs.stop())
     return best
 
 
@@ -69,7 +81,9 @@ def line(cfg, what, dt, prof, extra=None, alg=None):
     # evals = evaluated pair-kernel evaluations (the library's profile leaves out the pairs of tiles
     # skipped as exactly zero); alg = algorithmic evaluations (all pairs x candidates), when known
     ev = prof["pair_evals"]
-    d = {"config": cfg, "what": what, "gpus": 1, "sm_clock_mhz": sm_clock(), "wall_ms": dt * 1e3, "pair_ms": prof["pair_ms"],
+    clk = dict(_CLOCKS) if _CLOCKS.get("sm_mhz") else {"sm_mhz": sm_clock(), "reasons": ["sampled after the call"]}
+    d = {"config": cfg, "what": what, "gpus": 1, "sm_clock_mhz": clk.get("sm_mhz"), "clocks": clk,
+         "wall_ms": dt * 1e3, "pair_ms": prof["pair_ms"],
          "pair_launches": prof["pair_launches"], "evals": ev,
          "evals_per_s_pair": ev / (prof["pair_ms"] / 1e3) if prof["pair_ms"] > 0 else None,
          "frac_mufu_peak": (ev / (prof["pair_ms"] / 1e3)) / PEAK if prof["pair_ms"] > 0 else None}
@@ -149,7 +163,7 @@ def run(cfg, reps):
         tiles = ((n + T - 1) // T) * ((n + T - 1) // T + 1) // 2
         buf_bytes = tiles * T * T * 4
         for B in (1, 4, 16):
-            dt, prof, g = timed(lambda: ctx.lscv_h_scores_materialized(Xd, grid, h_per_pass=B), 1)
+            dt, prof, g = timed(lambda: ctx.lscv_h_scores_materialized(Xd, grid, h_per_pass=B), 2)
             passes = (1024 + B - 1) // B
             gbs = buf_bytes * passes / (prof["pair_ms"] / 1e3) / 1e9
             line(cfg, f"materialised S(v) LSCV_h, 1024 h, {B} h per pass", dt, prof,
