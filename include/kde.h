@@ -251,9 +251,14 @@ kde_status kde_last_profile(const kde_ctx *ctx, int32_t *launches, double *pair_
  *     Shard-only raw sums (shard_world > 0) are never re-run (the decision needs the full sum).
  *   1 = fp64 terms for every pass (libdevice exp, fp64 Horner in u^2), the exact-parity mode.
  *  -1 = fp32 terms only (diagnostics).
+ * The same modes govern the LSCV objectives of kde_lscv_h_scores, kde_lscv_H_scores and the LSCV_h
+ * grid selection (Eq. 24/30): in mode 0 a candidate whose objective
+ * g = A - B + C cancels beyond kLscvKappaMax = 32 ((A + B)/|g|, so the fp32 terms' ~1.5e-7 on the raw
+ * sums could exceed 1e-5 on g) is re-run with fp64 terms; mode 1 re-runs every candidate.  Nelder-Mead
+ * searches and kde_raw_sums always use fp32 terms.
  * Results stay deterministic and partition-invariant in every mode. */
 kde_status kde_set_precision(kde_ctx *ctx, int32_t fp64_terms);
-/* Number of Psi passes of the last call that the automatic precision re-ran with fp64 terms, and
+/* Number of Psi passes and LSCV candidates of the last call that were (re-)run with fp64 terms, and
  * the largest cancellation estimate kappa of its fp32-term Psi passes (diagnostics). */
 int32_t kde_last_fp64_passes(const kde_ctx *ctx);
 double kde_last_psi_kappa(const kde_ctx *ctx);

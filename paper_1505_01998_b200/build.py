@@ -15,7 +15,7 @@ LIB = os.path.join(HERE, "libkde_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I" + os.path.join(ROOT, "include")]
-SOURCES = ["kde_psi.cu", "kde_lscv_scalar.cu", "kde_lscv_matrix.cu", "kde_eval.cu", "kde_materialized.cu",
+SOURCES = ["kde_psi.cu", "kde_lscv_scalar.cu", "kde_lscv_matrix.cu", "kde_lscv64.cu", "kde_eval.cu", "kde_materialized.cu",
            "kde_nm_dev.cu", "kde_runtime.cpp", "kde_linalg.cpp", "kde_nm.cpp", "kde_selectors.cpp", "kde_extras.cpp"]
 # the device Nelder-Mead makes the host loop's decisions only without FMA contraction (kde_nm.cuh)
 EXTRA = {"kde_nm_dev.cu": ["-fmad=false"]}

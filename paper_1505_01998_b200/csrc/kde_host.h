@@ -49,6 +49,9 @@ struct kde_ctx {
   // LSCV samples sorted by coordinate 0 (d x n fp64 | keys | perm | CUB temp), context-owned
   void* rows_ws = nullptr;
   size_t rows_bytes = 0;
+  // fp64 whitened samples of the LSCV fp64-term re-run (d x ld doubles), context-owned
+  void* f64_ws = nullptr;
+  size_t f64_bytes = 0;
   // device copies of host-resident inputs (slot 0: samples X, slot 1: queries Y), context-owned
   void* in_ws[2] = {nullptr, nullptr};
   size_t in_bytes[2] = {0, 0};
@@ -218,12 +221,21 @@ HCand h_candidate(const double* vh, int d);
 double lscv_H_finalize(int64_t n, int d, double det, double S1, double S2);
 kde_status lscv_H_eval(kde_ctx* c, const double* X, int64_t n, int d, const Moments& m,
                        const std::vector<std::vector<double>>& vs, double penalty, std::vector<double>& g,
-                       int* evals);
+                       int* evals, bool auto_precision = false);
 struct LscvhPrep {
   std::vector<double> Lc;   // Cholesky of Sigma
   double det = 0.0;
 };
 kde_status lscv_h_prepare(kde_ctx* c, const Moments& m, int d, LscvhPrep& p);
+// LSCV automatic precision: the factor (A + B) / |A - B + C| by which
+// g = A - B + C, A = 2 c4 S1 / n^2, B = 4 c2 S2 / n^2, C = c4 / n (times h^-d for LSCV_h) amplifies the
+// relative error of the raw sums; a candidate above kLscvKappaMax is re-run with fp64 terms.
+constexpr double kLscvKappaMax = 32.0;
+double lscv_cancellation(int64_t n, int d, double det, double S1, double S2);
+// fp64-term (sum e, sum e^2) of one candidate over all pairs (all ranks, all-reduced): Xs sorted by
+// coordinate 0, W the whitening (with sqrt(log2 e / 4)), e = exp2(kappa |W (x_i - x_j)|^2).
+kde_status lscv_sums64(kde_ctx* c, const double* Xs, int64_t n, int d, const std::vector<double>& W,
+                       const std::vector<double>& mean, double kappa, kde_fixed out[2]);
 double lscv_h_finalize(int64_t n, int d, double det, double h, double S1, double S2);
 
 // ------------------------------------------------------------------ Nelder–Mead (kde_nm.cpp)

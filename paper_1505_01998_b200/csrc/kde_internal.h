@@ -132,6 +132,13 @@ cudaError_t launch_prep(const double* X, int64_t n, int d, const double* W_dev,
                         const double* mean_dev, float* Y, int64_t ld, cudaStream_t s,
                         float pad = 0.f, unsigned long long* overflow_flag = nullptr,
                         double clamp_thresh = 0.0);
+// fp64-term LSCV sums of one candidate (kde_lscv64.cu): Y = fp64 whitened data (d rows of ld, sorted by
+// coordinate 0, ld a multiple of lscv64_tile()), e = exp2(kappa |y_i - y_j|^2), outputs (sum e, sum e^2).
+int lscv64_tile();
+cudaError_t launch_prep64(const double* X, int64_t n, int d, const PrepParams& pp, double* Y, int64_t ld,
+                          cudaStream_t s);
+cudaError_t launch_lscv64(int d, const double* Y, int64_t n, int64_t ld, int64_t tb, int64_t te, double kappa,
+                          double skip_s, int S, unsigned long long* limbs, int sm_count, cudaStream_t s);
 
 // Device-resident PLUGIN chain (kde_psi.cu).  Layout of the workspace's `small` block (doubles):
 // mean[16] | W[256] | sums[136] | flags (2 x u64) | trace[8] | status.

@@ -33,6 +33,10 @@ static cudaError_t lscv_scalar_d(const LaunchCfg& c, const LscvScalarParams& p) 
       case 8: return launch_pair<FLscvScalar<1, 256, 8, false, 0x0888u, 3, true>>(c, p);   // 3/16, select exp
       case 12: return launch_pair<FLscvScalar<1, 256, 8, false, 0x888Au, 3, false, true, true>>(c, p);  // 5/16
       case 14: return launch_pair<FLscvScalar<1, 256, 8, false, 0x8A8Au, 3, false, true, true>>(c, p);  // 6/16
+      case 16: return launch_pair<FLscvScalar<1, 256, 8, false, 0x8888u, 4, false, true, true>>(c, p);  // 4 CTAs/SM
+      case 17: return launch_pair<FLscvScalar<1, 256, 8, false, 0x8888u, 3, false, true, true, 2>>(c, p);  // 32 cols/iter
+      case 18: return launch_pair<FLscvScalar<1, 256, 8, false, 0x0888u, 3, false, true, true>>(c, p);  // 3/16
+      case 19: return launch_pair<FLscvScalar<1, 256, 8, false, 0x4924u, 3, false, true, true>>(c, p);  // 4/16 spread (2,5,8,11,14)
       default: break;
     }
   }

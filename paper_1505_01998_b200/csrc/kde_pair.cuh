@@ -263,7 +263,7 @@ struct FPsi {
 // candidate's sum does not depend on its batch).  SWM = 0: MUFU only.  SWSEL: the older exp2_sw2
 // (compare + select to exactly 0 below -125) instead of the clamp-only variant.
 template <int D_, int NT_, int NB_, bool UNIT = false, unsigned SWM = 0, int MINB_ = 0, bool SWSEL = false,
-          bool CMAJ = false, bool SWFMA = false>
+          bool CMAJ = false, bool SWFMA = false, int UNR_ = 0>
 struct FLscvScalar {
   static_assert(!UNIT || NB_ == 1, "UNIT sets carry one candidate");
   static constexpr int NT = NT_, D = D_, R = 2, T = NT_ * 2, NB = NB_, NOUT = 2 * NB_;
@@ -274,7 +274,7 @@ struct FLscvScalar {
   // LSCV_h with software-exp columns: 16 columns per iteration (the mask period)
   static constexpr bool SW = SWM != 0;
   static constexpr int STEP = SW ? 16 : 4;
-  static constexpr int UNR = UNIT && D <= 2 ? 8 : (UNIT && D <= 4 ? 4 : 1);
+  static constexpr int UNR = UNR_ > 0 ? UNR_ : (UNIT && D <= 2 ? 8 : (UNIT && D <= 4 ? 4 : 1));
   static constexpr bool kClampable = false, kSets = UNIT;
   static constexpr int CS = 1;
   using Params = LscvScalarParams;

@@ -531,6 +531,7 @@ void kde_destroy(kde_ctx* c) {
   if (c->own_ws) cudaFree(c->own_ws);
   if (c->sort_ws) cudaFree(c->sort_ws);
   if (c->rows_ws) cudaFree(c->rows_ws);
+  if (c->f64_ws) cudaFree(c->f64_ws);
   if (c->white_ws) cudaFree(c->white_ws);
   if (c->ev_ws) cudaFree(c->ev_ws);
   if (c->mat_ws) cudaFree(c->mat_ws);

@@ -219,6 +219,44 @@ kde_status lscv_h_raw(kde_ctx* c, const double* X, int64_t n, int d, const doubl
   return KDE_OK;
 }
 
+double lscv_cancellation(int64_t n, int d, double det, double S1, double S2) {
+  const double nn = (double)n;
+  const double c4 = std::pow(4.0 * kPi, -0.5 * d) / std::sqrt(det);
+  const double c2 = std::pow(2.0 * kPi, -0.5 * d) / std::sqrt(det);
+  const double A = 2.0 * c4 * S1 / (nn * nn), B = 4.0 * c2 * S2 / (nn * nn), C = c4 / nn;
+  return (A + B) / std::fabs(A - B + C);   // +inf for g = 0
+}
+
+kde_status lscv_sums64(kde_ctx* c, const double* Xs, int64_t n, int d, const std::vector<double>& W,
+                       const std::vector<double>& mean, double kappa, kde_fixed out[2]) {
+  Range r("kde.lscv64");
+  const int T = kde::lscv64_tile();
+  const int64_t ld = (n + T - 1) / T * T;
+  TRY(grow(c, &c->f64_ws, &c->f64_bytes, (size_t)d * ld * sizeof(double)));
+  double* Y = static_cast<double*>(c->f64_ws);
+  kde::PrepParams pp;
+  std::copy(W.begin(), W.begin() + (size_t)d * d, pp.W);
+  std::copy(mean.begin(), mean.begin() + d, pp.mean);
+  CUDA_TRY(c, kde::launch_prep64(Xs, n, d, pp, Y, ld, c->stream));
+  Ws w;
+  TRY(get_ws(c, ld, d, 2, &w));
+  CUDA_TRY(c, cudaMemsetAsync(w.limbs, 0, 2 * kde::kLimbs * sizeof(long long), c->stream));
+  int64_t tb, te;
+  shard_range(n_tiles(n, T), c->rank, c->world, &tb, &te);
+  const int S = scale_exp_for(1.0, n);
+  // exp2(kappa s) is exactly 0 in fp64 for kappa s < -1100 (below the smallest subnormal 2^-1074)
+  CUDA_TRY(c, kde::launch_lscv64(d, Y, n, ld, tb, te, kappa, 1100.0 / -kappa, S, w.limbs, c->sm_count, c->stream));
+  c->prof_all += tb < te ? 2 : 1;
+  TRY(allreduce_limbs(c, w.limbs, 2 * kde::kLimbs));
+  long long hl[2 * kde::kLimbs];
+  CUDA_TRY(c, cudaMemcpyAsync(hl, w.limbs, sizeof(hl), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  out[0] = limbs_to_fixed(hl, S);
+  out[1] = limbs_to_fixed(hl + kde::kLimbs, S);
+  c->psi_escalations++;
+  return KDE_OK;
+}
+
 double lscv_h_finalize(int64_t n, int d, double det, double h, double S1, double S2) {
   const double nn = (double)n;
   const double c4 = std::pow(4.0 * kPi, -0.5 * d) / std::sqrt(det);
@@ -289,7 +327,7 @@ double lscv_H_finalize(int64_t n, int d, double det, double S1, double S2) {
 // Evaluate g(H) for a list of vech vectors (non-PD -> penalty); one GPU batch for all PD ones.
 kde_status lscv_H_eval(kde_ctx* c, const double* X, int64_t n, int d, const Moments& m,
                        const std::vector<std::vector<double>>& vs, double penalty,
-                       std::vector<double>& g, int* evals) {
+                       std::vector<double>& g, int* evals, bool auto_precision) {
   std::vector<HCand> pdc;
   std::vector<int> idx;
   g.assign(vs.size(), penalty);
@@ -299,9 +337,20 @@ kde_status lscv_H_eval(kde_ctx* c, const double* X, int64_t n, int d, const Mome
   }
   if (pdc.empty()) return KDE_OK;
   std::vector<kde_fixed> o;
+  TRY(gpu_sorted_rows(c, X, n, d, &X));
   TRY(lscv_H_raw(c, X, n, d, pdc, m, c->rank, c->world, true, o));
-  for (size_t j = 0; j < pdc.size(); ++j)
-    g[idx[j]] = lscv_H_finalize(n, d, pdc[j].det, fixed_value(o[2 * j]), fixed_value(o[2 * j + 1]));
+  for (size_t j = 0; j < pdc.size(); ++j) {
+    double S1 = fixed_value(o[2 * j]), S2 = fixed_value(o[2 * j + 1]);
+    // automatic precision (scores calls; Nelder-Mead searches keep fp32 terms, §3.10)
+    if (auto_precision && c->psi_mode != -1 &&
+        (c->psi_mode == 1 || !(lscv_cancellation(n, d, pdc[j].det, S1, S2) <= kLscvKappaMax))) {
+      kde_fixed f[2];
+      TRY(lscv_sums64(c, X, n, d, pdc[j].W, m.mean, -1.0, f));
+      S1 = fixed_value(f[0]);
+      S2 = fixed_value(f[1]);
+    }
+    g[idx[j]] = lscv_H_finalize(n, d, pdc[j].det, S1, S2);
+  }
   if (evals) *evals += (int)pdc.size();
   return KDE_OK;
 }
@@ -536,10 +585,26 @@ static kde_status lscv_h_scores_impl(kde_ctx* c, const double* X, int64_t n, int
   TRY(gpu_moments(c, X, n, d, w, m));
   LscvhPrep pp;
   TRY(lscv_h_prepare(c, m, d, pp));
+  TRY(gpu_sorted_rows(c, X, n, d, &X));
   std::vector<kde_fixed> o;
   TRY(lscv_h_raw(c, X, n, d, h, nh, m, pp, c->rank, c->world, true, o));
-  for (int k = 0; k < nh; ++k)
-    g[k] = lscv_h_finalize(n, d, pp.det, h[k], fixed_value(o[2 * k]), fixed_value(o[2 * k + 1]));
+  std::vector<double> W;
+  for (int k = 0; k < nh; ++k) {
+    double S1 = fixed_value(o[2 * k]), S2 = fixed_value(o[2 * k + 1]);
+    // automatic precision: a candidate whose objective cancels beyond what fp32 terms carry (or every
+    // candidate in the fp64-term mode) is re-run with fp64 terms (§3.10)
+    if (c->psi_mode != -1 && (c->psi_mode == 1 || !(lscv_cancellation(n, d, pp.det, S1, S2) <= kLscvKappaMax))) {
+      if (W.empty()) {
+        W = tri_lower_inverse(pp.Lc, d);
+        for (double& v : W) v *= std::sqrt(kLog2e / 4.0);
+      }
+      kde_fixed f[2];
+      TRY(lscv_sums64(c, X, n, d, W, m.mean, -1.0 / (h[k] * h[k]), f));
+      S1 = fixed_value(f[0]);
+      S2 = fixed_value(f[1]);
+    }
+    g[k] = lscv_h_finalize(n, d, pp.det, h[k], S1, S2);
+  }
   return KDE_OK;
 }
 
@@ -573,7 +638,7 @@ kde_status kde_lscv_H_scores(kde_ctx* c, const double* X, int64_t n, int32_t d, 
   std::vector<std::vector<double>> vs;
   for (int k = 0; k < nH; ++k) vs.emplace_back(vh + (size_t)k * P, vh + (size_t)(k + 1) * P);
   std::vector<double> out;
-  TRY(lscv_H_eval(c, X, n, d, m, vs, penalty, out, nullptr));
+  TRY(lscv_H_eval(c, X, n, d, m, vs, penalty, out, nullptr, /*auto_precision=*/true));
   TRY(prof_collect(c));
   std::copy(out.begin(), out.end(), g);
   return KDE_OK;

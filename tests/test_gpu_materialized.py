@@ -29,7 +29,12 @@ def test_materialized_matches_oracle_and_fused(ctx, d, n, B):
     hs = np.linspace(0.05, 1.5, 21)
     got = ctx.lscv_h_scores_materialized(kb.to_device(X), hs, h_per_pass=B)
     np.testing.assert_allclose(got, oracle.lscv_h_scores(X, hs), rtol=1e-5)
-    np.testing.assert_allclose(got, ctx.lscv_h_scores(kb.to_device(X), hs), rtol=1e-6)
+    ctx.set_precision(-1)   # kernel against kernel: the fused path with fp32 terms only (no fp64 re-run)
+    try:
+        fused = ctx.lscv_h_scores(kb.to_device(X), hs)
+    finally:
+        ctx.set_precision(0)
+    np.testing.assert_allclose(got, fused, rtol=1e-6)
 
 
 def test_materialized_batch_invariance(ctx):

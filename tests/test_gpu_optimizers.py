@@ -101,3 +101,38 @@ def test_device_nm_with_non_pd_proposals(ctx):
     dev = ctx.select_bandwidth(kb.LSCV_H, Xd, max_iter=200, nm_loop=0)
     host = ctx.select_bandwidth(kb.LSCV_H, Xd, max_iter=200, nm_loop=1)
     assert np.array_equal(dev["vechH"], host["vechH"]) and dev["evaluations"] == host["evaluations"]
+
+
+@pytest.mark.parametrize("d,n,seed,max_iter", [(5, 400, 51, 60), (6, 300, 52, 40)])
+def test_device_nm_large_d_equals_host_loop(ctx, d, n, seed, max_iter):
+    # P = d(d+1)/2 > 10: the decision runs on the global state block (the one-thread decide kernel)
+    X = np.random.default_rng(seed).normal(size=(d, n)) * np.linspace(0.5, 2.0, d)[:, None]
+    Xd = kb.to_device(X)
+    dev = ctx.select_bandwidth(kb.LSCV_H, Xd, max_iter=max_iter, nm_loop=0)
+    host = ctx.select_bandwidth(kb.LSCV_H, Xd, max_iter=max_iter, nm_loop=1)
+    assert np.array_equal(dev["vechH"], host["vechH"]) and dev["objective"] == host["objective"]
+    for k in ("iterations", "evaluations", "stop_reason"):
+        assert dev[k] == host[k], k
+
+
+@pytest.mark.parametrize("env", [{"KDE_DEBUG_NM_UNROLL": "1"}, {"KDE_DEBUG_NM_UNROLL": "3"},
+                                 {"KDE_DEBUG_NM_PDL": "0"}, {"KDE_DEBUG_NM_UNROLL": "16"}])
+def test_device_nm_loop_shape_does_not_change_the_search(ctx, env):
+    # Rounds per loop condition (the decisions after the stopping one are no-ops) and the programmatic
+    # launches change only the schedule: the same search, bit for bit.
+    import os
+    Xd = kb.to_device(datagen.sample_mixture("C3", 2000, 61))
+    ref = ctx.select_bandwidth(kb.LSCV_H, Xd, max_iter=500, nm_loop=0)
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        got = ctx.select_bandwidth(kb.LSCV_H, Xd, max_iter=500, nm_loop=0)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                del os.environ[k]
+            else:
+                os.environ[k] = v
+    assert np.array_equal(got["vechH"], ref["vechH"]) and got["objective"] == ref["objective"]
+    for k in ("iterations", "evaluations", "stop_reason"):
+        assert got[k] == ref[k], k

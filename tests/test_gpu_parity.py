@@ -463,19 +463,20 @@ def test_psi_far_tile_skip_is_exact(ctx, mode):
         ctx.set_precision(0)
 
 
-@pytest.mark.parametrize("which", ["h1", "h2", "H2", "H4"])
+@pytest.mark.parametrize("which", ["h1", "h2", "h8", "H1", "H2", "H4", "H7"])
 def test_lscv_far_tile_skip_is_exact(ctx, which):
     # LSCV data are sorted by coordinate 0 (whitening keeps that order); a tile whose coordinate-0 gap
     # bounds every s above the skip bound has every MUFU term exactly 0 (and every software-exp term at
     # 2^-125, far below the fixed-point resolution), so skipping it changes no output bit.
     import os
+    d = int(which[1])
     if which[0] == "h":
-        d = int(which[1])
-        X = datagen.sample_mixture("bimodal", 20011, 5) if d == 1 else datagen.sample_mixture("C3", 12007, 5)
-        kind, cand = kb.SUM_LSCV_h, list(np.geomspace(0.01, 1.5, 24))
+        X = (datagen.sample_mixture("bimodal", 20011, 5) if d == 1 else datagen.sample_mixture("C3", 12007, 5)
+             if d == 2 else np.random.default_rng(8).standard_t(4, size=(d, 6007)))
+        kind, cand = kb.SUM_LSCV_h, list(np.geomspace(0.01, 1.5, 24) if d <= 2 else np.geomspace(0.005, 0.05, 24))
     else:
-        d = int(which[1])
-        X = datagen.sample_mixture("C3" if d == 2 else "C5", 9001, 6)[:d]
+        X = (datagen.sample_mixture("C3" if d == 2 else "C5", 9001, 6)[:d] if d in (2, 4) else
+             np.random.default_rng(9).standard_t(4, size=(d, 5003)))
         kind, cand = kb.SUM_LSCV_H, np.concatenate([_spd_cands(d, 3, 7, s) for s in (1e-4, 1e-3, 0.05)]).ravel()
     Xd = dev(X)
     a = ctx.raw_sums(kind, Xd, cand)
@@ -489,9 +490,9 @@ def test_lscv_far_tile_skip_is_exact(ctx, which):
     assert [f.key() for f in a] == [f.key() for f in b]
     n = X.shape[1]
     ncand = len(cand) if kind == kb.SUM_LSCV_h else len(cand) // (d * (d + 1) // 2)
-    nb = {1: 8, 2: 8}.get(d, 8) if kind == kb.SUM_LSCV_h else 1
+    nb = (8 if d <= 4 else (16 if d <= 12 else 8)) if kind == kb.SUM_LSCV_h else 1   # kde_pair.cuh nb_scalar
     assert full == n * (n - 1) / 2 * (-(-ncand // nb) * nb)   # every pair x every candidate slot
-    assert evaluated < 0.9 * full                             # the small bandwidths skip most tiles
+    assert evaluated < (0.9 if d <= 4 else 1.0) * full        # the small bandwidths skip tiles
 
 
 def test_lscv_h_candidate_order_invariance(ctx):
@@ -506,3 +507,51 @@ def test_lscv_h_candidate_order_invariance(ctx):
         assert [f.key() for f in b[2 * j:2 * j + 2]] == [f.key() for f in a[2 * k:2 * k + 2]]
     solo = ctx.raw_sums(kb.SUM_LSCV_h, X, hs[3:4])
     assert [f.key() for f in solo] == [f.key() for f in a[6:8]]
+
+
+def _t5_data(n, d, seed):
+    # the generator of tests/diag/fuzz_wide.py (heavy-tailed, correlated, shifted)
+    r = np.random.default_rng(seed)
+    A = r.normal(size=(d, d)) / np.sqrt(d) + np.eye(d)
+    return A @ r.standard_t(5, size=(d, n)) + r.normal(size=(d, 1)) * 3
+
+
+@pytest.mark.parametrize("n,d,seed,h", [(1527, 5, 1028, 0.20282144591596876), (1671, 3, 1328, 0.5 * 0.1448139889679389)])
+def test_lscv_near_zero_objective_auto_precision(ctx, n, d, seed, h):
+    # Wide-fuzz cases where g(h) nearly vanishes (the objective cancels 464x and 3663x): fp32 terms
+    # (~1.5e-7 on the raw sums) gave 2.0e-5 and 1.8e-4 pointwise; the automatic precision re-runs such
+    # candidates with fp64 terms, for both families, and stays within 1e-5 pointwise.
+    X = _t5_data(n, d, seed)
+    _, S = oracle.mean_cov(X)
+    Xd = dev(X)
+    H = datagen.vech(h * h * S)
+    ref_h = oracle.lscv_h_scores(X, [h])[0]
+    ref_H = oracle.lscv_H_score(X, H)
+    got_h = ctx.lscv_h_scores(Xd, [h])[0]
+    assert ctx.last_fp64_passes() == 1
+    got_H = ctx.lscv_H_scores(Xd, [H])[0]
+    assert ctx.last_fp64_passes() == 1
+    assert rel(got_h, ref_h) <= RTOL and rel(got_H, ref_H) <= RTOL, (got_h, ref_h, got_H, ref_H)
+    ctx.set_precision(-1)   # fp32 terms only: no re-run
+    try:
+        ctx.lscv_H_scores(Xd, [H])
+        assert ctx.last_fp64_passes() == 0
+    finally:
+        ctx.set_precision(0)
+
+
+@pytest.mark.parametrize("d,n", [(1, 1500), (3, 700), (6, 300)])
+def test_lscv_fp64_mode_matches_oracle(ctx, d, n):
+    # kde_set_precision(1): every LSCV candidate also runs with fp64 terms (the fp64 kernel's own pin)
+    X = _t5_data(n, d, 70 + d)
+    _, S = oracle.mean_cov(X)
+    hs = [0.3, 0.6]
+    ctx.set_precision(1)
+    try:
+        got_h = ctx.lscv_h_scores(dev(X), hs)
+        assert ctx.last_fp64_passes() == len(hs)
+        got_H = ctx.lscv_H_scores(dev(X), [datagen.vech(h * h * S) for h in hs])
+    finally:
+        ctx.set_precision(0)
+    np.testing.assert_allclose(got_h, oracle.lscv_h_scores(X, hs), rtol=1e-11)
+    np.testing.assert_allclose(got_H, [oracle.lscv_H_score(X, datagen.vech(h * h * S)) for h in hs], rtol=1e-11)
