@@ -255,7 +255,9 @@ kde_status kde_last_profile(const kde_ctx *ctx, int32_t *launches, double *pair_
  * grid selection (Eq. 24/30): in mode 0 a candidate whose objective
  * g = A - B + C cancels beyond kLscvKappaMax = 32 ((A + B)/|g|, so the fp32 terms' ~1.5e-7 on the raw
  * sums could exceed 1e-5 on g) is re-run with fp64 terms; mode 1 re-runs every candidate.  Nelder-Mead
- * searches and kde_raw_sums always use fp32 terms.
+ * searches use fp32 terms in modes 0 and -1 (host and device loops decide identically); in mode 1 the
+ * search runs on the host loop with fp64 terms for every g(H) (the exact-parity search).  kde_raw_sums
+ * always returns fp32-term sums.
  * Results stay deterministic and partition-invariant in every mode. */
 kde_status kde_set_precision(kde_ctx *ctx, int32_t fp64_terms);
 /* Number of Psi passes and LSCV candidates of the last call that were (re-)run with fp64 terms, and

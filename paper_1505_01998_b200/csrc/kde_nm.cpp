@@ -48,7 +48,9 @@ kde_status nelder_mead_multi(kde_ctx* c, const double* X, int64_t n, int d, cons
     }
     if (batch.empty()) break;
     std::vector<double> g;
-    TRY(lscv_H_eval(c, X, n, d, m, batch, penalty, g, &evals));
+    // fp64-term mode (kde_set_precision(ctx, 1)): every candidate with fp64 terms, the exact-parity
+    // search of SURVEY c5; otherwise fp32 terms, as the device-resident loop
+    TRY(lscv_H_eval(c, X, n, d, m, batch, penalty, g, &evals, /*auto_precision=*/c->psi_mode == 1));
     size_t off = 0;
     for (auto& sp : span) {
       kde::nm_accept(*runs[sp.first], g.data() + off);

@@ -799,7 +799,7 @@ kde_status kde_select_bandwidth(kde_ctx* c, kde_method method, const double* X, 
     TRY(gpu_sorted_rows(c, X, n, d, &X));   // once for the whole search (far-tile skip)
     // device-resident loop: one GPU, one start, serial rounds, whitened sets within ~1 GiB
     const int64_t Tm = kde::tile_for(Kind::LscvMatrix, d, n), ldT = (n + Tm - 1) / Tm * Tm;
-    const bool dev_loop = o.nm_loop == 0 && K == 1 && o.speculative == 0 && c->world == 1 && !c->comm &&
+    const bool dev_loop = o.nm_loop == 0 && K == 1 && o.speculative == 0 && c->world == 1 && !c->comm && c->psi_mode != 1 &&
                           !c->har_fn && (double)(P + 1) * d * (double)ldT * 4.0 <= (double)(1LL << 30);
     if (dev_loop)
       TRY(nelder_mead_device(c, X, n, d, m, sims[0], o.max_iter, o.tol_rel, o.penalty, nm));

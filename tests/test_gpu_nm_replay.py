@@ -57,3 +57,20 @@ def test_nm_path_library_gpu_driven_and_oracle_agree(mix, d, n, seed, max_iter):
     assert len(to) == len(tg)
     for (xo, _), (xg, _) in zip(to, tg):
         assert np.array_equal(xo, xg)
+
+
+@pytest.mark.parametrize("mix,d,n,seed,max_iter", [("C3", 2, 1200, 43, 300), ("C5", 3, 600, 44, 200)])
+def test_nm_fp64_term_mode_reproduces_the_oracle_search(mix, d, n, seed, max_iter):
+    # SURVEY c5's optional exact-parity mode: with kde_set_precision(1) every g(H) of the search runs
+    # with fp64 terms (host loop), so the library's search and the all-oracle search make the same
+    # decisions and end at the same H (to the last bits of the start point's square root).
+    X = datagen.sample_mixture(mix, n, seed)[:d]
+    ctx = kb.Context()
+    ctx.set_precision(1)
+    got = ctx.select_bandwidth(kb.LSCV_H, kb.to_device(X), max_iter=max_iter)
+    ctx.close()
+    sim0 = oracle.initial_simplex(oracle.vech(oracle.H_start(X)), d)
+    ref = oracle.nelder_mead(lambda v: oracle.lscv_H_score(X, v, threads=THREADS), sim0, max_iter=max_iter)
+    assert got["iterations"] == ref["iterations"]
+    assert np.max(np.abs(got["vechH"] - ref["x"])) <= 1e-9 * np.max(np.abs(ref["x"]))
+    assert abs(got["objective"] - ref["f"]) <= 1e-10 * abs(ref["f"])
