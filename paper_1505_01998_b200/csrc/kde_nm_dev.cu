@@ -268,6 +268,8 @@ kde_status nelder_mead_device(kde_ctx* c, const double* X, int64_t n, int d, con
   // prep flags .. the skipped-pair counter (kSkippedSlot)
   CUDA_TRY(c, cudaMemsetAsync(w.flag(), 0, (kSkippedSlot - 408 + 1) * sizeof(unsigned long long), st));
   if (tracing) CUDA_TRY(c, cudaMemsetAsync(h.trace, 0, tr_b, st));
+  // g, det, slot: the decide kernel copies all kSmallP + 1 entries (only the first n_prop are ever used)
+  CUDA_TRY(c, cudaMemsetAsync(&dblk->g, 0, offsetof(NMDevBlock, L) - offsetof(NMDevBlock, g), st));
   // the graph (built once per key, replayed afterwards)
   const std::vector<uintptr_t> key = {(uintptr_t)X, (uintptr_t)n, (uintptr_t)d, (uintptr_t)w.limbs,
                                       (uintptr_t)Yw, (uintptr_t)dblk, (uintptr_t)T, (uintptr_t)tracing,

@@ -32,3 +32,13 @@ print("plugin x3 (graph capture + replay)", [ctx.plugin_h(xs)[0] for _ in range(
 ctx.set_precision(True)
 print("fp64 psi + plugin", ctx.psi_r(x, 6, [0.3]), ctx.plugin_h(x)[0])
 ctx.set_precision(False)
+# round 2: LSCV far-tile skip on sorted data, fp64-term LSCV (prep64 + lscv64), the device Nelder-Mead
+# loop (PDL launches, 4 rounds per condition), skipped-tile NM
+Xb = kb.to_device(datagen.sample_mixture("bimodal", 3001, 4))
+print("lscv_h skip", ctx.lscv_h_scores(Xb, [0.005, 0.01, 0.5]))
+X3 = kb.to_device(datagen.sample_mixture("C5", 2100, 5)[:3])
+print("lscv_H skip", ctx.lscv_H_scores(X3, [datagen.vech(np.eye(3) * 1e-4), datagen.vech(np.eye(3) * 0.05)]))
+ctx.set_precision(1)
+print("fp64 lscv", ctx.lscv_h_scores(X, [0.3]), ctx.lscv_H_scores(X3, [datagen.vech(np.eye(3) * 0.05)]))
+ctx.set_precision(0)
+print("select H device loop", ctx.select_bandwidth(kb.LSCV_H, X, max_iter=40)["objective"])
