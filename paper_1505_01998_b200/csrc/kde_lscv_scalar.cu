@@ -7,7 +7,7 @@
 
 namespace kde {
 
-// d <= 4: 8 candidates per pair visit at 3 CTAs/SM, a quarter of the exponentials in software on
+// d <= 4: 8 candidates per pair visit at 4 CTAs/SM (3 until round 2), a quarter of the exponentials in software on
 // the FMA pipe (measured on C2: 478 ms vs 490 ms for 16 candidates, all on MUFU); d > 4: the
 // per-pair work dominates, 16 candidates on MUFU.
 // Software-exp column masks (bit j mod 16): KDE_DEBUG_LSCVh_SW selects an A/B variant for d = 1
@@ -37,6 +37,11 @@ static cudaError_t lscv_scalar_d(const LaunchCfg& c, const LscvScalarParams& p) 
       case 17: return launch_pair<FLscvScalar<1, 256, 8, false, 0x8888u, 3, false, true, true, 2>>(c, p);  // 32 cols/iter
       case 18: return launch_pair<FLscvScalar<1, 256, 8, false, 0x0888u, 3, false, true, true>>(c, p);  // 3/16
       case 19: return launch_pair<FLscvScalar<1, 256, 8, false, 0x4924u, 3, false, true, true>>(c, p);  // 4/16 spread (2,5,8,11,14)
+      case 20: return launch_pair<FLscvScalar<1, 256, 8, false, 0x888Au, 4, false, true, true>>(c, p);  // 4 CTAs, 5/16
+      case 21: return launch_pair<FLscvScalar<1, 256, 8, false, 0x8A8Au, 4, false, true, true>>(c, p);  // 4 CTAs, 6/16
+      case 22: return launch_pair<FLscvScalar<1, 256, 8, false, 0x8888u, 4, false, false, true>>(c, p); // 4 CTAs, col-major
+      case 23: return launch_pair<FLscvScalar<1, 256, 8, false, 0x8888u, 4, false, true, false>>(c, p); // 4 CTAs, plain exp
+      case 25: return launch_pair<FLscvScalar<1, 256, 8, false, 0x0888u, 4, false, true, true>>(c, p);  // 4 CTAs, 3/16
       default: break;
     }
   }
@@ -45,11 +50,14 @@ static cudaError_t lscv_scalar_d(const LaunchCfg& c, const LscvScalarParams& p) 
       case 9: return launch_pair<FLscvScalar<D, 256, 8, false, kSwDefault, 3, false, true, false>>(c, p);    // cand-major
       case 10: return launch_pair<FLscvScalar<D, 256, 8, false, kSwDefault, 3, false, false, true>>(c, p);   // fma exp
       case 15: return launch_pair<FLscvScalar<D, 256, 8, false, kSwDefault, 3, false, false, false>>(c, p);  // round-2 kernel
+      case 24: return launch_pair<FLscvScalar<D, 256, 8, false, kSwDefault, 4, false, true, true>>(c, p);    // 4 CTAs/SM
+      case 26: return launch_pair<FLscvScalar<D, 256, 8, false, kSwDefault, 3, false, true, true>>(c, p);    // 3 CTAs/SM
       default: break;
     }
     // default (C2 A/B, profiles/r02_lscv_h_variants2.jsonl): candidate-major order, product folded into
-    // the software exp's range reduction
-    return launch_pair<FLscvScalar<D, 256, nb_scalar(D), false, kSwDefault, 3, false, true, true>>(c, p);
+    // the software exp's range reduction, 4 CTAs/SM (64 registers; the spills sit outside the column loop):
+    // C2 405.5 (round-2 kernel) -> 400.5 (3 CTAs) -> 385.5 ms
+    return launch_pair<FLscvScalar<D, 256, nb_scalar(D), false, kSwDefault, 4, false, true, true>>(c, p);
   } else {
     return launch_pair<FLscvScalar<D, 256, nb_scalar(D)>>(c, p);
   }

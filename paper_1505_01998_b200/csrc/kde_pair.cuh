@@ -30,7 +30,7 @@
 
 namespace kde {
 
-// LSCV_h candidates per pair visit: d <= 4: 8 at 3 CTAs/SM (80 registers); larger d: 16, then 8,
+// LSCV_h candidates per pair visit: d <= 4: 8 at 4 CTAs/SM (64 registers); larger d: 16, then 8,
 // so that no instantiation spills.
 constexpr int nb_scalar(int d) { return d <= 4 ? 8 : (d <= 12 ? 16 : 8); }
 
