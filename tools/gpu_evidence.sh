@@ -18,3 +18,11 @@ timeout 1200 python tools/bench_configs.py ${CONFIGS:-C1 C4 C2 C5 C3 F1 F2 F3 F4
 stamp configs
 if [ -z "$NO_NCU" ]; then bash tools/gpu_prof.sh psi lscv; stamp ncu; fi
 tail -3 gpurun_out/pytest_gpu.txt; cat gpurun_out/smoke.txt; cut -c1-400 gpurun_out/bench.json; cat gpurun_out/timeline.txt
+# summarise the ncu reports on the box (the .ncu-rep files would exceed gpurun's 64 MiB copy-back)
+if [ -z "$NO_NCU" ]; then
+  python tools/ncu_summary.py launches gpurun_out/launches.csv gpurun_out/launches.md > /dev/null 2>&1
+  for r in gpurun_out/prof_*.ncu-rep; do python tools/ncu_summary.py full "$r" "${r%.ncu-rep}" > /dev/null 2>&1; done
+  mkdir -p gpurun_out/reps && mv gpurun_out/prof_*.ncu-rep gpurun_out/reps/ 2>/dev/null
+  [ -n "$KEEP_REPS" ] || rm -rf gpurun_out/reps
+fi
+du -sh gpurun_out

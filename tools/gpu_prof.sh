@@ -12,7 +12,7 @@ ncu --set full --clock-control none --import-source on -k regex:pair_kernel -s $
 done
 fi
 if [[ " $* " == *" lscv "* || $# -eq 0 ]]; then
-ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:FLscvScalar -s 3 -c 1 \
+ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:FLscvScalar -s 250 -c 1 \
     -o gpurun_out/prof_c2 -f python tools/bench_configs.py C2 --reps 1 > gpurun_out/ncu_c2.log 2>&1
 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:FLscvScalar -s 0 -c 1 \
     -o gpurun_out/prof_c5p -f python tools/bench_configs.py C5P --reps 1 > gpurun_out/ncu_c5p.log 2>&1
