@@ -167,8 +167,18 @@ kde_status kde_lscv_H_scores(kde_ctx *ctx, const double *X_dev, int64_t n, int32
                              const double *vechH_host, int32_t n_H, double penalty_or_nan,
                              double *g_host);
 
-/* Full selector: PLUGIN (d = 1), LSCV_h (grid argmin on Z(h0), ties -> smaller h), or LSCV_H
- * (Nelder-Mead over vech(H) from H_start of Eq. 35).  opts_or_null: NULL = kde_default_opts. */
+/* Full selector (Sec. 4.4), samples X_dev as for the score calls (device or host fp64,
+ * d x n row-major; owned by the caller, read only):
+ *   KDE_PLUGIN (d = 1): the chain of Sec. 4.4.1, P:199-256 (out->h, out->trace);
+ *   KDE_LSCV_h: h0 of Eq. 25 (reading Z3), grid of opts->n_grid points on
+ *     Z(h0) = [h0/f, f h0] (Eq. 27, f = opts->range_factor, readings Z4), argmin of g(h)
+ *     (Eq. 28; ties -> smaller h), optional bracket refinement (opts->refine_steps);
+ *   KDE_LSCV_H: Nelder-Mead over vech(H) (readings Z8) from H_start of Eq. 35,
+ *     non-PD vertices get opts->penalty; opts->nm_starts starts, opts->nm_loop 0 = device-resident
+ *     loop when eligible (one GPU, one start).
+ * opts_or_null: NULL = kde_default_opts.  out: host struct written on KDE_OK only.
+ * Errors: KDE_E_NOT_UNIVARIATE (PLUGIN with d > 1), KDE_E_SINGULAR_COV, KDE_E_NO_FEASIBLE (no PD H
+ * found), KDE_E_INVALID (bad options), and those of the score calls. */
 kde_status kde_select_bandwidth(kde_ctx *ctx, kde_method method, const double *X_dev, int64_t n,
                                 int32_t d, const kde_select_opts *opts_or_null, kde_bandwidth *out);
 
