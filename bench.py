@@ -177,28 +177,29 @@ def relaunch_under_torchrun(n: int):
 
 def run_dry(args, rank, world):
     """CPU check of the N-rank plumbing (gloo): rendezvous, each rank's contiguous tile range of
-    the C4 pair partition (the library's own kde_shard_tiles), barrier and max-over-ranks
+    the C4 pair partition (the library's own kde_shard_tiles: round-robin chunks), barrier and max-over-ranks
     reduction as in the timed path; rank 0 prints the JSON line.  No kernels run."""
     import torch
     import torch.distributed as dist
     import paper_1505_01998_b200 as kb
     if world > 1:
         dist.init_process_group("gloo")
-    T, total, tb, te = kb.shard_tiles(kb.SUM_PSI6, args.n, 1, rank, world)
-    t = torch.tensor([float(te - tb), float(rank)], dtype=torch.float64)
+    T, total, cnt, chunk = kb.shard_tiles(kb.SUM_PSI6, args.n, 1, rank, world)
+    t = torch.tensor([float(cnt), float(rank)], dtype=torch.float64)
+    mine = (cnt, chunk, kb.shard_tile(0, rank, world) if cnt else None)
     ranges = [None] * world
     if world > 1:
         dist.barrier()
-        dist.all_gather_object(ranges, (tb, te))
+        dist.all_gather_object(ranges, mine)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     else:
-        ranges = [(tb, te)]
+        ranges = [mine]
     if rank == 0:
         print(json.dumps({"metric": METRIC, "value": None, "unit": "evals/s", "n_gpus": world, "steps": 0,
                           "warmup": 0, "dry_run": True, "scaling": "strong",
                           "config": {"workload": "C4 PLUGIN n=2^20 skewed mixture (MW#2), seed 4", "n": args.n,
                                      "parallelism": f"pair-range x{world}", "tile": T, "tiles": total,
-                                     "rank_tiles": ranges, "max_rank_tiles": float(t[0])}}), flush=True)
+                                     "rank_tiles_chunk_first": ranges, "max_rank_tiles": float(t[0])}}), flush=True)
     if world > 1:
         dist.destroy_process_group()
 

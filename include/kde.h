@@ -239,13 +239,17 @@ kde_fixed kde_fixed_add(kde_fixed a, kde_fixed b);
  * column l and row q (q <= l) of the upper-triangular tile grid, column l holding l+1 tiles. */
 void kde_tile_coords(int64_t bx, int64_t *l, int64_t *q);
 
-/* The work partition the library uses for a sum of `kind` over n samples in d dimensions:
- * tile edge T, total tiles of the upper-triangular grid, and the contiguous tile range
- * [*tile_begin, *tile_end) that rank `rank` of `world` evaluates.  Pure host
- * function (no GPU needed).  Returns KDE_E_INVALID for bad arguments. */
+/* The work partition the library uses for a sum of `kind` over n samples in d dimensions
+ * (SURVEY §8(e)): tile edge T and the total tiles of the upper-triangular grid (tile ids of Eq.
+ * 42-43, column by column).  Rank `rank` of `world` evaluates the tile ids
+ *   (c * world + rank) * chunk + w,   c = 0, 1, ...,  0 <= w < chunk,  id < tiles_total
+ * (round-robin chunks of *chunk = 16 consecutive ids for world > 1, so that every rank gets the same
+ * mix of diagonal, near and exactly-zero tiles on sorted data), *rank_tiles of them; its local index
+ * i in [0, *rank_tiles) is tile id kde_shard_tile(i, rank, world).  world = 1: every id, in order.
+ * Pure host functions (no GPU needed).  KDE_E_INVALID / -1 for bad arguments. */
 kde_status kde_shard_tiles(kde_sum_kind kind, int64_t n, int32_t d, int32_t rank, int32_t world,
-                           int32_t *tile_edge, int64_t *tiles_total, int64_t *tile_begin,
-                           int64_t *tile_end);
+                           int32_t *tile_edge, int64_t *tiles_total, int64_t *rank_tiles, int32_t *chunk);
+int64_t kde_shard_tile(int64_t i, int32_t rank, int32_t world);
 
 /* Kernel timing of the last call on this context: number of pair-kernel launches, their
  * summed device time (ms, CUDA events on the context stream) and the algorithmic pair-kernel

@@ -34,7 +34,7 @@ EXPORTS = ["kde_create", "kde_destroy", "kde_last_error", "kde_nccl_unique_id",
            "kde_workspace_bytes", "kde_set_workspace", "kde_default_opts", "kde_psi_r",
            "kde_plugin_h", "kde_lscv_h_scores", "kde_lscv_H_scores", "kde_select_bandwidth",
            "kde_raw_sums", "kde_fixed_value", "kde_fixed_add", "kde_tile_coords",
-           "kde_last_profile", "kde_set_profiling", "kde_shard_tiles", "kde_evaluate", "kde_aqp_1d",
+           "kde_last_profile", "kde_set_profiling", "kde_shard_tiles", "kde_shard_tile", "kde_evaluate", "kde_aqp_1d",
            "kde_lscv_h_scores_materialized", "kde_last_aux_ms", "kde_set_host_allreduce", "kde_set_precision",
            "kde_last_fp64_passes", "kde_last_psi_kappa"]
 
@@ -114,8 +114,9 @@ def lib():
     L.kde_last_profile.argtypes = [vp, ctypes.POINTER(i32), dp, dp, ctypes.POINTER(i32)]
     L.kde_set_profiling.argtypes = [vp, i32]
     L.kde_shard_tiles.argtypes = [ctypes.c_int, i64, i32, i32, i32, ctypes.POINTER(i32), ctypes.POINTER(i64),
-                                  ctypes.POINTER(i64), ctypes.POINTER(i64)]
+                                  ctypes.POINTER(i64), ctypes.POINTER(i32)]
     L.kde_shard_tiles.restype = ctypes.c_int
+    L.kde_shard_tile.argtypes = [i64, i32, i32]; L.kde_shard_tile.restype = i64
     L.kde_evaluate.argtypes = [vp, vp, i64, i32, vp, i64, dp, dp]
     L.kde_evaluate.restype = ctypes.c_int
     L.kde_aqp_1d.argtypes = [vp, vp, i64, f64, dp, dp, i32, dp, dp, dp]
@@ -160,13 +161,19 @@ def fixed_add(a: Fixed, b: Fixed) -> Fixed:
 
 
 def shard_tiles(kind: int, n: int, d: int, rank: int, world: int):
-    """(tile edge T, total tiles, first tile, end tile) of `rank`'s share (host-only query)."""
-    T, tot, b, e = ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    """(tile edge T, total tiles, rank's tile count, chunk) of `rank`'s share (host-only query); the
+    rank's local index i is tile id shard_tile(i, rank, world) (round-robin chunks)."""
+    T, tot, cnt, ch = ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int32()
     rc = lib().kde_shard_tiles(int(kind), int(n), int(d), int(rank), int(world), ctypes.byref(T),
-                               ctypes.byref(tot), ctypes.byref(b), ctypes.byref(e))
+                               ctypes.byref(tot), ctypes.byref(cnt), ctypes.byref(ch))
     if rc != 0:
         raise KDEError(rc, "bad shard query")
-    return T.value, tot.value, b.value, e.value
+    return T.value, tot.value, cnt.value, ch.value
+
+
+def shard_tile(i: int, rank: int, world: int) -> int:
+    """Tile id of local index i of `rank` of `world` (kde_shard_tile)."""
+    return int(lib().kde_shard_tile(int(i), int(rank), int(world)))
 
 
 def nccl_unique_id() -> bytes:

@@ -157,12 +157,12 @@ kde_status kde_lscv_h_scores_materialized(kde_ctx* c, const double* X, int64_t n
   float* buf = (float*)c->mat_ws;
   cudaEvent_t a0 = nullptr, a1 = nullptr;
   if (c->profiling) { a0 = next_event(c); a1 = next_event(c); cudaEventRecord(a0, c->stream); }
-  CUDA_TRY(c, kde::launch_mat_write(d, w.Y, n, ld, tb, te, buf, c->sm_count, c->stream));   // phase 1
+  CUDA_TRY(c, kde::launch_mat_write(d, w.Y, n, ld, tb, te, buf, c->sm_count, c->stream, c->rank, c->world));   // phase 1
   c->prof_all += 1;
   if (c->profiling) cudaEventRecord(a1, c->stream);
   CUDA_TRY(c, cudaMemsetAsync(w.limbs, 0, (size_t)n_out * kde::kLimbs * sizeof(long long), c->stream));
   const int S = scale_exp_for(1.0, n);
-  const double pairs = c->profiling ? pairs_in_range(n, T, tb, te) : 0.0;
+  const double pairs = c->profiling ? pairs_in_shard(n, T, te, c->rank, c->world) : 0.0;
   for (int b = 0; b < nbatch; ++b) {                                                          // phase 2
     kde::LscvScalarParams p;
     for (int j = 0; j < kde::kMaxCand; ++j) {

@@ -181,6 +181,7 @@ kde_status gpu_prep(kde_ctx* c, const double* X, int64_t n, int d, const std::ve
 int64_t n_tiles(int64_t n, int T);
 void shard_range(int64_t tiles, int rank, int world, int64_t* b, int64_t* e);
 double pairs_in_range(int64_t n, int T, int64_t b, int64_t e);
+double pairs_in_shard(int64_t n, int T, int64_t count, int rank, int world);
 cudaEvent_t next_event(kde_ctx* c);
 void prof_reset(kde_ctx* c);
 kde_status prof_collect(kde_ctx* c);

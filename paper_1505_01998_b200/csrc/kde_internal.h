@@ -51,7 +51,10 @@ double psi_skip_gap(bool fp64);
 struct LaunchCfg {
   const float* X;          // D rows of ld floats (fp32, prepared), device
   int64_t n, ld;           // samples, padded row length (multiple of the tile)
+  // this launch's tiles: local indices [tile_begin, tile_end) of rank part_rank of part_world
+  // (kde_tiles.cuh shard_tile: round-robin chunks; world 1 = the tile ids themselves)
   int64_t tile_begin, tile_end;
+  int part_rank = 0, part_world = 1;
   int tile;                // tile edge T (rows = columns)
   int scale_exp;           // fixed-point exponent S
   unsigned long long* limbs;   // [n_out][3] accumulators, device
@@ -99,7 +102,8 @@ cudaError_t launch_psi_prep(const double* x, int64_t n, const double* mean_dev, 
 constexpr int kPsi64Tile = 256;
 cudaError_t launch_psi64(int r, const double* y, int64_t n, int64_t tile_begin, int64_t tile_end, int S,
                          unsigned long long* limbs, int sm_count, cudaStream_t s,
-                         const unsigned long long* gate = nullptr, double skip_gap = kPsiSkipGap64);
+                         const unsigned long long* gate = nullptr, double skip_gap = kPsiSkipGap64,
+                         int part_rank = 0, int part_world = 1);
 
 cudaError_t launch_lscv_scalar(int d, int nb, const LaunchCfg& c, const LscvScalarParams& p);
 // LSCV_H with per-candidate whitened data (one candidate per set, c.n_sets sets).
@@ -138,7 +142,8 @@ int lscv64_tile();
 cudaError_t launch_prep64(const double* X, int64_t n, int d, const PrepParams& pp, double* Y, int64_t ld,
                           cudaStream_t s);
 cudaError_t launch_lscv64(int d, const double* Y, int64_t n, int64_t ld, int64_t tb, int64_t te, double kappa,
-                          double skip_s, int S, unsigned long long* limbs, int sm_count, cudaStream_t s);
+                          double skip_s, int S, unsigned long long* limbs, int sm_count, cudaStream_t s,
+                          int part_rank = 0, int part_world = 1);
 
 // Device-resident PLUGIN chain (kde_psi.cu).  Layout of the workspace's `small` block (doubles):
 // mean[16] | W[256] | sums[136] | flags (2 x u64) | trace[8] | status.
@@ -186,7 +191,7 @@ cudaError_t eval_splits(int d, int sm_count, int64_t ldm, int64_t ldn, int* spli
 int mat_tile();
 int64_t mat_chunk();
 cudaError_t launch_mat_write(int d, const float* X, int64_t n, int64_t ld, int64_t tb, int64_t te, float* buf,
-                             int sm_count, cudaStream_t s);
+                             int sm_count, cudaStream_t s, int part_rank = 0, int part_world = 1);
 cudaError_t launch_mat_reduce(int B, const float* buf, int64_t nvalues, const LscvScalarParams& p, int S,
                               unsigned long long* limbs, int sm_count, cudaStream_t s);
 // Univariate AQP closed forms (kde_eval.cu): out[2q] = COUNT, out[2q+1] = SUM.

@@ -39,13 +39,14 @@ __global__ void prep64_kernel(const double* __restrict__ X, int64_t n, int d, co
 template <int D>
 __global__ void __launch_bounds__(kL64Tile) lscv64_kernel(const double* __restrict__ Y, int64_t n, int64_t ld,
                                                           int64_t tb, int64_t te, double kappa, double skip_s, int S,
-                                                          unsigned long long* __restrict__ limbs) {
+                                                          unsigned long long* __restrict__ limbs, int part_rank,
+                                                          int part_world) {
   __shared__ double cs[D][kL64Tile];
   __shared__ double red[(kL64Tile / 32) * 2];
   const int tid = threadIdx.x;
-  for (int64_t t = tb + blockIdx.x; t < te; t += gridDim.x) {
+  for (int64_t u = tb + blockIdx.x; u < te; u += gridDim.x) {   // this rank's local tile indices
     int64_t l, q;
-    tile_coords(t, l, q);
+    tile_coords(shard_tile(u, part_rank, part_world), l, q);
     if (q < l) {
       const double g = Y[l * kL64Tile] - Y[q * kL64Tile + kL64Tile - 1];
       if (g * g > skip_s) continue;   // uniform per CTA
@@ -89,32 +90,34 @@ cudaError_t launch_prep64(const double* X, int64_t n, int d, const PrepParams& p
 
 template <int D>
 static cudaError_t launch64_d(const double* Y, int64_t n, int64_t ld, int64_t tb, int64_t te, double kappa,
-                              double skip_s, int S, unsigned long long* limbs, int sm_count, cudaStream_t s) {
+                              double skip_s, int S, unsigned long long* limbs, int sm_count, cudaStream_t s,
+                              int pr, int pw) {
   const int64_t grid = std::min<int64_t>(te - tb, (int64_t)sm_count * 8);
-  lscv64_kernel<D><<<(unsigned)grid, kL64Tile, 0, s>>>(Y, n, ld, tb, te, kappa, skip_s, S, limbs);
+  lscv64_kernel<D><<<(unsigned)grid, kL64Tile, 0, s>>>(Y, n, ld, tb, te, kappa, skip_s, S, limbs, pr, pw);
   return cudaGetLastError();
 }
 
 cudaError_t launch_lscv64(int d, const double* Y, int64_t n, int64_t ld, int64_t tb, int64_t te, double kappa,
-                          double skip_s, int S, unsigned long long* limbs, int sm_count, cudaStream_t s) {
+                          double skip_s, int S, unsigned long long* limbs, int sm_count, cudaStream_t s, int pr,
+                          int pw) {
   if (te <= tb) return cudaSuccess;
   switch (d) {
-    case 1: return launch64_d<1>(Y, n, ld, tb, te, kappa, skip_s, S, limbs, sm_count, s);
-    case 2: return launch64_d<2>(Y, n, ld, tb, te, kappa, skip_s, S, limbs, sm_count, s);
-    case 3: return launch64_d<3>(Y, n, ld, tb, te, kappa, skip_s, S, limbs, sm_count, s);
-    case 4: return launch64_d<4>(Y, n, ld, tb, te, kappa, skip_s, S, limbs, sm_count, s);
-    case 5: return launch64_d<5>(Y, n, ld, tb, te, kappa, skip_s, S, limbs, sm_count, s);
-    case 6: return launch64_d<6>(Y, n, ld, tb, te, kappa, skip_s, S, limbs, sm_count, s);
-    case 7: return launch64_d<7>(Y, n, ld, tb, te, kappa, skip_s, S, limbs, sm_count, s);
-    case 8: return launch64_d<8>(Y, n, ld, tb, te, kappa, skip_s, S, limbs, sm_count, s);
-    case 9: return launch64_d<9>(Y, n, ld, tb, te, kappa, skip_s, S, limbs, sm_count, s);
-    case 10: return launch64_d<10>(Y, n, ld, tb, te, kappa, skip_s, S, limbs, sm_count, s);
-    case 11: return launch64_d<11>(Y, n, ld, tb, te, kappa, skip_s, S, limbs, sm_count, s);
-    case 12: return launch64_d<12>(Y, n, ld, tb, te, kappa, skip_s, S, limbs, sm_count, s);
-    case 13: return launch64_d<13>(Y, n, ld, tb, te, kappa, skip_s, S, limbs, sm_count, s);
-    case 14: return launch64_d<14>(Y, n, ld, tb, te, kappa, skip_s, S, limbs, sm_count, s);
-    case 15: return launch64_d<15>(Y, n, ld, tb, te, kappa, skip_s, S, limbs, sm_count, s);
-    case 16: return launch64_d<16>(Y, n, ld, tb, te, kappa, skip_s, S, limbs, sm_count, s);
+    case 1: return launch64_d<1>(Y, n, ld, tb, te, kappa, skip_s, S, limbs, sm_count, s, pr, pw);
+    case 2: return launch64_d<2>(Y, n, ld, tb, te, kappa, skip_s, S, limbs, sm_count, s, pr, pw);
+    case 3: return launch64_d<3>(Y, n, ld, tb, te, kappa, skip_s, S, limbs, sm_count, s, pr, pw);
+    case 4: return launch64_d<4>(Y, n, ld, tb, te, kappa, skip_s, S, limbs, sm_count, s, pr, pw);
+    case 5: return launch64_d<5>(Y, n, ld, tb, te, kappa, skip_s, S, limbs, sm_count, s, pr, pw);
+    case 6: return launch64_d<6>(Y, n, ld, tb, te, kappa, skip_s, S, limbs, sm_count, s, pr, pw);
+    case 7: return launch64_d<7>(Y, n, ld, tb, te, kappa, skip_s, S, limbs, sm_count, s, pr, pw);
+    case 8: return launch64_d<8>(Y, n, ld, tb, te, kappa, skip_s, S, limbs, sm_count, s, pr, pw);
+    case 9: return launch64_d<9>(Y, n, ld, tb, te, kappa, skip_s, S, limbs, sm_count, s, pr, pw);
+    case 10: return launch64_d<10>(Y, n, ld, tb, te, kappa, skip_s, S, limbs, sm_count, s, pr, pw);
+    case 11: return launch64_d<11>(Y, n, ld, tb, te, kappa, skip_s, S, limbs, sm_count, s, pr, pw);
+    case 12: return launch64_d<12>(Y, n, ld, tb, te, kappa, skip_s, S, limbs, sm_count, s, pr, pw);
+    case 13: return launch64_d<13>(Y, n, ld, tb, te, kappa, skip_s, S, limbs, sm_count, s, pr, pw);
+    case 14: return launch64_d<14>(Y, n, ld, tb, te, kappa, skip_s, S, limbs, sm_count, s, pr, pw);
+    case 15: return launch64_d<15>(Y, n, ld, tb, te, kappa, skip_s, S, limbs, sm_count, s, pr, pw);
+    case 16: return launch64_d<16>(Y, n, ld, tb, te, kappa, skip_s, S, limbs, sm_count, s, pr, pw);
   }
   return cudaErrorInvalidValue;
 }

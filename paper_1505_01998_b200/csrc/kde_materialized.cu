@@ -30,12 +30,13 @@ int64_t mat_chunk() { return kP2Chunk; }
 
 template <int D>
 __global__ void __launch_bounds__(kMatT) mat_write_kernel(const float* __restrict__ X, int64_t n, int64_t ld,
-                                                          int64_t tb, int64_t te, float* __restrict__ buf) {
+                                                          int64_t tb, int64_t te, float* __restrict__ buf,
+                                                          int part_rank, int part_world) {
   __shared__ float cs[D][kMatT];
   const int tid = threadIdx.x;
-  for (int64_t t = tb + blockIdx.x; t < te; t += gridDim.x) {
+  for (int64_t t = tb + blockIdx.x; t < te; t += gridDim.x) {   // local tile indices of this rank
     int64_t l, q;
-    tile_coords(t, l, q);
+    tile_coords(shard_tile(t, part_rank, part_world), l, q);
     __syncthreads();
 #pragma unroll
     for (int d = 0; d < D; ++d) cs[d][tid] = X[d * ld + l * kMatT + tid];
@@ -102,12 +103,12 @@ __global__ void __launch_bounds__(kP2Threads) mat_reduce_kernel(const float4* __
 }
 
 cudaError_t launch_mat_write(int d, const float* X, int64_t n, int64_t ld, int64_t tb, int64_t te, float* buf,
-                             int sm_count, cudaStream_t s) {
+                             int sm_count, cudaStream_t s, int pr, int pw) {
   if (te <= tb) return cudaSuccess;
   int64_t grid = te - tb;
   if (grid > (int64_t)sm_count * 8) grid = (int64_t)sm_count * 8;
   switch (d) {
-#define W(DD) case DD: mat_write_kernel<DD><<<(unsigned)grid, kMatT, 0, s>>>(X, n, ld, tb, te, buf); break;
+#define W(DD) case DD: mat_write_kernel<DD><<<(unsigned)grid, kMatT, 0, s>>>(X, n, ld, tb, te, buf, pr, pw); break;
     W(1) W(2) W(3) W(4) W(5) W(6) W(7) W(8) W(9) W(10) W(11) W(12) W(13) W(14) W(15) W(16)
 #undef W
     default: return cudaErrorInvalidValue;

@@ -74,6 +74,7 @@ struct Args {
   double skip_gap;                   // Psi: tiles with a larger sorted gap are exactly zero
   unsigned long long* work;          // dynamic scheduling: unit counter (zero at launch), or null
   float skip_s;                      // LSCV on coordinate-0-sorted data: skip bound on s (+inf: never)
+  int part_rank, part_world;         // tile_begin/tile_end index this rank's round-robin tiles (shard_tile)
 };
 
 // Work distribution.  Static: CTA b takes units b, b + grid, ...  Dynamic (a.work != null): CTA b
@@ -500,7 +501,7 @@ __global__ void __launch_bounds__(F::NT, F::MINB) pair_kernel(const Args a,
   // thread 0 stages unit u's column chunk into buffer `buf` (TMA) and decides its skip flag
   auto issue = [&](int64_t u, int buf) {
     int64_t l, q;
-    tile_coords(a.tile_begin + u / CS, l, q);
+    tile_coords(shard_tile(a.tile_begin + u / CS, a.part_rank, a.part_world), l, q);
     s_skip[buf] = lscv_tile_skipped<F>(a, a.X, l, q);
     float* dst = cols + buf * D * T;
     mbar_expect_tx(&bar[buf], (uint32_t)(D * T * sizeof(float)));
@@ -519,7 +520,7 @@ __global__ void __launch_bounds__(F::NT, F::MINB) pair_kernel(const Args a,
   const bool clamp = F::kClampable && a.clamp != nullptr && *a.clamp != 0;   // uniform per launch
   uint32_t k = 0;
   while (u < units) {
-    const int64_t tile = a.tile_begin + u / CS;
+    const int64_t tile = shard_tile(a.tile_begin + u / CS, a.part_rank, a.part_world);
     int64_t l, q;
     tile_coords(tile, l, q);
     const int64_t un = next_unit_issue(a, u, s_next, k);
@@ -554,7 +555,7 @@ __global__ void __launch_bounds__(F::NT, F::MINB) pair_kernel_sets(const Args a,
   auto issue = [&](int64_t u, int buf) {
     const int64_t set = u / per;
     int64_t l, q;
-    tile_coords(a.tile_begin + (u - set * per), l, q);
+    tile_coords(shard_tile(a.tile_begin + (u - set * per), a.part_rank, a.part_world), l, q);
     const float* Xs = a.X + set * a.set_stride;
     s_skip[buf] = lscv_tile_skipped<F>(a, Xs, l, q);
     float* dst = cols + buf * D * T;
@@ -575,7 +576,7 @@ __global__ void __launch_bounds__(F::NT, F::MINB) pair_kernel_sets(const Args a,
   uint32_t k = 0;
   while (u < units) {
     const int64_t set = u / per;
-    const int64_t tile = a.tile_begin + (u - set * per);
+    const int64_t tile = shard_tile(a.tile_begin + (u - set * per), a.part_rank, a.part_world);
     int64_t l, q;
     tile_coords(tile, l, q);
     const int64_t un = next_unit_issue(a, u, s_next, k);
@@ -624,7 +625,7 @@ inline cudaError_t launch_pair(const LaunchCfg& c, const typename F::Params& p) 
   if (grid > units) grid = units;
   if (grid < 1) grid = 1;
   Args a{c.X, c.n, c.ld, c.tile_begin, c.tile_end, c.scale_exp, c.limbs, c.clamp, c.n_sets, c.set_stride,
-         c.Y64, c.centres, c.skipped, c.n_sets_dev, c.skip_gap, c.work, c.skip_s};
+         c.Y64, c.centres, c.skipped, c.n_sets_dev, c.skip_gap, c.work, c.skip_s, c.part_rank, c.part_world};
   if constexpr (F::kSets) {
     if (c.pdl) {
       cudaLaunchConfig_t lc = {};

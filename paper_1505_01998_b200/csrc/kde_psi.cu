@@ -339,14 +339,14 @@ template <int R>
 __global__ void __launch_bounds__(kPsi64Tile) psi64_kernel(const double* __restrict__ y, int64_t n, int64_t tb,
                                                            int64_t te, int S, unsigned long long* __restrict__ limbs,
                                                            const unsigned long long* __restrict__ gate,
-                                                           double skip_gap) {
+                                                           double skip_gap, int part_rank, int part_world) {
   __shared__ double cs[kPsi64Tile];
   __shared__ double red[kPsi64Tile / 32];
   const int tid = threadIdx.x;
   if (gate != nullptr && *gate == 0) return;   // device-side decision: the fp32 pass sufficed
-  for (int64_t t = tb + blockIdx.x; t < te; t += gridDim.x) {
+  for (int64_t u = tb + blockIdx.x; u < te; u += gridDim.x) {   // this rank's local tile indices
     int64_t l, q;
-    tile_coords(t, l, q);
+    tile_coords(shard_tile(u, part_rank, part_world), l, q);
     if (q < l && y[l * kPsi64Tile] - y[q * kPsi64Tile + kPsi64Tile - 1] > skip_gap) continue;   // exact 0
     const int64_t jc = l * kPsi64Tile + tid, i = q * kPsi64Tile + tid;
     __syncthreads();
@@ -369,14 +369,14 @@ __global__ void __launch_bounds__(kPsi64Tile) psi64_kernel(const double* __restr
 
 cudaError_t launch_psi64(int r, const double* y, int64_t n, int64_t tb, int64_t te, int S,
                          unsigned long long* limbs, int sm_count, cudaStream_t s, const unsigned long long* gate,
-                         double skip_gap) {
+                         double skip_gap, int part_rank, int part_world) {
   if (te <= tb) return cudaSuccess;
   int64_t grid = te - tb;
   if (grid > (int64_t)sm_count * 8) grid = (int64_t)sm_count * 8;
   switch (r) {
-    case 4: psi64_kernel<4><<<(unsigned)grid, kPsi64Tile, 0, s>>>(y, n, tb, te, S, limbs, gate, skip_gap); break;
-    case 6: psi64_kernel<6><<<(unsigned)grid, kPsi64Tile, 0, s>>>(y, n, tb, te, S, limbs, gate, skip_gap); break;
-    case 8: psi64_kernel<8><<<(unsigned)grid, kPsi64Tile, 0, s>>>(y, n, tb, te, S, limbs, gate, skip_gap); break;
+    case 4: psi64_kernel<4><<<(unsigned)grid, kPsi64Tile, 0, s>>>(y, n, tb, te, S, limbs, gate, skip_gap, part_rank, part_world); break;
+    case 6: psi64_kernel<6><<<(unsigned)grid, kPsi64Tile, 0, s>>>(y, n, tb, te, S, limbs, gate, skip_gap, part_rank, part_world); break;
+    case 8: psi64_kernel<8><<<(unsigned)grid, kPsi64Tile, 0, s>>>(y, n, tb, te, S, limbs, gate, skip_gap, part_rank, part_world); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();

@@ -8,12 +8,14 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdint>
 #include <cstring>
 #include <numeric>
 #include <string>
 #include <vector>
 
 #include "kde_host.h"
+#include "kde_tiles.cuh"
 
 using kde::Kind;
 using namespace kde::host;
@@ -267,9 +269,11 @@ int64_t n_tiles(int64_t n, int T) {
   return nb * (nb + 1) / 2;
 }
 
+// Local tile-index range [0, shard_count) of rank `rank` of `world` (round-robin chunks, kde_tiles.cuh);
+// the kernels map a local index to its tile id with shard_tile.
 void shard_range(int64_t tiles, int rank, int world, int64_t* b, int64_t* e) {
-  *b = (int64_t)((__int128)tiles * rank / world);
-  *e = (int64_t)((__int128)tiles * (rank + 1) / world);
+  *b = 0;
+  *e = kde::shard_count(tiles, rank, world);
 }
 
 // Algorithmic pairs i<j inside tiles [b, e), one column of tiles at a time (the tile numbering
@@ -286,6 +290,18 @@ double pairs_in_range(int64_t n, int T, int64_t b, int64_t e) {
     const int64_t off = std::min<int64_t>(q1, l - 1) - q0 + 1;          // q < l: T x cols pairs
     if (off > 0) s += (double)off * (double)T * cols;
     if (q1 == l) s += cols * (cols - 1.0) * 0.5;                        // diagonal tile
+  }
+  return s;
+}
+
+// Algorithmic pairs in a rank's tiles (local range [0, count) of shard_range): one contiguous run of
+// tile ids per round-robin chunk.
+double pairs_in_shard(int64_t n, int T, int64_t count, int rank, int world) {
+  if (world <= 1) return pairs_in_range(n, T, 0, count);
+  double s = 0.0;
+  for (int64_t i = 0; i < count; i += kde::kShardChunk) {
+    const int64_t t0 = kde::shard_tile(i, rank, world);
+    s += pairs_in_range(n, T, t0, t0 + std::min<int64_t>(kde::kShardChunk, count - i));
   }
   return s;
 }
@@ -373,10 +389,11 @@ kde_status run_sums(kde_ctx* c, int d, int64_t n, int64_t ld, int T, int scale, 
   if (c->profiling && any_skip) CUDA_TRY(c, cudaMemsetAsync(lscv_skipped, 0, sizeof(unsigned long long), c->stream));
   int64_t tiles = n_tiles(n, T), tb, te;
   shard_range(tiles, shard_rank, shard_world, &tb, &te);
-  const double pairs = c->profiling ? pairs_in_range(n, T, tb, te) : 0.0;
+  const double pairs = c->profiling ? pairs_in_shard(n, T, te, shard_rank, shard_world) : 0.0;
   for (const SumLaunch& L : launches) {
     kde::LaunchCfg cfg;
     cfg.X = w.Y; cfg.n = n; cfg.ld = ld; cfg.tile_begin = tb; cfg.tile_end = te; cfg.tile = T;
+    cfg.part_rank = shard_rank; cfg.part_world = shard_world;
     cfg.scale_exp = scale; cfg.limbs = w.limbs + (size_t)L.out_offset * kde::kLimbs;
     cfg.n_out = L.n_out; cfg.stream = c->stream; cfg.sm_count = c->sm_count;
     cfg.clamp = w.flag() + 1;
@@ -599,7 +616,7 @@ void kde_tile_coords(int64_t bx, int64_t* l, int64_t* q) {
 }
 
 kde_status kde_shard_tiles(kde_sum_kind kind, int64_t n, int32_t d, int32_t rank, int32_t world,
-                           int32_t* tile_edge, int64_t* tiles_total, int64_t* tb, int64_t* te) {
+                           int32_t* tile_edge, int64_t* tiles_total, int64_t* rank_tiles, int32_t* chunk) {
   if (n < 1 || d < 1 || d > kde::kMaxDim || world < 1 || rank < 0 || rank >= world) return KDE_E_INVALID;
   Kind k;
   switch (kind) {
@@ -612,13 +629,15 @@ kde_status kde_shard_tiles(kde_sum_kind kind, int64_t n, int32_t d, int32_t rank
   }
   const int T = kde::tile_for(k, d, n);
   const int64_t tiles = n_tiles(n, T);
-  int64_t b, e;
-  shard_range(tiles, rank, world, &b, &e);
   if (tile_edge) *tile_edge = T;
   if (tiles_total) *tiles_total = tiles;
-  if (tb) *tb = b;
-  if (te) *te = e;
+  if (rank_tiles) *rank_tiles = kde::shard_count(tiles, rank, world);
+  if (chunk) *chunk = world > 1 ? kde::kShardChunk : (int32_t)std::min<int64_t>(tiles, INT32_MAX);
   return KDE_OK;
+}
+
+int64_t kde_shard_tile(int64_t i, int32_t rank, int32_t world) {
+  return (world < 1 || rank < 0 || rank >= world || i < 0) ? -1 : kde::shard_tile(i, rank, world);
 }
 
 double kde_fixed_value(const kde_fixed* v) { return v ? fixed_value(*v) : NAN; }

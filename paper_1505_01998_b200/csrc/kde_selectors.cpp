@@ -73,11 +73,12 @@ kde_status psi64_pass(kde_ctx* c, int r, const double* y, int64_t n, int S, unsi
     e0 = next_event(c); e1 = next_event(c);
     CUDA_TRY(c, cudaEventRecordWithFlags(e0, c->stream, rec));
   }
-  CUDA_TRY(c, kde::launch_psi64(r, y, n, tb, te, S, limbs, c->sm_count, c->stream, gate, kde::psi_skip_gap(true)));
+  CUDA_TRY(c, kde::launch_psi64(r, y, n, tb, te, S, limbs, c->sm_count, c->stream, gate, kde::psi_skip_gap(true),
+                                c->rank, c->world));
   if (tb < te) c->prof_all += 1;
   if (c->profiling) {
     CUDA_TRY(c, cudaEventRecordWithFlags(e1, c->stream, rec));
-    const double pairs = pairs_in_range(n, kde::kPsi64Tile, tb, te);
+    const double pairs = pairs_in_shard(n, kde::kPsi64Tile, te, c->rank, c->world);
     if (gate) {
       c->gate_evals[slot] = pairs;
     } else {
@@ -145,7 +146,7 @@ kde_status psi_raw(kde_ctx* c, const double* x, int64_t n, int r, const double* 
       int64_t tb, te;
       shard_range(n_tiles(n, kde::kPsi64Tile), shard_rank, shard_world, &tb, &te);
       CUDA_TRY(c, kde::launch_psi64(r, b.Y64, n, tb, te, S, w.limbs, c->sm_count, c->stream, nullptr,
-                                    kde::psi_skip_gap(true)));
+                                    kde::psi_skip_gap(true), shard_rank, shard_world));
       if (tb < te) c->prof_all += 1;
     }
     long long hl[2 + kde::kLimbs];   // prep flags, then the limbs
@@ -245,7 +246,8 @@ kde_status lscv_sums64(kde_ctx* c, const double* Xs, int64_t n, int d, const std
   shard_range(n_tiles(n, T), c->rank, c->world, &tb, &te);
   const int S = scale_exp_for(1.0, n);
   // exp2(kappa s) is exactly 0 in fp64 for kappa s < -1100 (below the smallest subnormal 2^-1074)
-  CUDA_TRY(c, kde::launch_lscv64(d, Y, n, ld, tb, te, kappa, 1100.0 / -kappa, S, w.limbs, c->sm_count, c->stream));
+  CUDA_TRY(c, kde::launch_lscv64(d, Y, n, ld, tb, te, kappa, 1100.0 / -kappa, S, w.limbs, c->sm_count, c->stream,
+                                 c->rank, c->world));
   c->prof_all += tb < te ? 2 : 1;
   TRY(allreduce_limbs(c, w.limbs, 2 * kde::kLimbs));
   long long hl[2 * kde::kLimbs];
@@ -391,6 +393,7 @@ static kde_status plugin_pass(kde_ctx* c, int r, int64_t n, int64_t ld, int T, i
   Range rr("kde.pair_pass");
   kde::LaunchCfg cfg;
   cfg.X = b.Yc; cfg.n = n; cfg.ld = ld; cfg.tile_begin = tb; cfg.tile_end = te; cfg.tile = T;
+  cfg.part_rank = c->rank; cfg.part_world = c->world;
   cfg.scale_exp = S; cfg.limbs = limbs; cfg.n_out = 2; cfg.stream = c->stream; cfg.sm_count = c->sm_count;
   cfg.clamp = clamp; cfg.Y64 = b.Y64; cfg.centres = b.centres;
   cfg.skipped = skipped;
@@ -442,7 +445,7 @@ static kde_status plugin_enqueue(kde_ctx* c, const double* x, int64_t n, int T, 
   TRY(gpu_sorted(c, x, n, &xs));
   int64_t tb, te;
   shard_range(n_tiles(n, T), c->rank, c->world, &tb, &te);
-  const double pairs = c->profiling ? pairs_in_range(n, T, tb, te) : 0.0;
+  const double pairs = c->profiling ? pairs_in_shard(n, T, te, c->rank, c->world) : 0.0;
   const int S6 = scale_exp_for(2.0 * 15.0, n), S4 = scale_exp_for(2.0 * 3.0, n);
   const int mode = c->psi_mode;
   unsigned long long* L = w.limbs;                       // [S6, A6, S4, A4, S6 fp64, S4 fp64]

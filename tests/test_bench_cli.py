@@ -25,12 +25,14 @@ def test_bench_gpus_2_runs_two_ranks():
     r = _run("--gpus", "2", "--dry-run")
     assert r["n_gpus"] == 2 and r["dry_run"]
     cfg = r["config"]
-    (b0, e0), (b1, e1) = cfg["rank_tiles"]
-    assert b0 == 0 and e0 == b1 and e1 == cfg["tiles"]          # contiguous, complete, disjoint
-    assert cfg["max_rank_tiles"] == max(e0 - b0, e1 - b1)
+    (c0, k0, f0), (c1, k1, f1) = cfg["rank_tiles_chunk_first"]
+    assert c0 + c1 == cfg["tiles"] and abs(c0 - c1) <= k0          # complete, balanced to one chunk
+    assert k0 == k1 == 16 and f0 == 0 and f1 == 16                  # round-robin chunks of 16 tile ids
+    assert cfg["max_rank_tiles"] == max(c0, c1)
     assert cfg["parallelism"] == "pair-range x2"
 
 
 def test_bench_single_rank_dry_run():
     r = _run("--dry-run")
-    assert r["n_gpus"] == 1 and r["config"]["rank_tiles"] == [[0, r["config"]["tiles"]]]
+    cnt, _, first = r["config"]["rank_tiles_chunk_first"][0]
+    assert r["n_gpus"] == 1 and cnt == r["config"]["tiles"] and first == 0

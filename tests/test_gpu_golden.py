@@ -133,7 +133,7 @@ def test_psi_2048_row_tiles_ragged_n(ctx, case):
     c = gold["cases"][case]
     x = datagen.sample_mixture("skewed", 300001, 8)[:, :c["n"]]
     kind = {4: kb.SUM_PSI4, 6: kb.SUM_PSI6, 8: kb.SUM_PSI8}[c["r"]]
-    T, _, _, _ = kb.shard_tiles(kind, c["n"], 1, 0, 1)
+    T, _, _, _ = kb.shard_tiles(kind, c["n"], 1, 0, 1)   # (edge, total, rank tiles, chunk)
     assert T == 2048
     got = kb.fixed_value(ctx.raw_sums(kind, kb.to_device(x), [c["g"]])[0]) / math.sqrt(2 * math.pi)
     n, he0 = c["n"], {4: 3.0, 6: -15.0, 8: 105.0}[c["r"]]

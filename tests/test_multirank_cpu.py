@@ -1,7 +1,8 @@
 """World-size-2 (and 3) gloo tests of the multi-GPU host logic, on CPU.
 
-Each rank asks the library for its tile range (kde_shard_tiles), enumerates the pairs i<j of
-its tiles through the library's tile map (kde_tile_coords, Eq. 42-43), and sums an exact
+Each rank asks the library for its tiles (kde_shard_tiles / kde_shard_tile: round-robin chunks of
+tile ids), enumerates the pairs i<j of its tiles through the library's tile map (kde_tile_coords,
+Eq. 42-43), and sums an exact
 integer weight per pair.  The ranks all-reduce (gloo, int64 SUM) exactly like the GPU path
 all-reduces its int64 fixed-point limbs; the result must equal the closed-form total over all
 pairs, i.e. the shards cover every pair exactly once."""
@@ -30,10 +31,11 @@ def _weight(i, j):
 
 
 def _rank_sum(kind, n, d, rank, world):
-    T, tot, b, e = kb.shard_tiles(kind, n, d, rank, world)
+    T, tot, cnt, chunk = kb.shard_tiles(kind, n, d, rank, world)
     s = 0
     pairs = 0
-    for t in range(b, e):
+    ids = [kb.shard_tile(i, rank, world) for i in range(cnt)]
+    for t in ids:
         l, q = kb.tile_coords(t)
         rows = np.arange(q * T, min((q + 1) * T, n))
         cols = np.arange(l * T, min((l + 1) * T, n))
@@ -44,7 +46,7 @@ def _rank_sum(kind, n, d, rank, world):
         w = (I[m] * 7919 + J[m] * 104729) % 1000003
         s += int(w.sum())
         pairs += int(m.sum())
-    return s, pairs, (b, e, tot)
+    return s, pairs, (ids, tot)
 
 
 def _worker(rank, world, port, cases, q):
@@ -81,7 +83,6 @@ def test_shards_cover_every_pair_once(world):
         i, j = np.triu_indices(n, 1)
         assert pairs == n * (n - 1) // 2
         assert s == int(((i * 7919 + j * 104729) % 1000003).sum())
-        # contiguous, disjoint, covering
-        assert ranges[0][0] == 0 and ranges[-1][1] == ranges[-1][2]
-        for a, b in zip(ranges[:-1], ranges[1:]):
-            assert a[1] == b[0]
+        # disjoint and covering every tile id exactly once
+        allids = sorted(t for ids, _ in ranges for t in ids)
+        assert allids == list(range(ranges[0][1]))

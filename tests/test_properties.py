@@ -42,17 +42,24 @@ def test_fixed_point_addition_is_exact_and_order_free(vals, S):
        st.integers(min_value=1, max_value=2 ** 31 - 1), st.integers(min_value=1, max_value=16),
        st.integers(min_value=1, max_value=64))
 def test_shard_ranges_partition_the_tile_grid(kind, n, d, world):
-    prev_end = 0
-    total = None
+    # round-robin chunks: counts add up, balanced to one chunk, and the local -> id map of every rank
+    # hits exactly the ids whose chunk index is congruent to the rank (checked at both ends)
+    counts = []
     for r in range(world):
-        T, tot, b, e = kb.shard_tiles(kind, n, d, r, world)
+        T, tot, cnt, chunk = kb.shard_tiles(kind, n, d, r, world)
         nb = (n + T - 1) // T
         assert tot == nb * (nb + 1) // 2
-        total = tot
-        assert b == prev_end and b <= e
-        assert e - b <= tot // world + 1          # balanced to one tile
-        prev_end = e
-    assert prev_end == total
+        counts.append(cnt)
+        if world > 1:
+            assert chunk == 16
+            for i in {0, cnt - 1, cnt // 2} - {-1}:
+                if 0 <= i < cnt:
+                    t = kb.shard_tile(i, r, world)
+                    assert 0 <= t < tot and (t // chunk) % world == r and t % chunk == i % chunk
+        else:
+            assert cnt == tot and kb.shard_tile(5, 0, 1) == 5
+    assert sum(counts) == tot
+    assert max(counts) - min(counts) <= 16
 
 
 @settings(max_examples=40, deadline=None)
