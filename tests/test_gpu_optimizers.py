@@ -136,3 +136,27 @@ def test_device_nm_loop_shape_does_not_change_the_search(ctx, env):
     assert np.array_equal(got["vechH"], ref["vechH"]) and got["objective"] == ref["objective"]
     for k in ("iterations", "evaluations", "stop_reason"):
         assert got[k] == ref[k], k
+
+
+def test_device_nm_loop_equals_host_loop_seeded_sweep(ctx):
+    # 24 seeded small problems (d = 1..4, n = 4..500, stretched / correlated / near-degenerate data):
+    # the device-resident loop and the host loop take identical decisions on every one.
+    rng = np.random.default_rng(2024)
+    for case in range(24):
+        d = int(rng.integers(1, 5))
+        n = int(rng.integers(4, 500))
+        A = rng.normal(size=(d, d)) * (1.0 + 3.0 * rng.random())
+        X = A @ rng.standard_t(4, size=(d, n)) + rng.normal(size=(d, 1))
+        if case % 6 == 5:            # near-degenerate covariance: non-PD proposals are likely
+            X[-1] = X[0] + 1e-3 * rng.normal(size=n)
+        Xd = kb.to_device(X)
+        try:
+            dev = ctx.select_bandwidth(kb.LSCV_H, Xd, max_iter=150, nm_loop=0)
+        except kb.KDEError as e:
+            with pytest.raises(kb.KDEError) as e2:
+                ctx.select_bandwidth(kb.LSCV_H, Xd, max_iter=150, nm_loop=1)
+            assert e2.value.status == e.status
+            continue
+        host = ctx.select_bandwidth(kb.LSCV_H, Xd, max_iter=150, nm_loop=1)
+        assert np.array_equal(dev["vechH"], host["vechH"]), (case, d, n)
+        assert dev["objective"] == host["objective"] and dev["evaluations"] == host["evaluations"], (case, d, n)
