@@ -18,7 +18,7 @@
  *    host results are available (it synchronises that stream).
  *  - Multi-GPU (SPMD): with world > 1 every rank calls the same function with identical
  *    arguments (each on its own copy of X).  The upper-triangular tile set is split into
- *    contiguous ranges across ranks and one NCCL all-reduce of exact fixed-point partial sums
+ *    round-robin chunks of tile ids across ranks (kde_shard_tiles) and one NCCL all-reduce of exact fixed-point partial sums
  *    combines them, so every rank returns bit-identical results, equal to the 1-GPU result.
  *  - Determinism: results are bit-for-bit reproducible for a given (X, n, d, candidates),
  *    independent of the number of GPUs, the grid size and of which candidates share a batch.

@@ -1,4 +1,4 @@
-// kde_device.cuh — device helpers shared by the sm_100a kernels (kde_kernels.cu, kde_eval.cu).
+// kde_device.cuh — device helpers shared by the sm_100a kernels (kde_pair.cuh and every kernel unit).
 #pragma once
 #include <cuda_runtime.h>
 #include <math.h>

@@ -1,5 +1,6 @@
-// kde_internal.h — declarations shared by the host library (kde_host.cpp) and the CUDA
-// launchers (kde_kernels.cu).  Product code only; nothing here is shared with oracle/.
+// kde_internal.h — declarations shared by the host library (kde_*.cpp) and the CUDA
+// launchers (kde_psi.cu, kde_lscv_*.cu, kde_eval.cu, kde_materialized.cu, kde_nm_dev.cu).  Product code
+// only; nothing here is shared with oracle/.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>

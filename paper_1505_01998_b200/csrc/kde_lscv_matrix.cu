@@ -1,5 +1,5 @@
 // kde_lscv_matrix.cu — LSCV_H pair-kernel instantiations: FLscvScalar<D, NT, 1, UNIT> over one
-// per-candidate whitened data set per candidate (see kde_pair.cuh, kde_host.cpp lscv_H_raw).
+// per-candidate whitened data set per candidate (see kde_pair.cuh, kde_selectors.cpp lscv_H_raw).
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>

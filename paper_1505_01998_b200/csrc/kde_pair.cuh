@@ -8,7 +8,8 @@
 //    numbered column by column and mapped back with Eq. 42-43 + an integer fix-up;
 //    variants: a column chunk of a tile (small-n Psi, CS > 1) or a (data set, tile) pair
 //    (LSCV_H: one whitened data set per candidate, pair_kernel_sets);
-//  * persistent CTAs stride over their rank's contiguous tile range;
+//  * persistent CTAs claim the units of their rank's tiles (round-robin chunks of tile ids,
+//    kde_tiles.cuh shard_tile) dynamically, one unit ahead of the one they evaluate;
 //  * the T column samples (D rows) of the next tile are staged in shared memory by TMA bulk
 //    copies (cp.async.bulk + mbarrier, double-buffered); the T row samples sit in registers
 //    (R per thread); columns are read back with broadcast LDS.128;
@@ -482,7 +483,7 @@ __device__ __forceinline__ void pair_unit(const Args& a, const typename F::Param
   commit_tile<NOUT, F::NT>(v, red, limbs, a.scale_exp);
 }
 
-// Work unit u of the rank's range: tile tile_begin + u / CS, column chunk u % CS (CS = 1: whole
+// Work unit u of the rank's share: local tile tile_begin + u / CS (tile id shard_tile(...)), column chunk u % CS (CS = 1: whole
 // tiles).  Persistent CTAs stride over the units; the next unit's column chunk is staged by TMA
 // into the other buffer while the current one is evaluated.
 template <class F>
@@ -548,7 +549,7 @@ __global__ void __launch_bounds__(F::NT, F::MINB) pair_kernel_sets(const Args a,
 
   pdl_trigger();   // a programmatic successor (the Nelder–Mead decision) may take its slot right away
   pdl_wait();      // a programmatic launch (device-resident Nelder–Mead) waits for the whitening here
-  // Work units u in [0, n_sets * tiles): set = u / tiles, tile = tile_begin + u % tiles (set-major,
+  // Work units u in [0, n_sets * tiles): set = u / tiles, local tile = tile_begin + u % tiles (set-major,
   // so consecutive CTAs share a set's data in L2).
   const int64_t per = a.tile_end - a.tile_begin;
   const int64_t units = per * (a.n_sets_dev != nullptr ? *a.n_sets_dev : a.n_sets);
