@@ -3,7 +3,7 @@
 Calls only oracle/ (and datagen for the seeded inputs).  Each JSON file records the workload,
 the oracle outputs and the PAPER.md passages they follow.  Run (CPU, all cores, ~1 h):
 
-    python tests/golden/make_golden.py [C1] [C4] [C2] [C3] [C5] [C4b] [T2048] [C5small] [ESC]
+    python tests/golden/make_golden.py [C1] [C4] [C2] [C3] [C5] [C4b] [T2048] [C5small] [ESC] [F1] [F2]
 """
 from __future__ import annotations
 
@@ -160,9 +160,46 @@ def c5small():
         "g": g, "oracle_seconds": time.time() - t0, "threads": THREADS})
 
 
+def f1():
+    """LSCV_h at d = 2 and 4 on the F1 workload (bench_configs F1: n = 65536, C5 mixture's first d
+    coordinates), six h of its 1024-point grid (row f1)."""
+    grid = np.linspace(0.05, 1.5, 1024)
+    idx = [0, 31, 100, 300, 700, 1023]
+    out = {}
+    t0 = time.time()
+    for d in (2, 4):
+        X = datagen.config_data("C5", n=65536)[:d]
+        out[str(d)] = {"h": [float(grid[k]) for k in idx], "indices": idx,
+                       "g": [float(v) for v in oracle.lscv_h_scores(X, grid[idx], threads=THREADS)]}
+    dump("F1_lscv_h.json", {
+        "config": "F1", "workload": "LSCV_h d=2 and d=4, n=65536 (datagen.config_data('C5', n=65536)[:d]), "
+        "grid np.linspace(0.05, 1.5, 1024)", "cite": "PAPER.md P:308-322 (Eq. 24), P:402-449 (Eq. 36-41)",
+        "cases": out, "oracle_seconds": time.time() - t0, "threads": THREADS})
+
+
+def f2():
+    """KDE evaluation at full F2 size on sampled queries (row f2): n = 2^20 C4 samples, d = 1, h = 0.05,
+    64 of the 2^16 linspace(-3, 4) queries; n = 32768 C3 samples, d = 2, 64 of the 2^15 C3 queries."""
+    t0 = time.time()
+    x = datagen.config_data("C4")
+    y = np.linspace(-3, 4, 1 << 16)
+    qi = list(range(0, 1 << 16, 1024))
+    f1d = oracle.kde_eval(x, y[qi][None, :], [0.05 ** 2])
+    X = datagen.config_data("C3")
+    Y = datagen.sample_mixture("C3", 1 << 15, 99)
+    qj = list(range(0, 1 << 15, 512))
+    f2d = oracle.kde_eval(X, Y[:, qj], [0.012, 0.002, 0.011])
+    dump("F2_eval.json", {
+        "config": "F2", "workload": "fhat at sampled queries: d=1 C4 samples (n=2^20), H=[0.05^2], queries "
+        "np.linspace(-3, 4, 2^16)[::1024]; d=2 C3 samples (n=32768), vechH=[0.012, 0.002, 0.011], queries "
+        "datagen.sample_mixture('C3', 2^15, 99)[:, ::512]", "cite": "PAPER.md P:114-140 (Eq. kde-def-H, K_H)",
+        "d1": {"query_index": qi, "f": [float(v) for v in f1d]}, "d2": {"query_index": qj, "f": [float(v) for v in f2d]},
+        "oracle_seconds": time.time() - t0})
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["C1", "C4", "C2", "C3", "C5"]
     for w in which:
         print("golden", w, flush=True)
         {"C1": c1, "C4": c4, "C2": c2, "C3": c3, "C5": c5, "C4b": c4b, "T2048": t2048,
-         "C5small": c5small, "ESC": esc}[w]()
+         "C5small": c5small, "ESC": esc, "F1": f1, "F2": f2}[w]()

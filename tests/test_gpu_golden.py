@@ -148,3 +148,32 @@ def test_c5_all_256_candidates_small_n(ctx):
     X = datagen.config_data("C5", n=4096)
     got = ctx.lscv_H_scores(kb.to_device(X), datagen.c5_candidates(4096, 256))
     np.testing.assert_allclose(got, gold["g"], rtol=1e-5)
+
+
+@pytest.mark.parametrize("d", [2, 4])
+def test_f1_full_grid_matches_oracle_golden(ctx, d):
+    # Row f1 at its benchmark size and launch configuration (tools/bench_configs.py F1: the whole
+    # 1024-point grid in one call); six sampled grid points against the fp64 oracle.
+    gold = load("F1_lscv_h.json")["cases"][str(d)]
+    X = datagen.config_data("C5", n=65536)[:d]
+    grid = np.linspace(0.05, 1.5, 1024)
+    g = ctx.lscv_h_scores(kb.to_device(X), grid)
+    for k, h, ref in zip(gold["indices"], gold["h"], gold["g"]):
+        assert grid[k] == h
+        assert rel(g[k], ref) <= 1e-5, (d, k, g[k], ref)
+
+
+def test_f2_full_size_eval_matches_oracle_golden(ctx):
+    # Row f2 at its benchmark size (n = 2^20 samples x 2^16 queries, d = 1; n = m = 32768, d = 2),
+    # 64 sampled queries each against the fp64 oracle; tolerance as tests/test_gpu_eval.py.
+    gold = load("F2_eval.json")
+    x = datagen.config_data("C4")
+    y = np.linspace(-3, 4, 1 << 16)[None, :]
+    f = ctx.evaluate(kb.to_device(x), kb.to_device(y), [0.05 ** 2])
+    ref = np.array(gold["d1"]["f"])
+    np.testing.assert_allclose(f[gold["d1"]["query_index"]], ref, rtol=1e-5, atol=1e-12 * ref.max())
+    X = datagen.config_data("C3")
+    Y = datagen.sample_mixture("C3", 1 << 15, 99)
+    f = ctx.evaluate(kb.to_device(X), kb.to_device(Y), [0.012, 0.002, 0.011])
+    ref = np.array(gold["d2"]["f"])
+    np.testing.assert_allclose(f[gold["d2"]["query_index"]], ref, rtol=1e-5, atol=1e-12 * ref.max())
