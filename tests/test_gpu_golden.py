@@ -177,3 +177,13 @@ def test_f2_full_size_eval_matches_oracle_golden(ctx):
     f = ctx.evaluate(kb.to_device(X), kb.to_device(Y), [0.012, 0.002, 0.011])
     ref = np.array(gold["d2"]["f"])
     np.testing.assert_allclose(f[gold["d2"]["query_index"]], ref, rtol=1e-5, atol=1e-12 * ref.max())
+
+
+def test_f3_materialized_full_size_matches_c2_golden(ctx):
+    # Row f3 (the paper's two-phase LSCV_h) at the C2 size: the materialised S(v) buffer (8.6 GB) and
+    # 16 h per streaming pass, at the 81 grid points of the C2 oracle golden.
+    gd = load("C2_lscv_h.json")
+    X = datagen.config_data("C2")
+    g = ctx.lscv_h_scores_materialized(kb.to_device(X), gd["h"], h_per_pass=16)
+    err = np.max(np.abs(g - np.array(gd["g"])) / np.abs(gd["g"]))
+    assert err <= 1e-5, err
