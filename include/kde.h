@@ -80,6 +80,11 @@ typedef struct {
                             pair kernel per round, no host round trip; same decisions as the host
                             loop); 1 = host loop (one synchronisation per round).  Multi-start,
                             speculative and multi-rank selections always use the host loop; 0 */
+  int32_t nm_param;      /* LSCV_H search variables (row f4): 0 = vech(H) with the penalty for
+                            non-positive-definite vertices (reading Z8); 1 = vech(L) of a
+                            lower-triangular factor, H = L L^T (every vertex is positive semi-definite,
+                            only a zero diagonal is penalised), start L = chol(H_start), the initial
+                            simplex and the 4^-k start scaling applied to L; host loop; 0 */
 } kde_select_opts;
 
 typedef struct {

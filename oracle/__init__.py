@@ -506,23 +506,39 @@ def nelder_mead(f, sim, max_iter: int = 500, tol: float = 1e-7, trace=None):
     return dict(x=sim[0], f=fs[0], iterations=it, stop=stop, simplex=sim, fvals=fs)
 
 
+def vech_llt(x, d: int):
+    """vech(L L^T) for x = vech(L), L lower triangular (the Cholesky-factor search variables, row f4)."""
+    L = np.tril(unvech(x, d))
+    return vech(L @ L.T)
+
+
 def lscv_H_select(X, max_iter: int = 500, tol: float = 1e-7, penalty: float = PENALTY,
-                  threads: int = 1, trace=None, nm_starts: int = 1):
+                  threads: int = 1, trace=None, nm_starts: int = 1, param: str = "vech"):
     """LSCV_H: minimise g(H) (Eq. 30) over vech(H) by Nelder–Mead from H_start (Eq. 35).
     nm_starts > 1 (row f4): independent runs from the initial simplex scaled by 4^-k, best kept
-    (ties -> earlier run)."""
+    (ties -> earlier run).  param = "chol" (row f4): the search variables are vech(L) of a lower
+    triangular L with H = L L^T (every vertex positive semi-definite), starting from
+    L = chol(H_start); the simplex rule of reading Z8 and the 4^-k scaling apply to L."""
     X = _as_X(X)
     d, n = X.shape
-    x0 = vech(H_start(X))
+    Hs = H_start(X)
+    if param == "chol":
+        x0 = vech(cholesky_pd(Hs))
+        to_H = lambda v: vech_llt(v, d)
+    elif param == "vech":
+        x0 = vech(Hs)
+        to_H = lambda v: v
+    else:
+        raise ValueError("param must be 'vech' or 'chol'")
     sim0 = initial_simplex(x0, d)
     best = None
     for k in range(max(1, nm_starts)):
         sim = [v * 4.0 ** (-k) for v in sim0]
-        res = nelder_mead(lambda v: lscv_H_score(X, v, threads, penalty), sim, max_iter, tol, trace)
+        res = nelder_mead(lambda v: lscv_H_score(X, to_H(v), threads, penalty), sim, max_iter, tol, trace)
         if best is None or res["f"] < best["f"]:
             best = res
-    best["H"] = unvech(best["x"], d)
-    best["H_start"] = unvech(x0, d)
+    best["H"] = unvech(to_H(best["x"]), d)
+    best["H_start"] = Hs
     return best
 
 

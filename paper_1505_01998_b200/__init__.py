@@ -59,7 +59,7 @@ class SelectOpts(ctypes.Structure):
                 ("max_iter", ctypes.c_int32), ("tol_rel", ctypes.c_double),
                 ("penalty", ctypes.c_double), ("speculative", ctypes.c_int32),
                 ("refine_steps", ctypes.c_int32), ("refine_tol", ctypes.c_double),
-                ("nm_starts", ctypes.c_int32), ("nm_loop", ctypes.c_int32)]
+                ("nm_starts", ctypes.c_int32), ("nm_loop", ctypes.c_int32), ("nm_param", ctypes.c_int32)]
 
 
 class Bandwidth(ctypes.Structure):

@@ -247,7 +247,10 @@ struct NMResult {
 };
 kde_status nelder_mead_multi(kde_ctx* c, const double* X, int64_t n, int d, const Moments& m,
                              const std::vector<std::vector<std::vector<double>>>& sims, int max_iter,
-                             double tol, double penalty, bool speculative, NMResult& best, int* total_evals);
+                             double tol, double penalty, bool speculative, NMResult& best, int* total_evals,
+                             bool chol_param = false);
+// vech(L L^T) for x = vech(L), L lower triangular (the Cholesky-factor search variables, row f4).
+void vech_llt(const double* x, int d, double* out);
 // The same serial NM as one CUDA graph with a device-side loop (kde_nm_dev.cu): single GPU, one start.
 kde_status nelder_mead_device(kde_ctx* c, const double* X, int64_t n, int d, const Moments& m,
                               const std::vector<std::vector<double>>& sim, int max_iter, double tol,

@@ -117,5 +117,20 @@ void vech(const std::vector<double>& A, int d, double* v) {
     for (int i = j; i < d; ++i) v[t++] = A[i * d + j];
 }
 
+void vech_llt(const double* x, int d, double* out) {
+  std::vector<double> L((size_t)d * d, 0.0);
+  int t = 0;
+  for (int j = 0; j < d; ++j)
+    for (int i = j; i < d; ++i) L[(size_t)i * d + j] = x[t++];
+  std::vector<double> H((size_t)d * d, 0.0);
+  for (int i = 0; i < d; ++i)
+    for (int j = 0; j <= i; ++j) {
+      double s = 0.0;
+      for (int k = 0; k <= j; ++k) s += L[(size_t)i * d + k] * L[(size_t)j * d + k];   // (L L^T)_ij, k <= min(i, j)
+      H[(size_t)i * d + j] = H[(size_t)j * d + i] = s;
+    }
+  vech(H, d, out);
+}
+
 }  // namespace host
 }  // namespace kde

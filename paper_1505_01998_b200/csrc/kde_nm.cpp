@@ -24,7 +24,8 @@ namespace host {
 // proposals as one GPU batch (lscv_H_eval), so per-run decisions equal those of a lone run.
 kde_status nelder_mead_multi(kde_ctx* c, const double* X, int64_t n, int d, const Moments& m,
                              const std::vector<std::vector<std::vector<double>>>& sims, int max_iter,
-                             double tol, double penalty, bool speculative, NMResult& best, int* total_evals) {
+                             double tol, double penalty, bool speculative, NMResult& best, int* total_evals,
+                             bool chol_param) {
   const int P = d * (d + 1) / 2;
   std::vector<std::unique_ptr<kde::NMState>> runs;
   for (const auto& sim : sims) {
@@ -44,7 +45,10 @@ kde_status nelder_mead_multi(kde_ctx* c, const double* X, int64_t n, int d, cons
       if (runs[r]->phase == kde::NMState::DONE) continue;
       const int cnt = kde::nm_propose(*runs[r], rows);
       span.push_back({r, (size_t)cnt});
-      for (int v = 0; v < cnt; ++v) batch.emplace_back(rows[v], rows[v] + P);
+      for (int v = 0; v < cnt; ++v) {
+        batch.emplace_back(rows[v], rows[v] + P);
+        if (chol_param) vech_llt(rows[v], d, batch.back().data());   // H = L L^T of the vertex
+      }
     }
     if (batch.empty()) break;
     std::vector<double> g;

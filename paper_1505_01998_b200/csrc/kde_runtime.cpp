@@ -496,6 +496,7 @@ void kde_default_opts(kde_select_opts* o) {
   o->refine_tol = 1e-9;
   o->nm_starts = 1;
   o->nm_loop = 0;           // device-resident Nelder-Mead where it applies
+  o->nm_param = 0;          // search over vech(H) (the paper's reading); 1 = over the Cholesky factor
 }
 
 kde_status kde_nccl_unique_id(void* out128) {

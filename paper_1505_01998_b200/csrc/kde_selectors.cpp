@@ -773,6 +773,13 @@ kde_status kde_select_bandwidth(kde_ctx* c, kde_method method, const double* X, 
     const double f = std::pow(4.0 / (d + 2), 1.0 / (d + 4)) * std::pow((double)n, -1.0 / (d + 4));
     for (double& v : root) v *= f;
     const int P = d * (d + 1) / 2;
+    if (o.nm_param != 0 && o.nm_param != 1) return fail(c, KDE_E_INVALID, "nm_param must be 0 or 1");
+    const bool chol_param = o.nm_param == 1;
+    if (chol_param) {   // search over the Cholesky factor (row f4): start from L = chol(H_start)
+      std::vector<double> L;
+      if (!cholesky(root, d, L)) return fail(c, KDE_E_SINGULAR_COV, "H_start not positive definite");
+      root = L;         // lower triangular; the simplex rule below reads its diagonal
+    }
     std::vector<double> x0(P);
     vech(root, d, x0.data());
     std::vector<std::vector<double>> sim = {x0};
@@ -803,12 +810,19 @@ kde_status kde_select_bandwidth(kde_ctx* c, kde_method method, const double* X, 
     // device-resident loop: one GPU, one start, serial rounds, whitened sets within ~1 GiB
     const int64_t Tm = kde::tile_for(Kind::LscvMatrix, d, n), ldT = (n + Tm - 1) / Tm * Tm;
     const bool dev_loop = o.nm_loop == 0 && K == 1 && o.speculative == 0 && c->world == 1 && !c->comm && c->psi_mode != 1 &&
+                          !chol_param &&
                           !c->har_fn && (double)(P + 1) * d * (double)ldT * 4.0 <= (double)(1LL << 30);
     if (dev_loop)
       TRY(nelder_mead_device(c, X, n, d, m, sims[0], o.max_iter, o.tol_rel, o.penalty, nm));
     else
-      TRY(nelder_mead_multi(c, X, n, d, m, sims, o.max_iter, o.tol_rel, o.penalty, o.speculative != 0, nm, nullptr));
+      TRY(nelder_mead_multi(c, X, n, d, m, sims, o.max_iter, o.tol_rel, o.penalty, o.speculative != 0, nm, nullptr,
+                            chol_param));
     if (!(nm.f < o.penalty)) return fail(c, KDE_E_NO_FEASIBLE, "no positive-definite H found");
+    if (chol_param) {
+      std::vector<double> h(P);
+      vech_llt(nm.x.data(), d, h.data());
+      nm.x = h;
+    }
     for (int k = 0; k < P; ++k) r.vechH[k] = nm.x[k];
     r.objective = nm.f;
     r.iterations = nm.iterations;

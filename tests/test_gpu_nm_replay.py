@@ -74,3 +74,23 @@ def test_nm_fp64_term_mode_reproduces_the_oracle_search(mix, d, n, seed, max_ite
     assert got["iterations"] == ref["iterations"]
     assert np.max(np.abs(got["vechH"] - ref["x"])) <= 1e-9 * np.max(np.abs(ref["x"]))
     assert abs(got["objective"] - ref["f"]) <= 1e-10 * abs(ref["f"])
+
+
+@pytest.mark.parametrize("mix,d,n,seed,max_iter", [("C3", 2, 900, 45, 300), ("C5", 3, 500, 46, 200)])
+def test_nm_cholesky_parametrisation_matches_oracle(mix, d, n, seed, max_iter):
+    # Row f4 variant (kde_select_opts.nm_param = 1: search over vech(L), H = L L^T).  With fp64 terms the
+    # library's search equals the oracle's (same iterations, H to 1e-9); with the default fp32 terms the
+    # selected H's fp64 objective is within the NM tolerance band of the oracle's optimum.
+    X = datagen.sample_mixture(mix, n, seed)[:d]
+    ref = oracle.lscv_H_select(X, max_iter=max_iter, param="chol", threads=THREADS)
+    ctx = kb.Context()
+    ctx.set_precision(1)
+    exact = ctx.select_bandwidth(kb.LSCV_H, kb.to_device(X), max_iter=max_iter, nm_param=1)
+    ctx.set_precision(0)
+    fast = ctx.select_bandwidth(kb.LSCV_H, kb.to_device(X), max_iter=max_iter, nm_param=1)
+    ctx.close()
+    assert exact["iterations"] == ref["iterations"]
+    Href = oracle.vech(ref["H"])
+    assert np.max(np.abs(exact["vechH"] - Href)) <= 1e-9 * np.max(np.abs(Href))
+    g_fast = oracle.lscv_H_score(X, fast["vechH"], threads=THREADS)
+    assert g_fast <= ref["f"] + max(1e-7, 2e-6) * abs(ref["f"])

@@ -204,3 +204,33 @@ def test_mean_cov_matches_numpy():
     n = x.size
     V11 = (x ** 2).sum() / (n - 1) - x.sum() ** 2 / (n * (n - 1))
     assert S[0, 0] == pytest.approx(V11, rel=1e-12)
+
+
+def test_vech_llt_hand_example():
+    # L = [[2, 0], [1, 3]]: vech(L) = [2, 1, 3] (P:351-363 order), L L^T = [[4, 2], [2, 10]]
+    np.testing.assert_array_equal(oracle.vech_llt([2.0, 1.0, 3.0], 2), [4.0, 2.0, 10.0])
+    # d = 3, checked against numpy's product of the unpacked factor
+    x = np.array([1.5, -0.5, 0.25, 2.0, 0.75, 0.5])
+    L = np.array([[1.5, 0, 0], [-0.5, 2.0, 0], [0.25, 0.75, 0.5]])
+    H = L @ L.T
+    np.testing.assert_allclose(oracle.vech_llt(x, 3), [H[0, 0], H[1, 0], H[2, 0], H[1, 1], H[2, 1], H[2, 2]], rtol=1e-15)
+
+
+def test_lscv_H_select_cholesky_parametrisation():
+    # Row f4 variant: the search over vech(L), H = L L^T.  d = 1 pins it to a dense scalar scan of the
+    # same objective (the optimum L^2 = h*^2, within the scan and tolerance resolution), and at d = 2
+    # it reaches an objective no worse than the vech(H) search's within the NM tolerance band.
+    x = datagen.sample_mixture("bimodal", 150, 5)
+    r = oracle.lscv_H_select(x, max_iter=300, tol=1e-10, param="chol")
+    hs = np.linspace(0.02, 1.5, 400)
+    gs = [oracle.lscv_H_score(x, [h * h]) for h in hs]
+    assert math.sqrt(r["H"][0, 0]) == pytest.approx(hs[int(np.argmin(gs))], rel=0.05)
+    assert r["f"] == pytest.approx(oracle.lscv_H_score(x, [r["H"][0, 0]]), rel=1e-15)
+    X = datagen.sample_mixture("C3", 200, 9)
+    rc = oracle.lscv_H_select(X, max_iter=400, param="chol")
+    rv = oracle.lscv_H_select(X, max_iter=400)
+    assert oracle.cholesky_pd(rc["H"]) is not None
+    assert rc["f"] <= rv["f"] + 1e-4 * abs(rv["f"])
+    # the start: L = chol(H_start), so the first vertex is H_start itself
+    L0 = oracle.cholesky_pd(rc["H_start"])
+    np.testing.assert_allclose(oracle.vech_llt(oracle.vech(L0), 2), oracle.vech(rc["H_start"]), rtol=1e-14)
