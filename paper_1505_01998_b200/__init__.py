@@ -34,7 +34,7 @@ EXPORTS = ["kde_create", "kde_destroy", "kde_last_error", "kde_nccl_unique_id",
            "kde_workspace_bytes", "kde_set_workspace", "kde_default_opts", "kde_psi_r",
            "kde_plugin_h", "kde_lscv_h_scores", "kde_lscv_H_scores", "kde_select_bandwidth",
            "kde_raw_sums", "kde_fixed_value", "kde_fixed_add", "kde_tile_coords",
-           "kde_last_profile", "kde_set_profiling", "kde_shard_tiles", "kde_shard_tile", "kde_evaluate", "kde_aqp_1d",
+           "kde_last_profile", "kde_set_profiling", "kde_shard_tiles", "kde_shard_tile", "kde_psi_skip_gap", "kde_lscv_skip_theta", "kde_evaluate", "kde_aqp_1d",
            "kde_lscv_h_scores_materialized", "kde_last_aux_ms", "kde_set_host_allreduce", "kde_set_precision",
            "kde_last_fp64_passes", "kde_last_psi_kappa"]
 
@@ -117,6 +117,8 @@ def lib():
                                   ctypes.POINTER(i64), ctypes.POINTER(i32)]
     L.kde_shard_tiles.restype = ctypes.c_int
     L.kde_shard_tile.argtypes = [i64, i32, i32]; L.kde_shard_tile.restype = i64
+    L.kde_psi_skip_gap.argtypes = [i32, f64, f64]; L.kde_psi_skip_gap.restype = f64
+    L.kde_lscv_skip_theta.argtypes = [i64]; L.kde_lscv_skip_theta.restype = f64
     L.kde_evaluate.argtypes = [vp, vp, i64, i32, vp, i64, dp, dp]
     L.kde_evaluate.restype = ctypes.c_int
     L.kde_aqp_1d.argtypes = [vp, vp, i64, f64, dp, dp, i32, dp, dp, dp]
@@ -150,6 +152,14 @@ def tile_coords(bx: int):
     l, q = ctypes.c_int64(), ctypes.c_int64()
     lib().kde_tile_coords(int(bx), ctypes.byref(l), ctypes.byref(q))
     return l.value, q.value
+
+
+def psi_skip_gap(r: int, g: float, var: float) -> float:
+    return lib().kde_psi_skip_gap(int(r), float(g), float(var))
+
+
+def lscv_skip_theta(n: int) -> float:
+    return lib().kde_lscv_skip_theta(int(n))
 
 
 def fixed_value(f: Fixed) -> float:

@@ -138,7 +138,7 @@ struct Ws {
   float* Y;                 // prepared fp32 data, d x ld
   unsigned long long* limbs;
   double* part;             // moments partials
-  double* small;            // mean[16], W[256], sums[136], flags (2 x 8 bytes) at small + 408
+  double* small;            // mean[16], W[256], sums[136], flags (2 x 8 bytes) at small + 408, ... (kSmallDoubles)
   unsigned long long* flag() const { return reinterpret_cast<unsigned long long*>(small + 408); }
 };
 size_t align256(size_t b);
@@ -173,7 +173,10 @@ kde_status gpu_sorted(kde_ctx* c, const double* x, int64_t n, const double** out
 kde_status gpu_sorted_rows(kde_ctx* c, const double* X, int64_t n, int d, const double** out);
 // Skip bound on s for LSCV sums: every term exp2(s * kappa) with s * |kappa| > 130 is exactly 0
 // (ex2.approx.ftz flushes results below 2^-126); +inf when KDE_DEBUG_LSCV_NOSKIP=1.
-float lscv_skip_s(double min_abs_kappa);
+// Far-tile bound on s for terms 2^(kappa s), |kappa| >= min_abs_kappa, at n samples: 130/|kappa| (every
+// term exactly 0) or, bounded skip (default), min(130, log2 n + 34)/|kappa| (kde_internal.h);
+// +inf under KDE_DEBUG_LSCV_NOSKIP=1.
+float lscv_skip_s(double min_abs_kappa, int64_t n);
 kde_status gpu_prep_into(kde_ctx* c, const double* X, int64_t n, int d, const std::vector<double>& W,
                          const std::vector<double>& mean, int64_t ld, Ws& w, float* Y, double clamp_thresh = 0.0);
 kde_status gpu_prep(kde_ctx* c, const double* X, int64_t n, int d, const std::vector<double>& W,

@@ -2,6 +2,7 @@
 // launchers (kde_psi.cu, kde_lscv_*.cu, kde_eval.cu, kde_materialized.cu, kde_nm_dev.cu).  Product code
 // only; nothing here is shared with oracle/.
 #pragma once
+#include <cmath>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -41,6 +42,10 @@ struct PsiParams {
 struct LscvScalarParams {
   float kappa[kMaxCand];   // -1/h_c^2 (data pre-scaled by sqrt(log2 e / 4) L^-1)
   float smax[kMaxCand];    // 125 / |kappa_c|: software-exp clamp on s (exp2_sw2_fma)
+  // Per-candidate far-tile bound on s (lscv_skip_s of this candidate alone): a tile whose coordinate-0
+  // gap g has fp32(g^2) > skip_c[c] adds nothing to candidate c, whether or not the whole tile is
+  // skipped for its batch, so a candidate's sums do not depend on the batch it travels in.
+  float skip_c[kMaxCand];
 };
 // Tiles whose sorted gap min|y_i - y_j| exceeds these contribute exactly 0 and are skipped:
 // fp32 path: MUFU input <= -0.72 s - 16 < -126 (flushed to 0) for s > 152.5; fp64: exp(-s/2)
@@ -48,6 +53,49 @@ struct LscvScalarParams {
 constexpr double kPsiSkipGap32 = 13.0, kPsiSkipGap64 = 40.0;
 // (KDE_DEBUG_PSI_NOSKIP=1 in the environment disables the skip: results are bit-identical.)
 double psi_skip_gap(bool fp64);
+
+// Bounded far-tile skip.  The fp32-term passes also skip tiles whose terms are not
+// exactly 0 but provably negligible: at most kSkipEps relative to the result.
+//   Psi: (-1)^{r/2} Psi-hat_r(g) = R(f^(r/2)) exactly, f = the KDE of the sample with bandwidth g/sqrt(2)
+//   (Eq. 15/17 with the diagonal, reading Z1), a density of variance V_b + g^2/2 <= V + g^2/2.  Among
+//   densities of variance v, R(f^(s)) >= R*_s v^{-(2s+1)/2}, attained by f ~ (1 - x^2/((2s+5)v))^{s+1}
+//   (Terrell 1990, maximal smoothing; R*_2 = 35/243).  Every dropped pair has u >= tau and
+//   |He_r(u)| e^{-u^2/2} <= tau^r e^{-tau^2/2} (tau >= 6), there are at most n^2/2 of them, so
+//   |dropped| / |Psi-hat| <= tau^r e^{-tau^2/2} / (sqrt(2 pi) R*_s q^{(r+1)/2}), q = g^2 / (V + g^2/2);
+//   psi_bounded_gap returns a tau <= kPsiSkipGap32 that makes this <= kSkipEps (the smallest, from
+//   above, to Newton's accuracy).
+//   LSCV (Eq. 24/30, g = A - B + C, C = c4/n the diagonal term): every dropped term e <= 2^-theta, at
+//   most n^2/2 of them, so |dA| <= c4 2^-theta = C n 2^-theta; theta = log2 n + 34 (lscv_skip_theta)
+//   gives |dA| <= 2^-34 C <= 5.9e-11 (1 + kappa') |g|, kappa' = (A + B)/|g|.
+// KDE_DEBUG_SKIP_EXACT=1 keeps only the exact-zero skips (bit-identical to no skip at all).
+constexpr double kSkipEps = 1e-9;
+#ifdef __CUDACC__
+#define KDE_HDI __host__ __device__ inline
+#else
+#define KDE_HDI inline
+#endif
+KDE_HDI double psi_bounded_gap(int r, double g, double var) {
+  if (!(g > 0.0) || !(var >= 0.0) || !(var < 1e300) || !(g < 1e150)) return kPsiSkipGap32;
+  const double Rs = r == 4 ? 35.0 / 243.0
+                           : (r == 6 ? 14175.0 * sqrt(11.0) / 161051.0 : 1091475.0 * sqrt(13.0) / 4826809.0);
+  const double q = g * g / (var + 0.5 * g * g);
+  const double lt = log(kSkipEps * 2.5066282746310002 * Rs) + 0.5 * (r + 1) * log(q);   // log of the target
+  // f(tau) = r log tau - tau^2/2 - lt is concave and decreasing for tau > sqrt(r): Newton from the right
+  // of the root stays right of it (tangents lie above a concave f), so every iterate satisfies f <= 0.
+  double t = kPsiSkipGap32;
+  if (r * log(t) - 0.5 * t * t - lt > 0.0) return kPsiSkipGap32;
+  for (int it = 0; it < 8; ++it) {
+    const double f = r * log(t) - 0.5 * t * t - lt, fp = r / t - t;
+    const double tn = t - f / fp;
+    if (!(tn < t) || tn < 6.0) break;
+    t = tn;
+  }
+  return t;
+}
+// Psi skip threshold of one pass: bounded (default), exact-zero (KDE_DEBUG_SKIP_EXACT=1) or none
+// (KDE_DEBUG_PSI_NOSKIP=1).  Host only (reads the environment at every call).
+double psi_skip_gap_for(int r, double g, double var);
+bool skip_bounded();   // false under KDE_DEBUG_SKIP_EXACT=1
 
 struct LaunchCfg {
   const float* X;          // D rows of ld floats (fp32, prepared), device
@@ -73,6 +121,7 @@ struct LaunchCfg {
   const float* centres = nullptr;
   unsigned long long* skipped = nullptr;   // Psi: pairs of skipped (exactly zero) tiles, or null
   double skip_gap = kPsiSkipGap32;         // Psi: skip tiles whose sorted gap exceeds this (inf: never)
+  const double* skip_gap_dev = nullptr;    // Psi: the threshold in device memory (PLUGIN chain), or null
   // Dynamic tile scheduling: a unit counter that is 0 when the launch starts (the caller zeroes it
   // with the limbs), or null for the static stride.
   unsigned long long* work = nullptr;
@@ -161,7 +210,8 @@ struct PluginDev {
 };
 constexpr int kPluginOuts = 6;
 constexpr int kSkippedSlot = 423;   // small + 423: skipped-pair counter (PLUGIN chain and psi_raw)
-constexpr int kSmallDoubles = 424;
+constexpr int kGapSlot = 424;       // small + 424, 425: the PLUGIN passes' bounded skip thresholds (chain)
+constexpr int kSmallDoubles = 426;
 cudaError_t launch_plugin_chain(int stage, int64_t n, double* small, const unsigned long long* limbs, int S,
                                 cudaStream_t s, int psi_mode = 0);
 // Automatic Psi precision: an fp32-term pass (S = sum t, A ~ sum |t| at 16-column-group level) is

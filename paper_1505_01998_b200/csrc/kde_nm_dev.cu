@@ -326,7 +326,7 @@ kde_status nelder_mead_device(kde_ctx* c, const double* X, int64_t n, int d, con
           cfg.n_out = 2; cfg.stream = c->cap_stream; cfg.sm_count = c->sm_count; cfg.clamp = nullptr;
           cfg.n_sets = max_sets; cfg.set_stride = set_floats; cfg.n_sets_dev = &dblk->h.n_sets;
           cfg.work = w.limbs + (size_t)2 * max_sets * kLimbs;
-          cfg.skip_s = lscv_skip_s(1.0);
+          cfg.skip_s = lscv_skip_s(1.0, n);
           cfg.skipped = reinterpret_cast<unsigned long long*>(w.small + kSkippedSlot);
           cfg.pdl = pdl;
           cfg.reserve_ctas = pdl && u + 1 < U ? 1 : 0;   // the next decide's slot

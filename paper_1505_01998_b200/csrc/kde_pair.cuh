@@ -76,6 +76,7 @@ struct Args {
   unsigned long long* work;          // dynamic scheduling: unit counter (zero at launch), or null
   float skip_s;                      // LSCV on coordinate-0-sorted data: skip bound on s (+inf: never)
   int part_rank, part_world;         // tile_begin/tile_end index this rank's round-robin tiles (shard_tile)
+  const double* skip_gap_dev;        // Psi: skip_gap in device memory (PLUGIN chain), or null
 };
 
 // Work distribution.  Static: CTA b takes units b, b + grid, ...  Dynamic (a.work != null): CTA b
@@ -433,17 +434,18 @@ __device__ __forceinline__ bool lscv_tile_skipped(const Args& a, const float* X,
 
 // Evaluate one work unit (tile (l, q), column chunk `chunk` when F::CS > 1) whose column samples
 // are in shared memory at `sc`, and commit its outputs.  Sorted Psi data: a tile whose smallest
-// pair distance exceeds kPsiSkipGap32 contributes exactly 0 (every MUFU input underflows) and is
-// skipped, so small bandwidths cost only the tiles near the diagonal.
+// pair distance exceeds `gap` (kPsiSkipGap32: every MUFU input underflows, the tile adds exactly 0;
+// psi_bounded_gap: its terms are provably negligible, kde_internal.h) is skipped, so small
+// bandwidths cost only the tiles near the diagonal.
 template <class F>
 __device__ __forceinline__ void pair_unit(const Args& a, const typename F::Params& p, int64_t tile,
                                           int64_t l, int64_t q, int chunk, const float* sc, double* red,
                                           unsigned long long* limbs, bool clamp, uint64_t* bar, uint32_t parity,
-                                          bool skip) {
+                                          bool skip, double gap) {
   constexpr int T = F::T, NOUT = F::NOUT;
   F f;
   if constexpr (IsCentred<F>::value) {
-    if (q < l && a.Y64[l * T] - a.Y64[q * T + T - 1] > a.skip_gap) {   // uniform per CTA
+    if (q < l && a.Y64[l * T] - a.Y64[q * T + T - 1] > gap) {   // uniform per CTA
       if (threadIdx.x == 0 && a.skipped != nullptr) {   // pairs of this unit, for the profile
         int64_t c0 = 0, c1 = a.n - l * (int64_t)T;
         if (F::CS > 1) c0 = (int64_t)chunk * (T / F::CS), c1 = c1 < c0 + T / F::CS ? c1 : c0 + T / F::CS;
@@ -480,6 +482,17 @@ __device__ __forceinline__ void pair_unit(const Args& a, const typename F::Param
   }
   double v[NOUT];
   f.outputs(v, p);
+  if constexpr (std::is_same<typename F::Params, LscvScalarParams>::value && !F::kSets) {
+    // LSCV_h batch: the tile was evaluated for the batch's widest h, but a candidate whose own bound
+    // skips it takes nothing from it (the same as in any other batch: batch-independent sums)
+    if (q < l) {
+      const float g = __fsub_rn(a.X[l * T], a.X[q * T + T - 1]);
+      const float g2 = __fmul_rn(g, g);
+#pragma unroll
+      for (int c = 0; c < NOUT / 2; ++c)
+        if (g2 > p.skip_c[c]) v[2 * c] = v[2 * c + 1] = 0.0;
+    }
+  }
   commit_tile<NOUT, F::NT>(v, red, limbs, a.scale_exp);
 }
 
@@ -519,6 +532,7 @@ __global__ void __launch_bounds__(F::NT, F::MINB) pair_kernel(const Args a,
   }
   __syncthreads();
   const bool clamp = F::kClampable && a.clamp != nullptr && *a.clamp != 0;   // uniform per launch
+  const double gap = a.skip_gap_dev != nullptr ? *a.skip_gap_dev : a.skip_gap;
   uint32_t k = 0;
   while (u < units) {
     const int64_t tile = shard_tile(a.tile_begin + u / CS, a.part_rank, a.part_world);
@@ -528,7 +542,7 @@ __global__ void __launch_bounds__(F::NT, F::MINB) pair_kernel(const Args a,
     const bool skip = s_skip[k & 1];   // read before the issue below can rewrite the other slot
     if (tid == 0 && un < units) issue(un, (k + 1) & 1);
     pair_unit<F>(a, p, tile, l, q, (int)(u % CS), cols + (k & 1) * D * T, red, a.limbs, clamp, &bar[k & 1],
-                 (k >> 1) & 1, skip);
+                 (k >> 1) & 1, skip, gap);
     u = un;
     ++k;
   }
@@ -586,7 +600,7 @@ __global__ void __launch_bounds__(F::NT, F::MINB) pair_kernel_sets(const Args a,
     Args as = a;
     as.X = a.X + set * a.set_stride;
     pair_unit<F>(as, p, tile, l, q, 0, cols + (k & 1) * D * T, red, a.limbs + set * NOUT * kLimbs, clamp,
-                 &bar[k & 1], (k >> 1) & 1, skip);
+                 &bar[k & 1], (k >> 1) & 1, skip, a.skip_gap);
     u = un;
     ++k;
   }
@@ -626,7 +640,8 @@ inline cudaError_t launch_pair(const LaunchCfg& c, const typename F::Params& p) 
   if (grid > units) grid = units;
   if (grid < 1) grid = 1;
   Args a{c.X, c.n, c.ld, c.tile_begin, c.tile_end, c.scale_exp, c.limbs, c.clamp, c.n_sets, c.set_stride,
-         c.Y64, c.centres, c.skipped, c.n_sets_dev, c.skip_gap, c.work, c.skip_s, c.part_rank, c.part_world};
+         c.Y64, c.centres, c.skipped, c.n_sets_dev, c.skip_gap, c.work, c.skip_s, c.part_rank, c.part_world,
+         c.skip_gap_dev};
   if constexpr (F::kSets) {
     if (c.pdl) {
       cudaLaunchConfig_t lc = {};

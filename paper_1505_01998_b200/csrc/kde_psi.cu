@@ -17,6 +17,17 @@ double psi_skip_gap(bool fp64) {
   return fp64 ? kPsiSkipGap64 : kPsiSkipGap32;
 }
 
+bool skip_bounded() {
+  const char* e = getenv("KDE_DEBUG_SKIP_EXACT");   // tests / diagnostics: read at every call
+  return !(e && atoi(e) == 1);
+}
+
+double psi_skip_gap_for(int r, double g, double var) {
+  const double exact = psi_skip_gap(false);
+  if (!(exact < INFINITY) || !skip_bounded()) return exact;
+  return psi_bounded_gap(r, g, var);
+}
+
 // ------------------------------------------------------------------ dispatch
 
 int tile_for(Kind k, int d, int64_t n) {
@@ -418,6 +429,7 @@ __global__ void plugin_chain_kernel(int stage, int64_t n, double* small, const u
     const double K6_0 = -15.0 / s2p;
     t[3] = pow(-2.0 * K6_0 / (t[2] * nn), 1.0 / 9.0);                      // Eq. 14
     dv.W[0] = 1.0 / t[3];
+    small[kGapSlot] = psi_bounded_gap(6, t[3], V);                         // bounded skip (§3.11)
   } else if (stage == 4 || stage == 5) {
     const int k = stage - 4;                                               // 0: Psi6, 1: Psi4
     const unsigned long long* L = limbs + (size_t)(2 * k) * kLimbs;
@@ -432,6 +444,7 @@ __global__ void plugin_chain_kernel(int stage, int64_t n, double* small, const u
     const double K4_0 = 3.0 / s2p;
     t[5] = pow(-2.0 * K4_0 / (t[4] * nn), 1.0 / 7.0);                      // Eq. 16
     dv.W[0] = 1.0 / t[5];
+    small[kGapSlot + 1] = psi_bounded_gap(4, t[5], t[0]);
   } else {
     const double Sr = limbs_value_dev(limbs + (size_t)(dv.gate[1] ? 5 : 2) * kLimbs, S);
     t[6] = (2.0 * Sr / s2p + nn * 3.0 / s2p) / (nn * nn * pow(t[5], 5.0));     // Eq. 17

@@ -73,7 +73,7 @@ size_t ws_bytes(int64_t ld, int32_t d, int32_t n_out) {
   return align256((size_t)d * ld * sizeof(float)) +
          align256((size_t)std::max(n_out, 1) * kde::kLimbs * sizeof(long long) +
                   (size_t)kde::kWorkCounters * sizeof(long long)) +
-         align256((size_t)1024 * 136 * sizeof(double)) + align256((16 + 256 + 136 + 16) * sizeof(double));
+         align256((size_t)1024 * 136 * sizeof(double)) + align256(kde::kSmallDoubles * sizeof(double));
 }
 
 kde_status get_ws(kde_ctx* c, int64_t ld, int32_t d, int32_t n_out, Ws* w) {
@@ -102,7 +102,7 @@ kde_status get_ws(kde_ctx* c, int64_t ld, int32_t d, int32_t n_out, Ws* w) {
   w->part = (double*)base;
   base += align256((size_t)1024 * 136 * sizeof(double));
   w->small = (double*)base;
-  base += align256((16 + 256 + 136 + 16) * sizeof(double));
+  base += align256(kde::kSmallDoubles * sizeof(double));
   w->limbs = (unsigned long long*)base;
   return KDE_OK;
 }
@@ -237,10 +237,11 @@ kde_status gpu_sorted_rows(kde_ctx* c, const double* X, int64_t n, int d, const 
   return KDE_OK;
 }
 
-float lscv_skip_s(double min_abs_kappa) {
+float lscv_skip_s(double min_abs_kappa, int64_t n) {
   const char* e = getenv("KDE_DEBUG_LSCV_NOSKIP");   // tests / diagnostics: read at every call
   if ((e && atoi(e) == 1) || !(min_abs_kappa > 0.0)) return __builtin_inff();
-  const double b = 130.0 / min_abs_kappa;
+  const double theta = kde::skip_bounded() ? kde_lscv_skip_theta(n) : 130.0;
+  const double b = theta / min_abs_kappa;
   return b < 1e30 ? (float)b : __builtin_inff();
 }
 
@@ -636,6 +637,12 @@ kde_status kde_shard_tiles(kde_sum_kind kind, int64_t n, int32_t d, int32_t rank
   if (chunk) *chunk = world > 1 ? kde::kShardChunk : (int32_t)std::min<int64_t>(tiles, INT32_MAX);
   return KDE_OK;
 }
+
+double kde_psi_skip_gap(int32_t r, double g, double var) {
+  return (r == 4 || r == 6 || r == 8) ? kde::psi_bounded_gap(r, g, var) : kde::kPsiSkipGap32;
+}
+
+double kde_lscv_skip_theta(int64_t n) { return std::min(130.0, std::log2((double)std::max<int64_t>(n, 2)) + 34.0); }
 
 int64_t kde_shard_tile(int64_t i, int32_t rank, int32_t world) {
   return (world < 1 || rank < 0 || rank >= world || i < 0) ? -1 : kde::shard_tile(i, rank, world);

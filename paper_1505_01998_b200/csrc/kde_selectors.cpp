@@ -121,7 +121,7 @@ kde_status psi_raw(kde_ctx* c, const double* x, int64_t n, int r, const double* 
       L.kind = psi_kind(r); L.r = r; L.nb = 1; L.out_offset = 0; L.n_out = 2;
       L.X = b.Yc; L.Y64 = b.Y64; L.centres = b.centres;
       L.skipped = reinterpret_cast<unsigned long long*>(w.small + kde::kSkippedSlot);
-      L.skip_gap = kde::psi_skip_gap(false);
+      L.skip_gap = kde::psi_skip_gap_for(r, g[k], m.cov.empty() ? 0.0 : m.cov[0]);
       psi_coeffs(r, L.psi);
       std::vector<kde_fixed> o;
       TRY(run_sums(c, 1, n, ld, T, S, w, {L}, 2, shard_rank, shard_world, allreduce, o));
@@ -205,9 +205,10 @@ kde_status lscv_h_raw(kde_ctx* c, const double* X, int64_t n, int d, const doubl
       int idx = order[std::min(b * nb + j, nh - 1)];   // pad with a valid candidate
       L.ls.kappa[j] = (float)(-1.0 / (h[idx] * h[idx]));
       L.ls.smax[j] = (float)(125.0 / -(double)L.ls.kappa[j]);
+      L.ls.skip_c[j] = lscv_skip_s(-(double)L.ls.kappa[j], n);   // this candidate's own bound
       if (j < nb) kmin = std::min(kmin, -(double)L.ls.kappa[j]);
     }
-    L.skip_s = lscv_skip_s(kmin);   // the batch's widest h bounds every candidate's terms
+    L.skip_s = lscv_skip_s(kmin, n);   // the batch's widest h bounds every candidate's terms
     Ls.push_back(L);
   }
   std::vector<kde_fixed> o;
@@ -313,7 +314,7 @@ kde_status lscv_H_raw(kde_ctx* c, const double* X, int64_t n, int d, const std::
     SumLaunch L;
     L.kind = Kind::LscvMatrix; L.nb = 1; L.out_offset = 0; L.n_out = 2 * cnt;
     L.X = Yw; L.n_sets = cnt; L.set_stride = set_floats;
-    L.skip_s = lscv_skip_s(1.0);   // e = 2^-s with s = |x'_i - x'_j|^2
+    L.skip_s = lscv_skip_s(1.0, n);   // e = 2^-s with s = |x'_i - x'_j|^2
     std::vector<kde_fixed> o;
     TRY(run_sums(c, d, n, ld, T, scale_exp_for(1.0, n), w, {L}, 2 * cnt, shard_rank, shard_world, allreduce, o,
                  /*limbs_zeroed=*/true));
@@ -389,7 +390,8 @@ kde_status kde_psi_r(kde_ctx* c, const double* x, int64_t n, int32_t r, const do
 // tiles into `limbs` (S, A), then (world > 1) the all-reduce, all enqueued on the context stream.
 static kde_status plugin_pass(kde_ctx* c, int r, int64_t n, int64_t ld, int T, int S, const PsiBufs& b,
                               unsigned long long* clamp, unsigned long long* limbs, int64_t tb, int64_t te,
-                              double pairs, unsigned long long* skipped, unsigned long long* work) {
+                              double pairs, unsigned long long* skipped, unsigned long long* work,
+                              const double* gap_dev) {
   Range rr("kde.pair_pass");
   kde::LaunchCfg cfg;
   cfg.X = b.Yc; cfg.n = n; cfg.ld = ld; cfg.tile_begin = tb; cfg.tile_end = te; cfg.tile = T;
@@ -398,6 +400,8 @@ static kde_status plugin_pass(kde_ctx* c, int r, int64_t n, int64_t ld, int T, i
   cfg.clamp = clamp; cfg.Y64 = b.Y64; cfg.centres = b.centres;
   cfg.skipped = skipped;
   cfg.skip_gap = kde::psi_skip_gap(false);
+  // bounded far-tile skip: the chain computed this pass's threshold from g and V-hat (stage 1 / 2)
+  if (cfg.skip_gap < INFINITY && kde::skip_bounded()) cfg.skip_gap_dev = gap_dev;
   cfg.work = work;
   kde::PsiParams p;
   psi_coeffs(r, p);
@@ -457,7 +461,8 @@ static kde_status plugin_enqueue(kde_ctx* c, const double* x, int64_t n, int T, 
     CUDA_TRY(c, kde::launch_psi_prep(xs, n, dv.mean, dv.W, T, b.Y64, b.Yc, b.centres, ld, st, w.flag(), 3.0e4));
     if (mode != 1)
       TRY(plugin_pass(c, r, n, ld, T, Ss[k], b, w.flag() + 1, L + (size_t)(2 * k) * kde::kLimbs, tb, te, pairs,
-                      reinterpret_cast<unsigned long long*>(w.small + kde::kSkippedSlot), work + k));
+                      reinterpret_cast<unsigned long long*>(w.small + kde::kSkippedSlot), work + k,
+                      w.small + kde::kGapSlot + k));
     CUDA_TRY(c, kde::launch_plugin_chain(4 + k, n, w.small, L, Ss[k], st, mode));     // fp64 re-run?
     TRY(psi64_pass(c, r, b.Y64, n, Ss[k], L + (size_t)(4 + k) * kde::kLimbs, dv.gate + k, k));
     CUDA_TRY(c, kde::launch_plugin_chain(k == 0 ? 2 : 3, n, w.small, L, Ss[k], st));  // steps 5-6 / 7-8
@@ -492,7 +497,8 @@ static kde_status plugin_impl(kde_ctx* c, const double* x, int64_t n, kde_plugin
   cudaStream_t st = c->stream;
   const std::vector<uintptr_t> key = {(uintptr_t)x, (uintptr_t)n, (uintptr_t)w.Y, (uintptr_t)c->sort_ws,
                                       (uintptr_t)c->h_limbs, (uintptr_t)c->profiling, (uintptr_t)c->comm,
-                                      (uintptr_t)(c->psi_mode + 1)};
+                                      (uintptr_t)(c->psi_mode + 1),
+                                      (uintptr_t)(kde::psi_skip_gap(false) < INFINITY) + 2 * kde::skip_bounded()};
   // The first call with a given key runs directly (and does any lazy module loading and library
   // setup outside a capture); a second call with the same key captures, later ones replay.
   // (single-GPU contexts only: with a communicator the all-reduces stay plain stream operations)

@@ -439,23 +439,41 @@ def test_psi_automatic_precision_decisions(ctx):
         assert rel(psi, ref) <= RTOL, (c, psi, ref)
 
 
+class _env:
+    """Set diagnostic environment switches for the duration of a block (the library reads them per call)."""
+
+    def __init__(self, **kv):
+        self.kv = kv
+
+    def __enter__(self):
+        import os
+        self.old = {k: os.environ.get(k) for k in self.kv}
+        os.environ.update({k: str(v) for k, v in self.kv.items()})
+
+    def __exit__(self, *a):
+        import os
+        for k, v in self.old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
 @pytest.mark.parametrize("mode", [-1, 1])
 def test_psi_far_tile_skip_is_exact(ctx, mode):
-    # Sorted data: a tile whose smallest pair distance exceeds the skip gap has every term exactly
-    # 0 (fp32: the MUFU input underflows; fp64: exp underflows), so skipping it changes no bit.
-    import os
+    # Sorted data: a tile whose smallest pair distance exceeds the exact skip gap has every term exactly
+    # 0 (fp32: the MUFU input underflows; fp64: exp underflows), so skipping it changes no bit
+    # (KDE_DEBUG_SKIP_EXACT=1: only those skips; the default bounded skip is tested below).
     X = dev(datagen.sample_mixture("skewed", 131109 if mode < 0 else 20000, 7))
     ctx.set_precision(mode)
     try:
         for kind in (kb.SUM_PSI4, kb.SUM_PSI6, kb.SUM_PSI8):
-            a = ctx.raw_sums(kind, X, [0.03, 0.2])
-            evaluated = ctx.last_profile()["pair_evals"]
-            os.environ["KDE_DEBUG_PSI_NOSKIP"] = "1"
-            try:
+            with _env(KDE_DEBUG_SKIP_EXACT=1):
+                a = ctx.raw_sums(kind, X, [0.03, 0.2])
+                evaluated = ctx.last_profile()["pair_evals"]
+            with _env(KDE_DEBUG_PSI_NOSKIP=1):
                 b = ctx.raw_sums(kind, X, [0.03, 0.2])
                 full = ctx.last_profile()["pair_evals"]
-            finally:
-                del os.environ["KDE_DEBUG_PSI_NOSKIP"]
             assert [f.key() for f in a] == [f.key() for f in b]
             if mode < 0:
                 assert evaluated < full   # g = 0.03: most tiles are skipped
@@ -463,12 +481,66 @@ def test_psi_far_tile_skip_is_exact(ctx, mode):
         ctx.set_precision(0)
 
 
+@pytest.mark.parametrize("case", ["skewed", "normal", "spikes"])
+def test_psi_bounded_skip_within_bound(ctx, case):
+    # the default fp32-term pass also skips tiles beyond tau = kde_psi_skip_gap(r, g, V) < 13;
+    # what it drops is at most 1e-9 |2S + n He_r(0)| (= 1e-9 |Psi-hat| in the kernel's units), and it
+    # evaluates fewer pairs than the exact-zero skip whenever tau < 13.
+    n = 60013
+    if case == "spikes":   # 12 narrow clusters far apart (much separated mass, small V-relative g)
+        r_ = np.random.default_rng(3)
+        X = (r_.integers(0, 12, n) * 3.0 + r_.normal(0, 0.05, n))[None, :]
+    else:
+        X = datagen.sample_mixture(case if case == "skewed" else "N01", n, 11)
+    Xd = dev(X)
+    V = float(np.var(X[0], ddof=1))
+    sd = math.sqrt(V)
+    ctx.set_precision(-1)
+    try:
+        for kind, r in ((kb.SUM_PSI4, 4), (kb.SUM_PSI6, 6), (kb.SUM_PSI8, 8)):
+            gs = [0.02 * sd, 0.1 * sd, 0.3 * sd]
+            a = ctx.raw_sums(kind, Xd, gs)
+            ev_b = ctx.last_profile()["pair_evals"]
+            with _env(KDE_DEBUG_SKIP_EXACT=1):
+                e = ctx.raw_sums(kind, Xd, gs)
+                ev_e = ctx.last_profile()["pair_evals"]
+            with _env(KDE_DEBUG_PSI_NOSKIP=1):
+                b = ctx.raw_sums(kind, Xd, gs)
+            he0 = {4: 3.0, 6: -15.0, 8: 105.0}[r]
+            for k, g in enumerate(gs):
+                assert e[k].key() == b[k].key()   # the exact skip changes no bit
+                Sa, Sb = kb.fixed_value(a[k]), kb.fixed_value(b[k])
+                tau = kb.psi_skip_gap(r, g, V)
+                assert 6.0 <= tau <= 13.0
+                assert abs(Sa - Sb) <= 1e-9 * abs(2 * Sb + n * he0), (case, r, g, tau, Sa, Sb)
+            assert ev_b < ev_e, (case, r, ev_b, ev_e)   # the bounded skip drops more tiles
+    finally:
+        ctx.set_precision(0)
+
+
+def test_plugin_bounded_skip(ctx):
+    # The PLUGIN chain computes each pass's tau on the device from g and V-hat (stages 1 and 2): the
+    # trace equals the exact-skip run to 1e-9 relative per Psi (each pass's bound), fewer pairs evaluated.
+    X = datagen.config_data("C4", n=200003)
+    Xd = dev(X)
+    h, tr = ctx.plugin_h(Xd)
+    ev = ctx.last_profile()["pair_evals"]
+    with _env(KDE_DEBUG_SKIP_EXACT=1):
+        h2, tr2 = ctx.plugin_h(Xd)
+        ev2 = ctx.last_profile()["pair_evals"]
+    for k in ("psi6", "g2", "psi4"):
+        assert rel(tr[k], tr2[k]) <= 3e-9, (k, tr[k], tr2[k])
+    assert rel(h, h2) <= 1e-9
+    assert ev < 0.95 * ev2, (ev, ev2)
+
+
 @pytest.mark.parametrize("which", ["h1", "h2", "h8", "H1", "H2", "H4", "H7"])
 def test_lscv_far_tile_skip_is_exact(ctx, which):
     # LSCV data are sorted by coordinate 0 (whitening keeps that order); a tile whose coordinate-0 gap
-    # bounds every s above the skip bound has every MUFU term exactly 0 (and every software-exp term at
-    # 2^-125, far below the fixed-point resolution), so skipping it changes no output bit.
-    import os
+    # bounds every s above the exact skip bound has every MUFU term exactly 0 (and every software-exp
+    # term at 2^-125, far below the fixed-point resolution), so skipping it changes no output bit
+    # (KDE_DEBUG_SKIP_EXACT=1).  The default bounded skip (theta = min(130, log2 n + 34))
+    # moves each raw sum by at most n(n-1)/2 2^-theta (S1) and n(n-1)/2 2^-2theta (S2).
     d = int(which[1])
     if which[0] == "h":
         X = (datagen.sample_mixture("bimodal", 20011, 5) if d == 1 else datagen.sample_mixture("C3", 12007, 5)
@@ -479,20 +551,28 @@ def test_lscv_far_tile_skip_is_exact(ctx, which):
              np.random.default_rng(9).standard_t(4, size=(d, 5003)))
         kind, cand = kb.SUM_LSCV_H, np.concatenate([_spd_cands(d, 3, 7, s) for s in (1e-4, 1e-3, 0.05)]).ravel()
     Xd = dev(X)
-    a = ctx.raw_sums(kind, Xd, cand)
-    evaluated = ctx.last_profile()["pair_evals"]
-    os.environ["KDE_DEBUG_LSCV_NOSKIP"] = "1"
-    try:
+    with _env(KDE_DEBUG_SKIP_EXACT=1):
+        a = ctx.raw_sums(kind, Xd, cand)
+        evaluated = ctx.last_profile()["pair_evals"]
+    bnd = ctx.raw_sums(kind, Xd, cand)
+    ev_bounded = ctx.last_profile()["pair_evals"]
+    with _env(KDE_DEBUG_LSCV_NOSKIP=1):
         b = ctx.raw_sums(kind, Xd, cand)
         full = ctx.last_profile()["pair_evals"]
-    finally:
-        del os.environ["KDE_DEBUG_LSCV_NOSKIP"]
     assert [f.key() for f in a] == [f.key() for f in b]
     n = X.shape[1]
     ncand = len(cand) if kind == kb.SUM_LSCV_h else len(cand) // (d * (d + 1) // 2)
     nb = (8 if d <= 4 else (16 if d <= 12 else 8)) if kind == kb.SUM_LSCV_h else 1   # kde_pair.cuh nb_scalar
     assert full == n * (n - 1) / 2 * (-(-ncand // nb) * nb)   # every pair x every candidate slot
     assert evaluated < (0.9 if d <= 4 else 1.0) * full        # the small bandwidths skip tiles
+    assert ev_bounded <= evaluated
+    theta = kb.lscv_skip_theta(n)
+    assert theta == min(130.0, math.log2(n) + 34)
+    pairs = n * (n - 1) / 2
+    for k in range(ncand):
+        for j, p in ((0, 1.0), (1, 2.0)):
+            x, y = kb.fixed_value(bnd[2 * k + j]), kb.fixed_value(b[2 * k + j])
+            assert 0.0 <= y - x <= pairs * 2.0 ** (-p * theta) * 1.0001, (which, k, j, x, y)
 
 
 def test_lscv_h_candidate_order_invariance(ctx):
