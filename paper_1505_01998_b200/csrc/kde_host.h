@@ -75,6 +75,9 @@ struct kde_ctx {
   // CUDA graph of the PLUGIN chain, replayed while its key (pointers, n, mode) is unchanged
   bool graphs = true;
   cudaStream_t cap_stream = nullptr;          // capture stream (the caller's may be the legacy one)
+  // second stream of a multi-launch pass (run_sums): launch k+1 fills launch k's tail
+  cudaStream_t side_stream = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaGraphExec_t plug_exec = nullptr;
   std::vector<uintptr_t> plug_key, plug_seen;   // captured key; key of the last direct run
   int32_t plug_prof_launches = 0, plug_prof_all = 0;

@@ -391,6 +391,20 @@ kde_status run_sums(kde_ctx* c, int d, int64_t n, int64_t ld, int T, int scale, 
   int64_t tiles = n_tiles(n, T), tb, te;
   shard_range(tiles, shard_rank, shard_world, &tb, &te);
   const double pairs = c->profiling ? pairs_in_shard(n, T, te, shard_rank, shard_world) : 0.0;
+  // Several launches (LSCV_h candidate batches): alternate two streams, so that launch k+1's CTAs take the
+  // SM slots launch k's CTAs free during its tail (its last units; the outputs and the scheduling
+  // counters of the launches are disjoint).  Profiling then times the whole span as one window.
+  static const bool one_stream = [] { const char* e = getenv("KDE_DEBUG_ONE_STREAM"); return e && atoi(e) == 1; }();
+  const bool two = launches.size() >= 2 && !one_stream && !(c->cap_stream && c->stream == c->cap_stream);
+  cudaEvent_t span0 = nullptr, span1 = nullptr;
+  if (two) {
+    if (!c->side_stream) CUDA_TRY(c, cudaStreamCreateWithFlags(&c->side_stream, cudaStreamNonBlocking));
+    if (!c->ev_fork) CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+    if (!c->ev_join) CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+    if (c->profiling) { span0 = next_event(c); span1 = next_event(c); CUDA_TRY(c, cudaEventRecord(span0, c->stream)); }
+    CUDA_TRY(c, cudaEventRecord(c->ev_fork, c->stream));
+    CUDA_TRY(c, cudaStreamWaitEvent(c->side_stream, c->ev_fork, 0));
+  }
   for (const SumLaunch& L : launches) {
     kde::LaunchCfg cfg;
     cfg.X = w.Y; cfg.n = n; cfg.ld = ld; cfg.tile_begin = tb; cfg.tile_end = te; cfg.tile = T;
@@ -408,8 +422,9 @@ kde_status run_sums(kde_ctx* c, int d, int64_t n, int64_t ld, int T, int scale, 
     cfg.skip_s = L.skip_s;
     if (c->profiling && L.skip_s < __builtin_inff()) cfg.skipped = lscv_skipped;
     cfg.work = work + (&L - launches.data());
+    if (two && ((&L - launches.data()) & 1)) cfg.stream = c->side_stream;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (c->profiling) { e0 = next_event(c); e1 = next_event(c); cudaEventRecord(e0, c->stream); }
+    if (c->profiling && !two) { e0 = next_event(c); e1 = next_event(c); cudaEventRecord(e0, c->stream); }
     cudaError_t err = cudaSuccess;
     switch (L.kind) {
       case Kind::Psi4: case Kind::Psi6: case Kind::Psi8: err = kde::launch_psi(L.r, cfg, L.psi); break;
@@ -419,10 +434,15 @@ kde_status run_sums(kde_ctx* c, int d, int64_t n, int64_t ld, int T, int scale, 
     if (err != cudaSuccess) return fail(c, KDE_E_CUDA, "pair kernel launch: %s", cudaGetErrorString(err));
     if (tb < te) c->prof_all += 1;
     if (c->profiling) {
-      cudaEventRecord(e1, c->stream);
+      if (!two) cudaEventRecord(e1, c->stream);
       c->prof_launches++;
       c->prof_evals += pairs * (double)L.nb * (double)L.n_sets;
     }
+  }
+  if (two) {
+    CUDA_TRY(c, cudaEventRecord(c->ev_join, c->side_stream));
+    CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+    if (c->profiling) CUDA_TRY(c, cudaEventRecord(span1, c->stream));
   }
   if (allreduce) TRY(allreduce_limbs(c, w.limbs, (size_t)n_out * kde::kLimbs));
   // one device-to-host copy of [prep flags .. limbs): the workspace places the limbs right after
@@ -546,6 +566,9 @@ void kde_destroy(kde_ctx* c) {
   if (c->nm_ws) cudaFree(c->nm_ws);
   if (c->nm_host) cudaFreeHost(c->nm_host);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
+  if (c->side_stream) cudaStreamDestroy(c->side_stream);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
   if (c->comm) nccl().CommDestroy(c->comm);
   if (c->own_ws) cudaFree(c->own_ws);
   if (c->sort_ws) cudaFree(c->sort_ws);
