@@ -288,7 +288,9 @@ kde_status kde_last_profile(const kde_ctx *ctx, int32_t *launches, double *pair_
  * sums could exceed 1e-5 on g) is re-run with fp64 terms; mode 1 re-runs every candidate.  Nelder-Mead
  * searches use fp32 terms in modes 0 and -1 (host and device loops decide identically); in mode 1 the
  * search runs on the host loop with fp64 terms for every g(H) (the exact-parity search).  kde_raw_sums
- * always returns fp32-term sums.
+ * always returns fp32-term sums.  The fp32-term passes skip far tiles whose terms are provably
+ * negligible (kde_psi_skip_gap, kde_lscv_skip_theta: at most 1e-9 |Psi-hat| resp. 5.9e-11 (1 + kappa') |g|);
+ * the fp64-term passes skip only tiles whose terms are exactly 0.
  * Results stay deterministic and partition-invariant in every mode. */
 kde_status kde_set_precision(kde_ctx *ctx, int32_t fp64_terms);
 /* Number of Psi passes and LSCV candidates of the last call that were (re-)run with fp64 terms, and
