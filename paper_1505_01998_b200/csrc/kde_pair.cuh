@@ -457,7 +457,7 @@ __device__ __forceinline__ void pair_unit(const Args& a, const typename F::Param
     }
     f.load_rows_c(a.Y64, row_origin<F>(q), a.centres[l]);
   } else {
-    if (skip) {   // LSCV far tile (lscv_tile_skipped, decided at issue: a plain arrival, no TMA)
+    if (skip) {   // LSCV far tile (lscv_tile_skipped, decided when the unit's TMA was issued)
       if (threadIdx.x == 0 && a.skipped != nullptr) {
         const int64_t c1 = a.n - l * (int64_t)T;
         atomicAdd(a.skipped, (unsigned long long)(T * (c1 < T ? c1 : T)));
@@ -517,7 +517,6 @@ __global__ void __launch_bounds__(F::NT, F::MINB) pair_kernel(const Args a,
     int64_t l, q;
     tile_coords(shard_tile(a.tile_begin + u / CS, a.part_rank, a.part_world), l, q);
     s_skip[buf] = lscv_tile_skipped<F>(a, a.X, l, q);
-    if (s_skip[buf]) { mbar_arrive(&bar[buf]); return; }   // a skipped tile needs no column data
     float* dst = cols + buf * D * T;
     mbar_expect_tx(&bar[buf], (uint32_t)(D * T * sizeof(float)));
 #pragma unroll
@@ -574,7 +573,6 @@ __global__ void __launch_bounds__(F::NT, F::MINB) pair_kernel_sets(const Args a,
     tile_coords(shard_tile(a.tile_begin + (u - set * per), a.part_rank, a.part_world), l, q);
     const float* Xs = a.X + set * a.set_stride;
     s_skip[buf] = lscv_tile_skipped<F>(a, Xs, l, q);
-    if (s_skip[buf]) { mbar_arrive(&bar[buf]); return; }   // a skipped tile needs no column data
     float* dst = cols + buf * D * T;
     mbar_expect_tx(&bar[buf], (uint32_t)(D * T * sizeof(float)));
 #pragma unroll

@@ -394,7 +394,8 @@ kde_status run_sums(kde_ctx* c, int d, int64_t n, int64_t ld, int T, int scale, 
   // Several launches (LSCV_h candidate batches): alternate two streams, so that launch k+1's CTAs take the
   // SM slots launch k's CTAs free during its tail (its last units; the outputs and the scheduling
   // counters of the launches are disjoint).  Profiling then times the whole span as one window.
-  static const bool one_stream = [] { const char* e = getenv("KDE_DEBUG_ONE_STREAM"); return e && atoi(e) == 1; }();
+  const char* one_env = getenv("KDE_DEBUG_ONE_STREAM");   // A/B and tests: read at every call
+  const bool one_stream = one_env && atoi(one_env) == 1;
   const bool two = launches.size() >= 2 && !one_stream && !(c->cap_stream && c->stream == c->cap_stream);
   cudaEvent_t span0 = nullptr, span1 = nullptr;
   if (two) {

@@ -575,6 +575,18 @@ def test_lscv_far_tile_skip_is_exact(ctx, which):
             assert 0.0 <= y - x <= pairs * 2.0 ** (-p * theta) * 1.0001, (which, k, j, x, y)
 
 
+def test_lscv_h_two_stream_launches_are_bit_identical(ctx):
+    # A pass of several LSCV_h batch launches alternates two streams (run_sums); the outputs and the
+    # scheduling counters of the launches are disjoint, so the bits equal the one-stream pass.
+    X = dev(datagen.sample_mixture("bimodal", 12007, 9))
+    hs = np.geomspace(0.005, 1.5, 45)   # 6 launches of 8
+    a = ctx.raw_sums(kb.SUM_LSCV_h, X, hs)
+    with _env(KDE_DEBUG_ONE_STREAM=1):
+        b = ctx.raw_sums(kb.SUM_LSCV_h, X, hs)
+    assert [f.key() for f in a] == [f.key() for f in b]
+    np.testing.assert_array_equal(ctx.lscv_h_scores(X, hs), ctx.lscv_h_scores(X, hs))
+
+
 def test_lscv_h_candidate_order_invariance(ctx):
     # Candidates are batched in ascending h (the batch's widest h bounds its far-tile skip); each
     # candidate's sums are the same bits whatever order or company it is given in.
