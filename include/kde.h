@@ -246,9 +246,9 @@ kde_fixed kde_fixed_add(kde_fixed a, kde_fixed b);
  *   variance var >= 0 (Eq. 11).  The skipped terms sum to at most 1e-9 |Psi-hat_r(g)| (a lower bound on
  *   |Psi-hat_r(g)| = R(f^(r/2)) over densities of f's variance, Terrell's maximal smoothing); 13 (only
  *   tiles whose fp32 terms are all exactly 0) when no smaller tau guarantees that, and for bad arguments.
- * kde_lscv_skip_theta: theta = min(130, log2 n + 34); an LSCV tile whose pairs all have terms
+ * kde_lscv_skip_theta: theta = min(130, log2 n + 30); an LSCV tile whose pairs all have terms
  *   e = exp(-S/(4h^2)) <= 2^-theta (Eq. 24/30) is skipped, which moves g(h) / g(H)
- *   by at most 5.9e-11 (1 + kappa') |g|, kappa' = (A + B)/|g| its cancellation (<= 32 on fp32 terms). */
+ *   by at most 9.4e-10 (1 + kappa') |g|, kappa' = (A + B)/|g| its cancellation (<= 32 on fp32 terms). */
 double kde_psi_skip_gap(int32_t r, double g, double var);
 double kde_lscv_skip_theta(int64_t n);
 
@@ -289,7 +289,7 @@ kde_status kde_last_profile(const kde_ctx *ctx, int32_t *launches, double *pair_
  * searches use fp32 terms in modes 0 and -1 (host and device loops decide identically); in mode 1 the
  * search runs on the host loop with fp64 terms for every g(H) (the exact-parity search).  kde_raw_sums
  * always returns fp32-term sums.  The fp32-term passes skip far tiles whose terms are provably
- * negligible (kde_psi_skip_gap, kde_lscv_skip_theta: at most 1e-9 |Psi-hat| resp. 5.9e-11 (1 + kappa') |g|);
+ * negligible (kde_psi_skip_gap, kde_lscv_skip_theta: at most 1e-9 |Psi-hat| resp. 9.4e-10 (1 + kappa') |g|);
  * the fp64-term passes skip only tiles whose terms are exactly 0.
  * Results stay deterministic and partition-invariant in every mode. */
 kde_status kde_set_precision(kde_ctx *ctx, int32_t fp64_terms);

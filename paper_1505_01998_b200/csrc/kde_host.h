@@ -177,7 +177,7 @@ kde_status gpu_sorted_rows(kde_ctx* c, const double* X, int64_t n, int d, const 
 // Skip bound on s for LSCV sums: every term exp2(s * kappa) with s * |kappa| > 130 is exactly 0
 // (ex2.approx.ftz flushes results below 2^-126); +inf when KDE_DEBUG_LSCV_NOSKIP=1.
 // Far-tile bound on s for terms 2^(kappa s), |kappa| >= min_abs_kappa, at n samples: 130/|kappa| (every
-// term exactly 0) or, bounded skip (default), min(130, log2 n + 34)/|kappa| (kde_internal.h);
+// term exactly 0) or, bounded skip (default), min(130, log2 n + 30)/|kappa| (kde_internal.h);
 // +inf under KDE_DEBUG_LSCV_NOSKIP=1.
 float lscv_skip_s(double min_abs_kappa, int64_t n);
 kde_status gpu_prep_into(kde_ctx* c, const double* X, int64_t n, int d, const std::vector<double>& W,

@@ -65,8 +65,9 @@ double psi_skip_gap(bool fp64);
 //   psi_bounded_gap returns a tau <= kPsiSkipGap32 that makes this <= kSkipEps (the smallest, from
 //   above, to Newton's accuracy).
 //   LSCV (Eq. 24/30, g = A - B + C, C = c4/n the diagonal term): every dropped term e <= 2^-theta, at
-//   most n^2/2 of them, so |dA| <= c4 2^-theta = C n 2^-theta; theta = log2 n + 34 (lscv_skip_theta)
-//   gives |dA| <= 2^-34 C <= 5.9e-11 (1 + kappa') |g|, kappa' = (A + B)/|g|.
+//   most n^2/2 of them, so |dA| <= c4 2^-theta = C n 2^-theta; theta = log2 n + 30 (lscv_skip_theta)
+//   gives |dA| <= 2^-30 C <= 9.4e-10 (1 + kappa') |g|, kappa' = (A + B)/|g|: at most 0.6% of the
+//   fp32 terms' own ~1.5e-7 kappa'.
 // KDE_DEBUG_SKIP_EXACT=1 keeps only the exact-zero skips (bit-identical to no skip at all).
 constexpr double kSkipEps = 1e-9;
 #ifdef __CUDACC__

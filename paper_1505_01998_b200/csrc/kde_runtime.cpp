@@ -666,7 +666,7 @@ double kde_psi_skip_gap(int32_t r, double g, double var) {
   return (r == 4 || r == 6 || r == 8) ? kde::psi_bounded_gap(r, g, var) : kde::kPsiSkipGap32;
 }
 
-double kde_lscv_skip_theta(int64_t n) { return std::min(130.0, std::log2((double)std::max<int64_t>(n, 2)) + 34.0); }
+double kde_lscv_skip_theta(int64_t n) { return std::min(130.0, std::log2((double)std::max<int64_t>(n, 2)) + 30.0); }
 
 int64_t kde_shard_tile(int64_t i, int32_t rank, int32_t world) {
   return (world < 1 || rank < 0 || rank >= world || i < 0) ? -1 : kde::shard_tile(i, rank, world);

@@ -539,7 +539,7 @@ def test_lscv_far_tile_skip_is_exact(ctx, which):
     # LSCV data are sorted by coordinate 0 (whitening keeps that order); a tile whose coordinate-0 gap
     # bounds every s above the exact skip bound has every MUFU term exactly 0 (and every software-exp
     # term at 2^-125, far below the fixed-point resolution), so skipping it changes no output bit
-    # (KDE_DEBUG_SKIP_EXACT=1).  The default bounded skip (theta = min(130, log2 n + 34))
+    # (KDE_DEBUG_SKIP_EXACT=1).  The default bounded skip (theta = min(130, log2 n + 30))
     # moves each raw sum by at most n(n-1)/2 2^-theta (S1) and n(n-1)/2 2^-2theta (S2).
     d = int(which[1])
     if which[0] == "h":
@@ -567,7 +567,7 @@ def test_lscv_far_tile_skip_is_exact(ctx, which):
     assert evaluated < (0.9 if d <= 4 else 1.0) * full        # the small bandwidths skip tiles
     assert ev_bounded <= evaluated
     theta = kb.lscv_skip_theta(n)
-    assert theta == min(130.0, math.log2(n) + 34)
+    assert theta == min(130.0, math.log2(n) + 30)
     pairs = n * (n - 1) / 2
     for k in range(ncand):
         for j, p in ((0, 1.0), (1, 2.0)):

@@ -42,7 +42,7 @@ ctx.set_precision(1)
 print("fp64 lscv", ctx.lscv_h_scores(X, [0.3]), ctx.lscv_H_scores(X3, [datagen.vech(np.eye(3) * 0.05)]))
 ctx.set_precision(0)
 print("select H device loop", ctx.select_bandwidth(kb.LSCV_H, X, max_iter=40)["objective"])
-# round 2, second part: bounded far-tile skip (Psi tau from g/sigma, LSCV theta = log2 n + 34, per-candidate
+# round 2, second part: bounded far-tile skip (Psi tau from g/sigma, LSCV theta = log2 n + 30, per-candidate
 # tile bound inside an LSCV_h batch) and multi-launch passes on two streams (24 h = 3 launches)
 print("lscv_h two streams + per-candidate skip", ctx.lscv_h_scores(Xb, np.geomspace(0.003, 1.0, 24))[[0, 23]])
 print("psi bounded skip", ctx.psi_r(x, 4, [0.02, 0.3]))
