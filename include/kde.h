@@ -297,6 +297,12 @@ kde_status kde_set_precision(kde_ctx *ctx, int32_t fp64_terms);
  * the largest cancellation estimate kappa of its fp32-term Psi passes (diagnostics). */
 int32_t kde_last_fp64_passes(const kde_ctx *ctx);
 double kde_last_psi_kappa(const kde_ctx *ctx);
+/* Far-tile skip thresholds (in units of g, on the sorted gap) of the last call's fp32-term Psi passes, in
+ * pass order: the data-aware bounded threshold (the smallest tau of the grid
+ * 6, 6.25, ..., 12.75 whose skipped tiles provably move Psi-hat by at most 1e-9 relative, never above
+ * kde_psi_skip_gap), 13 under KDE_DEBUG_SKIP_EXACT=1, inf under KDE_DEBUG_PSI_NOSKIP=1.  Writes at most
+ * `max` values to out (host) and returns the number of passes (diagnostics). */
+int32_t kde_last_psi_gaps(const kde_ctx *ctx, double *out, int32_t max);
 /* Turn per-launch event timing on/off (default off; adds an event pair per launch). */
 kde_status kde_set_profiling(kde_ctx *ctx, int32_t on);
 

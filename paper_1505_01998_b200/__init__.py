@@ -36,7 +36,7 @@ EXPORTS = ["kde_create", "kde_destroy", "kde_last_error", "kde_nccl_unique_id",
            "kde_raw_sums", "kde_fixed_value", "kde_fixed_add", "kde_tile_coords",
            "kde_last_profile", "kde_set_profiling", "kde_shard_tiles", "kde_shard_tile", "kde_psi_skip_gap", "kde_lscv_skip_theta", "kde_evaluate", "kde_aqp_1d",
            "kde_lscv_h_scores_materialized", "kde_last_aux_ms", "kde_set_host_allreduce", "kde_set_precision",
-           "kde_last_fp64_passes", "kde_last_psi_kappa"]
+           "kde_last_fp64_passes", "kde_last_psi_kappa", "kde_last_psi_gaps"]
 
 
 class KDEError(RuntimeError):
@@ -133,6 +133,8 @@ def lib():
     L.kde_last_fp64_passes.restype = i32
     L.kde_last_psi_kappa.argtypes = [vp]
     L.kde_last_psi_kappa.restype = f64
+    L.kde_last_psi_gaps.argtypes = [vp, dp, i32]
+    L.kde_last_psi_gaps.restype = i32
     L.kde_set_host_allreduce.argtypes = [vp, HOST_ALLREDUCE_FN, vp]
     L.kde_set_host_allreduce.restype = ctypes.c_int
     for f in ("kde_create", "kde_nccl_unique_id", "kde_set_workspace", "kde_psi_r", "kde_plugin_h",
@@ -341,6 +343,12 @@ class Context:
     def last_psi_kappa(self) -> float:
         """Largest cancellation estimate 2A/|2S + n He_r(0)| of the last call's fp32 Psi passes."""
         return float(lib().kde_last_psi_kappa(self._h))
+
+    def last_psi_gaps(self):
+        """Far-tile skip thresholds of the last call's fp32-term Psi passes (kde_last_psi_gaps)."""
+        buf = (ctypes.c_double * 8)()
+        cnt = lib().kde_last_psi_gaps(self._h, buf, 8)
+        return [buf[k] for k in range(min(cnt, 8))]
 
     def set_profiling(self, on: bool):
         self._check(lib().kde_set_profiling(self._h, 1 if on else 0))

@@ -99,6 +99,7 @@ struct kde_ctx {
   // Psi passes re-run with fp64 terms by the automatic precision during the last call
   int32_t psi_escalations = 0;
   double psi_kappa_max = 0.0;   // largest cancellation estimate of the last call's fp32 Psi passes
+  std::vector<double> psi_gaps;  // far-tile skip thresholds of the last call's fp32 Psi passes
 };
 
 namespace kde {
@@ -207,6 +208,7 @@ struct SumLaunch {
   const float* centres = nullptr;   // Psi: per-column-tile centres
   unsigned long long* skipped = nullptr;   // Psi: skipped-pair counter
   double skip_gap = kPsiSkipGap32;         // Psi: exact-zero tile skip threshold
+  const double* skip_gap_dev = nullptr;    // Psi: the threshold in device memory (data-aware selection)
   float skip_s = __builtin_inff();         // LSCV on sorted data: exact-zero tile skip bound on s
   int n_sets = 1;                   // LSCV_H: candidates (one data set each), n_out per set
   int64_t set_stride = 0;

@@ -75,12 +75,21 @@ constexpr double kSkipEps = 1e-9;
 #else
 #define KDE_HDI inline
 #endif
-KDE_HDI double psi_bounded_gap(int r, double g, double var) {
-  if (!(g > 0.0) || !(var >= 0.0) || !(var < 1e300) || !(g < 1e150)) return kPsiSkipGap32;
+// log of the per-pair target kSkipEps sqrt(2 pi) R*_{r/2} q^{(r+1)/2}, q = g^2/(var + g^2/2): n^2 times the
+// target is kSkipEps times Terrell's lower bound on |2S + n He_r(0)| = n^2 g^{r+1} sqrt(2 pi) |Psi-hat_r(g)|.
+KDE_HDI double psi_skip_log_target(int r, double g, double var) {
   const double Rs = r == 4 ? 35.0 / 243.0
                            : (r == 6 ? 14175.0 * sqrt(11.0) / 161051.0 : 1091475.0 * sqrt(13.0) / 4826809.0);
   const double q = g * g / (var + 0.5 * g * g);
-  const double lt = log(kSkipEps * 2.5066282746310002 * Rs) + 0.5 * (r + 1) * log(q);   // log of the target
+  return log(kSkipEps * 2.5066282746310002 * Rs) + 0.5 * (r + 1) * log(q);
+}
+KDE_HDI bool psi_skip_args_ok(double g, double var) {
+  return g > 0.0 && var >= 0.0 && var < 1e300 && g < 1e150;
+}
+// Closed form (data-independent): every one of the n^2/2 pairs could sit at u = tau.
+KDE_HDI double psi_bounded_gap(int r, double g, double var) {
+  if (!psi_skip_args_ok(g, var)) return kPsiSkipGap32;
+  const double lt = psi_skip_log_target(r, g, var);
   // f(tau) = r log tau - tau^2/2 - lt is concave and decreasing for tau > sqrt(r): Newton from the right
   // of the root stays right of it (tangents lie above a concave f), so every iterate satisfies f <= 0.
   double t = kPsiSkipGap32;
@@ -89,10 +98,23 @@ KDE_HDI double psi_bounded_gap(int r, double g, double var) {
     const double f = r * log(t) - 0.5 * t * t - lt, fp = r / t - t;
     const double tn = t - f / fp;
     if (!(tn < t) || tn < 6.0) break;
+    const bool done = t - tn < 1e-9;   // quadratic convergence: 4-5 steps from 13
     t = tn;
+    if (done) break;
   }
   return t;
 }
+// Data-aware threshold: one CTA bounds, for each tau of the grid 6, 6.25, ..., 12.75, the
+// terms of the tiles a pass would skip, sum over tiles (l, q < l) with sorted gap > tau of
+// 2 T cols(l) gap^r e^{-gap^2/2} (each pair of such a tile has u >= gap >= 6), and writes to *out the
+// smallest tau whose bound is at most n^2 e^{psi_skip_log_target} (kSkipEps of Terrell's lower bound), or
+// the closed form psi_bounded_gap if that is smaller.  y = the pass's sorted scaled samples (launch_psi_prep),
+// g and var from device memory (g_dev, var_dev) or the values.  Deterministic (fixed order).
+cudaError_t launch_psi_gap_select(int r, const double* y, int64_t n, int T, const double* g_dev, double g_val,
+                                  const double* var_dev, double var_val, double* out, cudaStream_t s);
+// Below this many tiles per side the selection is not run (a few tiles hardly skip; small-n latency) and
+// the pass keeps the exact-zero threshold.
+constexpr int64_t kGapSelectMinTiles = 16;
 // Psi skip threshold of one pass: bounded (default), exact-zero (KDE_DEBUG_SKIP_EXACT=1) or none
 // (KDE_DEBUG_PSI_NOSKIP=1).  Host only (reads the environment at every call).
 double psi_skip_gap_for(int r, double g, double var);

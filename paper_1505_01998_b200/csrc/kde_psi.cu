@@ -405,6 +405,63 @@ __device__ __forceinline__ void set_status(double* st, int code) {
   if (st[0] == 0.0) st[0] = (double)code;   // first failure wins
 }
 
+// Data-aware bounded-skip threshold (kde_internal.h launch_psi_gap_select).
+constexpr int kGapCands = 28;   // tau_c = 6 + c/4 < 13
+__global__ void __launch_bounds__(256) psi_gap_select_kernel(int r, const double* __restrict__ y, int64_t n, int T,
+                                                              const double* g_dev, double g_val,
+                                                              const double* var_dev, double var_val, double* out) {
+  __shared__ double red[8][kGapCands];
+  const double g = g_dev != nullptr ? *g_dev : g_val, var = var_dev != nullptr ? *var_dev : var_val;
+  double acc[kGapCands];
+#pragma unroll
+  for (int c = 0; c < kGapCands; ++c) acc[c] = 0.0;
+  const int64_t nt = (n + T - 1) / T, tiles = nt * (nt + 1) / 2;
+  for (int64_t id = threadIdx.x; id < tiles; id += blockDim.x) {   // fixed per-thread order
+    int64_t l, q;
+    tile_coords(id, l, q);
+    if (q >= l) continue;
+    const double gap = y[l * T] - y[q * T + T - 1];   // the Psi kernel's skip test (pair_unit)
+    if (!(gap > 6.0)) continue;
+    const int64_t cols = n - l * T < T ? n - l * T : T;
+    const double b = 2.0 * (double)T * (double)cols * exp((double)r * log(gap) - 0.5 * gap * gap);
+#pragma unroll
+    for (int c = 0; c < kGapCands; ++c)
+      if (gap > 6.0 + 0.25 * c) acc[c] += b;
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int c = 0; c < kGapCands; ++c) {
+    double v = acc[c];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[wid][c] = v;
+  }
+  __syncthreads();
+  __shared__ int ok[kGapCands];
+  if (threadIdx.x < kGapCands) {   // one candidate per thread: its warp partials in fixed order
+    double v = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v += red[w][threadIdx.x];
+    const double lim = (double)n * (double)n * exp(psi_skip_log_target(r, g, var));
+    ok[threadIdx.x] = psi_skip_args_ok(g, var) && v * (1.0 + 1e-9) <= lim;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tau = psi_bounded_gap(r, g, var);
+    for (int c = 0; c < kGapCands; ++c)
+      if (ok[c]) {   // acc is non-increasing in c: the first admissible candidate is the smallest tau
+        tau = fmin(tau, 6.0 + 0.25 * c);
+        break;
+      }
+    *out = tau;
+  }
+}
+
+cudaError_t launch_psi_gap_select(int r, const double* y, int64_t n, int T, const double* g_dev, double g_val,
+                                  const double* var_dev, double var_val, double* out, cudaStream_t s) {
+  psi_gap_select_kernel<<<1, 256, 0, s>>>(r, y, n, T, g_dev, g_val, var_dev, var_val, out);
+  return cudaGetLastError();
+}
+
 // stage 0: mean = sum / n.  stage 1: V-hat, sigma-hat, Psi8^NS, g1 (steps 1-4), W = 1/g1.
 // stage 4 (5): after the fp32-term Psi6 (Psi4) pass, decide whether it is re-run with fp64 terms
 // (gate): psi_mode 1 always, 0 when kappa = 2A / |2S + n He_r(0)| > kPsiKappaMax, -1 never.
@@ -429,7 +486,7 @@ __global__ void plugin_chain_kernel(int stage, int64_t n, double* small, const u
     const double K6_0 = -15.0 / s2p;
     t[3] = pow(-2.0 * K6_0 / (t[2] * nn), 1.0 / 9.0);                      // Eq. 14
     dv.W[0] = 1.0 / t[3];
-    small[kGapSlot] = psi_bounded_gap(6, t[3], V);                         // bounded skip (§3.11)
+    small[kGapSlot] = psi_bounded_gap(6, t[3], V);   // closed-form skip bound (§3.11; refined by the selection)
   } else if (stage == 4 || stage == 5) {
     const int k = stage - 4;                                               // 0: Psi6, 1: Psi4
     const unsigned long long* L = limbs + (size_t)(2 * k) * kLimbs;

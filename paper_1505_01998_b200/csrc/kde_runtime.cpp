@@ -321,6 +321,7 @@ void prof_reset(kde_ctx* c) {
   c->ev_excl.clear();
   c->psi_escalations = 0;
   c->psi_kappa_max = 0.0;
+  c->psi_gaps.clear();
   c->prof_launches = 0;
   c->prof_all = 0;
   c->prof_ms = 0.0;
@@ -420,6 +421,7 @@ kde_status run_sums(kde_ctx* c, int d, int64_t n, int64_t ld, int T, int scale, 
     cfg.centres = L.centres;
     cfg.skipped = L.skipped;
     cfg.skip_gap = L.skip_gap;
+    cfg.skip_gap_dev = L.skip_gap_dev;
     cfg.skip_s = L.skip_s;
     if (c->profiling && L.skip_s < __builtin_inff()) cfg.skipped = lscv_skipped;
     cfg.work = work + (&L - launches.data());
@@ -618,6 +620,13 @@ kde_status kde_set_host_allreduce(kde_ctx* c, kde_host_allreduce_fn fn, void* us
 int32_t kde_last_fp64_passes(const kde_ctx* c) { return c ? c->psi_escalations : 0; }
 
 double kde_last_psi_kappa(const kde_ctx* c) { return c ? c->psi_kappa_max : 0.0; }
+
+int32_t kde_last_psi_gaps(const kde_ctx* c, double* out, int32_t max) {
+  if (!c) return 0;
+  const int32_t cnt = (int32_t)c->psi_gaps.size();
+  for (int32_t k = 0; k < cnt && k < max && out; ++k) out[k] = c->psi_gaps[k];
+  return cnt;
+}
 
 kde_status kde_set_profiling(kde_ctx* c, int32_t on) {
   if (!c) return KDE_E_INVALID;

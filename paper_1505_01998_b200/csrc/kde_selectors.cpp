@@ -121,10 +121,23 @@ kde_status psi_raw(kde_ctx* c, const double* x, int64_t n, int r, const double* 
       L.kind = psi_kind(r); L.r = r; L.nb = 1; L.out_offset = 0; L.n_out = 2;
       L.X = b.Yc; L.Y64 = b.Y64; L.centres = b.centres;
       L.skipped = reinterpret_cast<unsigned long long*>(w.small + kde::kSkippedSlot);
-      L.skip_gap = kde::psi_skip_gap_for(r, g[k], m.cov.empty() ? 0.0 : m.cov[0]);
+      const double var = m.cov.empty() ? 0.0 : m.cov[0];
+      L.skip_gap = kde::psi_skip_gap_for(r, g[k], var);
+      const bool select = L.skip_gap < INFINITY && kde::skip_bounded() && (n + T - 1) / T >= kde::kGapSelectMinTiles;
+      if (select) {   // data-aware threshold on the device, read by the pass
+        CUDA_TRY(c, kde::launch_psi_gap_select(r, b.Y64, n, T, nullptr, g[k], nullptr, var, w.small + kde::kGapSlot,
+                                               c->stream));
+        c->prof_all += 1;
+        L.skip_gap_dev = w.small + kde::kGapSlot;
+      }
       psi_coeffs(r, L.psi);
       std::vector<kde_fixed> o;
       TRY(run_sums(c, 1, n, ld, T, S, w, {L}, 2, shard_rank, shard_world, allreduce, o));
+      {   // run_sums copied the small block's tail (prep flags .. limbs) to the host
+        double gap = L.skip_gap;
+        if (L.skip_gap_dev) std::memcpy(&gap, c->h_limbs + (kde::kGapSlot - 408), sizeof(gap));
+        c->psi_gaps.push_back(gap);
+      }
       if (c->profiling) {   // run_sums copied the small block's tail with the limbs
         unsigned long long sk = 0;
         std::memcpy(&sk, c->h_limbs + (kde::kSkippedSlot - 408), sizeof(sk));
@@ -386,6 +399,14 @@ kde_status kde_psi_r(kde_ctx* c, const double* x, int64_t n, int32_t r, const do
   return KDE_OK;
 }
 
+// PLUGIN passes read their bounded skip threshold from the chain's small block: the closed form written by
+// the chain stage that produces g (psi_plugin_bounded), replaced by the data-aware one when enough tiles
+// make the selection worth its launch (psi_plugin_select).
+static bool psi_plugin_bounded() { return kde::psi_skip_gap(false) < INFINITY && kde::skip_bounded(); }
+static bool psi_plugin_select(int64_t n, int T) {
+  return psi_plugin_bounded() && (n + T - 1) / T >= kde::kGapSelectMinTiles;
+}
+
 // One fp32-term Psi_r pair pass of the device-resident PLUGIN chain: kernel over this rank's
 // tiles into `limbs` (S, A), then (world > 1) the all-reduce, all enqueued on the context stream.
 static kde_status plugin_pass(kde_ctx* c, int r, int64_t n, int64_t ld, int T, int S, const PsiBufs& b,
@@ -400,8 +421,8 @@ static kde_status plugin_pass(kde_ctx* c, int r, int64_t n, int64_t ld, int T, i
   cfg.clamp = clamp; cfg.Y64 = b.Y64; cfg.centres = b.centres;
   cfg.skipped = skipped;
   cfg.skip_gap = kde::psi_skip_gap(false);
-  // bounded far-tile skip: the chain computed this pass's threshold from g and V-hat (stage 1 / 2)
-  if (cfg.skip_gap < INFINITY && kde::skip_bounded()) cfg.skip_gap_dev = gap_dev;
+  // bounded far-tile skip: the pass's data-aware threshold (launch_psi_gap_select, after the prep)
+  if (psi_plugin_bounded()) cfg.skip_gap_dev = gap_dev;
   cfg.work = work;
   kde::PsiParams p;
   psi_coeffs(r, p);
@@ -459,6 +480,11 @@ static kde_status plugin_enqueue(kde_ctx* c, const double* x, int64_t n, int T, 
   for (int k = 0; k < 2; ++k) {                                                        // Psi6(g1), Psi4(g2)
     const int r = k == 0 ? 6 : 4;
     CUDA_TRY(c, kde::launch_psi_prep(xs, n, dv.mean, dv.W, T, b.Y64, b.Yc, b.centres, ld, st, w.flag(), 3.0e4));
+    if (mode != 1 && psi_plugin_select(n, T)) {   // data-aware threshold
+      CUDA_TRY(c, kde::launch_psi_gap_select(r, b.Y64, n, T, dv.trace + (k == 0 ? 3 : 5), 0.0, dv.trace, 0.0,
+                                             w.small + kde::kGapSlot + k, st));
+      c->prof_all += 1;
+    }
     if (mode != 1)
       TRY(plugin_pass(c, r, n, ld, T, Ss[k], b, w.flag() + 1, L + (size_t)(2 * k) * kde::kLimbs, tb, te, pairs,
                       reinterpret_cast<unsigned long long*>(w.small + kde::kSkippedSlot), work + k,
@@ -545,7 +571,15 @@ static kde_status plugin_impl(kde_ctx* c, const double* x, int64_t n, kde_plugin
   const unsigned long long* gates = flags + 11;
   double kap[2];                                  // small[421..422]
   std::memcpy(kap, c->h_limbs + 13, sizeof(kap));
-  if (c->psi_mode != 1) c->psi_kappa_max = std::max(kap[0], kap[1]);
+  if (c->psi_mode != 1) {
+    c->psi_kappa_max = std::max(kap[0], kap[1]);
+    const double exact = kde::psi_skip_gap(false);
+    for (int k = 0; k < 2; ++k) {
+      double gap = exact;
+      if (psi_plugin_bounded()) std::memcpy(&gap, c->h_limbs + (kde::kGapSlot - 408 + k), sizeof(gap));
+      c->psi_gaps.push_back(gap);
+    }
+  }
   if (c->profiling) {                             // pairs of exactly-zero tiles the kernels skipped
     unsigned long long sk = 0;
     std::memcpy(&sk, c->h_limbs + (kde::kSkippedSlot - 408), sizeof(sk));

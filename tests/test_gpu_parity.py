@@ -481,6 +481,27 @@ def test_psi_far_tile_skip_is_exact(ctx, mode):
         ctx.set_precision(0)
 
 
+def _tile_bound(x, r, g, T, tau):
+    """Sum over tiles (l, q < l) of sorted (x - mean)/g with gap > tau of 2 T cols(l) gap^r e^{-gap^2/2}: the
+    data-aware bound on what a pass with threshold tau drops, in fp64 numpy."""
+    y = (np.sort(x) - np.mean(x)) / g
+    n = y.size
+    nt = -(-n // T)
+    lo = y[::T]
+    hi = y[np.minimum(np.arange(nt) * T + T - 1, n - 1)]
+    cols = np.minimum(T, n - np.arange(nt) * T)
+    gap = lo[:, None] - hi[None, :]
+    m = (np.arange(nt)[None, :] < np.arange(nt)[:, None]) & (gap > tau)
+    gg = gap[m]
+    return float(np.sum(2.0 * T * np.broadcast_to(cols[:, None], gap.shape)[m] * np.exp(r * np.log(gg) - 0.5 * gg * gg)))
+
+
+def _terrell_target(r, g, V, n):
+    Rs = {4: 35 / 243, 6: 14175 * math.sqrt(11) / 161051, 8: 1091475 * math.sqrt(13) / 4826809}[r]
+    q = g * g / (V + 0.5 * g * g)
+    return n * n * 1e-9 * math.sqrt(2 * math.pi) * Rs * q ** ((r + 1) / 2)
+
+
 @pytest.mark.parametrize("case", ["skewed", "normal", "spikes"])
 def test_psi_bounded_skip_within_bound(ctx, case):
     # DESIGN §3.11: the default fp32-term pass also skips tiles beyond tau = kde_psi_skip_gap(r, g, V) < 13;
@@ -501,6 +522,18 @@ def test_psi_bounded_skip_within_bound(ctx, case):
             gs = [0.02 * sd, 0.1 * sd, 0.3 * sd]
             a = ctx.raw_sums(kind, Xd, gs)
             ev_b = ctx.last_profile()["pair_evals"]
+            taus = ctx.last_psi_gaps()
+            T = kb.shard_tiles(kind, n, 1, 0, 1)[0]
+            assert len(taus) == len(gs)
+            for g, tau in zip(gs, taus):
+                # the data-aware threshold: on the grid 6 + k/4 or the closed form, never above it, and its
+                # skipped tiles within the bound (fp64 numpy; the grid point below it is not admissible)
+                cf = kb.psi_skip_gap(r, g, V)
+                assert tau <= cf and (tau == cf or abs(tau * 4 - round(tau * 4)) < 1e-12), (tau, cf)
+                lim = _terrell_target(r, g, V, n)
+                assert _tile_bound(X[0], r, g, T, tau) <= lim * (1 + 1e-6)
+                if tau < cf and tau > 6.0:
+                    assert _tile_bound(X[0], r, g, T, tau - 0.25) > lim * (1 - 1e-6)
             with _env(KDE_DEBUG_SKIP_EXACT=1):
                 e = ctx.raw_sums(kind, Xd, gs)
                 ev_e = ctx.last_profile()["pair_evals"]
@@ -530,6 +563,15 @@ def test_plugin_bounded_skip(ctx):
         ev2 = ctx.last_profile()["pair_evals"]
     for k in ("psi6", "g2", "psi4"):
         assert rel(tr[k], tr2[k]) <= 3e-9, (k, tr[k], tr2[k])
+    V = tr["V_hat"]
+    h3, tr3 = ctx.plugin_h(Xd)
+    taus = ctx.last_psi_gaps()
+    assert len(taus) == 2 and h3 == h
+    n = X.shape[1]
+    T = kb.shard_tiles(kb.SUM_PSI6, n, 1, 0, 1)[0]
+    for tau, r, g in zip(taus, (6, 4), (tr["g1"], tr["g2"])):
+        assert tau <= kb.psi_skip_gap(r, g, V) + 1e-12
+        assert _tile_bound(X[0], r, g, T, tau) <= _terrell_target(r, g, V, n) * (1 + 1e-6)
     assert rel(h, h2) <= 1e-9
     assert ev < 0.95 * ev2, (ev, ev2)
 
