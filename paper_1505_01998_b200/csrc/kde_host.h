@@ -210,6 +210,7 @@ struct SumLaunch {
   double skip_gap = kPsiSkipGap32;         // Psi: exact-zero tile skip threshold
   const double* skip_gap_dev = nullptr;    // Psi: the threshold in device memory (data-aware selection)
   float skip_s = __builtin_inff();         // LSCV on sorted data: exact-zero tile skip bound on s
+  const float* skip_s_sets = nullptr;      // LSCV_H sets: per-set data-aware bounds (device), or null
   int n_sets = 1;                   // LSCV_H: candidates (one data set each), n_out per set
   int64_t set_stride = 0;
 };

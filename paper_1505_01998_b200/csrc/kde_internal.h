@@ -112,6 +112,13 @@ KDE_HDI double psi_bounded_gap(int r, double g, double var) {
 // g and var from device memory (g_dev, var_dev) or the values.  Deterministic (fixed order).
 cudaError_t launch_psi_gap_select(int r, const double* y, int64_t n, int T, const double* g_dev, double g_val,
                                   const double* var_dev, double var_val, double* out, cudaStream_t s);
+// LSCV_H sets, data-aware bounded skip: one CTA per prepared set (whitened coordinate
+// 0 at X + s * set_stride, sorted) bounds what a pass drops for each theta of the grid theta_cf,
+// theta_cf - 1, ..., 8 — sum over tiles (l, q < l) with fp32(g^2) > theta of T cols(l) 2^-fp32(g^2), the
+// pair kernel's own skip test — and writes to out[s] the smallest theta whose bound is at most
+// n(n-1)/2 2^-theta_cf (the closed form's worst case, so the objective bound is unchanged).
+cudaError_t launch_lscv_sets_skip_select(const float* X, int64_t set_stride, int n_sets, int64_t n, int T,
+                                         float theta_cf, float* out, cudaStream_t s);
 // Below this many tiles per side the selection is not run (a few tiles hardly skip; small-n latency) and
 // the pass keeps the exact-zero threshold.
 constexpr int64_t kGapSelectMinTiles = 16;
@@ -155,6 +162,7 @@ struct LaunchCfg {
   // fp32(x_{lT} - x_{qT+T-1})^2 > skip_s, a lower bound on every s of its pairs under which every
   // term is exactly 0 (lscv_skip_s; +inf = never).  `skipped` then counts the skipped pairs.
   float skip_s = __builtin_inff();
+  const float* skip_s_sets = nullptr;   // LSCV_H sets: per-set bounds (launch_lscv_sets_skip_select), or null
   // Programmatic dependent launch (the device-resident Nelder–Mead graph): the kernel may start while
   // the previous one finishes and waits for it (griddepcontrol.wait) before reading its outputs.
   bool pdl = false;

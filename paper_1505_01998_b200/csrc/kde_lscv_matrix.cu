@@ -54,4 +54,62 @@ cudaError_t launch_lscv_white(int d, const LaunchCfg& c) {
   return cudaErrorInvalidValue;
 }
 
+// Data-aware bounded skip for LSCV_H sets (kde_internal.h launch_lscv_sets_skip_select).
+constexpr int kThetaCands = 48;   // theta_c = theta_cf - c, c < 48, not below 8
+__global__ void __launch_bounds__(256) lscv_sets_skip_select_kernel(const float* __restrict__ X, int64_t set_stride,
+                                                                    int64_t n, int T, float theta_cf,
+                                                                    float* __restrict__ out) {
+  __shared__ double red[8][kThetaCands];
+  __shared__ int ok[kThetaCands];
+  const float* Xs = X + (int64_t)blockIdx.x * set_stride;   // the set's whitened coordinate 0 (sorted)
+  double acc[kThetaCands];
+#pragma unroll
+  for (int c = 0; c < kThetaCands; ++c) acc[c] = 0.0;
+  const int64_t nt = (n + T - 1) / T, tiles = nt * (nt + 1) / 2;
+  for (int64_t id = threadIdx.x; id < tiles; id += blockDim.x) {   // fixed per-thread order
+    int64_t l, q;
+    tile_coords(id, l, q);
+    if (q >= l) continue;
+    const float g = __fsub_rn(Xs[l * T], Xs[q * T + T - 1]);   // lscv_tile_skipped's test, exactly
+    const float g2 = __fmul_rn(g, g);
+    if (!(g2 > 8.0f)) continue;
+    const int64_t cols = n - l * T < T ? n - l * T : T;
+    const double b = (double)T * (double)cols * exp2(-(double)g2);   // every term e = 2^-s, s >= g2
+#pragma unroll
+    for (int c = 0; c < kThetaCands; ++c)
+      if (g2 > theta_cf - (float)c) acc[c] += b;
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int c = 0; c < kThetaCands; ++c) {
+    double v = acc[c];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[wid][c] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < kThetaCands) {
+    double v = 0.0;
+    for (int w = 0; w < 8; ++w) v += red[w][threadIdx.x];
+    const double budget = (double)n * (double)(n - 1) * 0.5 * exp2(-(double)theta_cf);
+    ok[threadIdx.x] = theta_cf - (float)threadIdx.x >= 8.0f && v * (1.0 + 1e-9) <= budget;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float th = theta_cf;
+    for (int c = 0; c < kThetaCands; ++c) {   // the bound grows as theta falls: stop at the first failure
+      if (!ok[c]) break;
+      th = theta_cf - (float)c;
+    }
+    out[blockIdx.x] = th;
+  }
+}
+
+cudaError_t launch_lscv_sets_skip_select(const float* X, int64_t set_stride, int n_sets, int64_t n, int T,
+                                         float theta_cf, float* out, cudaStream_t s) {
+  if (n_sets <= 0) return cudaSuccess;
+  lscv_sets_skip_select_kernel<<<(unsigned)n_sets, 256, 0, s>>>(X, set_stride, n, T, theta_cf, out);
+  return cudaGetLastError();
+}
+
 }  // namespace kde

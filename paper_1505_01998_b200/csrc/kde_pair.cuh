@@ -77,6 +77,7 @@ struct Args {
   float skip_s;                      // LSCV on coordinate-0-sorted data: skip bound on s (+inf: never)
   int part_rank, part_world;         // tile_begin/tile_end index this rank's round-robin tiles (shard_tile)
   const double* skip_gap_dev;        // Psi: skip_gap in device memory (PLUGIN chain), or null
+  const float* skip_s_sets;          // LSCV_H sets: per-set skip bound on s (data-aware selection), or null
 };
 
 // Work distribution.  Static: CTA b takes units b, b + grid, ...  Dynamic (a.work != null): CTA b
@@ -422,13 +423,13 @@ struct IsCentred<F, std::enable_if_t<F::kCentred>> : std::true_type {};
 // (rounding is monotone) and s >= fp32(g^2) (the other squares only add), so fp32(g^2) > skip_s makes
 // every term exactly 0.  X = the (set's) prepared data; false for skip_s = +inf and for Psi functors.
 template <class F>
-__device__ __forceinline__ bool lscv_tile_skipped(const Args& a, const float* X, int64_t l, int64_t q) {
+__device__ __forceinline__ bool lscv_tile_skipped(const float* X, int64_t l, int64_t q, float skip_s) {
   if constexpr (IsCentred<F>::value) {
     return false;
   } else {
     if (q >= l) return false;
     const float g = __fsub_rn(X[l * F::T], X[q * F::T + F::T - 1]);
-    return __fmul_rn(g, g) > a.skip_s;
+    return __fmul_rn(g, g) > skip_s;
   }
 }
 
@@ -516,7 +517,7 @@ __global__ void __launch_bounds__(F::NT, F::MINB) pair_kernel(const Args a,
   auto issue = [&](int64_t u, int buf) {
     int64_t l, q;
     tile_coords(shard_tile(a.tile_begin + u / CS, a.part_rank, a.part_world), l, q);
-    s_skip[buf] = lscv_tile_skipped<F>(a, a.X, l, q);
+    s_skip[buf] = lscv_tile_skipped<F>(a.X, l, q, a.skip_s);
     float* dst = cols + buf * D * T;
     mbar_expect_tx(&bar[buf], (uint32_t)(D * T * sizeof(float)));
 #pragma unroll
@@ -572,7 +573,7 @@ __global__ void __launch_bounds__(F::NT, F::MINB) pair_kernel_sets(const Args a,
     int64_t l, q;
     tile_coords(shard_tile(a.tile_begin + (u - set * per), a.part_rank, a.part_world), l, q);
     const float* Xs = a.X + set * a.set_stride;
-    s_skip[buf] = lscv_tile_skipped<F>(a, Xs, l, q);
+    s_skip[buf] = lscv_tile_skipped<F>(Xs, l, q, a.skip_s_sets != nullptr ? a.skip_s_sets[set] : a.skip_s);
     float* dst = cols + buf * D * T;
     mbar_expect_tx(&bar[buf], (uint32_t)(D * T * sizeof(float)));
 #pragma unroll
@@ -641,7 +642,7 @@ inline cudaError_t launch_pair(const LaunchCfg& c, const typename F::Params& p) 
   if (grid < 1) grid = 1;
   Args a{c.X, c.n, c.ld, c.tile_begin, c.tile_end, c.scale_exp, c.limbs, c.clamp, c.n_sets, c.set_stride,
          c.Y64, c.centres, c.skipped, c.n_sets_dev, c.skip_gap, c.work, c.skip_s, c.part_rank, c.part_world,
-         c.skip_gap_dev};
+         c.skip_gap_dev, c.skip_s_sets};
   if constexpr (F::kSets) {
     if (c.pdl) {
       cudaLaunchConfig_t lc = {};

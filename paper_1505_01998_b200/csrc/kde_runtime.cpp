@@ -423,6 +423,7 @@ kde_status run_sums(kde_ctx* c, int d, int64_t n, int64_t ld, int T, int scale, 
     cfg.skip_gap = L.skip_gap;
     cfg.skip_gap_dev = L.skip_gap_dev;
     cfg.skip_s = L.skip_s;
+    cfg.skip_s_sets = L.skip_s_sets;
     if (c->profiling && L.skip_s < __builtin_inff()) cfg.skipped = lscv_skipped;
     cfg.work = work + (&L - launches.data());
     if (two && ((&L - launches.data()) & 1)) cfg.stream = c->side_stream;

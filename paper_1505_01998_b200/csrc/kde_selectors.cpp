@@ -301,9 +301,11 @@ HCand h_candidate(const double* vh, int d) {
 // form (2d + 2 FP32 ops per eval instead of d(d+1)/2 + 2 per candidate plus the monomials), and
 // the sum of squares does not lose accuracy with cond(H).  Candidates are
 // independent work units, so a candidate's sums are bit-identical alone or inside any batch.
+// data_aware: per-set bounded skip thresholds chosen on the device (launch_lscv_sets_skip_select) —
+// scores and raw sums; the Nelder–Mead searches keep the closed form, so host and device loops agree.
 kde_status lscv_H_raw(kde_ctx* c, const double* X, int64_t n, int d, const std::vector<HCand>& cands,
                       const Moments& m, int shard_rank, int shard_world, bool allreduce,
-                      std::vector<kde_fixed>& out) {
+                      std::vector<kde_fixed>& out, bool data_aware = false) {
   const int T = kde::tile_for(Kind::LscvMatrix, d, n);
   const int64_t ld = (n + T - 1) / T * T;
   const int64_t set_floats = (int64_t)d * ld;
@@ -316,8 +318,9 @@ kde_status lscv_H_raw(kde_ctx* c, const double* X, int64_t n, int d, const std::
   out.clear();
   for (int b0 = 0; b0 < nc; b0 += per_launch) {
     const int cnt = std::min(per_launch, nc - b0);
-    TRY(grow(c, &c->white_ws, &c->white_bytes, (size_t)cnt * set_floats * sizeof(float)));
+    TRY(grow(c, &c->white_ws, &c->white_bytes, (size_t)cnt * set_floats * sizeof(float) + (size_t)cnt * sizeof(float)));
     float* Yw = static_cast<float*>(c->white_ws);
+    float* thr = Yw + (size_t)cnt * set_floats;   // per-set skip bounds (data-aware selection)
     // prep flags and this launch's limbs are one contiguous span of the workspace (get_ws): one memset
     const size_t span = (size_t)(reinterpret_cast<char*>(w.limbs + (size_t)2 * cnt * kde::kLimbs + 1) -
                                  reinterpret_cast<char*>(w.flag()));   // + run_sums' one work counter
@@ -328,6 +331,11 @@ kde_status lscv_H_raw(kde_ctx* c, const double* X, int64_t n, int d, const std::
     L.kind = Kind::LscvMatrix; L.nb = 1; L.out_offset = 0; L.n_out = 2 * cnt;
     L.X = Yw; L.n_sets = cnt; L.set_stride = set_floats;
     L.skip_s = lscv_skip_s(1.0, n);   // e = 2^-s with s = |x'_i - x'_j|^2
+    if (data_aware && L.skip_s < __builtin_inff() && kde::skip_bounded() && (n + T - 1) / T >= kde::kGapSelectMinTiles) {
+      CUDA_TRY(c, kde::launch_lscv_sets_skip_select(Yw, set_floats, cnt, n, T, L.skip_s, thr, c->stream));
+      c->prof_all += 1;
+      L.skip_s_sets = thr;
+    }
     std::vector<kde_fixed> o;
     TRY(run_sums(c, d, n, ld, T, scale_exp_for(1.0, n), w, {L}, 2 * cnt, shard_rank, shard_world, allreduce, o,
                  /*limbs_zeroed=*/true));
@@ -354,7 +362,7 @@ kde_status lscv_H_eval(kde_ctx* c, const double* X, int64_t n, int d, const Mome
   if (pdc.empty()) return KDE_OK;
   std::vector<kde_fixed> o;
   TRY(gpu_sorted_rows(c, X, n, d, &X));
-  TRY(lscv_H_raw(c, X, n, d, pdc, m, c->rank, c->world, true, o));
+  TRY(lscv_H_raw(c, X, n, d, pdc, m, c->rank, c->world, true, o, /*data_aware=*/auto_precision));
   for (size_t j = 0; j < pdc.size(); ++j) {
     double S1 = fixed_value(o[2 * j]), S2 = fixed_value(o[2 * j + 1]);
     // automatic precision (scores calls; Nelder-Mead searches keep fp32 terms, §3.10)
@@ -726,7 +734,7 @@ kde_status kde_raw_sums(kde_ctx* c, kde_sum_kind kind, const double* X, int64_t 
       if (!hc.back().pd) return fail(c, KDE_E_INVALID, "candidate %d is not positive definite", k);
     }
     if (n < 2) m.mean.assign(d, 0.0);
-    TRY(lscv_H_raw(c, X, n, d, hc, m, srank, sworld, allreduce, o));
+    TRY(lscv_H_raw(c, X, n, d, hc, m, srank, sworld, allreduce, o, /*data_aware=*/true));
   } else {
     return fail(c, KDE_E_INVALID, "unknown sum kind");
   }
