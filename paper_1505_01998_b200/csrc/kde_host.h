@@ -35,6 +35,8 @@ struct kde_ctx {
   size_t own_bytes = 0;
   // materialised S(v) buffer (f3 ablation), context-owned
   void* mat_ws = nullptr;
+  void* skip_ws = nullptr;   // LSCV_h data-aware skip: candidates' kappa and bounds
+  size_t skip_bytes = 0;
   size_t mat_bytes = 0;
   double prof_aux_ms = 0.0;
   // KDE evaluation / AQP scratch, context-owned
@@ -211,6 +213,7 @@ struct SumLaunch {
   const double* skip_gap_dev = nullptr;    // Psi: the threshold in device memory (data-aware selection)
   float skip_s = __builtin_inff();         // LSCV on sorted data: exact-zero tile skip bound on s
   const float* skip_s_sets = nullptr;      // LSCV_H sets: per-set data-aware bounds (device), or null
+  const float* skip_c_dev = nullptr;       // LSCV_h: the batch's per-candidate data-aware bounds (device), or null
   int n_sets = 1;                   // LSCV_H: candidates (one data set each), n_out per set
   int64_t set_stride = 0;
 };

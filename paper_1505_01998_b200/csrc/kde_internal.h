@@ -119,6 +119,13 @@ cudaError_t launch_psi_gap_select(int r, const double* y, int64_t n, int T, cons
 // n(n-1)/2 2^-theta_cf (the closed form's worst case, so the objective bound is unchanged).
 cudaError_t launch_lscv_sets_skip_select(const float* X, int64_t set_stride, int n_sets, int64_t n, int T,
                                          float theta_cf, float* out, cudaStream_t s);
+// LSCV_h, data-aware bounded skip: one CTA per candidate c (kappa[c] < 0, device) on the prepared data's
+// coordinate 0 (sorted); bounds on s are fp32(theta/|kappa_c|) for theta = theta_cf, theta_cf - 1, ..., 8
+// and the bound on what candidate c drops is the sum over tiles with fp32(g^2) > that of
+// T cols(l) 2^(kappa_c g^2) (x 1.0001: the kernel's fp32 exponent); out[c] = the smallest admissible bound
+// within n(n-1)/2 2^-theta_cf.
+cudaError_t launch_lscv_h_skip_select(const float* X0, int64_t n, int T, const float* kappa, int n_cand,
+                                      float theta_cf, float* out, cudaStream_t s);
 // Below this many tiles per side the selection is not run (a few tiles hardly skip; small-n latency) and
 // the pass keeps the exact-zero threshold.
 constexpr int64_t kGapSelectMinTiles = 16;
@@ -163,6 +170,7 @@ struct LaunchCfg {
   // term is exactly 0 (lscv_skip_s; +inf = never).  `skipped` then counts the skipped pairs.
   float skip_s = __builtin_inff();
   const float* skip_s_sets = nullptr;   // LSCV_H sets: per-set bounds (launch_lscv_sets_skip_select), or null
+  const float* skip_c_dev = nullptr;    // LSCV_h batch: per-candidate bounds (launch_lscv_h_skip_select), or null
   // Programmatic dependent launch (the device-resident Nelder–Mead graph): the kernel may start while
   // the previous one finishes and waits for it (griddepcontrol.wait) before reading its outputs.
   bool pdl = false;

@@ -78,4 +78,63 @@ cudaError_t launch_lscv_scalar(int d, int nb, const LaunchCfg& c, const LscvScal
   return cudaErrorInvalidValue;
 }
 
+// Data-aware bounded skip for LSCV_h (kde_internal.h launch_lscv_h_skip_select).
+constexpr int kThetaCandsH = 48;   // theta_c = theta_cf - c, c < 48, not below 8
+__global__ void __launch_bounds__(256) lscv_h_skip_select_kernel(const float* __restrict__ X0, int64_t n, int T,
+                                                                 const float* __restrict__ kappa, float theta_cf,
+                                                                 float* __restrict__ out) {
+  __shared__ double red[8][kThetaCandsH];
+  __shared__ int ok[kThetaCandsH];
+  const float k = kappa[blockIdx.x];   // < 0
+  const float ak = -k;
+  double acc[kThetaCandsH];
+#pragma unroll
+  for (int c = 0; c < kThetaCandsH; ++c) acc[c] = 0.0;
+  const int64_t nt = (n + T - 1) / T, tiles = nt * (nt + 1) / 2;
+  for (int64_t id = threadIdx.x; id < tiles; id += blockDim.x) {   // fixed per-thread order
+    int64_t l, q;
+    tile_coords(id, l, q);
+    if (q >= l) continue;
+    const float g = __fsub_rn(X0[l * T], X0[q * T + T - 1]);   // the pair kernel's skip test, exactly
+    const float g2 = __fmul_rn(g, g);
+    if (!(g2 > __fdiv_rn(8.0f, ak))) continue;
+    const int64_t cols = n - l * T < T ? n - l * T : T;
+    const double b = (double)T * (double)cols * exp2((double)k * (double)g2);   // e <= 2^(kappa g^2)
+#pragma unroll
+    for (int c = 0; c < kThetaCandsH; ++c)
+      if (g2 > __fdiv_rn(theta_cf - (float)c, ak)) acc[c] += b;
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int c = 0; c < kThetaCandsH; ++c) {
+    double v = acc[c];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[wid][c] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < kThetaCandsH) {
+    double v = 0.0;
+    for (int w = 0; w < 8; ++w) v += red[w][threadIdx.x];
+    const double budget = (double)n * (double)(n - 1) * 0.5 * exp2(-(double)theta_cf);
+    ok[threadIdx.x] = theta_cf - (float)threadIdx.x >= 8.0f && v * 1.0001 <= budget;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float th = theta_cf;
+    for (int c = 0; c < kThetaCandsH; ++c) {   // the bound grows as theta falls: stop at the first failure
+      if (!ok[c]) break;
+      th = theta_cf - (float)c;
+    }
+    out[blockIdx.x] = __fdiv_rn(th, ak);
+  }
+}
+
+cudaError_t launch_lscv_h_skip_select(const float* X0, int64_t n, int T, const float* kappa, int n_cand,
+                                      float theta_cf, float* out, cudaStream_t s) {
+  if (n_cand <= 0) return cudaSuccess;
+  lscv_h_skip_select_kernel<<<(unsigned)n_cand, 256, 0, s>>>(X0, n, T, kappa, theta_cf, out);
+  return cudaGetLastError();
+}
+
 }  // namespace kde

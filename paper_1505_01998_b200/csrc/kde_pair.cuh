@@ -78,6 +78,7 @@ struct Args {
   int part_rank, part_world;         // tile_begin/tile_end index this rank's round-robin tiles (shard_tile)
   const double* skip_gap_dev;        // Psi: skip_gap in device memory (PLUGIN chain), or null
   const float* skip_s_sets;          // LSCV_H sets: per-set skip bound on s (data-aware selection), or null
+  const float* skip_c_dev;           // LSCV_h batch: per-candidate skip bounds on s (data-aware), or null
 };
 
 // Work distribution.  Static: CTA b takes units b, b + grid, ...  Dynamic (a.work != null): CTA b
@@ -491,7 +492,7 @@ __device__ __forceinline__ void pair_unit(const Args& a, const typename F::Param
       const float g2 = __fmul_rn(g, g);
 #pragma unroll
       for (int c = 0; c < NOUT / 2; ++c)
-        if (g2 > p.skip_c[c]) v[2 * c] = v[2 * c + 1] = 0.0;
+        if (g2 > (a.skip_c_dev != nullptr ? a.skip_c_dev[c] : p.skip_c[c])) v[2 * c] = v[2 * c + 1] = 0.0;
     }
   }
   commit_tile<NOUT, F::NT>(v, red, limbs, a.scale_exp);
@@ -513,11 +514,17 @@ __global__ void __launch_bounds__(F::NT, F::MINB) pair_kernel(const Args a,
   __shared__ int s_skip[2];   // per buffer: the staged unit is an exactly-zero LSCV tile
 
   const int64_t units = (a.tile_end - a.tile_begin) * CS;
+  // LSCV_h batch: the tile skip bound is the widest of the candidates' own (data-aware) bounds
+  float skip_s = a.skip_s;
+  if (a.skip_c_dev != nullptr && tid == 0) {
+    skip_s = a.skip_c_dev[0];
+    for (int c = 1; c < NOUT / 2; ++c) skip_s = fmaxf(skip_s, a.skip_c_dev[c]);
+  }
   // thread 0 stages unit u's column chunk into buffer `buf` (TMA) and decides its skip flag
   auto issue = [&](int64_t u, int buf) {
     int64_t l, q;
     tile_coords(shard_tile(a.tile_begin + u / CS, a.part_rank, a.part_world), l, q);
-    s_skip[buf] = lscv_tile_skipped<F>(a.X, l, q, a.skip_s);
+    s_skip[buf] = lscv_tile_skipped<F>(a.X, l, q, skip_s);
     float* dst = cols + buf * D * T;
     mbar_expect_tx(&bar[buf], (uint32_t)(D * T * sizeof(float)));
 #pragma unroll
@@ -642,7 +649,7 @@ inline cudaError_t launch_pair(const LaunchCfg& c, const typename F::Params& p) 
   if (grid < 1) grid = 1;
   Args a{c.X, c.n, c.ld, c.tile_begin, c.tile_end, c.scale_exp, c.limbs, c.clamp, c.n_sets, c.set_stride,
          c.Y64, c.centres, c.skipped, c.n_sets_dev, c.skip_gap, c.work, c.skip_s, c.part_rank, c.part_world,
-         c.skip_gap_dev, c.skip_s_sets};
+         c.skip_gap_dev, c.skip_s_sets, c.skip_c_dev};
   if constexpr (F::kSets) {
     if (c.pdl) {
       cudaLaunchConfig_t lc = {};

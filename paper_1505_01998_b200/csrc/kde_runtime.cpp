@@ -424,6 +424,7 @@ kde_status run_sums(kde_ctx* c, int d, int64_t n, int64_t ld, int T, int scale, 
     cfg.skip_gap_dev = L.skip_gap_dev;
     cfg.skip_s = L.skip_s;
     cfg.skip_s_sets = L.skip_s_sets;
+    cfg.skip_c_dev = L.skip_c_dev;
     if (c->profiling && L.skip_s < __builtin_inff()) cfg.skipped = lscv_skipped;
     cfg.work = work + (&L - launches.data());
     if (two && ((&L - launches.data()) & 1)) cfg.stream = c->side_stream;
@@ -581,6 +582,7 @@ void kde_destroy(kde_ctx* c) {
   if (c->white_ws) cudaFree(c->white_ws);
   if (c->ev_ws) cudaFree(c->ev_ws);
   if (c->mat_ws) cudaFree(c->mat_ws);
+  if (c->skip_ws) cudaFree(c->skip_ws);
   for (void* p : c->in_ws)
     if (p) cudaFree(p);
   if (c->h_limbs) cudaFreeHost(c->h_limbs);

@@ -224,6 +224,21 @@ kde_status lscv_h_raw(kde_ctx* c, const double* X, int64_t n, int d, const doubl
     L.skip_s = lscv_skip_s(kmin, n);   // the batch's widest h bounds every candidate's terms
     Ls.push_back(L);
   }
+  // data-aware bounds: one selection CTA per (padded) candidate, read by the batches
+  if (Ls.front().skip_s < __builtin_inff() && kde::skip_bounded() && (n + T - 1) / T >= kde::kGapSelectMinTiles) {
+    const size_t cnt = (size_t)nbatch * nb;
+    TRY(grow(c, &c->skip_ws, &c->skip_bytes, 2 * cnt * sizeof(float)));
+    float* kap_dev = static_cast<float*>(c->skip_ws);
+    float* thr_dev = kap_dev + cnt;
+    std::vector<float> kap(cnt);
+    for (int b = 0; b < nbatch; ++b)
+      for (int j = 0; j < nb; ++j) kap[(size_t)b * nb + j] = Ls[b].ls.kappa[j];
+    CUDA_TRY(c, cudaMemcpyAsync(kap_dev, kap.data(), cnt * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(c, kde::launch_lscv_h_skip_select(w.Y, n, T, kap_dev, (int)cnt, (float)kde_lscv_skip_theta(n), thr_dev,
+                                               c->stream));
+    c->prof_all += 1;
+    for (int b = 0; b < nbatch; ++b) Ls[b].skip_c_dev = thr_dev + (size_t)b * nb;
+  }
   std::vector<kde_fixed> o;
   TRY(run_sums(c, d, n, ld, T, scale_exp_for(1.0, n), w, Ls, n_out, shard_rank, shard_world, allreduce, o));
   out.resize(2 * (size_t)nh);
