@@ -277,7 +277,7 @@ def main():
         pair_ms += prof["pair_ms"]
         pair_launches += prof["pair_launches"]
         kernel_launches += prof["kernel_launches"]
-        pair_evals += prof["pair_evals"]        # MUFU-evaluated pairs (skipped exact-zero tiles excluded)
+        pair_evals += prof["pair_evals"]        # MUFU-evaluated pairs (skipped far tiles excluded)
     kappa = ctx.last_psi_kappa()
     barrier()
     clocks = sampler.stop()
@@ -330,7 +330,7 @@ def main():
                        "h": h, "time_to_bandwidth_ms": total_ms / args.steps,
                        "psi_kappa": kappa, "psi_fp64_passes": ctx.last_fp64_passes(),
                        "evaluated_pair_fraction": evaluated_fraction},
-            "roofline": {"bound": "alu", "pipe": "MUFU.EX2 (1 per evaluated pair; tiles whose every term is exactly 0 are skipped and not counted)",
+            "roofline": {"bound": "alu", "pipe": "MUFU.EX2 (1 per evaluated pair; far tiles whose terms are exactly 0 or provably < 1e-9 of Psi-hat are skipped and not counted, DESIGN.md 3.11)",
                          "achieved": achieved / 1e12,
                          "peak": peak / 1e12, "unit": "Tex2/s", "frac": achieved / peak,
                          "traffic": load_traffic(), "kernel": "pair_kernel<FPsi<6|4,8>>",
