@@ -241,14 +241,18 @@ double kde_fixed_value(const kde_fixed *v);
 kde_fixed kde_fixed_add(kde_fixed a, kde_fixed b);
 
 /* Bounded far-tile skips of the fp32-term passes.  Pure host functions (no GPU).
- * kde_psi_skip_gap: the threshold tau on the sorted gap min|x_i - x_j|/g above which a tile of the
- *   Psi_r(g) sum (Eq. 15/17) is skipped, given r in {4,6,8}, g > 0 and the unbiased sample
- *   variance var >= 0 (Eq. 11).  The skipped terms sum to at most 1e-9 |Psi-hat_r(g)| (a lower bound on
- *   |Psi-hat_r(g)| = R(f^(r/2)) over densities of f's variance, Terrell's maximal smoothing); 13 (only
- *   tiles whose fp32 terms are all exactly 0) when no smaller tau guarantees that, and for bad arguments.
- * kde_lscv_skip_theta: theta = min(130, log2 n + 30); an LSCV tile whose pairs all have terms
- *   e = exp(-S/(4h^2)) <= 2^-theta (Eq. 24/30) is skipped, which moves g(h) / g(H)
- *   by at most 9.4e-10 (1 + kappa') |g|, kappa' = (A + B)/|g| its cancellation (<= 32 on fp32 terms). */
+ * kde_psi_skip_gap: the closed-form (data-independent) threshold tau on the sorted gap min|x_i - x_j|/g
+ *   above which a tile of the Psi_r(g) sum (Eq. 15/17) may be skipped, given r in {4,6,8},
+ *   g > 0 and the unbiased sample variance var >= 0 (Eq. 11): even if all n^2/2 pairs sat at u = tau, the
+ *   skipped terms would sum to at most 1e-9 |Psi-hat_r(g)| (a lower bound on |Psi-hat_r(g)| = R(f^(r/2))
+ *   over densities of f's variance, Terrell's maximal smoothing); 13 (only tiles whose fp32 terms are all
+ *   exactly 0) when no smaller tau guarantees that, and for bad arguments.  The passes themselves use the
+ *   data-aware threshold <= this one (same 1e-9 guarantee from the actual tile gaps; kde_last_psi_gaps).
+ * kde_lscv_skip_theta: theta_cf = min(130, log2 n + 30); LSCV tiles are skipped within the budget of
+ *   n(n-1)/2 terms e = exp(-S/(4h^2)) <= 2^-theta_cf (Eq. 24/30) — every skipped term
+ *   below 2^-theta_cf (Nelder-Mead searches), or a data-aware threshold whose skipped tiles provably stay
+ *   within the same total (scores, grid selection, raw sums) — which moves g(h) / g(H) by at most
+ *   9.4e-10 (1 + kappa') |g|, kappa' = (A + B)/|g| its cancellation (<= 32 on fp32 terms). */
 double kde_psi_skip_gap(int32_t r, double g, double var);
 double kde_lscv_skip_theta(int64_t n);
 
