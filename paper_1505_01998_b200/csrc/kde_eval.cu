@@ -26,15 +26,36 @@ constexpr int kEvTC = 1024;           // sample columns per tile
 constexpr int kEvG = 16;              // columns per compensated group
 
 struct EvalArgs {
-  const float* Y;     // D x ldm whitened queries (padded with 0)
-  const float* X;     // D x ldn whitened samples (padded with +inf -> term 0)
-  int64_t m, ldm, ldn;
+  const float* Y;     // D x ldm whitened queries (padded with 0), sorted by coordinate 0
+  const float* X;     // D x ldn whitened samples (padded with +inf -> term 0), sorted by coordinate 0
+  int64_t m, n, ldm, ldn;
   int row_blocks, splits, tiles_per_split, n_tiles;
+  float skip_s;       // far sample tiles: skipped when fp32(coordinate-0 gap)^2 > skip_s (+inf: never)
+  const int* range;   // per row block its sample tiles [ta, tb] (eval_range_kernel), or null: all
   double* part;       // [splits][ldm]
 };
 
+// Bounded far-tile skip (row f2): queries and samples are sorted by whitened coordinate
+// 0, so the sample tiles a block of sorted queries needs form one contiguous range [ta, tb]; every other
+// tile has all its terms 2^-s <= 2^-skip_s (s >= fp32(gap)^2, rounding is monotone).  Thread 0 finds the
+// range by binary search (eval_range_kernel, one thread per row block); the column split then divides
+// [ta, tb].
+__device__ __forceinline__ bool ev_tile_below(const EvalArgs& a, int t, float qmin) {   // skipped, below
+  const int64_t j = (int64_t)t * kEvTC + kEvTC - 1;
+  const float tmax = a.X[j < a.n ? j : a.n - 1];
+  if (!(tmax < qmin)) return false;
+  const float g = __fsub_rn(qmin, tmax);
+  return __fmul_rn(g, g) > a.skip_s;
+}
+__device__ __forceinline__ bool ev_tile_above(const EvalArgs& a, int t, float qmax) {   // skipped, above
+  const float tmin = a.X[(int64_t)t * kEvTC];
+  if (!(tmin > qmax)) return false;
+  const float g = __fsub_rn(tmin, qmax);
+  return __fmul_rn(g, g) > a.skip_s;
+}
+
 template <int D>
-__global__ void __launch_bounds__(kEvNT, 2) eval_kernel(const EvalArgs a) {
+__global__ void __launch_bounds__(kEvNT, D <= 4 ? 4 : 2) eval_kernel(const EvalArgs a) {   // d <= 4: <= 64 registers, 4 CTAs/SM
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* cols = reinterpret_cast<float*>(smem_raw);                        // [2][D][TC]
   uint64_t* bar = reinterpret_cast<uint64_t*>(cols + 2 * D * kEvTC);      // [2]
@@ -56,15 +77,27 @@ __global__ void __launch_bounds__(kEvNT, 2) eval_kernel(const EvalArgs a) {
   };
 
   const int units = a.row_blocks * a.splits;
+  __shared__ int s_range[2];
   uint32_t k = 0;   // running tile counter of this CTA (buffer = k & 1, parity = (k >> 1) & 1)
   for (int u = blockIdx.x; u < units; u += gridDim.x) {
     const int rb = u % a.row_blocks, cs = u / a.row_blocks;
-    const int t0 = cs * a.tiles_per_split;
-    const int t1 = min(a.n_tiles, t0 + a.tiles_per_split);
-    if (t0 >= t1) continue;
-    __syncthreads();   // previous unit finished reading both buffers
-    if (tid == 0) issue(t0, k & 1);
+    __syncthreads();   // previous unit finished reading both buffers (and s_range)
+    if (tid == 0) {    // this split's share of the row block's sample tiles [ta, tb]
+      const int ta = a.range != nullptr ? a.range[2 * rb] : 0;
+      const int tb = a.range != nullptr ? a.range[2 * rb + 1] : a.n_tiles - 1;
+      const int len = tb - ta + 1 > 0 ? tb - ta + 1 : 0;
+      s_range[0] = ta + (int)((int64_t)len * cs / a.splits);
+      s_range[1] = ta + (int)((int64_t)len * (cs + 1) / a.splits);
+    }
+    __syncthreads();
+    const int t0 = s_range[0], t1 = s_range[1];
     const int64_t r0 = (int64_t)rb * kEvRows + tid;
+    if (t0 >= t1) {   // nothing of this split is within reach: an exact zero partial
+      a.part[(int64_t)cs * a.ldm + r0] = 0.0;
+      a.part[(int64_t)cs * a.ldm + r0 + kEvNT] = 0.0;
+      continue;
+    }
+    if (tid == 0) issue(t0, k & 1);
     f2 y[D];
 #pragma unroll
     for (int d = 0; d < D; ++d) y[d] = pk(__ldg(a.Y + d * a.ldm + r0), __ldg(a.Y + d * a.ldm + r0 + kEvNT));
@@ -116,12 +149,26 @@ __global__ void __launch_bounds__(kEvNT, 2) eval_kernel(const EvalArgs a) {
   }
 }
 
+__global__ void eval_range_kernel(const EvalArgs a, int* __restrict__ range) {
+  const int rb = blockIdx.x * blockDim.x + threadIdx.x;
+  if (rb >= a.row_blocks) return;
+  const int64_t q0 = (int64_t)rb * kEvRows, q1 = q0 + kEvRows - 1 < a.m - 1 ? q0 + kEvRows - 1 : a.m - 1;
+  const float qmin = a.Y[q0], qmax = a.Y[q1];
+  int lo = 0, hi = a.n_tiles;   // first tile not skipped below the block
+  while (lo < hi) { const int mid = (lo + hi) >> 1; if (ev_tile_below(a, mid, qmin)) lo = mid + 1; else hi = mid; }
+  const int ta = lo;
+  lo = ta; hi = a.n_tiles;      // first tile skipped above it
+  while (lo < hi) { const int mid = (lo + hi) >> 1; if (ev_tile_above(a, mid, qmax)) hi = mid; else lo = mid + 1; }
+  range[2 * rb] = ta;
+  range[2 * rb + 1] = lo - 1;
+}
+
 __global__ void eval_reduce_kernel(const double* __restrict__ part, int splits, int64_t ldm,
-                                   int64_t m, double scale, double* __restrict__ out) {
+                                   int64_t m, double scale, const int* __restrict__ perm, double* __restrict__ out) {
   for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < m; q += (int64_t)gridDim.x * blockDim.x) {
     double s = 0.0;
     for (int c = 0; c < splits; ++c) s += part[(int64_t)c * ldm + q];
-    out[q] = s * scale;
+    out[perm != nullptr ? perm[q] : q] = s * scale;   // sorted query q is the caller's query perm[q]
   }
 }
 
@@ -174,12 +221,19 @@ static cudaError_t launch_eval_d(const EvalLaunch& c) {
   cudaError_t e0 = eval_occupancy<D>(&occ);
   if (e0 != cudaSuccess) return e0;
   EvalArgs a;
-  a.Y = c.Y; a.X = c.X; a.m = c.m; a.ldm = c.ldm; a.ldn = c.ldn;
+  a.Y = c.Y; a.X = c.X; a.m = c.m; a.n = c.n; a.ldm = c.ldm; a.ldn = c.ldn; a.skip_s = c.skip_s;
   a.row_blocks = (int)(c.ldm / kEvRows);
   a.n_tiles = (int)(c.ldn / kEvTC);
   a.splits = eval_split_count(c.sm_count, occ, c.ldm, c.ldn, &a.tiles_per_split);
   a.part = c.part;
+  a.range = nullptr;
   if ((size_t)a.splits * (size_t)c.ldm > c.part_capacity) return cudaErrorInvalidValue;
+  if (c.skip_s < INFINITY && c.range != nullptr) {
+    eval_range_kernel<<<(a.row_blocks + 127) / 128, 128, 0, c.stream>>>(a, c.range);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    a.range = c.range;
+  }
   const int units = a.row_blocks * a.splits;
   int grid = c.sm_count * occ;
   if (grid > units) grid = units;
@@ -189,7 +243,7 @@ static cudaError_t launch_eval_d(const EvalLaunch& c) {
   int blocks = (int)((c.m + 255) / 256);
   if (blocks > 4096) blocks = 4096;
   if (blocks < 1) blocks = 1;
-  eval_reduce_kernel<<<blocks, 256, 0, c.stream>>>(c.part, a.splits, c.ldm, c.m, c.scale, c.out);
+  eval_reduce_kernel<<<blocks, 256, 0, c.stream>>>(c.part, a.splits, c.ldm, c.m, c.scale, c.perm, c.out);
   return cudaGetLastError();
 }
 

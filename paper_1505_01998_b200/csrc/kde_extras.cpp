@@ -40,14 +40,38 @@ kde_status kde_evaluate(kde_ctx* c, const double* X, int64_t n, int32_t d, const
   int splits = 1;
   CUDA_TRY(c, kde::eval_splits(d, c->sm_count, ldm, ldn, &splits));
   const size_t parts = (size_t)splits * (size_t)ldm;
+  // bounded far-tile skip: samples and queries sorted by coordinate 0; a sample tile
+  // whose coordinate-0 gap to a query block has gap^2 > log2 n + 42 is skipped (every term <= 2^-gap^2):
+  // at most n terms of 2^-(log2 n + 42) each move fhat by <= 2^-42 n^-1 sum ... = 2.3e-13 (2 pi)^{-d/2}
+  // |H|^{-1/2}, which is <= 2.3e-13 of max fhat (fhat at any sample point is at least that scale).
+  const char* e_nos = getenv("KDE_DEBUG_EVAL_NOSKIP");   // A/B and tests: read at every call
+  // (worth its two sorts from about 2^32 pairs on: below that the launch is a fraction of a millisecond)
+  const bool skip = kde::skip_bounded() && !(e_nos && atoi(e_nos) == 1) && (double)m * (double)n >= 4294967296.0;
+  const size_t sort_tmp = skip ? kde::sort_rows_temp_bytes(m) : 0;
   const size_t need = align256((size_t)d * ldm * 4) + align256((size_t)d * ldn * 4) + align256(parts * 8) +
-                      align256((size_t)m * 8);
+                      align256((size_t)m * 8) +
+                      (skip ? align256((size_t)m * d * 8) + align256((size_t)m * 8) + align256((size_t)2 * m * 4) +
+                                  align256((size_t)2 * (ldm / R) * 4) + align256(sort_tmp)
+                            : 0);
   TRY(grow(c, &c->ev_ws, &c->ev_bytes, need));
   char* p = (char*)c->ev_ws;
   float* Yw = (float*)p; p += align256((size_t)d * ldm * 4);
   float* Xw = (float*)p; p += align256((size_t)d * ldn * 4);
   double* part = (double*)p; p += align256(parts * 8);
-  double* out = (double*)p;
+  double* out = (double*)p; p += align256((size_t)m * 8);
+  const int* perm = nullptr;
+  int* range = nullptr;
+  if (skip) {
+    range = (int*)p; p += align256((size_t)2 * (ldm / R) * 4);
+    double* ys = (double*)p; p += align256((size_t)m * d * 8);
+    double* keys = (double*)p; p += align256((size_t)m * 8);
+    int* idx = (int*)p; p += align256((size_t)2 * m * 4);
+    CUDA_TRY(c, kde::launch_sort_rows(Y, m, d, ys, keys, idx, p, sort_tmp, c->stream));
+    c->prof_all += 12;
+    Y = ys;
+    perm = idx + m;                                 // sorted query q = the caller's query perm[q]
+    TRY(gpu_sorted_rows(c, X, n, d, &X));           // samples by coordinate 0 (context-owned copy)
+  }
   Ws w;
   TRY(get_ws(c, 256, d, 2, &w));
   // centre both sets on the sample mean (fp32 accuracy of the differences)
@@ -73,6 +97,8 @@ kde_status kde_evaluate(kde_ctx* c, const double* X, int64_t n, int32_t d, const
   el.Y = Yw; el.X = Xw; el.m = m; el.ldm = ldm; el.ldn = ldn; el.part = part; el.part_capacity = parts;
   el.scale = std::pow(2.0 * kPi, -0.5 * d) / std::sqrt(det) / (double)n;
   el.out = out; el.stream = c->stream; el.sm_count = c->sm_count;
+  el.n = n; el.perm = perm; el.range = range;
+  el.skip_s = skip ? (float)(std::log2((double)std::max<int64_t>(n, 2)) + 42.0) : __builtin_inff();
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (c->profiling) { e0 = next_event(c); e1 = next_event(c); cudaEventRecord(e0, c->stream); }
   c->prof_all += 1 + 2 + 2 + 2;   // moments1 + reduce, 2 x prep, eval + reduce

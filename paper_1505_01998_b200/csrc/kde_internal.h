@@ -261,9 +261,13 @@ constexpr double kPsiKappaMax = 1.0e4;
 
 // KDE evaluation on an m x n rectangle (kde_eval.cu).
 struct EvalLaunch {
-  const float* Y;        // D x ldm whitened queries
-  const float* X;        // D x ldn whitened samples, padded with +inf
+  const float* Y;        // D x ldm whitened queries (sorted by coordinate 0 when skip_s is finite)
+  const float* X;        // D x ldn whitened samples, padded with +inf (sorted likewise)
   int64_t m, ldm, ldn;   // ldm multiple of eval_rows_per_block(), ldn of eval_cols_per_tile()
+  int64_t n = 0;         // samples
+  float skip_s = __builtin_inff();   // bounded far-tile skip on the coordinate-0 gap^2
+  const int* perm = nullptr;         // out[perm[q]] = fhat(sorted query q), or null (identity)
+  int* range = nullptr;              // scratch: 2 ints per block of eval_rows_per_block() queries
   double* part;          // scratch [splits][ldm]
   size_t part_capacity;  // doubles available in part
   double scale;          // n^-1 (2 pi)^{-d/2} |H|^{-1/2}

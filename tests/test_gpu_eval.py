@@ -63,3 +63,19 @@ def test_aqp_matches_oracle(ctx):
         assert sm[q] == pytest.approx(s, rel=1e-8, abs=1e-9)
         if c > 1e-9:
             assert avg[q] == pytest.approx(a, rel=1e-8)
+
+
+@pytest.mark.parametrize("d", [1, 2])
+def test_evaluate_sorted_skip_path_unsorted_queries(ctx, d):
+    # >= 2^32 pairs: samples and queries are sorted by coordinate 0, far sample tiles skipped (DESIGN
+    # §3.11) and the results scattered back to the caller's query order; 64 random queries (tails
+    # included) against the fp64 oracle, same tolerance as above.
+    n, m = 1 << 17, 1 << 15
+    X = datagen.sample_mixture("C5", n, 31)[:d]
+    Y = datagen.sample_mixture("C5", m, 32)[:d] * 1.6          # unsorted, some far in the tails
+    H = _H(d, 5, 0.02)
+    got = ctx.evaluate(kb.to_device(X), kb.to_device(Y), H)
+    idx = np.random.default_rng(7).choice(m, 64, replace=False)
+    ref = oracle.kde_eval(X, Y[:, idx], H)
+    peak = oracle.kde_eval(X, X[:, :256], H).max()
+    np.testing.assert_allclose(got[idx], ref, rtol=1e-5, atol=1e-12 * peak)
