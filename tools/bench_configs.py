@@ -121,8 +121,12 @@ def run(cfg, reps):
         grid = np.linspace(h0 / 4, 4 * h0, 1024)
         dt, prof, g = timed(lambda: ctx.lscv_h_scores(Xd, grid), reps)
         pairs = n * (n - 1) / 2
-        line(cfg, "lscv_h_scores 1024 h, n=65536", dt, prof, {"argmin": int(np.argmin(g)), "g_min": float(g.min())},
-             alg=pairs * 1024)
+        # a quarter of the exponentials come from the FMA pipe, so the kernel's own bound is
+        # the MUFU peak / 0.75 (21.3 evals/clk/SM)
+        mixed = PEAK / 0.75
+        eps = prof["pair_evals"] / (prof["pair_ms"] / 1e3) if prof["pair_ms"] > 0 else 0.0
+        line(cfg, "lscv_h_scores 1024 h, n=65536", dt, prof, {"argmin": int(np.argmin(g)), "g_min": float(g.min()),
+             "mixed_bound_evals_per_s": mixed, "frac_mixed_bound": eps / mixed}, alg=pairs * 1024)
         dt, prof, r = timed(lambda: ctx.select_bandwidth(kb.LSCV_h, Xd, n_grid=1024), 1)
         gd = gold("C2_lscv_h.json")
         gs = ctx.lscv_h_scores(Xd, gd["h"])
