@@ -104,14 +104,16 @@ KDE_HDI double psi_bounded_gap(int r, double g, double var) {
   }
   return t;
 }
-// Data-aware threshold: one CTA bounds, for each tau of the grid 6, 6.25, ..., 12.75, the
+// Data-aware threshold: up to 296 CTAs (fixed shares of the tile ids) and one
+// finalising warp, in a fixed order, bound, for each tau of the grid 6, 6.25, ..., 12.75, the
 // terms of the tiles a pass would skip, sum over tiles (l, q < l) with sorted gap > tau of
 // 2 T cols(l) gap^r e^{-gap^2/2} (each pair of such a tile has u >= gap >= 6), and writes to *out the
 // smallest tau whose bound is at most n^2 e^{psi_skip_log_target} (kSkipEps of Terrell's lower bound), or
 // the closed form psi_bounded_gap if that is smaller.  y = the pass's sorted scaled samples (launch_psi_prep),
 // g and var from device memory (g_dev, var_dev) or the values.  Deterministic (fixed order).
 cudaError_t launch_psi_gap_select(int r, const double* y, int64_t n, int T, const double* g_dev, double g_val,
-                                  const double* var_dev, double var_val, double* out, cudaStream_t s);
+                                  const double* var_dev, double var_val, double* out, double* scratch,
+                                  cudaStream_t s);   // scratch: 296 x 28 doubles (two launches)
 // LSCV_H sets, data-aware bounded skip: one CTA per prepared set (whitened coordinate
 // 0 at X + s * set_stride, sorted) bounds what a pass drops for each theta of the grid theta_cf,
 // theta_cf - 1, ..., 8 — sum over tiles (l, q < l) with fp32(g^2) > theta of T cols(l) 2^-fp32(g^2), the

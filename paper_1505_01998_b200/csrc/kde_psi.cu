@@ -406,17 +406,25 @@ __device__ __forceinline__ void set_status(double* st, int code) {
 }
 
 // Data-aware bounded-skip threshold (kde_internal.h launch_psi_gap_select).
-constexpr int kGapCands = 28;   // tau_c = 6 + c/4 < 13
-__global__ void __launch_bounds__(256) psi_gap_select_kernel(int r, const double* __restrict__ y, int64_t n, int T,
-                                                              const double* g_dev, double g_val,
-                                                              const double* var_dev, double var_val, double* out) {
+constexpr int kGapCands = 28;     // tau_c = 6 + c/4 < 13
+constexpr int kGapMaxCtas = 296;  // partial sums of at most this many CTAs (scratch: kGapMaxCtas x kGapCands)
+static int gap_ctas(int64_t tiles) {
+  const int64_t g = (tiles + 1023) / 1024;
+  return (int)(g < 1 ? 1 : (g > kGapMaxCtas ? kGapMaxCtas : g));
+}
+
+// Stage 1: CTA b bounds the skippable mass of its contiguous share of tile ids for every candidate tau
+// (fixed per-thread order and warp/CTA reduction order) and writes kGapCands partials.
+__global__ void __launch_bounds__(256) psi_gap_partial_kernel(int r, const double* __restrict__ y, int64_t n, int T,
+                                                              double* __restrict__ part) {
   __shared__ double red[8][kGapCands];
-  const double g = g_dev != nullptr ? *g_dev : g_val, var = var_dev != nullptr ? *var_dev : var_val;
   double acc[kGapCands];
 #pragma unroll
   for (int c = 0; c < kGapCands; ++c) acc[c] = 0.0;
   const int64_t nt = (n + T - 1) / T, tiles = nt * (nt + 1) / 2;
-  for (int64_t id = threadIdx.x; id < tiles; id += blockDim.x) {   // fixed per-thread order
+  const int64_t chunk = (tiles + gridDim.x - 1) / gridDim.x;
+  const int64_t b0 = (int64_t)blockIdx.x * chunk, b1 = b0 + chunk < tiles ? b0 + chunk : tiles;
+  for (int64_t id = b0 + threadIdx.x; id < b1; id += blockDim.x) {
     int64_t l, q;
     tile_coords(id, l, q);
     if (q >= l) continue;
@@ -437,18 +445,31 @@ __global__ void __launch_bounds__(256) psi_gap_select_kernel(int r, const double
     if (lane == 0) red[wid][c] = v;
   }
   __syncthreads();
-  __shared__ int ok[kGapCands];
-  if (threadIdx.x < kGapCands) {   // one candidate per thread: its warp partials in fixed order
+  if (threadIdx.x < kGapCands) {
     double v = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v += red[w][threadIdx.x];
+    for (int w = 0; w < 8; ++w) v += red[w][threadIdx.x];
+    part[(int64_t)blockIdx.x * kGapCands + threadIdx.x] = v;
+  }
+}
+
+// Stage 2 (one warp): the CTAs' partials in CTA order, then the smallest admissible tau (acc is
+// non-increasing in c), never above the closed form.
+__global__ void psi_gap_finalize_kernel(int r, int64_t n, int nparts, const double* __restrict__ part,
+                                        const double* g_dev, double g_val, const double* var_dev, double var_val,
+                                        double* out) {
+  __shared__ int ok[kGapCands];
+  const double g = g_dev != nullptr ? *g_dev : g_val, var = var_dev != nullptr ? *var_dev : var_val;
+  if (threadIdx.x < kGapCands) {
+    double v = 0.0;
+    for (int b = 0; b < nparts; ++b) v += part[(int64_t)b * kGapCands + threadIdx.x];
     const double lim = (double)n * (double)n * exp(psi_skip_log_target(r, g, var));
     ok[threadIdx.x] = psi_skip_args_ok(g, var) && v * (1.0 + 1e-9) <= lim;
   }
-  __syncthreads();
+  __syncwarp();
   if (threadIdx.x == 0) {
     double tau = psi_bounded_gap(r, g, var);
     for (int c = 0; c < kGapCands; ++c)
-      if (ok[c]) {   // acc is non-increasing in c: the first admissible candidate is the smallest tau
+      if (ok[c]) {
         tau = fmin(tau, 6.0 + 0.25 * c);
         break;
       }
@@ -457,8 +478,14 @@ __global__ void __launch_bounds__(256) psi_gap_select_kernel(int r, const double
 }
 
 cudaError_t launch_psi_gap_select(int r, const double* y, int64_t n, int T, const double* g_dev, double g_val,
-                                  const double* var_dev, double var_val, double* out, cudaStream_t s) {
-  psi_gap_select_kernel<<<1, 256, 0, s>>>(r, y, n, T, g_dev, g_val, var_dev, var_val, out);
+                                  const double* var_dev, double var_val, double* out, double* scratch,
+                                  cudaStream_t s) {
+  const int64_t nt = (n + T - 1) / T;
+  const int G = gap_ctas(nt * (nt + 1) / 2);
+  psi_gap_partial_kernel<<<G, 256, 0, s>>>(r, y, n, T, scratch);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  psi_gap_finalize_kernel<<<1, 32, 0, s>>>(r, n, G, scratch, g_dev, g_val, var_dev, var_val, out);
   return cudaGetLastError();
 }
 

@@ -126,8 +126,8 @@ kde_status psi_raw(kde_ctx* c, const double* x, int64_t n, int r, const double* 
       const bool select = L.skip_gap < INFINITY && kde::skip_bounded() && (n + T - 1) / T >= kde::kGapSelectMinTiles;
       if (select) {   // data-aware threshold on the device, read by the pass
         CUDA_TRY(c, kde::launch_psi_gap_select(r, b.Y64, n, T, nullptr, g[k], nullptr, var, w.small + kde::kGapSlot,
-                                               c->stream));
-        c->prof_all += 1;
+                                               w.part, c->stream));
+        c->prof_all += 2;
         L.skip_gap_dev = w.small + kde::kGapSlot;
       }
       psi_coeffs(r, L.psi);
@@ -505,8 +505,8 @@ static kde_status plugin_enqueue(kde_ctx* c, const double* x, int64_t n, int T, 
     CUDA_TRY(c, kde::launch_psi_prep(xs, n, dv.mean, dv.W, T, b.Y64, b.Yc, b.centres, ld, st, w.flag(), 3.0e4));
     if (mode != 1 && psi_plugin_select(n, T)) {   // data-aware threshold
       CUDA_TRY(c, kde::launch_psi_gap_select(r, b.Y64, n, T, dv.trace + (k == 0 ? 3 : 5), 0.0, dv.trace, 0.0,
-                                             w.small + kde::kGapSlot + k, st));
-      c->prof_all += 1;
+                                             w.small + kde::kGapSlot + k, w.part, st));
+      c->prof_all += 2;
     }
     if (mode != 1)
       TRY(plugin_pass(c, r, n, ld, T, Ss[k], b, w.flag() + 1, L + (size_t)(2 * k) * kde::kLimbs, tb, te, pairs,
