@@ -207,7 +207,10 @@ double kde_last_aux_ms(const kde_ctx *ctx);
  *   f_host[q] = n^-1 sum_i |H|^{-1/2} (2 pi)^{-d/2} exp(-1/2 (y_q - X_i)^T H^-1 (y_q - X_i)).
  * vechH_host: d(d+1)/2 doubles; the scalar-h estimator of Eq. kde-def is H = h^2 I.
  * Non-positive-definite H -> KDE_E_NONPOSITIVE_BW.  With world > 1 every rank computes all m
- * values (no collective). */
+ * values (no collective).  Accuracy: relative 1e-5 (fp32 terms) or, in the far tails, absolute
+ * 1e-12 of max fhat: from m n >= 2^32 on, samples and queries are sorted by coordinate 0 and sample
+ * tiles farther than sqrt(log2 n + 42) whitened units from a block of queries are skipped, which moves
+ * any f_host[q] by at most 2.3e-13 of max fhat. */
 kde_status kde_evaluate(kde_ctx *ctx, const double *X_dev, int64_t n, int32_t d, const double *Y_dev,
                         int64_t m, const double *vechH_host, double *f_host);
 
